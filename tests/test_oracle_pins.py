@@ -1,0 +1,312 @@
+"""Pins of the fp64 docking oracle (oracle/oracle.c) to things other than itself.
+
+Each test names the SURVEY 8(c) pin it implements and the DESIGN.md reading it
+freezes.  Independent references used here: closed forms (multilinear and
+linear grids), scipy.ndimage.map_coordinates (library trilinear interpolation),
+scipy.spatial.transform.Rotation (library Rodrigues rotation), invariants of
+rigid motions, and an exhaustive numpy brute force over all K^R angle
+combinations on tiny ligands.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+from scipy.ndimage import map_coordinates
+from scipy.spatial.transform import Rotation
+
+import oracle
+import vsgen
+
+
+def mkpocket(G, origin=(0.0, 0.0, 0.0), h=1.0, center=None, kappa=1.0):
+    G = np.ascontiguousarray(G, np.float32)
+    nz, ny, nx = G.shape
+    if center is None:
+        center = tuple(origin[a] + h * (n - 1) / 2 for a, n in enumerate((nx, ny, nz)))
+    return vsgen.Pocket(G, tuple(origin), float(h), tuple(center), float(kappa))
+
+
+def lib_ref_score(pk, pts):
+    """Independent g: scipy trilinear (clamped, 'nearest') + kappa*h*L1 excess (reading Q9)."""
+    u = (np.asarray(pts, np.float64) - np.array(pk.origin)) / pk.spacing
+    nx, ny, nz = pk.dims
+    top = np.array([nx - 1, ny - 1, nz - 1], np.float64)
+    uc = np.clip(u, 0.0, top)
+    e = np.abs(u - uc).sum(axis=1)
+    v = map_coordinates(pk.grid.astype(np.float64), [uc[:, 2], uc[:, 1], uc[:, 0]], order=1, mode="nearest")
+    return v + pk.out_slope * pk.spacing * e
+
+
+# ----------------------------------------------------------------------------- a8 interpolation
+
+def test_grid_node_exactness():
+    rng = np.random.default_rng(0)
+    G = rng.normal(size=(5, 6, 7)).astype(np.float32)
+    pk = mkpocket(G, origin=(1.0, -2.0, 0.5), h=0.5)
+    pts, want = [], []
+    for k in range(5):
+        for j in range(6):
+            for i in range(7):
+                pts.append([1.0 + 0.5 * i, -2.0 + 0.5 * j, 0.5 + 0.5 * k])
+                want.append(float(G[k, j, i]))
+    got = oracle.grid_score(pk, np.array(pts))
+    assert np.array_equal(got, np.array(want))          # bitwise, incl. upper edges (i0 = n-2, f = 1)
+
+
+def test_grid_multilinear_closed_form():
+    # trilinear interpolation reproduces any multilinear polynomial exactly (closed form)
+    a, b, c, d, e, f, g, h = 3, -2, 5, 1, 2, -1, 4, -3
+    poly = lambda x, y, z: a + b * x + c * y + d * z + e * x * y + f * y * z + g * z * x + h * x * y * z
+    Z, Y, X = np.meshgrid(np.arange(6), np.arange(7), np.arange(8), indexing="ij")
+    G = poly(X, Y, Z).astype(np.float32)                 # integers: exact in fp32
+    pk = mkpocket(G)
+    rng = np.random.default_rng(1)
+    p = rng.uniform([0, 0, 0], [7, 6, 5], size=(2000, 3))
+    got = oracle.grid_score(pk, p)
+    want = poly(p[:, 0], p[:, 1], p[:, 2])
+    assert np.max(np.abs(got - want)) < 1e-9
+
+
+def test_grid_matches_scipy_trilinear_inside_and_outside():
+    rng = np.random.default_rng(2)
+    G = rng.normal(size=(9, 10, 11)).astype(np.float32)
+    pk = mkpocket(G, origin=(-3.0, 2.0, 1.0), h=0.75, kappa=2.5)
+    lo = np.array(pk.origin) - 4.0
+    hi = np.array(pk.origin) + 0.75 * np.array([10, 9, 8]) + 4.0
+    p = rng.uniform(lo, hi, size=(5000, 3))
+    assert np.max(np.abs(oracle.grid_score(pk, p) - lib_ref_score(pk, p))) < 1e-12
+
+
+def test_far_atom_penalty_closed_form():
+    G = np.full((4, 4, 4), 2.0, np.float32)
+    G[3, 3, 3] = 7.0
+    pk = mkpocket(G, h=2.0, kappa=1.5)
+    # 10 A beyond the upper corner on x, 4 A below 0 on y, inside on z at the top face
+    y = np.array([[6.0 + 10.0, -4.0, 6.0]])
+    # clamped point = node (3, 0, 3) -> 2.0; excess in grid units = 10/2 + 4/2 = 7
+    assert oracle.grid_score(pk, y)[0] == pytest.approx(2.0 + 1.5 * 2.0 * 7.0, abs=1e-12)
+    y = np.array([[6.0 + 3.0, 6.0 + 3.0, 6.0 + 3.0]])
+    assert oracle.grid_score(pk, y)[0] == pytest.approx(7.0 + 1.5 * 2.0 * 4.5, abs=1e-12)
+
+
+# ----------------------------------------------------------------------------- a6 placement
+
+@pytest.fixture(scope="module")
+def c1():
+    c = vsgen.CONFIGS["C1"]
+    L = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    return L, vsgen.pocket(101), vsgen.pose_table(c["P"]), vsgen.angle_table(c["K"])
+
+
+def test_identity_pose(c1):
+    L, pk, (rot, tr), _ = c1
+    assert np.array_equal(rot[0], np.eye(3, dtype=np.float32)) and not tr.any()
+    for i in range(L.n):
+        x, _ = L.ligand(i)
+        y = oracle.place(pk, x, rot[0], tr[0])
+        want = x.astype(np.float64) - x.astype(np.float64).mean(axis=0) + np.array(pk.center)
+        assert np.max(np.abs(y - want)) < 1e-12
+
+
+def test_pose_rotation_invariants(c1):
+    L, pk, (rot, tr), _ = c1
+    for p in range(rot.shape[0]):
+        R = rot[p].astype(np.float64)
+        assert np.max(np.abs(R.T @ R - np.eye(3))) < 1e-6
+        assert abs(np.linalg.det(R) - 1.0) < 1e-6
+    for i in range(4):
+        x, _ = L.ligand(i)
+        d0 = np.linalg.norm(x[:, None].astype(np.float64) - x[None].astype(np.float64), axis=-1)
+        for p in range(rot.shape[0]):
+            y = oracle.place(pk, x, rot[p], tr[p])
+            d = np.linalg.norm(y[:, None] - y[None], axis=-1)
+            assert np.max(np.abs(d - d0)) < 1e-5
+            assert np.max(np.abs(y.mean(axis=0) - np.array(pk.center))) < 1e-9
+            # closed form R (x - xbar) + c (numpy, independent of the oracle's loops)
+            want = (x.astype(np.float64) - x.astype(np.float64).mean(0)) @ rot[p].astype(np.float64).T
+            assert np.max(np.abs(y - (want + np.array(pk.center)))) < 1e-9
+
+
+# ----------------------------------------------------------------------------- a7 fragment rotation
+
+def test_fragment_rotation_matches_scipy_rodrigues(c1):
+    L, pk, (rot, tr), _ = c1
+    rng = np.random.default_rng(3)
+    for i in range(L.n):
+        x, fr = L.ligand(i)
+        if len(fr) == 0:
+            continue
+        y = oracle.place(pk, x, rot[1], tr[1])
+        for f in fr:
+            a, b, lo, hi = (int(v) for v in f)
+            theta = rng.uniform(-math.pi, math.pi)
+            got = oracle.rotate(y, f, math.cos(theta), math.sin(theta))
+            u = (y[b] - y[a]) / np.linalg.norm(y[b] - y[a])
+            want = y.copy()
+            want[lo:hi] = Rotation.from_rotvec(theta * u).apply(y[lo:hi] - y[b]) + y[b]
+            assert np.max(np.abs(got - want)) < 1e-12          # sign convention: right-hand rule about a->b
+
+
+def test_fragment_rotation_invariants(c1):
+    L, pk, (rot, tr), cs = c1
+    for i in range(L.n):
+        x, fr = L.ligand(i)
+        y = oracle.place(pk, x, rot[2], tr[2])
+        for f in fr:
+            a, b, lo, hi = (int(v) for v in f)
+            y0 = oracle.rotate(y, f, cs[0, 0], cs[0, 1])
+            assert np.array_equal(y0, y)                          # theta_0 = 0 -> identity, bitwise
+            y1 = oracle.rotate(y, f, cs[1, 0], cs[1, 1])
+            assert np.array_equal(y1[[a, b]], y[[a, b]])          # axis atoms fixed
+            mov = np.zeros(len(y), bool); mov[lo:hi] = True
+            for grp in (mov, ~mov):                               # both rigid bodies keep their shape
+                d0 = np.linalg.norm(y[grp][:, None] - y[grp][None], axis=-1)
+                d1 = np.linalg.norm(y1[grp][:, None] - y1[grp][None], axis=-1)
+                assert np.max(np.abs(d1 - d0)) < 1e-6
+            # distances from the axis atoms to moving atoms are preserved (bond lengths across the axis)
+            for ax in (a, b):
+                assert np.max(np.abs(np.linalg.norm(y1[lo:hi] - y1[ax], axis=1) - np.linalg.norm(y[lo:hi] - y[ax], axis=1))) < 1e-6
+            yk = y
+            for _ in range(cs.shape[0]):                          # K steps of 2 pi / K return to start
+                yk = oracle.rotate(yk, f, cs[1, 0], cs[1, 1])
+            assert np.max(np.abs(yk - y)) < 1e-4
+
+
+# ----------------------------------------------------------------------------- a7/a9 sweep + best pose
+
+def test_sweep_is_monotone_and_greedy(c1):
+    L, pk, (rot, tr), cs = c1
+    r = oracle.dock_batch(L, pk, rot, tr, cs)
+    P = rot.shape[0]
+    for i in range(L.n):
+        x, fr = L.ligand(i)
+        R = len(fr)
+        for p in range(P):
+            kseq = r.pose_angles[P * r_off(L, i) + p * R: P * r_off(L, i) + (p + 1) * R]
+            s, y, steps = oracle.replay_pose(pk, x, fr, rot[p], tr[p], cs, kseq)
+            assert s == r.pose_score[i, p]
+            prev = float(oracle.grid_score(pk, oracle.place(pk, x, rot[p], tr[p])).sum())
+            for st, k in zip(steps, kseq):
+                assert st[k] == st.min() and k == int(np.argmin(st))   # lowest k attaining the min (Q11)
+                assert abs(st[0] - prev) < 1e-9                        # k = 0 is the current pose
+                assert st[k] <= prev + 1e-12                           # monotone
+                prev = st[k]
+        assert r.best_pose[i] == int(np.argmin(r.pose_score[i]))
+        assert r.best_score[i] == r.pose_score[i].min()
+
+
+def r_off(L, i):
+    return int(L.frag_off[i])
+
+
+def test_constant_grid_ties_go_to_lowest_index(c1):
+    L, _, (rot, tr), cs = c1
+    pk = mkpocket(np.full((32, 32, 32), 0.25, np.float32), kappa=0.0)
+    r = oracle.dock_batch(L, pk, rot, tr, cs)
+    assert (r.best_pose == 0).all() and not r.angles.any()
+    assert np.allclose(r.best_score, 0.25 * L.n_atoms, atol=1e-9)
+
+
+def test_K1_or_R0_is_rigid_only(c1):
+    L, pk, (rot, tr), _ = c1
+    r = oracle.dock_batch(L, pk, rot, tr, np.array([[1.0, 0.0]], np.float32))
+    for i in range(L.n):
+        x, _ = L.ligand(i)
+        s = [oracle.grid_score(pk, oracle.place(pk, x, rot[p], tr[p])).sum() for p in range(rot.shape[0])]
+        assert abs(r.best_score[i] - min(s)) < 1e-9 and r.best_pose[i] == int(np.argmin(s))
+
+
+def test_linear_grid_closed_form():
+    """G = w.u + g0 with every atom inside the box: S = A*g0 + w.sum(u_i).  Every initial pose ties
+    (rigid rotation about the centroid keeps sum y), and each greedy step picks argmin_k w.M_k v_r with
+    v_r = sum_{i in M_r} (y_i - q) -- computed here with scipy's rotation."""
+    n, h = 32, 2.0
+    w = np.array([0.7, -1.3, 0.4])
+    Z, Y, X = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    G = (w[0] * X + w[1] * Y + w[2] * Z + 5.0).astype(np.float64)
+    pk = mkpocket(G.astype(np.float32), h=h)
+    Gf = pk.grid.astype(np.float64)
+    assert np.max(np.abs(Gf - G)) < 1e-5
+    L = vsgen.ligands(12, 11, (20, 60), (2, 6))
+    rot, tr = vsgen.pose_table(6)
+    K = 8
+    cs = vsgen.angle_table(K)
+    r = oracle.dock_batch(L, pk, rot, tr, cs)
+    for i in range(L.n):
+        x, fr = L.ligand(i)
+        p = int(r.best_pose[i])
+        y = (x.astype(np.float64) - x.astype(np.float64).mean(0)) @ rot[p].astype(np.float64).T + np.array(pk.center)
+        init = [oracle.grid_score(pk, oracle.place(pk, x, rot[q], tr[q])).sum() for q in range(6)]
+        assert np.ptp(init) < 1e-6 * max(1.0, abs(init[0]))
+        kseq = r.angles[r_off(L, i): r_off(L, i) + len(fr)]
+        for f, kg in zip(fr, kseq):
+            a, b, lo, hi = (int(v) for v in f)
+            u = (y[b] - y[a]) / np.linalg.norm(y[b] - y[a])
+            v = (y[lo:hi] - y[b]).sum(axis=0)
+            vals = [w @ Rotation.from_rotvec(math.atan2(cs[k, 1], cs[k, 0]) * u).apply(v) / h for k in range(K)]
+            assert vals[kg] <= min(vals) + 1e-6 * max(1.0, abs(min(vals)))
+            y[lo:hi] = Rotation.from_rotvec(math.atan2(cs[kg, 1], cs[kg, 0]) * u).apply(y[lo:hi] - y[b]) + y[b]
+        want = x.shape[0] * 5.0 + (w @ ((y - np.array(pk.origin)) / h).sum(axis=0))
+        assert abs(r.best_score[i] - want) < 1e-4 * max(1.0, abs(want))
+
+
+def _brute_force(pk, x, fr, rot, cs):
+    """Exhaustive min over all K^R angle combinations and all poses; numpy + scipy only."""
+    K = cs.shape[0]
+    thetas = [math.atan2(float(cs[k, 1]), float(cs[k, 0])) for k in range(K)]
+    best = math.inf
+    xc = x.astype(np.float64) - x.astype(np.float64).mean(0)
+    for p in range(rot.shape[0]):
+        y0 = xc @ rot[p].astype(np.float64).T + np.array(pk.center)
+        for combo in itertools.product(range(K), repeat=len(fr)):
+            y = y0.copy()
+            for f, k in zip(fr, combo):
+                a, b, lo, hi = (int(v) for v in f)
+                u = (y[b] - y[a]) / np.linalg.norm(y[b] - y[a])
+                y[lo:hi] = Rotation.from_rotvec(thetas[k] * u).apply(y[lo:hi] - y[b]) + y[b]
+            best = min(best, float(lib_ref_score(pk, y).sum()))
+    return best
+
+
+def _star_ligand(rng, arms):
+    """Centre atom 0 with `arms` branches (b, then 2 moving atoms), DFS preorder; disjoint M_r and no
+    axis atom inside another fragment's moving set -> the score separates over fragments."""
+    pts = [np.zeros(3)]
+    frags = []
+    dirs = [np.array(v, np.float64) / np.linalg.norm(v) for v in ([1, 1, 1], [-1, -1, 1], [-1, 1, -1], [1, -1, -1])]
+    for a in range(arms):
+        d = dirs[a]
+        b = len(pts)
+        pts.append(1.5 * d)
+        perp = np.cross(d, [0.3, 0.5, 0.8]); perp /= np.linalg.norm(perp)
+        pts.append(1.5 * d + 1.5 * (0.33 * d + 0.94 * perp) + rng.normal(scale=0.05, size=3))
+        pts.append(pts[-1] + 1.5 * d + rng.normal(scale=0.05, size=3))
+        frags.append([0, b, b + 1, b + 3])
+    x = (np.array(pts) + np.array([15.5, 15.5, 15.5])).astype(np.float32)
+    return x, np.array(frags, np.int32)
+
+
+def test_brute_force_star_ligands_greedy_is_exact():
+    rng = np.random.default_rng(4)
+    pk = vsgen.pocket(101)
+    rot, tr = vsgen.pose_table(3)
+    cs = vsgen.angle_table(8)
+    for arms in (1, 2, 3):
+        x, fr = _star_ligand(rng, arms)
+        lib = vsgen.Library(np.arange(1, dtype=np.uint64), np.array([0, len(x)], np.int64), x,
+                            np.array([0, len(fr)], np.int64), fr)
+        r = oracle.dock_batch(lib, pk, rot, tr, cs)
+        bf = _brute_force(pk, x, fr, rot, cs)
+        assert abs(r.best_score[0] - bf) < 1e-9 * max(1.0, abs(bf))
+
+
+def test_brute_force_general_ligands_greedy_upper_bounds(c1):
+    L, pk, (rot, tr), cs = c1
+    sel = [i for i in range(L.n) if 1 <= L.n_frags[i] <= 3][:4]
+    assert sel
+    r = oracle.dock_batch(L.subset(sel), pk, rot[:3], tr[:3], cs)
+    for j, i in enumerate(sel):
+        x, fr = L.ligand(i)
+        bf = _brute_force(pk, x, fr, rot[:3], cs)
+        assert r.best_score[j] >= bf - 1e-9 * max(1.0, abs(bf))

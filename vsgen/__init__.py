@@ -1,0 +1,226 @@
+"""vsgen -- seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+INPUT GENERATORS ONLY: this package draws ligands, pocket grids, pose tables
+and angle tables.  It holds none of the method's arithmetic (no placement, no
+rotation sweep, no interpolation, no bucketing); the oracle (``oracle/``) and
+the product (``paper_2303_06150_b200``) each implement that independently.
+
+The recipe (SURVEY.md 8(d) "Generators"):
+
+* ligands: ``gen.c`` (C, multithreaded, prefix-stable: ligand i depends only
+  on (seed, i)); atoms ~ U[alo, ahi], rotatable bonds ~ U[rlo, rhi]
+  independent ("weak relationship", l.412 "between 20 and 120
+  ... from 0 to 20 rotamers"; SPEC.md l.36-44 uniform).
+* pocket grid: 32^3 fp32 lattice at 1.0 A; a pseudo-receptor of 96 atoms on a
+  9-13 A shell around the centre with a 50 degree mouth; value
+  sum_j [5 exp(-d^2/2) - exp(-d^2/8)] + 0.01 |x - c|^2 evaluated in fp64.
+* pose table: p = 0 identity, p >= 1 Shoemake-uniform rotations from
+  splitmix64(pose_seed, p), fp64 -> fp32 3x3; translations 0 (reading Q7).
+* angle table: theta_k = 2 pi k / K, (cos, sin) fp64 -> fp32, entry 0 = (1, 0)
+  exactly (reading Q3).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libvsgen.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile gen.c into libvsgen.so (gcc, -O2, pthreads)."""
+    src = os.path.join(_HERE, "gen.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-fPIC", "-shared",
+                               "-o", _SO, src, "-lm", "-lpthread"])
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        i64, u64, i32 = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
+        p = ctypes.c_void_p
+        lib.vsgen_ligand_shapes.argtypes = [i64, u64, i64, i32, i32, i32, i32, p, p, p, i32]
+        lib.vsgen_ligand_shapes.restype = i32
+        lib.vsgen_ligand_fill.argtypes = [i64, u64, i64, i32, i32, i32, i32, p, p, p, p, i32]
+        lib.vsgen_ligand_fill.restype = i32
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+@dataclass
+class Library:
+    """A ligand batch in the C-ABI's CSR layout (include/vsdock.h vs_ligand_batch)."""
+    ligand_id: np.ndarray   # uint64 [n]
+    atom_off: np.ndarray    # int64 [n+1]
+    xyz: np.ndarray         # float32 [sum A, 3], Angstrom, AoS
+    frag_off: np.ndarray    # int64 [n+1]
+    frags: np.ndarray       # int32 [sum R, 4]: a, b, lo, hi (M_r = [lo, hi))
+    n_moving: np.ndarray = field(default=None)  # int32 [n]: sum_r |M_r| (generator metadata)
+
+    @property
+    def n(self) -> int:
+        return int(self.ligand_id.shape[0])
+
+    @property
+    def n_atoms(self) -> np.ndarray:
+        return np.diff(self.atom_off).astype(np.int32)
+
+    @property
+    def n_frags(self) -> np.ndarray:
+        return np.diff(self.frag_off).astype(np.int32)
+
+    def ligand(self, i: int):
+        """(xyz [A,3] float32, frags [R,4] int32) of ligand i."""
+        a0, a1 = int(self.atom_off[i]), int(self.atom_off[i + 1])
+        f0, f1 = int(self.frag_off[i]), int(self.frag_off[i + 1])
+        return self.xyz[a0:a1], self.frags[f0:f1]
+
+    def subset(self, idx) -> "Library":
+        idx = np.asarray(idx, dtype=np.int64)
+        A = self.n_atoms[idx].astype(np.int64)
+        R = self.n_frags[idx].astype(np.int64)
+        ao = np.zeros(len(idx) + 1, np.int64); ao[1:] = np.cumsum(A)
+        fo = np.zeros(len(idx) + 1, np.int64); fo[1:] = np.cumsum(R)
+        xyz = np.empty((int(ao[-1]), 3), np.float32)
+        fr = np.empty((int(fo[-1]), 4), np.int32)
+        for j, i in enumerate(idx):
+            x, f = self.ligand(int(i))
+            xyz[ao[j]:ao[j + 1]] = x
+            fr[fo[j]:fo[j + 1]] = f
+        nm = None if self.n_moving is None else self.n_moving[idx]
+        return Library(self.ligand_id[idx].copy(), ao, xyz, fo, fr, nm)
+
+
+def ligands(n: int, seed: int, atoms=(20, 120), rot=(0, 20), first: int = 0, nthreads: int | None = None) -> Library:
+    """Draw ligands first..first+n-1 of the seeded stream (prefix-stable)."""
+    if n < 0 or atoms[0] < 1 or atoms[1] < atoms[0] or rot[0] < 0 or rot[1] < rot[0]:
+        raise ValueError("inverted or invalid range")
+    if atoms[1] > 256 or rot[1] > 32:
+        raise ValueError("generator supports at most 256 atoms and 32 rotatable bonds")
+    lib = _load()
+    nthreads = nthreads or min(64, os.cpu_count() or 1)
+    A = np.zeros(n, np.int32); R = np.zeros(n, np.int32); M = np.zeros(n, np.int32)
+    rc = lib.vsgen_ligand_shapes(n, seed, first, atoms[0], atoms[1], rot[0], rot[1], _ptr(A), _ptr(R), _ptr(M), nthreads)
+    if rc != 0:
+        raise RuntimeError("vsgen_ligand_shapes failed")
+    ao = np.zeros(n + 1, np.int64); ao[1:] = np.cumsum(A, dtype=np.int64)
+    fo = np.zeros(n + 1, np.int64); fo[1:] = np.cumsum(R, dtype=np.int64)
+    xyz = np.empty((int(ao[-1]), 3), np.float32)
+    frags = np.empty((int(fo[-1]), 4), np.int32)
+    rc = lib.vsgen_ligand_fill(n, seed, first, atoms[0], atoms[1], rot[0], rot[1], _ptr(ao), _ptr(fo), _ptr(xyz), _ptr(frags), nthreads)
+    if rc != 0:
+        raise RuntimeError("vsgen_ligand_fill failed")
+    ids = np.arange(first, first + n, dtype=np.uint64)
+    return Library(ids, ao, xyz, fo, frags, M)
+
+
+# ----------------------------------------------------------------------------- pocket
+
+@dataclass
+class Pocket:
+    """A pocket grid: node (i,j,k) sits at origin + spacing*(i,j,k); values [nz,ny,nx] fp32, x fastest."""
+    grid: np.ndarray        # float32 [nz, ny, nx]
+    origin: tuple
+    spacing: float
+    center: tuple
+    out_slope: float = 1.0  # kappa, energy per Angstrom of out-of-box excess (reading Q9)
+
+    @property
+    def dims(self):
+        nz, ny, nx = self.grid.shape
+        return nx, ny, nz
+
+
+def pocket(seed: int, n: int = 32, spacing: float = 1.0, n_receptor: int = 96,
+           shell=(9.0, 13.0), mouth_deg: float = 50.0, out_slope: float = 1.0) -> Pocket:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    origin = np.zeros(3)
+    c = origin + spacing * (n - 1) / 2.0
+    pts = []
+    cos_half = math.cos(math.radians(mouth_deg / 2.0))
+    while len(pts) < n_receptor:
+        v = rng.normal(size=3)
+        v /= np.linalg.norm(v)
+        if v[2] > cos_half:          # the mouth: no receptor atoms inside the cone around +z
+            continue
+        r = rng.uniform(shell[0], shell[1])
+        pts.append(c + r * v)
+    P = np.array(pts)
+    ax = origin[0] + spacing * np.arange(n)
+    Z, Y, X = np.meshgrid(ax, ax, ax, indexing="ij")
+    node = np.stack([X, Y, Z], axis=-1)                  # [nz, ny, nx, 3]
+    G = 0.01 * np.sum((node - c) ** 2, axis=-1)
+    for p in P:
+        d2 = np.sum((node - p) ** 2, axis=-1)
+        G += 5.0 * np.exp(-d2 / 2.0) - np.exp(-d2 / 8.0)
+    return Pocket(G.astype(np.float32), tuple(float(v) for v in origin), float(spacing),
+                  tuple(float(v) for v in c), float(out_slope))
+
+
+# ----------------------------------------------------------------------------- tables
+
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64(state: int):
+    state = (state + 0x9E3779B97F4A7C15) & _M64
+    z = state
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return state, z ^ (z >> 31)
+
+
+def pose_table(P: int, seed: int = 7):
+    """(rot [P,3,3] float32 row-major, trans [P,3] float32).  p = 0 is the identity."""
+    rot = np.zeros((P, 3, 3), np.float64)
+    for p in range(P):
+        if p == 0:
+            rot[p] = np.eye(3)
+            continue
+        s = (seed * 0xD1B54A32D192ED03 ^ (p * 0x9E3779B97F4A7C15)) & _M64
+        s, a = _splitmix64(s)
+        s, b = _splitmix64(s)
+        s, d = _splitmix64(s)
+        u1, u2, u3 = [(x >> 11) / 9007199254740992.0 for x in (a, b, d)]
+        x = math.sqrt(1 - u1) * math.sin(2 * math.pi * u2)
+        y = math.sqrt(1 - u1) * math.cos(2 * math.pi * u2)
+        z = math.sqrt(u1) * math.sin(2 * math.pi * u3)
+        w = math.sqrt(u1) * math.cos(2 * math.pi * u3)
+        rot[p] = [[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                  [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                  [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]]
+    return rot.astype(np.float32), np.zeros((P, 3), np.float32)
+
+
+def angle_table(K: int) -> np.ndarray:
+    """[K,2] float32 (cos, sin) of theta_k = 2 pi k / K; entry 0 is exactly (1, 0)."""
+    t = np.array([[math.cos(2 * math.pi * k / K), math.sin(2 * math.pi * k / K)] for k in range(K)])
+    t[0] = (1.0, 0.0)
+    return t.astype(np.float32)
+
+
+# ----------------------------------------------------------------------------- configs
+
+# BASELINE.json configs[i] -> concrete synthetic inputs
+CONFIGS = {
+    "C1": dict(n=16, atoms=(20, 40), rot=(0, 4), seed=1, P=8, K=8, pockets=(101,)),
+    "C2": dict(n=10_000, atoms=(20, 120), rot=(0, 20), seed=2, P=64, K=8, pockets=(101,)),
+    "C3": dict(n=8_192, atoms=(80, 150), rot=(15, 25), seed=3, P=64, K=8, pockets=(101,)),
+    "C4": dict(n=1_000_000, atoms=(20, 120), rot=(0, 20), seed=4, P=64, K=8, pockets=(101,)),
+    "C5": dict(n=1_000_000, atoms=(20, 120), rot=(0, 20), seed=4, P=64, K=8, pockets=(101, 102, 103, 104)),
+}
