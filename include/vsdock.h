@@ -1,0 +1,205 @@
+/*
+ * vsdock.h -- C-ABI of the B200-native LiGen dock-and-score hot path
+ * (arXiv 2303.06150).  Library: paper_2303_06150_b200/libvsdock.so.
+ *
+ * Citation keys: P:n = PAPER.md line n, S:n = SPEC.md line n, BJ = BASELINE.json
+ * north_star, Qn = DESIGN.md reading n, a1..a11 = SURVEY.md 8(a) rows.
+ *
+ * The calls follow the paper's statement of the problem: identify docking
+ * sites (loaded as pocket grids), dock, score, and "for each
+ * docking site, we can rank the input chemical library"; and BJ's
+ * "load pocket grids; submit a ligand batch; return best score and pose per
+ * ligand".
+ *
+ * Conventions (all calls):
+ *  - every call returns vs_status: VS_OK (0) or a negative code; no exception
+ *    crosses the ABI; vs_last_error() returns a message naming the first
+ *    offending ligand index / axis where one exists;
+ *  - device memory is never allocated by the library: the caller provides one
+ *    device workspace (vs_set_workspace, sized by vs_workspace_size);
+ *  - host inputs are copied during the call that receives them; the caller may
+ *    free them on return.  Device inputs (on_device = 1) are borrowed until
+ *    vs_wait returns;
+ *  - one vs_ctx per GPU per process; a context is not thread-safe;
+ *  - results are deterministic: identical inputs give bit-identical outputs,
+ *    for any bucketing grid, bucket multiple and world size (Q22).
+ */
+#ifndef VSDOCK_H
+#define VSDOCK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t vs_status;
+enum {
+    VS_OK = 0,
+    VS_E_ARG = -1,              /* invalid argument / configuration */
+    VS_E_PARSE = -2,            /* invalid ligand record (a1): message names ligand index and field */
+    VS_E_OVERFLOW_ATOMS = -3,   /* atoms above the last atom boundary (axis "atoms") */
+    VS_E_OVERFLOW_ROTAMERS = -4,/* rotamers above the last rotamer boundary (axis "rotamers") */
+    VS_E_NOFIT = -5,            /* occupancy query returned b = 0: kernel does not fit */
+    VS_E_WORKSPACE = -6,        /* workspace missing or too small */
+    VS_E_CUDA = -7,             /* CUDA runtime error */
+    VS_E_STATE = -9             /* call out of order (e.g. results before submit) */
+};
+
+typedef struct vs_ctx vs_ctx;
+
+typedef struct {
+    int32_t device;            /* CUDA device ordinal */
+    int32_t n_sweeps;          /* S_w >= 1 (Q13) */
+    int32_t n_atom_clusters;   /* atom classes; 1 and 1 = unsorted baseline */
+    int32_t n_rot_clusters;    /* rotamer classes */
+    int32_t atom_upper_bound;  /* P:236 "upper bound"; 0 = observed maximum */
+    int32_t rot_upper_bound;   /* 0 = observed maximum */
+    int32_t bucket_multiple;   /* m: bucket capacity = m * l_c ("a multiple") */
+    int32_t n_streams;         /* concurrent bucket launches (1..16) */
+    int32_t rank, world_size;  /* this context docks the buckets LPT assigns to `rank` (a4) */
+    int32_t debug_poses;       /* 1: keep every pose's score and angle sequence (parity replay) */
+    void* stream;              /* cudaStream_t the library orders its work on (e.g. torch's); NULL = own */
+} vs_config;
+
+/* Create a context on cfg->device.  Fills the kernel class table (registers,
+ * shared memory) with cudaFuncGetAttributes.  Errors: VS_E_ARG, VS_E_CUDA. */
+vs_status vs_create(const vs_config* cfg, vs_ctx** out);
+void vs_destroy(vs_ctx* ctx);
+const char* vs_last_error(const vs_ctx* ctx);
+
+/* Upper bound of the device workspace for a batch of n_lig ligands with
+ * n_atoms atoms, n_frags fragments in total and at most max_atoms atoms per
+ * ligand, docked into n_pockets pockets with the current pose table.
+ * Requires the pose table.  Errors: VS_E_ARG, VS_E_STATE. */
+vs_status vs_workspace_size(vs_ctx* ctx, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int32_t max_atoms,
+                            int32_t n_pockets, size_t* bytes);
+/* Hand the library a device buffer (e.g. a torch uint8 tensor) of >= bytes; 256-B aligned. */
+vs_status vs_set_workspace(vs_ctx* ctx, void* dev_ptr, size_t bytes);
+
+/* D3: a pocket grid.  Node (i,j,k) sits at origin + spacing*(i,j,k) (Q9); values
+ * are fp32 [nz][ny][nx], x fastest.  out_slope = kappa, the continuous
+ * out-of-box penalty per Angstrom of L1 excess (Q9).  center = c of a6. */
+typedef struct {
+    int32_t nx, ny, nz;
+    float origin[3];
+    float spacing;
+    float center[3];
+    float out_slope;
+} vs_pocket_desc;
+
+/* Load (copy) a pocket grid; host or device pointer.  The grid must be finite,
+ * nx,ny,nz >= 2 and fit in shared memory together with the kernel's other
+ * buffers (else VS_E_NOFIT at submit).  Returns its id in *pocket_id.  The
+ * library keeps at most 16 pockets; each is nx*ny*nz*4 bytes of an internal
+ * host copy that is uploaded into the workspace at submit. */
+vs_status vs_load_pocket(vs_ctx* ctx, const vs_pocket_desc* desc, const float* grid, int32_t on_device, int32_t* pocket_id);
+
+/* a6 initial poses (Q7): P rotations rot[P*9] (row-major R_p) and translations
+ * trans[P*3] (tau_p), host memory, fp32.  1 <= P <= 1024. */
+vs_status vs_set_pose_table(vs_ctx* ctx, int32_t P, const float* rot, const float* trans);
+
+/* a7 angle steps (Q3): cos_sin[K*2], host, fp32; entry 0 must be exactly (1, 0);
+ * K must be a power of two, 1 <= K <= 32 (warp lane map). */
+vs_status vs_set_angle_table(vs_ctx* ctx, int32_t K, const float* cos_sin);
+
+/* D1: a ligand batch in CSR form.  Ligand i has atoms atom_off[i]..atom_off[i+1]
+ * (1 <= A <= 256) with coordinates xyz[3*atom] in Angstrom, and fragments
+ * frag_off[i]..frag_off[i+1] (0 <= R <= 32).  Fragment r is frags[4*f] =
+ * {a, b, lo, hi} in ligand-local atom indices: rotation axis a -> b, moving set
+ * M_r = [lo, hi) with a, b outside it (Q5, Q6).  on_device = 1: all
+ * pointers are device pointers (borrowed until vs_wait). */
+typedef struct {
+    int64_t n;
+    const int64_t* atom_off;
+    const float* xyz;
+    const int64_t* frag_off;
+    const int32_t* frags;
+    int32_t on_device;
+} vs_ligand_batch;
+
+/* Run the hot path a1..a9 for the batch against pockets pocket_ids[0..n_pockets):
+ * validate, classify, bucket (stable), LPT-shard, pack, and dock this rank's
+ * buckets into every pocket.  Asynchronous after the three small host syncs of
+ * the preparation phase; results are valid after vs_wait.
+ * Errors: VS_E_PARSE (first invalid ligand), VS_E_OVERFLOW_*, VS_E_NOFIT,
+ * VS_E_WORKSPACE, VS_E_STATE (tables/pockets/workspace missing), VS_E_CUDA. */
+vs_status vs_submit(vs_ctx* ctx, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets);
+vs_status vs_wait(vs_ctx* ctx);
+
+/* a9 per-ligand results for pocket slot s (index into the submit's pocket_ids),
+ * input order, length n: best score S_{p*}, best pose p*, and the angle index
+ * sequence of p*, CSR by n_sweeps*frag_off (angle_idx[S_w*frag_off[i] + sw*R_i + r]).
+ * Ligands docked by another rank: score NaN, pose -1, angles 0xFF.
+ * Any output pointer may be NULL.  on_device: outputs are device pointers. */
+vs_status vs_get_results(vs_ctx* ctx, int32_t slot, float* best_score, int32_t* best_pose, uint8_t* angle_idx,
+                         int32_t on_device);
+/* a9 best-pose coordinates (Angstrom, input atom order, [3*n_atoms]); replays p*
+ * on the GPU bit-identically to the dock kernel. */
+vs_status vs_get_coords(vs_ctx* ctx, int32_t slot, float* xyz_out, int32_t on_device);
+/* Parity hook (requires debug_poses): every pose's final score [n*P] and angle
+ * sequence [P*S_w*frag_off ...] (pose p of ligand i at P*S_w*frag_off[i] + p*S_w*R_i). */
+vs_status vs_get_pose_debug(vs_ctx* ctx, int32_t slot, float* pose_score, uint8_t* pose_angles);
+
+/* a10: the k smallest keys (ord(score) << 32 | ligand index) over this rank's
+ * ligands for pocket slot s, ascending, into keys_dev[k] (DEVICE); missing
+ * entries (fewer than k ligands) are UINT64_MAX.  *n_valid = min(k, owned).
+ * ord maps fp32 to unsigned order (sign-flip), -0 is canonicalised to +0. */
+vs_status vs_local_topk(vs_ctx* ctx, int32_t slot, int32_t k, uint64_t* keys_dev, int32_t* n_valid);
+/* a11: merge n_keys gathered keys (DEVICE, e.g. after an NCCL all_gather of W
+ * local top-k lists) into the global top-k: ligand index and score (HOST). */
+vs_status vs_merge_topk(vs_ctx* ctx, const uint64_t* keys_dev, int64_t n_keys, int32_t k, int64_t* index_out,
+                        float* score_out, int32_t* n_out);
+
+/* a3/a4 bucket manifest of the last submit (all buckets of all ranks). */
+typedef struct {
+    int32_t cell, atom_class, rot_class;
+    int32_t atom_bound;        /* inclusive upper atom threshold of the class */
+    int32_t kernel_atoms;      /* A_c: template atom capacity (multiple of 32) */
+    int32_t capacity;          /* m * l_c (Eq. 1) */
+    int32_t size;              /* ligands (<= capacity; the last of a cell may be partial) */
+    int32_t owner;             /* rank docking it (LPT) */
+    int32_t launch_order;      /* position in the owner's launch sequence */
+    int32_t pad;
+    int64_t start;             /* first position in perm */
+    uint64_t weight;           /* sum of E_alg over the bucket's ligands */
+} vs_bucket;
+/* n_buckets is always written; buckets[] (capacity max_buckets) and perm[n]
+ * (cell-major stable order of ligand indices) are written when non-NULL. */
+vs_status vs_get_manifest(vs_ctx* ctx, int32_t max_buckets, vs_bucket* buckets, int32_t* n_buckets, uint32_t* perm);
+
+/* The B200 analogue of Table 1 and Eq. 1 per atom class of
+ * the last submit (or of the grid implied by the config and pocket 0). */
+typedef struct {
+    int32_t atom_bound, kernel_atoms;
+    int32_t warps_per_cta, threads_per_cta;
+    int32_t regs_per_thread, static_smem, dyn_smem;
+    int32_t blocks_per_sm;     /* b: cudaOccupancyMaxActiveBlocksPerMultiprocessor */
+    int32_t sm_count;          /* SM */
+    int32_t ligands_per_cta;   /* t/ws (Q19) */
+    int32_t l;                 /* Eq. 1: b * SM * ligands_per_cta */
+    int32_t capacity;          /* bucket_multiple * l */
+} vs_class_info;
+vs_status vs_query_classes(vs_ctx* ctx, int32_t max_classes, vs_class_info* out, int32_t* n_classes);
+
+/* Test hook: g(y) (a8) of pocket_id at n points xyz[3n] (Angstrom, host), into
+ * g_out[n] (host), computed by the dock kernel's own device function. */
+vs_status vs_score_points(vs_ctx* ctx, int32_t pocket_id, int64_t n, const float* xyz, float* g_out);
+
+typedef struct {
+    int64_t n_ligands, n_owned;
+    int64_t n_buckets, n_owned_buckets;
+    int64_t kernel_launches;   /* kernels launched by the last submit (+ topk/coords calls since) */
+    int64_t dock_launches;
+    double evals_alg;          /* sum over owned ligands and pockets of E_alg (SURVEY 8 'E_alg') */
+    float prep_ms;             /* validate .. pack (CUDA events) */
+    float dock_ms;             /* all dock launches, first start to last end (CUDA events) */
+    float topk_ms;             /* last vs_local_topk */
+} vs_stats;
+vs_status vs_get_stats(vs_ctx* ctx, vs_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSDOCK_H */

@@ -1,0 +1,1018 @@
+// api.cpp -- host runtime behind include/vsdock.h: context, workspace planning,
+// the submit pipeline (a1..a9 orchestration), bucket table and LPT shard
+// (a4), multi-stream bucket launches, results, ranking (a10/a11).
+//
+// PAPER.md l.200-204 (workers, double buffering, one pipeline per GPU) and
+// l.219-231 (input preparation + Eq. 1 sizing) are the design being re-done:
+// on B200 the whole library is HBM-resident, so there is no worker pool and
+// no double-buffered device pool; buckets launch on several streams so that
+// partial buckets overlap (the tail effect of P:421-424).
+#include "vsdock.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace vsd;
+
+namespace {
+
+struct PocketHost {
+    vs_pocket_desc d;
+    std::vector<float> grid;
+};
+
+struct ClassInfo {
+    int atom_bound, AC, NW, LC, b, l, cap;
+    size_t smem;
+    cudaFuncAttributes attr;
+};
+
+struct Region {
+    size_t off = 0;
+    size_t add(size_t bytes) {
+        off = (off + 255) & ~(size_t)255;
+        const size_t o = off;
+        off += bytes;
+        return o;
+    }
+};
+
+int roundup32(int x) { return (x + 31) / 32 * 32; }
+
+// S:205-213 with reading Q16 (independent re-implementation of the boundary
+// formula; the oracle's Python copy is not used by the product).
+std::vector<int> atom_bounds(int n, int ub) {
+    std::vector<int> b;
+    const int last = ub >= 32 * (n - 1) + 1 ? ub : 32 * n;
+    for (int i = 1; i < n; ++i) b.push_back(32 * i);
+    b.push_back(last);
+    return b;
+}
+
+// S:215-223, prev_0 = -1, round half up in exact integer arithmetic (Q17)
+std::vector<int> rot_bounds(int n, int mx) {
+    std::vector<int> b;
+    if (n > mx) {
+        for (int v = 0; v <= mx; ++v) b.push_back(v);
+        return b;
+    }
+    long long prev = -1;
+    const unsigned long long den = (n >= 63) ? ~0ull : ((1ull << n) - 1ull);
+    for (int i = 1; i <= n; ++i) {
+        long long v;
+        if (i == n) v = mx;
+        else {
+            const unsigned long long num = (unsigned long long)mx * ((1ull << i) - 1ull);
+            v = (long long)((2ull * num + den) / (2ull * den));
+        }
+        if (v < prev + 1) v = prev + 1;
+        b.push_back((int)v);
+        prev = v;
+    }
+    return b;
+}
+
+}  // namespace
+
+struct vs_ctx {
+    vs_config cfg{};
+    int sm_count = 0;
+    cudaStream_t main = nullptr;
+    bool own_main = false;
+    std::vector<cudaStream_t> workers;
+    std::vector<cudaEvent_t> ev_worker;
+    cudaEvent_t ev_prep0 = nullptr, ev_prep1 = nullptr, ev_dock1 = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+    std::string err;
+
+    int P = 0, K = 0;
+    std::vector<float> pose_tab;  // P * 12
+    std::vector<float> cs;        // K * 2
+    std::vector<PocketHost> pockets;
+
+    uint8_t* ws = nullptr;
+    size_t ws_bytes = 0;
+    void* hpin = nullptr;
+    size_t hpin_bytes = 0;
+
+    // last job
+    bool submitted = false;
+    int64_t n = 0, nA = 0, nR = 0;
+    std::vector<int> job_pockets;
+    int64_t *d_atom_off = nullptr, *d_frag_off = nullptr;
+    float* d_xyz = nullptr;
+    int32_t* d_frags = nullptr;
+    int *d_featA = nullptr, *d_featR = nullptr, *d_featM = nullptr, *d_cell = nullptr, *d_hist = nullptr,
+        *d_cell_count = nullptr, *d_maxAR = nullptr;
+    unsigned long long* d_status = nullptr;  // [0] validation, [1] overflow
+    uint32_t* d_perm = nullptr;
+    int64_t* d_bstart = nullptr;
+    int* d_bsize = nullptr;
+    unsigned long long* d_weights = nullptr;
+    int64_t *d_own_start = nullptr, *d_own_rec_off = nullptr;
+    int *d_own_prefix = nullptr, *d_own_ac = nullptr;
+    float* d_rec = nullptr;
+    int4* d_meta = nullptr;
+    float* d_pose = nullptr;
+    float* d_cs = nullptr;
+    std::vector<float*> d_grid;
+    std::vector<float*> d_score;
+    std::vector<int*> d_pose_best;
+    std::vector<uint8_t*> d_ang;
+    std::vector<float*> d_dbg_score;
+    std::vector<uint8_t*> d_dbg_ang;
+    float* d_coords = nullptr;
+    unsigned long long* d_keys = nullptr;
+    int64_t keys_cap = 0;
+    unsigned long long* d_topk_out = nullptr;
+    void* d_sel = nullptr;
+
+    std::vector<int> atom_b, rot_b;
+    std::vector<ClassInfo> classes;
+    std::vector<vs_bucket> buckets;
+    std::vector<int> owned;             // bucket ids, launch order
+    std::vector<int> owned_prefix;      // slots
+    std::vector<int64_t> owned_rec_off; // floats
+    std::vector<PocketDev> pkdev;
+    int total_slots = 0;
+    vs_stats stats{};
+};
+
+namespace {
+
+vs_status fail(vs_ctx* c, vs_status code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(c, VS_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+vs_status ensure_pinned(vs_ctx* c, size_t bytes) {
+    if (c->hpin_bytes >= bytes) return VS_OK;
+    if (c->hpin) cudaFreeHost(c->hpin);
+    c->hpin = nullptr;
+    c->hpin_bytes = 0;
+    CK(cudaMallocHost(&c->hpin, bytes));
+    c->hpin_bytes = bytes;
+    return VS_OK;
+}
+
+PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
+    PocketDev p;
+    p.grid = dgrid;
+    p.nx = d.nx;
+    p.ny = d.ny;
+    p.nz = d.nz;
+    grid_strides(d.nx, d.ny, &p.rs, &p.ps);
+    p.top_x = (float)(d.nx - 1);
+    p.top_y = (float)(d.ny - 1);
+    p.top_z = (float)(d.nz - 1);
+    p.top2_x = (float)(d.nx - 2);
+    p.top2_y = (float)(d.ny - 2);
+    p.top2_z = (float)(d.nz - 2);
+    p.kh = (float)((double)d.out_slope * (double)d.spacing);
+    p.h = d.spacing;
+    p.inv_h = (float)(1.0 / (double)d.spacing);
+    p.ox = d.origin[0];
+    p.oy = d.origin[1];
+    p.oz = d.origin[2];
+    p.tx = (float)(((double)d.center[0] - d.origin[0]) / d.spacing);
+    p.ty = (float)(((double)d.center[1] - d.origin[1]) / d.spacing);
+    p.tz = (float)(((double)d.center[2] - d.origin[2]) / d.spacing);
+    return p;
+}
+
+// Stage-1 workspace (known from the batch sizes alone).
+struct Stage1 {
+    size_t atom_off, frag_off, xyz, frags, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
+        bsize, weights, own_start, own_prefix, own_ac, own_rec_off, pose, cs, grids, end;
+    int n_blocks;
+    int64_t max_buckets;
+};
+
+Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int P, int K, size_t grid_bytes, int n_pockets) {
+    Stage1 s;
+    Region r;
+    s.n_blocks = (int)((n + kPrepTile - 1) / kPrepTile);
+    if (s.n_blocks < 1) s.n_blocks = 1;
+    s.max_buckets = n + kMaxCells;
+    s.atom_off = r.add((n + 1) * 8);
+    s.frag_off = r.add((n + 1) * 8);
+    s.xyz = r.add(nA * 12);
+    s.frags = r.add(nR * 16);
+    s.featA = r.add(n * 4);
+    s.featR = r.add(n * 4);
+    s.featM = r.add(n * 4);
+    s.cell = r.add(n * 4);
+    s.status = r.add(16);
+    s.maxAR = r.add(8);
+    s.hist = r.add((size_t)kMaxCells * s.n_blocks * 4);
+    s.cell_count = r.add(kMaxCells * 4);
+    s.perm = r.add(n * 4);
+    s.bstart = r.add(s.max_buckets * 8);
+    s.bsize = r.add(s.max_buckets * 4);
+    s.weights = r.add(s.max_buckets * 8);
+    s.own_start = r.add(s.max_buckets * 8);
+    s.own_prefix = r.add((s.max_buckets + 1) * 4);
+    s.own_ac = r.add(s.max_buckets * 4);
+    s.own_rec_off = r.add(s.max_buckets * 8);
+    s.pose = r.add((size_t)P * 12 * 4);
+    s.cs = r.add((size_t)K * 2 * 4 + 16);
+    s.grids = r.add(grid_bytes * n_pockets);
+    s.end = r.off;
+    return s;
+}
+
+// Stage-2 workspace (records + results), placed after stage 1.
+struct Stage2 {
+    size_t rec, meta, score, pose_best, ang, dbg_score, dbg_ang, coords, keys, topk_out, sel, end;
+    size_t per_slot;  // bytes of results per pocket slot
+};
+
+Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats, int P, int S_w, int n_pockets,
+             bool debug) {
+    Stage2 s;
+    Region r;
+    r.off = base;
+    s.rec = r.add((size_t)rec_floats * 4);
+    s.meta = r.add(n * 16);
+    s.score = r.add(n * 4 * n_pockets + 256 * n_pockets);
+    s.pose_best = r.add(n * 4 * n_pockets + 256 * n_pockets);
+    s.ang = r.add((size_t)S_w * nR * n_pockets + 256 * n_pockets);
+    s.dbg_score = r.add(debug ? (size_t)n * P * 4 * n_pockets + 256 * n_pockets : 0);
+    s.dbg_ang = r.add(debug ? (size_t)P * S_w * nR * n_pockets + 256 * n_pockets : 0);
+    s.coords = r.add(nA * 12);
+    const int64_t kc = std::max<int64_t>(n, 65536);
+    s.keys = r.add(kc * 8);
+    s.topk_out = r.add(8192 * 8);
+    s.sel = r.add(4096);
+    s.end = r.off;
+    return s;
+}
+
+size_t max_grid_bytes(const vs_ctx* c) {
+    size_t m = 0;
+    for (auto& p : c->pockets) m = std::max(m, (size_t)p.d.nx * p.d.ny * p.d.nz * 4);
+    return m;
+}
+
+const char* vcode_msg(int code) {
+    switch (code) {
+        case 1: return "atom count outside [1, 256]";
+        case 2: return "fragment count outside [0, 32]";
+        case 3: return "non-finite coordinate";
+        case 4: return "fragment axis atom index out of range";
+        case 5: return "fragment axis atoms are equal";
+        case 6: return "fragment moving range invalid (need 0 <= lo < hi <= atoms)";
+        case 7: return "fragment axis atom inside its moving range";
+        case 8: return "fragment axis atoms closer than 1e-3 A";
+        default: return "invalid record";
+    }
+}
+
+// Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1.
+vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps) {
+    c->classes.clear();
+    for (size_t i = 0; i < atom_b.size(); ++i) {
+        ClassInfo ci{};
+        ci.atom_bound = atom_b[i];
+        ci.AC = std::max(32, roundup32(atom_b[i]));
+        if (ci.AC > kMaxAtoms) return fail(c, VS_E_ARG, "atom class bound %d exceeds %d", atom_b[i], kMaxAtoms);
+        ci.b = 0;
+        for (int NW : {32, 16}) {
+            const int wl = std::min(c->P, NW);
+            const int LC = std::max(1, NW / wl);
+            const DockLayout L = dock_layout(ci.AC, NW, nz, ps, c->P, c->K, c->cfg.n_sweeps, LC);
+            int b = 0;
+            CK(dock_occupancy(ci.AC, NW, L.total, &b));
+            if (b >= 1) {
+                ci.NW = NW;
+                ci.LC = LC;
+                ci.b = b;
+                ci.smem = L.total;
+                CK(dock_kernel_attrs(ci.AC, NW, &ci.attr));
+                break;
+            }
+        }
+        if (ci.b == 0)
+            return fail(c, VS_E_NOFIT, "kernel class %d (A_c = %d) does not fit: occupancy is 0 (grid %dx%d planes)",
+                        (int)i, ci.AC, nz, ps);
+        ci.l = ci.b * c->sm_count * ci.LC;       // Eq. 1: l = b * SM * t/ws  (Q19)
+        ci.cap = ci.l * std::max(1, c->cfg.bucket_multiple);
+        c->classes.push_back(ci);
+    }
+    return VS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+vs_status vs_create(const vs_config* cfg, vs_ctx** out) {
+    if (!cfg || !out) return VS_E_ARG;
+    *out = nullptr;
+    vs_ctx* c = new vs_ctx();
+    c->cfg = *cfg;
+    auto bad = [&](const char* m) {
+        c->err = m;
+        return VS_E_ARG;
+    };
+    vs_status st = VS_OK;
+    if (c->cfg.n_sweeps < 1 || c->cfg.n_sweeps > kMaxSweeps) st = bad("n_sweeps must be in [1, 4]");
+    else if (c->cfg.n_atom_clusters < 1 || c->cfg.n_atom_clusters > kMaxAtomClasses) st = bad("n_atom_clusters must be in [1, 8]");
+    else if (c->cfg.n_rot_clusters < 1 || c->cfg.n_rot_clusters > kMaxRotClasses) st = bad("n_rot_clusters must be in [1, 33]");
+    else if (c->cfg.atom_upper_bound < 0 || c->cfg.atom_upper_bound > kMaxAtoms) st = bad("atom_upper_bound must be in [0, 256]");
+    else if (c->cfg.rot_upper_bound < 0 || c->cfg.rot_upper_bound > kMaxFrags) st = bad("rot_upper_bound must be in [0, 32]");
+    else if (c->cfg.world_size < 1 || c->cfg.rank < 0 || c->cfg.rank >= c->cfg.world_size) st = bad("bad rank / world_size");
+    if (st != VS_OK) {
+        delete c;
+        return st;
+    }
+    if (c->cfg.bucket_multiple < 1) c->cfg.bucket_multiple = 1;
+    if (c->cfg.n_streams < 1) c->cfg.n_streams = 1;
+    if (c->cfg.n_streams > 16) c->cfg.n_streams = 16;
+    cudaError_t e = cudaSetDevice(c->cfg.device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->cfg.device);
+    if (e == cudaSuccess) {
+        if (c->cfg.stream) c->main = (cudaStream_t)c->cfg.stream;
+        else {
+            e = cudaStreamCreateWithFlags(&c->main, cudaStreamNonBlocking);
+            c->own_main = true;
+        }
+    }
+    for (int i = 0; e == cudaSuccess && i < c->cfg.n_streams; ++i) {
+        cudaStream_t s;
+        cudaEvent_t ev;
+        e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) {
+            c->workers.push_back(s);
+            c->ev_worker.push_back(ev);
+        }
+    }
+    for (cudaEvent_t* ev : {&c->ev_prep0, &c->ev_prep1, &c->ev_dock1, &c->ev_t0, &c->ev_t1})
+        if (e == cudaSuccess) e = cudaEventCreate(ev);
+    if (e != cudaSuccess) {
+        c->err = cudaGetErrorString(e);
+        vs_destroy(c);
+        return VS_E_CUDA;
+    }
+    *out = c;
+    return VS_OK;
+}
+
+void vs_destroy(vs_ctx* c) {
+    if (!c) return;
+    if (c->main) cudaStreamSynchronize(c->main);
+    for (auto s : c->workers) cudaStreamDestroy(s);
+    for (auto e : c->ev_worker) cudaEventDestroy(e);
+    for (cudaEvent_t e : {c->ev_prep0, c->ev_prep1, c->ev_dock1, c->ev_t0, c->ev_t1})
+        if (e) cudaEventDestroy(e);
+    if (c->own_main && c->main) cudaStreamDestroy(c->main);
+    if (c->hpin) cudaFreeHost(c->hpin);
+    delete c;
+}
+
+const char* vs_last_error(const vs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+vs_status vs_set_pose_table(vs_ctx* c, int32_t P, const float* rot, const float* trans) {
+    if (!c) return VS_E_ARG;
+    if (P < 1 || P > kMaxPoses || !rot || !trans) return fail(c, VS_E_ARG, "pose table: need 1 <= P <= %d", kMaxPoses);
+    c->P = P;
+    c->pose_tab.assign((size_t)P * 12, 0.f);
+    for (int p = 0; p < P; ++p) {
+        for (int t = 0; t < 9; ++t) {
+            if (!std::isfinite(rot[9 * p + t])) return fail(c, VS_E_ARG, "pose %d: non-finite rotation", p);
+            c->pose_tab[12 * p + t] = rot[9 * p + t];
+        }
+        for (int t = 0; t < 3; ++t) {
+            if (!std::isfinite(trans[3 * p + t])) return fail(c, VS_E_ARG, "pose %d: non-finite translation", p);
+            c->pose_tab[12 * p + 9 + t] = trans[3 * p + t];
+        }
+    }
+    return VS_OK;
+}
+
+vs_status vs_set_angle_table(vs_ctx* c, int32_t K, const float* cos_sin) {
+    if (!c) return VS_E_ARG;
+    if (K < 1 || K > 32 || (K & (K - 1)) || !cos_sin)
+        return fail(c, VS_E_ARG, "angle table: K must be a power of two in [1, 32]");
+    if (cos_sin[0] != 1.0f || cos_sin[1] != 0.0f) return fail(c, VS_E_ARG, "angle table: entry 0 must be (1, 0)");
+    for (int t = 0; t < 2 * K; ++t)
+        if (!std::isfinite(cos_sin[t])) return fail(c, VS_E_ARG, "angle table: non-finite entry %d", t / 2);
+    c->K = K;
+    c->cs.assign(cos_sin, cos_sin + 2 * K);
+    return VS_OK;
+}
+
+vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, int32_t on_device, int32_t* pocket_id) {
+    if (!c || !d || !grid) return VS_E_ARG;
+    if (c->pockets.size() >= 16) return fail(c, VS_E_ARG, "at most 16 pockets");
+    if (d->nx < 2 || d->ny < 2 || d->nz < 2) return fail(c, VS_E_ARG, "pocket dims must be >= 2");
+    if ((int64_t)d->nx * d->ny * d->nz > (1 << 22)) return fail(c, VS_E_ARG, "pocket grid too large");
+    if (!(d->spacing > 0.f) || !std::isfinite(d->spacing)) return fail(c, VS_E_ARG, "pocket spacing must be > 0");
+    for (int a = 0; a < 3; ++a)
+        if (!std::isfinite(d->origin[a]) || !std::isfinite(d->center[a]))
+            return fail(c, VS_E_ARG, "pocket origin/center must be finite");
+    if (!std::isfinite(d->out_slope) || d->out_slope < 0.f) return fail(c, VS_E_ARG, "out_slope must be finite and >= 0");
+    PocketHost ph;
+    ph.d = *d;
+    const size_t cnt = (size_t)d->nx * d->ny * d->nz;
+    ph.grid.resize(cnt);
+    if (on_device) {
+        CK(cudaMemcpy(ph.grid.data(), grid, cnt * 4, cudaMemcpyDeviceToHost));
+    } else {
+        std::memcpy(ph.grid.data(), grid, cnt * 4);
+    }
+    for (size_t i = 0; i < cnt; ++i)
+        if (!std::isfinite(ph.grid[i])) return fail(c, VS_E_ARG, "pocket grid value %zu is not finite", i);
+    c->pockets.push_back(std::move(ph));
+    if (pocket_id) *pocket_id = (int32_t)c->pockets.size() - 1;
+    return VS_OK;
+}
+
+vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int32_t max_atoms,
+                            int32_t n_pockets, size_t* bytes) {
+    if (!c || !bytes) return VS_E_ARG;
+    if (c->P < 1 || c->K < 1) return fail(c, VS_E_STATE, "set the pose and angle tables first");
+    if (c->pockets.empty()) return fail(c, VS_E_STATE, "load a pocket first");
+    if (n_lig < 0 || n_atoms < 0 || n_frags < 0 || max_atoms < 1 || max_atoms > kMaxAtoms || n_pockets < 1)
+        return fail(c, VS_E_ARG, "bad workspace query");
+    int ac_max = roundup32(std::max<int>(max_atoms, c->cfg.atom_upper_bound));
+    ac_max = std::max(ac_max, 32);
+    // Q16 fallback boundary 32*n for the last class can exceed the observed maximum
+    ac_max = std::min(kMaxAtoms, std::max(ac_max, std::min(kMaxAtoms, roundup32(max_atoms))));
+    const Stage1 s1 = plan1(n_lig, n_atoms, n_frags, c->P, c->K, max_grid_bytes(c), n_pockets);
+    const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * (3 * ac_max + 32), c->P,
+                            c->cfg.n_sweeps, n_pockets, c->cfg.debug_poses != 0);
+    *bytes = s2.end + 4096;
+    return VS_OK;
+}
+
+vs_status vs_set_workspace(vs_ctx* c, void* ptr, size_t bytes) {
+    if (!c) return VS_E_ARG;
+    if (((uintptr_t)ptr & 255) != 0) return fail(c, VS_E_ARG, "workspace must be 256-byte aligned");
+    c->ws = (uint8_t*)ptr;
+    c->ws_bytes = bytes;
+    c->submitted = false;
+    return VS_OK;
+}
+
+vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets) {
+    if (!c || !batch) return VS_E_ARG;
+    c->submitted = false;
+    c->stats = vs_stats{};
+    if (c->P < 1 || c->K < 1) return fail(c, VS_E_STATE, "set the pose and angle tables first");
+    if (n_pockets < 1 || n_pockets > 16 || !pocket_ids) return fail(c, VS_E_ARG, "need 1..16 pockets");
+    for (int i = 0; i < n_pockets; ++i)
+        if (pocket_ids[i] < 0 || pocket_ids[i] >= (int)c->pockets.size())
+            return fail(c, VS_E_ARG, "unknown pocket id %d", pocket_ids[i]);
+    if (!c->ws) return fail(c, VS_E_WORKSPACE, "no workspace (vs_set_workspace)");
+    const int64_t n = batch->n;
+    if (n < 0 || n >= (1ll << 31)) return fail(c, VS_E_ARG, "batch size out of range");
+    CK(cudaSetDevice(c->cfg.device));
+    cudaStream_t ms = c->main;
+    const int S_w = c->cfg.n_sweeps;
+    int64_t launches = 0;
+
+    // ---- batch sizes
+    int64_t nA = 0, nR = 0;
+    if (n > 0) {
+        if (!batch->atom_off || !batch->xyz || !batch->frag_off) return fail(c, VS_E_ARG, "null batch array");
+        if (batch->on_device) {
+            CK(cudaMemcpy(&nA, batch->atom_off + n, 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&nR, batch->frag_off + n, 8, cudaMemcpyDeviceToHost));
+            int64_t z[2];
+            CK(cudaMemcpy(&z[0], batch->atom_off, 8, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(&z[1], batch->frag_off, 8, cudaMemcpyDeviceToHost));
+            if (z[0] != 0 || z[1] != 0) return fail(c, VS_E_PARSE, "atom_off[0] and frag_off[0] must be 0");
+        } else {
+            if (batch->atom_off[0] != 0 || batch->frag_off[0] != 0)
+                return fail(c, VS_E_PARSE, "atom_off[0] and frag_off[0] must be 0");
+            nA = batch->atom_off[n];
+            nR = batch->frag_off[n];
+            for (int64_t i = 0; i < n; ++i)   // monotone offsets (cheap, O(n))
+                if (batch->atom_off[i + 1] < batch->atom_off[i] || batch->frag_off[i + 1] < batch->frag_off[i])
+                    return fail(c, VS_E_PARSE, "ligand %lld: decreasing CSR offsets", (long long)i);
+        }
+        if (nA < 0 || nR < 0) return fail(c, VS_E_PARSE, "negative CSR totals");
+        if (nR > 0 && !batch->frags) return fail(c, VS_E_ARG, "null frags");
+        if ((int64_t)S_w * nR >= (1ll << 31)) return fail(c, VS_E_ARG, "too many fragments in one batch");
+    }
+    c->n = n;
+    c->nA = nA;
+    c->nR = nR;
+    c->job_pockets.assign(pocket_ids, pocket_ids + n_pockets);
+
+    // ---- stage-1 workspace
+    size_t gmax = 0;
+    for (int i = 0; i < n_pockets; ++i) {
+        auto& d = c->pockets[pocket_ids[i]].d;
+        gmax = std::max(gmax, (size_t)d.nx * d.ny * d.nz * 4);
+    }
+    const Stage1 s1 = plan1(n, nA, nR, c->P, c->K, gmax, n_pockets);
+    if (s1.end > c->ws_bytes) return fail(c, VS_E_WORKSPACE, "workspace too small (stage 1 needs %zu bytes)", s1.end);
+    uint8_t* W = c->ws;
+    c->d_featA = (int*)(W + s1.featA);
+    c->d_featR = (int*)(W + s1.featR);
+    c->d_featM = (int*)(W + s1.featM);
+    c->d_cell = (int*)(W + s1.cell);
+    c->d_status = (unsigned long long*)(W + s1.status);
+    c->d_maxAR = (int*)(W + s1.maxAR);
+    c->d_hist = (int*)(W + s1.hist);
+    c->d_cell_count = (int*)(W + s1.cell_count);
+    c->d_perm = (uint32_t*)(W + s1.perm);
+    c->d_bstart = (int64_t*)(W + s1.bstart);
+    c->d_bsize = (int*)(W + s1.bsize);
+    c->d_weights = (unsigned long long*)(W + s1.weights);
+    c->d_own_start = (int64_t*)(W + s1.own_start);
+    c->d_own_prefix = (int*)(W + s1.own_prefix);
+    c->d_own_ac = (int*)(W + s1.own_ac);
+    c->d_own_rec_off = (int64_t*)(W + s1.own_rec_off);
+    c->d_pose = (float*)(W + s1.pose);
+    c->d_cs = (float*)(W + s1.cs);
+    c->d_grid.assign(n_pockets, nullptr);
+    for (int i = 0; i < n_pockets; ++i) c->d_grid[i] = (float*)(W + s1.grids + (size_t)i * gmax);
+    if (batch->on_device) {
+        c->d_atom_off = (int64_t*)batch->atom_off;
+        c->d_frag_off = (int64_t*)batch->frag_off;
+        c->d_xyz = (float*)batch->xyz;
+        c->d_frags = (int32_t*)batch->frags;
+    } else {
+        c->d_atom_off = (int64_t*)(W + s1.atom_off);
+        c->d_frag_off = (int64_t*)(W + s1.frag_off);
+        c->d_xyz = (float*)(W + s1.xyz);
+        c->d_frags = (int32_t*)(W + s1.frags);
+    }
+
+    CK(cudaEventRecord(c->ev_prep0, ms));
+    // tables + grids (small H2D)
+    CK(cudaMemcpyAsync(c->d_pose, c->pose_tab.data(), c->pose_tab.size() * 4, cudaMemcpyHostToDevice, ms));
+    CK(cudaMemcpyAsync(c->d_cs, c->cs.data(), c->cs.size() * 4, cudaMemcpyHostToDevice, ms));
+    c->pkdev.clear();
+    for (int i = 0; i < n_pockets; ++i) {
+        auto& ph = c->pockets[pocket_ids[i]];
+        CK(cudaMemcpyAsync(c->d_grid[i], ph.grid.data(), ph.grid.size() * 4, cudaMemcpyHostToDevice, ms));
+        c->pkdev.push_back(make_pocket_dev(ph.d, c->d_grid[i]));
+    }
+    if (n == 0) {
+        c->buckets.clear();
+        c->owned.clear();
+        c->total_slots = 0;
+        c->submitted = true;
+        return VS_OK;
+    }
+    if (!batch->on_device) {
+        CK(cudaMemcpyAsync(c->d_atom_off, batch->atom_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
+        CK(cudaMemcpyAsync(c->d_frag_off, batch->frag_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
+        if (nA) CK(cudaMemcpyAsync(c->d_xyz, batch->xyz, nA * 12, cudaMemcpyHostToDevice, ms));
+        if (nR) CK(cudaMemcpyAsync(c->d_frags, batch->frags, nR * 16, cudaMemcpyHostToDevice, ms));
+    }
+
+    // ---- a1 validate + features
+    CK(cudaMemsetAsync(c->d_status, 0xFF, 16, ms));
+    CK(cudaMemsetAsync(c->d_maxAR, 0, 8, ms));
+    CK(launch_validate(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frags, n, c->d_featA, c->d_featR, c->d_featM,
+                       c->d_status, c->d_maxAR, ms));
+    ++launches;
+    vs_status st = ensure_pinned(c, (size_t)(s1.max_buckets + 16) * 32 + kMaxCells * 8 + 64);
+    if (st) return st;
+    uint8_t* H = (uint8_t*)c->hpin;
+    CK(cudaMemcpyAsync(H, c->d_status, 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaMemcpyAsync(H + 8, c->d_maxAR, 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaStreamSynchronize(ms));
+    unsigned long long vstat;
+    int maxAR[2];
+    std::memcpy(&vstat, H, 8);
+    std::memcpy(maxAR, H + 8, 8);
+    if (vstat != ~0ull) {
+        const long long li = (long long)(vstat >> 8);
+        return fail(c, VS_E_PARSE, "ligand %lld: %s", li, vcode_msg((int)(vstat & 255)));
+    }
+
+    // ---- a2/a3 boundaries, classes (Eq. 1), classify, scan
+    const int ubA = c->cfg.atom_upper_bound > 0 ? c->cfg.atom_upper_bound : maxAR[0];
+    const int ubR = c->cfg.rot_upper_bound > 0 ? c->cfg.rot_upper_bound : maxAR[1];
+    c->atom_b = atom_bounds(c->cfg.n_atom_clusters, ubA);
+    c->rot_b = rot_bounds(c->cfg.n_rot_clusters, ubR);
+    if ((int)c->rot_b.size() > kMaxRotClasses) return fail(c, VS_E_ARG, "too many rotamer classes");
+    int nz_max = 0, ps_max = 0;
+    for (auto& pk : c->pkdev) {
+        if ((int64_t)pk.nz * pk.ps > (int64_t)nz_max * ps_max) {
+            nz_max = pk.nz;
+            ps_max = pk.ps;
+        }
+    }
+    st = plan_classes(c, c->atom_b, nz_max, ps_max);
+    if (st) return st;
+    const int nRc = (int)c->rot_b.size();
+    const int n_cells = (int)c->atom_b.size() * nRc;
+    CK(launch_classify_hist(c->d_featA, c->d_featR, n, c->atom_b.data(), (int)c->atom_b.size(), c->rot_b.data(), nRc,
+                            c->d_cell, c->d_hist, s1.n_blocks, c->d_status + 1, ms));
+    CK(launch_scan_hist(c->d_hist, n_cells, s1.n_blocks, c->d_cell_count, ms));
+    launches += 2;
+    CK(cudaMemcpyAsync(H, c->d_status + 1, 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaMemcpyAsync(H + 8, c->d_cell_count, n_cells * 4, cudaMemcpyDeviceToHost, ms));
+    CK(cudaStreamSynchronize(ms));
+    unsigned long long ovf;
+    std::memcpy(&ovf, H, 8);
+    if (ovf != ~0ull) {
+        const long long li = (long long)(ovf >> 8);
+        if ((ovf & 255) == 1)
+            return fail(c, VS_E_OVERFLOW_ATOMS, "ligand %lld: atoms above the last atom boundary %d (axis: atoms)", li,
+                        c->atom_b.back());
+        return fail(c, VS_E_OVERFLOW_ROTAMERS, "ligand %lld: rotamers above the last rotamer boundary %d (axis: rotamers)",
+                    li, c->rot_b.back());
+    }
+    std::vector<int> cc(n_cells);
+    std::memcpy(cc.data(), H + 8, n_cells * 4);
+
+    // bucket table: cell-major, chunks of the class capacity (Q18)
+    c->buckets.clear();
+    int64_t run = 0;
+    for (int cell = 0; cell < n_cells; ++cell) {
+        const int ai = cell / nRc, ri = cell % nRc;
+        const ClassInfo& ci = c->classes[ai];
+        for (int64_t s = 0; s < cc[cell]; s += ci.cap) {
+            vs_bucket b{};
+            b.cell = cell;
+            b.atom_class = ai;
+            b.rot_class = ri;
+            b.atom_bound = ci.atom_bound;
+            b.kernel_atoms = ci.AC;
+            b.capacity = ci.cap;
+            b.size = (int)std::min<int64_t>(ci.cap, cc[cell] - s);
+            b.start = run + s;
+            b.owner = -1;
+            b.launch_order = -1;
+            c->buckets.push_back(b);
+        }
+        run += cc[cell];
+    }
+    const int nb = (int)c->buckets.size();
+    {
+        int64_t* hs = (int64_t*)(H);
+        int* hz = (int*)(H + (size_t)nb * 8);
+        for (int b = 0; b < nb; ++b) {
+            hs[b] = c->buckets[b].start;
+            hz[b] = c->buckets[b].size;
+        }
+        CK(cudaMemcpyAsync(c->d_bstart, hs, (size_t)nb * 8, cudaMemcpyHostToDevice, ms));
+        CK(cudaMemcpyAsync(c->d_bsize, hz, (size_t)nb * 4, cudaMemcpyHostToDevice, ms));
+    }
+    CK(launch_scatter(c->d_cell, n, c->d_hist, n_cells, s1.n_blocks, c->d_perm, ms));
+    CK(launch_bucket_weights(c->d_perm, c->d_featA, c->d_featM, c->d_bstart, c->d_bsize, nb, c->P, c->K, S_w,
+                             c->d_weights, ms));
+    launches += 2;
+    CK(cudaStreamSynchronize(ms));  // pinned staging reused below
+    CK(cudaMemcpyAsync(H, c->d_weights, (size_t)nb * 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaStreamSynchronize(ms));
+    for (int b = 0; b < nb; ++b) std::memcpy(&c->buckets[b].weight, H + (size_t)b * 8, 8);
+
+    // ---- a4 LPT shard: weight descending (ties: id), least-loaded rank (ties: lowest rank)
+    std::vector<int> order(nb);
+    for (int b = 0; b < nb; ++b) order[b] = b;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        if (c->buckets[x].weight != c->buckets[y].weight) return c->buckets[x].weight > c->buckets[y].weight;
+        return x < y;
+    });
+    const int Wn = c->cfg.world_size;
+    std::vector<unsigned long long> load(Wn, 0);
+    std::vector<int> nlaunch(Wn, 0);
+    c->owned.clear();
+    for (int b : order) {
+        int r = 0;
+        for (int q = 1; q < Wn; ++q)
+            if (load[q] < load[r]) r = q;
+        load[r] += c->buckets[b].weight;
+        c->buckets[b].owner = r;
+        c->buckets[b].launch_order = nlaunch[r]++;
+        if (r == c->cfg.rank) c->owned.push_back(b);
+    }
+
+    // ---- stage-2 workspace and a5 pack
+    const int no = (int)c->owned.size();
+    c->owned_prefix.assign(no + 1, 0);
+    c->owned_rec_off.assign(no, 0);
+    int64_t rec_floats = 0;
+    double evals = 0;
+    for (int i = 0; i < no; ++i) {
+        const vs_bucket& b = c->buckets[c->owned[i]];
+        c->owned_prefix[i + 1] = c->owned_prefix[i] + b.size;
+        c->owned_rec_off[i] = rec_floats;
+        rec_floats += (int64_t)b.size * (3 * b.kernel_atoms + 32);
+        evals += (double)b.weight;
+    }
+    c->total_slots = c->owned_prefix[no];
+    const Stage2 s2 = plan2(s1.end, n, nA, nR, rec_floats, c->P, S_w, n_pockets, c->cfg.debug_poses != 0);
+    if (s2.end > c->ws_bytes) return fail(c, VS_E_WORKSPACE, "workspace too small (needs %zu bytes)", s2.end);
+    c->d_rec = (float*)(W + s2.rec);
+    c->d_meta = (int4*)(W + s2.meta);
+    c->d_score.assign(n_pockets, nullptr);
+    c->d_pose_best.assign(n_pockets, nullptr);
+    c->d_ang.assign(n_pockets, nullptr);
+    c->d_dbg_score.assign(n_pockets, nullptr);
+    c->d_dbg_ang.assign(n_pockets, nullptr);
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    for (int i = 0; i < n_pockets; ++i) {
+        c->d_score[i] = (float*)(W + s2.score + i * al(n * 4));
+        c->d_pose_best[i] = (int*)(W + s2.pose_best + i * al(n * 4));
+        c->d_ang[i] = W + s2.ang + i * al((size_t)S_w * nR);
+        if (c->cfg.debug_poses) {
+            c->d_dbg_score[i] = (float*)(W + s2.dbg_score + i * al((size_t)n * c->P * 4));
+            c->d_dbg_ang[i] = W + s2.dbg_ang + i * al((size_t)c->P * S_w * nR);
+        }
+    }
+    c->d_coords = (float*)(W + s2.coords);
+    c->d_keys = (unsigned long long*)(W + s2.keys);
+    c->keys_cap = std::max<int64_t>(n, 65536);
+    c->d_topk_out = (unsigned long long*)(W + s2.topk_out);
+    c->d_sel = W + s2.sel;
+    {
+        int64_t* h_start = (int64_t*)H;
+        int* h_prefix = (int*)(H + (size_t)no * 8);
+        int* h_ac = (int*)(H + (size_t)no * 12 + 4);
+        int64_t* h_roff = (int64_t*)(H + (((size_t)no * 16 + 4 + 7) & ~(size_t)7));
+        for (int i = 0; i < no; ++i) {
+            h_start[i] = c->buckets[c->owned[i]].start;
+            h_ac[i] = c->buckets[c->owned[i]].kernel_atoms;
+            h_roff[i] = c->owned_rec_off[i];
+        }
+        for (int i = 0; i <= no; ++i) h_prefix[i] = c->owned_prefix[i];
+        if (no) {
+            CK(cudaMemcpyAsync(c->d_own_start, h_start, (size_t)no * 8, cudaMemcpyHostToDevice, ms));
+            CK(cudaMemcpyAsync(c->d_own_prefix, h_prefix, (size_t)(no + 1) * 4, cudaMemcpyHostToDevice, ms));
+            CK(cudaMemcpyAsync(c->d_own_ac, h_ac, (size_t)no * 4, cudaMemcpyHostToDevice, ms));
+            CK(cudaMemcpyAsync(c->d_own_rec_off, h_roff, (size_t)no * 8, cudaMemcpyHostToDevice, ms));
+        }
+    }
+    CK(launch_pack(c->d_perm, c->d_own_start, c->d_own_prefix, c->d_own_ac, c->d_own_rec_off, no, c->total_slots,
+                   c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frags, S_w, c->d_rec, c->d_meta, ms));
+    ++launches;
+    for (int i = 0; i < n_pockets; ++i) {
+        CK(launch_fill_results(c->d_score[i], c->d_pose_best[i], n, c->d_ang[i], (int64_t)S_w * nR, ms));
+        ++launches;
+    }
+    CK(cudaEventRecord(c->ev_prep1, ms));
+
+    // ---- a6-a9 dock: one launch per (owned bucket, pocket), LPT order, round-robin over streams
+    const int NS = (int)c->workers.size();
+    for (int s = 0; s < NS; ++s) CK(cudaStreamWaitEvent(c->workers[s], c->ev_prep1, 0));
+    int64_t dock_launches = 0;
+    for (int i = 0; i < no; ++i) {
+        const vs_bucket& b = c->buckets[c->owned[i]];
+        const ClassInfo& ci = c->classes[b.atom_class];
+        for (int q = 0; q < n_pockets; ++q) {
+            DockArgs a{};
+            a.rec = c->d_rec + c->owned_rec_off[i];
+            a.meta = c->d_meta + c->owned_prefix[i];
+            a.n = b.size;
+            a.rec_floats = 3 * b.kernel_atoms + 32;
+            a.P = c->P;
+            a.K = c->K;
+            a.S_w = S_w;
+            a.ligs_per_cta = ci.LC;
+            a.pose_tab = c->d_pose;
+            a.cs = c->d_cs;
+            a.pk = c->pkdev[q];
+            a.best_score = c->d_score[q];
+            a.best_pose = c->d_pose_best[q];
+            a.angles = c->d_ang[q];
+            a.dbg_score = c->d_dbg_score[q];
+            a.dbg_angles = c->d_dbg_ang[q];
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, a.pk.nz, a.pk.ps, c->P, c->K, S_w, ci.LC);
+            const int rounds = (b.size + ci.LC - 1) / ci.LC;
+            const int grid = std::min(rounds, ci.b * c->sm_count);
+            cudaStream_t s = c->workers[(dock_launches) % NS];
+            CK(launch_dock(b.kernel_atoms, ci.NW, a, grid, L.total, s));
+            ++dock_launches;
+        }
+    }
+    for (int s = 0; s < NS; ++s) {
+        CK(cudaEventRecord(c->ev_worker[s], c->workers[s]));
+        CK(cudaStreamWaitEvent(ms, c->ev_worker[s], 0));
+    }
+    CK(cudaEventRecord(c->ev_dock1, ms));
+    launches += dock_launches;
+
+    c->stats.n_ligands = n;
+    c->stats.n_owned = c->total_slots;
+    c->stats.n_buckets = nb;
+    c->stats.n_owned_buckets = no;
+    c->stats.kernel_launches = launches;
+    c->stats.dock_launches = dock_launches;
+    c->stats.evals_alg = evals * n_pockets;
+    c->submitted = true;
+    return VS_OK;
+}
+
+vs_status vs_wait(vs_ctx* c) {
+    if (!c) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    CK(cudaStreamSynchronize(c->main));
+    if (c->n > 0) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev_prep0, c->ev_prep1));
+        c->stats.prep_ms = ms;
+        CK(cudaEventElapsedTime(&ms, c->ev_prep1, c->ev_dock1));
+        c->stats.dock_ms = ms;
+    }
+    return VS_OK;
+}
+
+vs_status vs_get_results(vs_ctx* c, int32_t slot, float* best_score, int32_t* best_pose, uint8_t* angle_idx,
+                         int32_t on_device) {
+    if (!c) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (c->n == 0) return VS_OK;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (best_score) CK(cudaMemcpyAsync(best_score, c->d_score[slot], c->n * 4, kind, c->main));
+    if (best_pose) CK(cudaMemcpyAsync(best_pose, c->d_pose_best[slot], c->n * 4, kind, c->main));
+    if (angle_idx && c->nR) CK(cudaMemcpyAsync(angle_idx, c->d_ang[slot], (size_t)c->cfg.n_sweeps * c->nR, kind, c->main));
+    CK(cudaStreamSynchronize(c->main));
+    return VS_OK;
+}
+
+vs_status vs_get_pose_debug(vs_ctx* c, int32_t slot, float* pose_score, uint8_t* pose_angles) {
+    if (!c) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (!c->cfg.debug_poses) return fail(c, VS_E_STATE, "debug_poses is off");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (c->n == 0) return VS_OK;
+    if (pose_score) CK(cudaMemcpyAsync(pose_score, c->d_dbg_score[slot], (size_t)c->n * c->P * 4, cudaMemcpyDeviceToHost, c->main));
+    if (pose_angles && c->nR)
+        CK(cudaMemcpyAsync(pose_angles, c->d_dbg_ang[slot], (size_t)c->P * c->cfg.n_sweeps * c->nR, cudaMemcpyDeviceToHost, c->main));
+    CK(cudaStreamSynchronize(c->main));
+    return VS_OK;
+}
+
+vs_status vs_get_coords(vs_ctx* c, int32_t slot, float* xyz_out, int32_t on_device) {
+    if (!c || !xyz_out) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (c->n == 0 || c->nA == 0) return VS_OK;
+    CK(cudaMemsetAsync(c->d_coords, 0xFF, c->nA * 12, c->main));   // NaN for ligands of other ranks
+    for (size_t i = 0; i < c->owned.size(); ++i) {
+        const vs_bucket& b = c->buckets[c->owned[i]];
+        DockArgs a{};
+        a.rec = c->d_rec + c->owned_rec_off[i];
+        a.meta = c->d_meta + c->owned_prefix[i];
+        a.n = b.size;
+        a.rec_floats = 3 * b.kernel_atoms + 32;
+        a.P = c->P;
+        a.K = c->K;
+        a.S_w = c->cfg.n_sweeps;
+        a.pose_tab = c->d_pose;
+        a.cs = c->d_cs;
+        a.pk = c->pkdev[slot];
+        a.best_pose = c->d_pose_best[slot];
+        a.angles = c->d_ang[slot];
+        CK(launch_finalize(b.kernel_atoms, a, c->d_atom_off, c->d_coords, c->main));
+        c->stats.kernel_launches++;
+    }
+    CK(cudaMemcpyAsync(xyz_out, c->d_coords, c->nA * 12, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       c->main));
+    CK(cudaStreamSynchronize(c->main));
+    return VS_OK;
+}
+
+vs_status vs_local_topk(vs_ctx* c, int32_t slot, int32_t k, uint64_t* keys_dev, int32_t* n_valid) {
+    if (!c || !keys_dev) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (k < 1 || k > 8192) return fail(c, VS_E_ARG, "k must be in [1, 8192]");
+    CK(cudaEventRecord(c->ev_t0, c->main));
+    int L = 0;
+    if (c->n > 0) {
+        CK(launch_make_keys(c->d_meta, c->total_slots, c->d_score[slot], c->d_keys, c->main));
+        ++L;
+    }
+    int l2 = 0;
+    CK(topk_select_sort(c->d_keys, c->total_slots, k, (unsigned long long*)keys_dev, c->d_sel, c->main, &l2));
+    CK(cudaEventRecord(c->ev_t1, c->main));
+    CK(cudaStreamSynchronize(c->main));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1));
+    c->stats.topk_ms = ms;
+    c->stats.kernel_launches += L + l2;
+    if (n_valid) *n_valid = std::min<int64_t>(k, c->total_slots);
+    return VS_OK;
+}
+
+vs_status vs_merge_topk(vs_ctx* c, const uint64_t* keys_dev, int64_t n_keys, int32_t k, int64_t* index_out,
+                        float* score_out, int32_t* n_out) {
+    if (!c || (!keys_dev && n_keys > 0)) return VS_E_ARG;
+    if (k < 1 || k > 8192) return fail(c, VS_E_ARG, "k must be in [1, 8192]");
+    if (!c->ws || !c->d_topk_out) return fail(c, VS_E_STATE, "submit a batch first (workspace scratch)");
+    int l2 = 0;
+    CK(topk_select_sort((const unsigned long long*)keys_dev, n_keys, k, c->d_topk_out, c->d_sel, c->main, &l2));
+    c->stats.kernel_launches += l2;
+    std::vector<unsigned long long> h(k);
+    CK(cudaMemcpyAsync(h.data(), c->d_topk_out, (size_t)k * 8, cudaMemcpyDeviceToHost, c->main));
+    CK(cudaStreamSynchronize(c->main));
+    int m = 0;
+    for (int i = 0; i < k; ++i) {
+        if (h[i] == ~0ull) break;
+        const uint32_t ord = (uint32_t)(h[i] >> 32);
+        const uint32_t bits = (ord & 0x80000000u) ? (ord & 0x7fffffffu) : ~ord;
+        float s;
+        std::memcpy(&s, &bits, 4);
+        if (index_out) index_out[i] = (int64_t)(h[i] & 0xffffffffull);
+        if (score_out) score_out[i] = s;
+        ++m;
+    }
+    if (n_out) *n_out = m;
+    return VS_OK;
+}
+
+vs_status vs_get_manifest(vs_ctx* c, int32_t max_buckets, vs_bucket* buckets, int32_t* n_buckets, uint32_t* perm) {
+    if (!c || !n_buckets) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    *n_buckets = (int32_t)c->buckets.size();
+    if (buckets) {
+        if (max_buckets < (int)c->buckets.size()) return fail(c, VS_E_ARG, "max_buckets too small");
+        std::copy(c->buckets.begin(), c->buckets.end(), buckets);
+    }
+    if (perm && c->n > 0) {
+        CK(cudaMemcpyAsync(perm, c->d_perm, c->n * 4, cudaMemcpyDeviceToHost, c->main));
+        CK(cudaStreamSynchronize(c->main));
+    }
+    return VS_OK;
+}
+
+vs_status vs_query_classes(vs_ctx* c, int32_t max_classes, vs_class_info* out, int32_t* n_classes) {
+    if (!c || !n_classes) return VS_E_ARG;
+    if (c->classes.empty()) return fail(c, VS_E_STATE, "no class table yet (submit a batch)");
+    *n_classes = (int32_t)c->classes.size();
+    if (out) {
+        if (max_classes < (int)c->classes.size()) return fail(c, VS_E_ARG, "max_classes too small");
+        for (size_t i = 0; i < c->classes.size(); ++i) {
+            const ClassInfo& ci = c->classes[i];
+            vs_class_info& o = out[i];
+            o.atom_bound = ci.atom_bound;
+            o.kernel_atoms = ci.AC;
+            o.warps_per_cta = ci.NW;
+            o.threads_per_cta = ci.NW * 32;
+            o.regs_per_thread = ci.attr.numRegs;
+            o.static_smem = (int32_t)ci.attr.sharedSizeBytes;
+            o.dyn_smem = (int32_t)ci.smem;
+            o.blocks_per_sm = ci.b;
+            o.sm_count = c->sm_count;
+            o.ligands_per_cta = ci.LC;
+            o.l = ci.l;
+            o.capacity = ci.cap;
+        }
+    }
+    return VS_OK;
+}
+
+vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* xyz, float* g_out) {
+    if (!c || (n > 0 && (!xyz || !g_out))) return VS_E_ARG;
+    if (pocket_id < 0 || pocket_id >= (int)c->pockets.size()) return fail(c, VS_E_ARG, "unknown pocket id");
+    if (n == 0) return VS_OK;
+    CK(cudaSetDevice(c->cfg.device));
+    // test hook: temporary device buffers (not on the product path)
+    const PocketHost& ph = c->pockets[pocket_id];
+    float *dg = nullptr, *dx = nullptr, *dout = nullptr;
+    const size_t gb = ph.grid.size() * 4;
+    CK(cudaMalloc(&dg, gb));
+    CK(cudaMalloc(&dx, (size_t)n * 12));
+    CK(cudaMalloc(&dout, (size_t)n * 4));
+    CK(cudaMemcpy(dg, ph.grid.data(), gb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dx, xyz, (size_t)n * 12, cudaMemcpyHostToDevice));
+    PocketDev pk = make_pocket_dev(ph.d, dg);
+    const size_t smem = align16((size_t)pk.nz * pk.ps * 4);
+    CK(launch_score_points(pk, dx, n, dout, smem, c->main));
+    CK(cudaMemcpyAsync(g_out, dout, (size_t)n * 4, cudaMemcpyDeviceToHost, c->main));
+    CK(cudaStreamSynchronize(c->main));
+    cudaFree(dg);
+    cudaFree(dx);
+    cudaFree(dout);
+    return VS_OK;
+}
+
+vs_status vs_get_stats(vs_ctx* c, vs_stats* out) {
+    if (!c || !out) return VS_E_ARG;
+    *out = c->stats;
+    return VS_OK;
+}
+
+}  // extern "C"

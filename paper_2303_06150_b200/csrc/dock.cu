@@ -1,0 +1,453 @@
+// dock.cu -- the docking kernel (a6-a9): rigid roto-translation from P initial
+// poses, greedy rotatable-bond sweep over K discrete angle steps, trilinear
+// pocket-grid score, best-pose reduction.  fp32 on CUDA cores (not a dense
+// contraction, BJ: "no tensor cores").
+//
+// B200 design:
+//  * one CTA per SM (persistent over the bucket's ligands, grid <= b * 148);
+//    the pocket grid (32^3 fp32 = 128 KB) lives in SHARED memory for the whole
+//    launch -- the 8 corner gathers of every evaluation hit smem, not L1/L2;
+//  * a CTA docks `LC` ligands at a time; its NW warps split the LC x P
+//    (ligand, pose) items, so one ligand's 64 poses run on 32 warps at once and
+//    every warp of the CTA runs the same control flow (same A, R, M_r);
+//  * sweep lane map: lane = j * K + k -- (moving atom j, angle k).  Each lane
+//    holds its angle's Rodrigues matrix in registers, lanes of equal k reduce
+//    their partial sums with xor shuffles K..16, the argmin over k takes log2 K
+//    more shuffle rounds (ties -> lowest k, Q11), and the chosen rotation is
+//    applied with atoms across lanes;
+//  * template<int AC, int NW> per atom class = the paper's "non-type template
+//    parameter for the kernel maximum number of atoms": AC sizes
+//    the per-warp pose buffers in shared memory and therefore the occupancy.
+//
+// All arithmetic that decides an angle or is replayed (placement, Rodrigues,
+// rotation, interpolation) uses explicit _rn intrinsics, so the trajectory is
+// reproducible bit for bit by the finalize kernel.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace vsd {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+struct Rot {
+    float m00, m01, m02, m10, m11, m12, m20, m21, m22;
+};
+
+// M = c I + s [u]x + (1 - c) u u^T (a7; Q3, Q6)
+__device__ __forceinline__ Rot rodrigues(float ux, float uy, float uz, float c, float s) {
+    const float omc = __fsub_rn(1.f, c);
+    const float a = __fmul_rn(omc, ux), b = __fmul_rn(omc, uy), d = __fmul_rn(omc, uz);
+    const float sx = __fmul_rn(s, ux), sy = __fmul_rn(s, uy), sz = __fmul_rn(s, uz);
+    Rot M;
+    M.m00 = __fmaf_rn(a, ux, c);
+    M.m01 = __fmaf_rn(a, uy, -sz);
+    M.m02 = __fmaf_rn(a, uz, sy);
+    M.m10 = __fmaf_rn(b, ux, sz);
+    M.m11 = __fmaf_rn(b, uy, c);
+    M.m12 = __fmaf_rn(b, uz, -sx);
+    M.m20 = __fmaf_rn(d, ux, -sy);
+    M.m21 = __fmaf_rn(d, uy, sx);
+    M.m22 = __fmaf_rn(d, uz, c);
+    return M;
+}
+
+// y' = M (y - q) + q
+__device__ __forceinline__ float3 rot_about(const Rot& M, float qx, float qy, float qz, float vx, float vy, float vz) {
+    const float dx = __fsub_rn(vx, qx), dy = __fsub_rn(vy, qy), dz = __fsub_rn(vz, qz);
+    float3 r;
+    r.x = __fmaf_rn(M.m00, dx, __fmaf_rn(M.m01, dy, __fmaf_rn(M.m02, dz, qx)));
+    r.y = __fmaf_rn(M.m10, dx, __fmaf_rn(M.m11, dy, __fmaf_rn(M.m12, dz, qy)));
+    r.z = __fmaf_rn(M.m20, dx, __fmaf_rn(M.m21, dy, __fmaf_rn(M.m22, dz, qz)));
+    return r;
+}
+
+// unit axis a -> b
+__device__ __forceinline__ void axis_of(const float4& ya, const float4& yb, float& ux, float& uy, float& uz) {
+    const float dx = __fsub_rn(yb.x, ya.x), dy = __fsub_rn(yb.y, ya.y), dz = __fsub_rn(yb.z, ya.z);
+    const float n2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    const float inv = rsqrtf(n2);
+    ux = __fmul_rn(dx, inv);
+    uy = __fmul_rn(dy, inv);
+    uz = __fmul_rn(dz, inv);
+}
+
+__device__ __forceinline__ float lerp(float a, float b, float t) { return __fmaf_rn(t, b, __fmaf_rn(-t, a, a)); }
+
+// a8: g(u), u in grid units (Q9, Q10).  G is the shared-memory copy with row
+// stride rs and plane stride ps.
+__device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
+    const float cx = fminf(fmaxf(ux, 0.f), pk.top_x);
+    const float cy = fminf(fmaxf(uy, 0.f), pk.top_y);
+    const float cz = fminf(fmaxf(uz, 0.f), pk.top_z);
+    const float e = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(ux, cx)), fabsf(__fsub_rn(uy, cy))), fabsf(__fsub_rn(uz, cz)));
+    const float fx = fminf(floorf(cx), pk.top2_x);
+    const float fy = fminf(floorf(cy), pk.top2_y);
+    const float fz = fminf(floorf(cz), pk.top2_z);
+    const float tx = __fsub_rn(cx, fx), ty = __fsub_rn(cy, fy), tz = __fsub_rn(cz, fz);
+    const int idx = __float2int_rn(__fmaf_rn(fz, (float)pk.ps, __fmaf_rn(fy, (float)pk.rs, fx)));
+    const float* p = G + idx;
+    const float c000 = p[0], c100 = p[1];
+    const float c010 = p[pk.rs], c110 = p[pk.rs + 1];
+    const float c001 = p[pk.ps], c101 = p[pk.ps + 1];
+    const float c011 = p[pk.ps + pk.rs], c111 = p[pk.ps + pk.rs + 1];
+    const float l00 = lerp(c000, c100, tx), l10 = lerp(c010, c110, tx);
+    const float l01 = lerp(c001, c101, tx), l11 = lerp(c011, c111, tx);
+    const float l0 = lerp(l00, l10, ty), l1 = lerp(l01, l11, ty);
+    return __fmaf_rn(pk.kh, e, lerp(l0, l1, tz));
+}
+
+// Pose p in grid units: R' = R / h, t' = (c + tau - o) / h, u = R' x + t'.
+__device__ __forceinline__ void scaled_pose(const float* raw, const PocketDev& pk, float* out) {
+#pragma unroll
+    for (int t = 0; t < 9; ++t) out[t] = __fmul_rn(raw[t], pk.inv_h);
+    out[9] =__fadd_rn(pk.tx, __fmul_rn(raw[9], pk.inv_h));
+    out[10] = __fadd_rn(pk.ty, __fmul_rn(raw[10], pk.inv_h));
+    out[11] = __fadd_rn(pk.tz, __fmul_rn(raw[11], pk.inv_h));
+}
+
+__device__ __forceinline__ float4 place_atom(const float* T, float x, float y, float z) {
+    return make_float4(__fmaf_rn(T[0], x, __fmaf_rn(T[1], y, __fmaf_rn(T[2], z, T[9]))),
+                       __fmaf_rn(T[3], x, __fmaf_rn(T[4], y, __fmaf_rn(T[5], z, T[10]))),
+                       __fmaf_rn(T[6], x, __fmaf_rn(T[7], y, __fmaf_rn(T[8], z, T[11]))), 0.f);
+}
+
+// Stage the pocket grid into shared memory with padded strides.
+__device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int row = w; row < pk.ny * pk.nz; row += nw) {
+        const int z = row / pk.ny, y = row - z * pk.ny;
+        const float* src = pk.grid + (size_t)row * pk.nx;
+        float* dst = sG + z * pk.ps + y * pk.rs;
+        for (int x = lane; x < pk.nx; x += 32) dst[x] = src[x];
+    }
+}
+
+// One (ligand, pose) item on one warp: a6 placement, a7 sweep, a9 pose score.
+template <int AC>
+__device__ __forceinline__ void dock_pose(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
+                                          float4* __restrict__ buf, const float* __restrict__ G, const PocketDev& pk,
+                                          int K, int kbits, int S_w, float ck, float sk,
+                                          const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
+                                          float* __restrict__ scoreOut, int lane) {
+    const float* rx = rec;
+    const float* ry = rec + AC;
+    const float* rz = rec + 2 * AC;
+    const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
+    float Tr[12];
+#pragma unroll
+    for (int t = 0; t < 12; ++t) Tr[t] = T[t];
+#pragma unroll
+    for (int s = 0; s < AC / 32; ++s) {
+        const int i = s * 32 + lane;
+        if (i < A) buf[i] = place_atom(Tr, rx[i], ry[i], rz[i]);
+    }
+    __syncwarp();
+    if (K > 1) {
+        const int k = lane & (K - 1);
+        const int jl = lane >> kbits;
+        const int apw = 32 >> kbits;
+        for (int sw = 0; sw < S_w; ++sw) {
+            for (int r = 0; r < R; ++r) {
+                const uint32_t f = rfr[r];
+                const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
+                const float4 ya = buf[fa], yb = buf[fb];
+                float ux, uy, uz;
+                axis_of(ya, yb, ux, uy, uz);
+                const Rot M = rodrigues(ux, uy, uz, ck, sk);
+                float acc = 0.f;
+                for (int base = lo; base < hi; base += apw) {
+                    const int j = base + jl;
+                    if (j < hi) {
+                        const float4 v = buf[j];
+                        const float3 p = rot_about(M, yb.x, yb.y, yb.z, v.x, v.y, v.z);
+                        const bool id = (k == 0);   // theta_0: the current pose itself (Q3)
+                        acc = __fadd_rn(acc, grid_g(G, id ? v.x : p.x, id ? v.y : p.y, id ? v.z : p.z, pk));
+                    }
+                }
+                for (int o = K; o < 32; o <<= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                float best = acc;
+                int bk = k;
+                for (int o = 1; o < K; o <<= 1) {
+                    const float ob = __shfl_xor_sync(FULL, best, o);
+                    const int ok = __shfl_xor_sync(FULL, bk, o);
+                    if (ob < best || (ob == best && ok < bk)) {
+                        best = ob;
+                        bk = ok;
+                    }
+                }
+                if (bk != 0) {  // warp-uniform
+                    const Rot Ms = rodrigues(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1]);
+                    for (int j = lo + lane; j < hi; j += 32) {
+                        const float4 v = buf[j];
+                        const float3 p = rot_about(Ms, yb.x, yb.y, yb.z, v.x, v.y, v.z);
+                        buf[j] = make_float4(p.x, p.y, p.z, 0.f);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) angOut[sw * R + r] = (uint8_t)bk;
+            }
+        }
+    } else {
+        for (int t = lane; t < S_w * R; t += 32) angOut[t] = 0;
+    }
+    // a9: pose score, canonical order (atom i -> lane i mod 32, ascending slots, xor tree) (Q22)
+    float acc = 0.f;
+#pragma unroll
+    for (int s = 0; s < AC / 32; ++s) {
+        const int i = s * 32 + lane;
+        if (i < A) {
+            const float4 v = buf[i];
+            acc = __fadd_rn(acc, grid_g(G, v.x, v.y, v.z, pk));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+    if (lane == 0) *scoreOut = acc;
+    __syncwarp();
+}
+
+template <int AC, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const PocketDev& pk = a.pk;
+    const int LC = a.ligs_per_cta;
+    const DockLayout L = dock_layout(AC, NW, pk.nz, pk.ps, a.P, a.K, a.S_w, LC);
+    float* sG = reinterpret_cast<float*>(smem + L.grid);
+    float* sPose = reinterpret_cast<float*>(smem + L.pose);
+    float* sCS = reinterpret_cast<float*>(smem + L.cs);
+    float* sRec = reinterpret_cast<float*>(smem + L.rec);
+    float4* sBuf = reinterpret_cast<float4*>(smem + L.buf);
+    float* sScore = reinterpret_cast<float*>(smem + L.score);
+    uint8_t* sAng = smem + L.ang;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    stage_grid(sG, pk);
+    for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
+    for (int t = tid; t < 2 * a.K; t += blockDim.x) sCS[t] = a.cs[t];
+    __syncthreads();
+
+    const int K = a.K, S_w = a.S_w, P = a.P;
+    const int kbits = 31 - __clz(K);
+    const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
+    float4* buf = sBuf + warp * AC;
+    const int rec_floats = a.rec_floats;
+    const int n_rounds = (a.n + LC - 1) / LC;
+    const int ang_stride = 32 * S_w;
+
+    for (int round = blockIdx.x; round < n_rounds; round += gridDim.x) {
+        const int slot0 = round * LC;
+        const int nl = min(LC, a.n - slot0);
+        {
+            const float4* src = reinterpret_cast<const float4*>(a.rec + (size_t)slot0 * rec_floats);
+            float4* dst = reinterpret_cast<float4*>(sRec);
+            const int n4 = nl * rec_floats / 4;
+            for (int t = tid; t < n4; t += blockDim.x) dst[t] = src[t];
+        }
+        __syncthreads();
+        for (int item = warp; item < nl * P; item += NW) {
+            const int l = item / P, p = item - l * P;
+            const int4 m = a.meta[slot0 + l];
+            dock_pose<AC>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * p, buf, sG, pk, K, kbits, S_w, ck, sk, sCS,
+                          sAng + (size_t)item * ang_stride, sScore + item, lane);
+        }
+        __syncthreads();
+        if (warp < nl) {  // a9 best pose: lowest score, ties -> lowest pose index (Q11)
+            const int l = warp;
+            const int4 m = a.meta[slot0 + l];
+            float best = __int_as_float(0x7f800000);
+            int bp = 0x7fffffff;
+            for (int p = lane; p < P; p += 32) {
+                const float s = sScore[l * P + p];
+                if (s < best || bp == 0x7fffffff) {
+                    best = s;
+                    bp = p;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ob = __shfl_xor_sync(FULL, best, o);
+                const int op = __shfl_xor_sync(FULL, bp, o);
+                if (ob < best || (ob == best && op < bp)) {
+                    best = ob;
+                    bp = op;
+                }
+            }
+            const int li = m.x, R = m.z, nang = S_w * R;
+            if (lane == 0) {
+                a.best_score[li] = best;
+                a.best_pose[li] = bp;
+            }
+            const uint8_t* sa = sAng + (size_t)(l * P + bp) * ang_stride;
+            for (int t = lane; t < nang; t += 32) a.angles[m.w + t] = sa[t];
+            if (a.dbg_score)
+                for (int p = lane; p < P; p += 32) a.dbg_score[(size_t)li * P + p] = sScore[l * P + p];
+            if (a.dbg_angles)
+                for (int t = lane; t < P * nang; t += 32) {
+                    const int p = t / nang, q = t - p * nang;
+                    a.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
+                }
+        }
+    }
+}
+
+// a9 coordinates: replay p* with the recorded angles, bit-identical to the
+// dock kernel (same placement, axis, Rodrigues and rotation code); one warp per
+// ligand; output in Angstrom, input atom order.
+template <int AC>
+__global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const int64_t* __restrict__ atom_off,
+                                                       float* __restrict__ xyz_out) {
+    __shared__ __align__(16) float4 sb[8][AC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int s = blockIdx.x * 8 + w;
+    if (s >= a.n) return;
+    const PocketDev& pk = a.pk;
+    const int4 m = a.meta[s];
+    const int li = m.x, A = m.y, R = m.z;
+    const int p = a.best_pose[li];
+    const float* rec = a.rec + (size_t)s * a.rec_floats;
+    const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
+    float T[12];
+    scaled_pose(a.pose_tab + 12 * p, pk, T);
+    float4* buf = sb[w];
+    for (int i = lane; i < A; i += 32) buf[i] = place_atom(T, rec[i], rec[AC + i], rec[2 * AC + i]);
+    __syncwarp();
+    for (int sw = 0; sw < a.S_w; ++sw) {
+        for (int r = 0; r < R; ++r) {
+            const int bk = a.angles[m.w + sw * R + r];
+            if (bk != 0) {
+                const uint32_t f = rfr[r];
+                const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
+                const float4 ya = buf[fa], yb = buf[fb];
+                float ux, uy, uz;
+                axis_of(ya, yb, ux, uy, uz);
+                const Rot Ms = rodrigues(ux, uy, uz, a.cs[2 * bk], a.cs[2 * bk + 1]);
+                for (int j = lo + lane; j < hi; j += 32) {
+                    const float4 v = buf[j];
+                    const float3 q = rot_about(Ms, yb.x, yb.y, yb.z, v.x, v.y, v.z);
+                    buf[j] = make_float4(q.x, q.y, q.z, 0.f);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    float* out = xyz_out + 3 * atom_off[li];
+    for (int i = lane; i < A; i += 32) {
+        const float4 v = buf[i];
+        out[3 * i] = __fmaf_rn(pk.h, v.x, pk.ox);
+        out[3 * i + 1] = __fmaf_rn(pk.h, v.y, pk.oy);
+        out[3 * i + 2] = __fmaf_rn(pk.h, v.z, pk.oz);
+    }
+}
+
+__global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, const float* __restrict__ xyz,
+                                                            int64_t n, float* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* sG = reinterpret_cast<float*>(smem);
+    stage_grid(sG, pk);
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
+        const float uy = __fmul_rn(__fsub_rn(xyz[3 * i + 1], pk.oy), pk.inv_h);
+        const float uz = __fmul_rn(__fsub_rn(xyz[3 * i + 2], pk.oz), pk.inv_h);
+        out[i] = grid_g(sG, ux, uy, uz, pk);
+    }
+}
+
+using DockFn = void (*)(const DockArgs);
+
+template <int AC, int NW>
+DockFn dock_fn() {
+    return dock_kernel<AC, NW>;
+}
+
+DockFn pick(int AC, int NW) {
+#define VSD_CASE(ac)                                   \
+    case ac:                                           \
+        return NW == 32 ? dock_fn<ac, 32>() : dock_fn<ac, 16>();
+    switch (AC) {
+        VSD_CASE(32)
+        VSD_CASE(64)
+        VSD_CASE(96)
+        VSD_CASE(128)
+        VSD_CASE(160)
+        VSD_CASE(192)
+        VSD_CASE(224)
+        VSD_CASE(256)
+        default:
+            return nullptr;
+    }
+#undef VSD_CASE
+}
+
+}  // namespace
+
+void grid_strides(int nx, int ny, int* rs, int* ps) {
+    *rs = nx;
+    *ps = nx * ny;
+}
+
+cudaError_t dock_kernel_attrs(int AC, int NW, cudaFuncAttributes* attr) {
+    DockFn f = pick(AC, NW);
+    if (!f || (NW != 32 && NW != 16)) return cudaErrorInvalidValue;
+    return cudaFuncGetAttributes(attr, reinterpret_cast<const void*>(f));
+}
+
+cudaError_t dock_occupancy(int AC, int NW, size_t smem, int* blocks_per_sm) {
+    DockFn f = pick(AC, NW);
+    if (!f || (NW != 32 && NW != 16)) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+        *blocks_per_sm = 0;
+        cudaGetLastError();
+        return cudaSuccess;
+    }
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, reinterpret_cast<const void*>(f), NW * 32,
+                                                         smem);
+}
+
+cudaError_t launch_dock(int AC, int NW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
+    DockFn f = pick(AC, NW);
+    if (!f || (NW != 32 && NW != 16)) return cudaErrorInvalidValue;
+    if (a.n <= 0) return cudaSuccess;
+    f<<<grid, NW * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st) {
+    if (a.n <= 0) return cudaSuccess;
+    const int grid = (a.n + 7) / 8;
+    switch (AC) {
+#define VSD_FIN(ac)                                                          \
+    case ac:                                                                 \
+        finalize_kernel<ac><<<grid, 256, 0, st>>>(a, atom_off, xyz_out);     \
+        break;
+        VSD_FIN(32)
+        VSD_FIN(64)
+        VSD_FIN(96)
+        VSD_FIN(128)
+        VSD_FIN(160)
+        VSD_FIN(192)
+        VSD_FIN(224)
+        VSD_FIN(256)
+#undef VSD_FIN
+        default:
+            return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
+                                cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(score_points_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    score_points_kernel<<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace vsd

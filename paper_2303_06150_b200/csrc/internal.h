@@ -1,0 +1,108 @@
+// internal.h -- structures shared by the host runtime (api.cpp) and the CUDA
+// kernels (prep.cu, dock.cu, topk.cu).  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vsd {
+
+constexpr int kMaxAtoms = 256;     // D1 bound per ligand ("up to a few hundred")
+constexpr int kMaxFrags = 32;      // rotatable bonds per ligand
+constexpr int kMaxAtomClasses = 8; // atom classes (warp multiples up to 256)
+constexpr int kMaxRotClasses = 33; // rotamer classes (0..32)
+constexpr int kMaxCells = kMaxAtomClasses * kMaxRotClasses;
+constexpr int kPrepTile = 4096;    // ligands per block in classify/scatter
+constexpr int kMaxPoses = 1024;
+constexpr int kMaxSweeps = 4;
+
+// Pocket as the dock kernel sees it: grid staged in shared memory with padded
+// row / plane strides (floats), coordinates in grid units u = (y - o)/h.
+struct PocketDev {
+    const float* grid;     // global copy [nz][ny][nx]
+    int nx, ny, nz;
+    int rs, ps;            // shared-memory row stride and plane stride (floats)
+    float top_x, top_y, top_z;    // n - 1
+    float top2_x, top2_y, top2_z; // n - 2
+    float kh;              // kappa * h  (penalty per grid unit of excess)
+    float h;
+    float ox, oy, oz;      // origin
+    float tx, ty, tz;      // (center - origin) / h
+    float inv_h;
+};
+
+// One bucket launch (a6-a9).
+struct DockArgs {
+    const float* rec;          // packed records of this bucket (slot s at rec + s * rec_floats)
+    const int4* meta;          // [slots] {ligand index, A, R, S_w * frag_off}
+    int n;                     // ligands in the bucket
+    int rec_floats;            // 3 * AC + 32
+    int P, K, S_w;
+    int ligs_per_cta;          // LC
+    const float* pose_tab;     // [P][12] raw: R (9, row-major) then tau (3)
+    const float* cs;           // [K][2]
+    PocketDev pk;
+    float* best_score;         // [n_total]
+    int* best_pose;            // [n_total]
+    uint8_t* angles;           // CSR S_w * frag_off
+    float* dbg_score;          // [n_total * P] or null
+    uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
+};
+
+// Shared-memory layout of dock<AC, NW> (byte offsets).  Used by the kernel and
+// by the host (occupancy query, launch) so both agree.
+struct DockLayout {
+    size_t grid, pose, cs, rec, buf, score, ang, total;
+};
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int nz, int ps, int P, int K, int S_w, int LC) {
+    DockLayout L;
+    size_t o = 0;
+    L.grid = o;  o += align16((size_t)nz * ps * 4);
+    L.pose = o;  o += align16((size_t)P * 12 * 4);
+    L.cs = o;    o += align16((size_t)K * 2 * 4);
+    L.rec = o;   o += align16((size_t)LC * (3 * AC + 32) * 4);
+    L.buf = o;   o += (size_t)NW * AC * 16;
+    L.score = o; o += align16((size_t)LC * P * 4);
+    L.ang = o;   o += align16((size_t)LC * P * S_w * 32);
+    L.total = o;
+    return L;
+}
+// Shared-memory grid strides: row stride rs >= nx, plane stride ps >= ny * rs.
+void grid_strides(int nx, int ny, int* rs, int* ps);
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_validate(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frags,
+                            int64_t n, int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR,
+                            cudaStream_t st);
+cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
+                                 const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
+                                 unsigned long long* ovf, cudaStream_t st);
+cudaError_t launch_scan_hist(int* hist, int n_cells, int n_blocks, int* cell_count, cudaStream_t st);
+cudaError_t launch_scatter(const int* cell, int64_t n, const int* hist_off, int n_cells, int n_blocks, uint32_t* perm,
+                           cudaStream_t st);
+cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const int* featM, const int64_t* bstart,
+                                  const int* bsize, int n_buckets, long long P, long long K, long long S_w,
+                                  unsigned long long* weights, cudaStream_t st);
+// Pack owned buckets.  slot_bucket_prefix[b] = first packed slot of owned bucket b (nb+1 entries).
+cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
+                        const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
+                        const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
+                        int4* meta, cudaStream_t st);
+cudaError_t launch_dock(int AC, int NW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
+cudaError_t dock_kernel_attrs(int AC, int NW, cudaFuncAttributes* attr);
+cudaError_t dock_occupancy(int AC, int NW, size_t smem, int* blocks_per_sm);
+cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
+cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
+                                cudaStream_t st);
+cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
+                                cudaStream_t st);
+// top-k
+cudaError_t launch_make_keys(const int4* meta, int n_slots, const float* best_score, unsigned long long* keys,
+                             cudaStream_t st);
+// Select the k smallest of keys[n] (unique), write them sorted to out[k] (UINT64_MAX padded).
+// scratch: >= (n + 2048) u64 + 4 KB.  Returns the number of kernels launched in *launches.
+cudaError_t topk_select_sort(const unsigned long long* keys, int64_t n, int k, unsigned long long* out,
+                             void* scratch, cudaStream_t st, int* launches);
+
+}  // namespace vsd

@@ -1,0 +1,392 @@
+// prep.cu -- the paper's out-of-kernel input preparation on the GPU (a1-a5):
+// validation + features, classification into (atom class x rotamer class)
+// cells, a STABLE counting sort by cell (histogram -> scan -> scatter), exact
+// per-bucket work for the LPT shard, and packing into SoA-padded records.
+//
+// PAPER.md l.206-240 (runtime input preparation that "collects the ligands in
+// buckets before virtual screening them", l.219-220)
+// (assignment and bucket membership); readings Q16-Q18, Q21.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace vsd {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// a1: one warp per ligand (grid-stride).  Error codes (low byte of the status
+// word, lowest ligand index wins through atomicMin on (index << 8 | code)):
+//  1 atoms outside [1, 256]      2 fragments outside [0, 32]
+//  3 non-finite coordinate       4 axis atom index out of range
+//  5 axis atoms equal            6 moving range invalid (need 0 <= lo < hi <= A)
+//  7 axis atom inside its moving range   8 axis atoms closer than 1e-3 A
+__global__ void __launch_bounds__(256) validate_kernel(const int64_t* __restrict__ atom_off,
+                                                       const float* __restrict__ xyz,
+                                                       const int64_t* __restrict__ frag_off,
+                                                       const int32_t* __restrict__ frags, int64_t n,
+                                                       int* __restrict__ featA, int* __restrict__ featR,
+                                                       int* __restrict__ featM, unsigned long long* status,
+                                                       int* maxAR) {
+    __shared__ int smax[2];
+    if (threadIdx.x < 2) smax[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int locA = 0, locR = 0;
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+        const int64_t a0 = atom_off[i], a1 = atom_off[i + 1];
+        const int64_t f0 = frag_off[i], f1 = frag_off[i + 1];
+        const int64_t A64 = a1 - a0, R64 = f1 - f0;
+        int code = 0;
+        if (A64 < 1 || A64 > kMaxAtoms) code = 1;
+        else if (R64 < 0 || R64 > kMaxFrags) code = 2;
+        int M = 0;
+        if (code == 0) {
+            const int A = (int)A64, R = (int)R64;
+            bool bad = false;
+            for (int t = lane; t < 3 * A; t += 32) bad |= !isfinite(xyz[3 * a0 + t]);
+            if (__any_sync(FULL, bad)) code = 3;
+            int fcode = 0, mv = 0;
+            if (code == 0 && lane < R) {
+                const int4 f = reinterpret_cast<const int4*>(frags)[f0 + lane];
+                if (f.x < 0 || f.x >= A || f.y < 0 || f.y >= A) fcode = 4;
+                else if (f.x == f.y) fcode = 5;
+                else if (!(0 <= f.z && f.z < f.w && f.w <= A)) fcode = 6;
+                else if ((f.x >= f.z && f.x < f.w) || (f.y >= f.z && f.y < f.w)) fcode = 7;
+                else {
+                    const float* pa = xyz + 3 * (a0 + f.x);
+                    const float* pb = xyz + 3 * (a0 + f.y);
+                    const float dx = pb[0] - pa[0], dy = pb[1] - pa[1], dz = pb[2] - pa[2];
+                    if (dx * dx + dy * dy + dz * dz < 1e-6f) fcode = 8;
+                    mv = f.w - f.z;
+                }
+            }
+            // lowest fragment code wins within the ligand (first error in field order)
+            unsigned any = __ballot_sync(FULL, fcode != 0);
+            if (any) code = __shfl_sync(FULL, fcode, __ffs(any) - 1);
+            M = warp_sum_int(mv);
+            if (code == 0) {
+                locA = max(locA, A);
+                locR = max(locR, R);
+            }
+        }
+        if (lane == 0) {
+            featA[i] = (int)(A64 > 0x7fffffff ? 0x7fffffff : A64);
+            featR[i] = (int)(R64 > 0x7fffffff ? 0x7fffffff : R64);
+            featM[i] = M;
+            if (code) atomicMin(status, ((unsigned long long)i << 8) | (unsigned long long)code);
+        }
+    }
+    if (lane == 0) {
+        atomicMax(&smax[0], locA);
+        atomicMax(&smax[1], locR);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMax(&maxAR[0], smax[0]);
+        atomicMax(&maxAR[1], smax[1]);
+    }
+}
+
+struct Bounds {
+    int atom_b[kMaxAtomClasses];
+    int rot_b[kMaxRotClasses];
+    int n_atom_b, n_rot_b;
+};
+
+// a2: cell = atom_class * n_rot + rot_class; each class index is the smallest
+// i with value <= boundary[i].  Block-local histogram -> hist[cell][block].
+__global__ void __launch_bounds__(1024) classify_hist_kernel(const int* __restrict__ featA,
+                                                             const int* __restrict__ featR, int64_t n, Bounds bd,
+                                                             int* __restrict__ cell, int* __restrict__ hist,
+                                                             int n_blocks, unsigned long long* ovf) {
+    __shared__ int h[kMaxCells];
+    const int n_cells = bd.n_atom_b * bd.n_rot_b;
+    for (int c = threadIdx.x; c < n_cells; c += blockDim.x) h[c] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kPrepTile;
+    for (int t = threadIdx.x; t < kPrepTile; t += blockDim.x) {
+        const int64_t i = base + t;
+        if (i >= n) break;
+        const int A = featA[i], R = featR[i];
+        int ai = 0, ri = 0;
+        while (ai < bd.n_atom_b && A > bd.atom_b[ai]) ++ai;
+        while (ri < bd.n_rot_b && R > bd.rot_b[ri]) ++ri;
+        int c = -1;
+        if (ai == bd.n_atom_b) atomicMin(ovf, ((unsigned long long)i << 8) | 1ull);
+        else if (ri == bd.n_rot_b) atomicMin(ovf, ((unsigned long long)i << 8) | 2ull);
+        else {
+            c = ai * bd.n_rot_b + ri;
+            atomicAdd(&h[c], 1);
+        }
+        cell[i] = c;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < n_cells; c += blockDim.x) hist[(int64_t)c * n_blocks + blockIdx.x] = h[c];
+}
+
+// a3 (scan): per-cell totals, then an exclusive scan of hist (cell-major) in place:
+// hist[c][b] becomes the first output position of block b's cell-c ligands.
+__global__ void __launch_bounds__(1024) scan_hist_kernel(int* __restrict__ hist, int n_cells, int n_blocks,
+                                                         int* __restrict__ cell_count) {
+    __shared__ int wsum[32];
+    for (int c = threadIdx.x; c < n_cells; c += blockDim.x) {
+        int s = 0;
+        for (int b = 0; b < n_blocks; ++b) s += hist[(int64_t)c * n_blocks + b];
+        cell_count[c] = s;
+    }
+    __syncthreads();
+    const int64_t N = (int64_t)n_cells * n_blocks;
+    const int64_t per = (N + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = threadIdx.x * per, hi = lo + per < N ? lo + per : N;
+    int s = 0;
+    for (int64_t j = lo; j < hi; ++j) s += hist[j];
+    // block exclusive scan of s
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int u = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += u;
+        }
+        wsum[lane] = inc - v;
+    }
+    __syncthreads();
+    int run = wsum[w] + incl - s;
+    for (int64_t j = lo; j < hi; ++j) {
+        const int v = hist[j];
+        hist[j] = run;
+        run += v;
+    }
+}
+
+// a3 (scatter): stable -- inside a tile, rank among equal cells by index
+// (warp match + popc, then warp-prefix per cell), tiles ordered by block.
+__global__ void __launch_bounds__(1024) scatter_kernel(const int* __restrict__ cell, int64_t n,
+                                                       const int* __restrict__ hist_off, int n_cells, int n_blocks,
+                                                       uint32_t* __restrict__ perm) {
+    __shared__ int wcnt[32][kMaxCells];
+    __shared__ int running[kMaxCells];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int c = threadIdx.x; c < n_cells; c += blockDim.x) running[c] = 0;
+    const int64_t base = (int64_t)blockIdx.x * kPrepTile;
+    for (int chunk = 0; chunk < kPrepTile; chunk += 1024) {
+        for (int e = threadIdx.x; e < 32 * n_cells; e += blockDim.x) wcnt[e / n_cells][e % n_cells] = 0;
+        __syncthreads();
+        const int64_t i = base + chunk + threadIdx.x;
+        const int c = (i < n) ? cell[i] : -1;
+        const unsigned peers = __match_any_sync(FULL, c);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if (c >= 0 && lane == __ffs(peers) - 1) wcnt[w][c] = __popc(peers);
+        __syncthreads();
+        for (int cc = threadIdx.x; cc < n_cells; cc += blockDim.x) {
+            int run = running[cc];
+            for (int ww = 0; ww < 32; ++ww) {
+                const int t = wcnt[ww][cc];
+                wcnt[ww][cc] = run;
+                run += t;
+            }
+            running[cc] = run;
+        }
+        __syncthreads();
+        if (c >= 0) perm[hist_off[(int64_t)c * n_blocks + blockIdx.x] + wcnt[w][c] + rank] = (uint32_t)i;
+        __syncthreads();
+    }
+}
+
+// a4 input: exact work of a bucket, sum of E_alg = P (A + S_w (K-1) sum|M_r|).
+__global__ void __launch_bounds__(256) bucket_weights_kernel(const uint32_t* __restrict__ perm,
+                                                             const int* __restrict__ featA,
+                                                             const int* __restrict__ featM,
+                                                             const int64_t* __restrict__ bstart,
+                                                             const int* __restrict__ bsize, long long P, long long K,
+                                                             long long S_w, unsigned long long* __restrict__ weights) {
+    __shared__ unsigned long long part[8];
+    const int b = blockIdx.x;
+    unsigned long long s = 0;
+    for (int t = threadIdx.x; t < bsize[b]; t += blockDim.x) {
+        const uint32_t li = perm[bstart[b] + t];
+        s += (unsigned long long)(P * ((long long)featA[li] + S_w * (K - 1) * (long long)featM[li]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+        weights[b] = t;
+    }
+}
+
+// a5: one warp per packed slot.  Record layout (floats): x[AC] | y[AC] | z[AC] |
+// frags u32[32] = a | b << 8 | lo << 16 | (hi - 1) << 24.  Coordinates are
+// centred on the ligand centroid (a6, Q8); padding is 0.  The centroid sum is
+// lane-strided then xor-reduced: an order that does not depend on AC (Q22).
+__global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ perm,
+                                                   const int64_t* __restrict__ owned_start,
+                                                   const int* __restrict__ owned_prefix,
+                                                   const int* __restrict__ owned_ac,
+                                                   const int64_t* __restrict__ owned_rec_off, int n_owned,
+                                                   int total_slots, const int64_t* __restrict__ atom_off,
+                                                   const float* __restrict__ xyz,
+                                                   const int64_t* __restrict__ frag_off,
+                                                   const int32_t* __restrict__ frags, int S_w,
+                                                   float* __restrict__ rec, int4* __restrict__ meta) {
+    const int lane = threadIdx.x & 31;
+    const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (slot >= total_slots) return;
+    int lo = 0, hi = n_owned;  // owned_prefix[b] <= slot < owned_prefix[b+1]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (owned_prefix[mid] <= slot) lo = mid; else hi = mid;
+    }
+    const int b = lo;
+    const int s = slot - owned_prefix[b];
+    const uint32_t li = perm[owned_start[b] + s];
+    const int AC = owned_ac[b];
+    float* r = rec + owned_rec_off[b] + (int64_t)s * (3 * AC + 32);
+    const int64_t a0 = atom_off[li];
+    const int A = (int)(atom_off[li + 1] - a0);
+    const int64_t f0 = frag_off[li];
+    const int R = (int)(frag_off[li + 1] - f0);
+    const float* x = xyz + 3 * a0;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    for (int i = lane; i < A; i += 32) {
+        sx = __fadd_rn(sx, x[3 * i]);
+        sy = __fadd_rn(sy, x[3 * i + 1]);
+        sz = __fadd_rn(sz, x[3 * i + 2]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sx = __fadd_rn(sx, __shfl_xor_sync(FULL, sx, o));
+        sy = __fadd_rn(sy, __shfl_xor_sync(FULL, sy, o));
+        sz = __fadd_rn(sz, __shfl_xor_sync(FULL, sz, o));
+    }
+    const float fa = (float)A;
+    const float cx = __fdiv_rn(sx, fa), cy = __fdiv_rn(sy, fa), cz = __fdiv_rn(sz, fa);
+    for (int i = lane; i < AC; i += 32) {
+        const bool in = i < A;
+        r[i] = in ? __fsub_rn(x[3 * i], cx) : 0.f;
+        r[AC + i] = in ? __fsub_rn(x[3 * i + 1], cy) : 0.f;
+        r[2 * AC + i] = in ? __fsub_rn(x[3 * i + 2], cz) : 0.f;
+    }
+    uint32_t f = 0;
+    if (lane < R) {
+        const int4 q = reinterpret_cast<const int4*>(frags)[f0 + lane];
+        f = (uint32_t)q.x | ((uint32_t)q.y << 8) | ((uint32_t)q.z << 16) | ((uint32_t)(q.w - 1) << 24);
+    }
+    reinterpret_cast<uint32_t*>(r + 3 * AC)[lane] = f;
+    if (lane == 0) meta[slot] = make_int4((int)li, A, R, (int)(S_w * f0));
+}
+
+__global__ void fill_results_kernel(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        best_score[i] = __int_as_float(0x7fc00000);
+        best_pose[i] = -1;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ang; i += stride) angles[i] = 0xFF;
+}
+
+// a10 keys: ord(score) << 32 | ligand index; ord is the order-preserving map of
+// fp32 onto uint32 (sign-magnitude flip); -0 is canonicalised to +0.
+__global__ void make_keys_kernel(const int4* __restrict__ meta, int n_slots, const float* __restrict__ best_score,
+                                 unsigned long long* __restrict__ keys) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_slots) return;
+    const int li = meta[s].x;
+    const float v = __fadd_rn(best_score[li], 0.0f);
+    const uint32_t bits = __float_as_uint(v);
+    const uint32_t ord = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
+    keys[s] = ((unsigned long long)ord << 32) | (uint32_t)li;
+}
+
+}  // namespace
+
+cudaError_t launch_validate(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frags,
+                            int64_t n, int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR,
+                            cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 7) / 8;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    validate_kernel<<<(int)blocks, 256, 0, st>>>(atom_off, xyz, frag_off, frags, n, featA, featR, featM, status, maxAR);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
+                                 const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
+                                 unsigned long long* ovf, cudaStream_t st) {
+    Bounds bd;
+    bd.n_atom_b = n_atom_b;
+    bd.n_rot_b = n_rot_b;
+    for (int i = 0; i < n_atom_b; ++i) bd.atom_b[i] = atom_b[i];
+    for (int i = 0; i < n_rot_b; ++i) bd.rot_b[i] = rot_b[i];
+    classify_hist_kernel<<<n_blocks, 1024, 0, st>>>(featA, featR, n, bd, cell, hist, n_blocks, ovf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_hist(int* hist, int n_cells, int n_blocks, int* cell_count, cudaStream_t st) {
+    scan_hist_kernel<<<1, 1024, 0, st>>>(hist, n_cells, n_blocks, cell_count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const int* cell, int64_t n, const int* hist_off, int n_cells, int n_blocks, uint32_t* perm,
+                           cudaStream_t st) {
+    scatter_kernel<<<n_blocks, 1024, 0, st>>>(cell, n, hist_off, n_cells, n_blocks, perm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const int* featM, const int64_t* bstart,
+                                  const int* bsize, int n_buckets, long long P, long long K, long long S_w,
+                                  unsigned long long* weights, cudaStream_t st) {
+    if (n_buckets <= 0) return cudaSuccess;
+    bucket_weights_kernel<<<n_buckets, 256, 0, st>>>(perm, featA, featM, bstart, bsize, P, K, S_w, weights);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
+                        const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
+                        const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
+                        int4* meta, cudaStream_t st) {
+    if (total_slots <= 0) return cudaSuccess;
+    pack_kernel<<<(total_slots + 7) / 8, 256, 0, st>>>(perm, owned_start, owned_prefix, owned_ac, owned_rec_off,
+                                                       n_owned_buckets, total_slots, atom_off, xyz, frag_off, frags,
+                                                       S_w, rec, meta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
+                                cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    fill_results_kernel<<<148 * 4, 256, 0, st>>>(best_score, best_pose, n, angles, n_ang);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_make_keys(const int4* meta, int n_slots, const float* best_score, unsigned long long* keys,
+                             cudaStream_t st) {
+    if (n_slots <= 0) return cudaSuccess;
+    make_keys_kernel<<<(n_slots + 255) / 256, 256, 0, st>>>(meta, n_slots, best_score, keys);
+    return cudaGetLastError();
+}
+
+}  // namespace vsd

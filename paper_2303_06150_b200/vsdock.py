@@ -1,0 +1,300 @@
+"""ctypes binding of include/vsdock.h (argument marshalling only).
+
+Every step of the hot path runs in libvsdock.so's CUDA kernels; this module
+only converts numpy / torch buffers to pointers, owns the device workspace (a
+torch uint8 tensor) and hands the library torch's current CUDA stream.  There
+is no CPU fallback: if the library or a CUDA device is missing, constructing an
+:class:`Engine` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libvsdock.so")
+
+VS_OK, VS_E_ARG, VS_E_PARSE, VS_E_OVERFLOW_ATOMS, VS_E_OVERFLOW_ROTAMERS = 0, -1, -2, -3, -4
+VS_E_NOFIT, VS_E_WORKSPACE, VS_E_CUDA, VS_E_STATE = -5, -6, -7, -9
+_NAMES = {0: "VS_OK", -1: "VS_E_ARG", -2: "VS_E_PARSE", -3: "VS_E_OVERFLOW_ATOMS", -4: "VS_E_OVERFLOW_ROTAMERS",
+          -5: "VS_E_NOFIT", -6: "VS_E_WORKSPACE", -7: "VS_E_CUDA", -9: "VS_E_STATE"}
+
+SYMBOLS = ["vs_create", "vs_destroy", "vs_last_error", "vs_workspace_size", "vs_set_workspace", "vs_load_pocket",
+           "vs_set_pose_table", "vs_set_angle_table", "vs_submit", "vs_wait", "vs_get_results", "vs_get_coords",
+           "vs_get_pose_debug", "vs_local_topk", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
+           "vs_score_points", "vs_get_stats"]
+
+
+class VsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class vs_config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("n_sweeps", ctypes.c_int32), ("n_atom_clusters", ctypes.c_int32),
+                ("n_rot_clusters", ctypes.c_int32), ("atom_upper_bound", ctypes.c_int32),
+                ("rot_upper_bound", ctypes.c_int32), ("bucket_multiple", ctypes.c_int32),
+                ("n_streams", ctypes.c_int32), ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32),
+                ("debug_poses", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+
+
+class vs_pocket_desc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("origin", ctypes.c_float * 3), ("spacing", ctypes.c_float), ("center", ctypes.c_float * 3),
+                ("out_slope", ctypes.c_float)]
+
+
+class vs_ligand_batch(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("atom_off", ctypes.c_void_p), ("xyz", ctypes.c_void_p),
+                ("frag_off", ctypes.c_void_p), ("frags", ctypes.c_void_p), ("on_device", ctypes.c_int32)]
+
+
+class vs_bucket(ctypes.Structure):
+    _fields_ = [("cell", ctypes.c_int32), ("atom_class", ctypes.c_int32), ("rot_class", ctypes.c_int32),
+                ("atom_bound", ctypes.c_int32), ("kernel_atoms", ctypes.c_int32), ("capacity", ctypes.c_int32),
+                ("size", ctypes.c_int32), ("owner", ctypes.c_int32), ("launch_order", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("start", ctypes.c_int64), ("weight", ctypes.c_uint64)]
+
+
+class vs_class_info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("atom_bound", "kernel_atoms", "warps_per_cta", "threads_per_cta",
+                                              "regs_per_thread", "static_smem", "dyn_smem", "blocks_per_sm",
+                                              "sm_count", "ligands_per_cta", "l", "capacity")]
+
+
+class vs_stats(ctypes.Structure):
+    _fields_ = [("n_ligands", ctypes.c_int64), ("n_owned", ctypes.c_int64), ("n_buckets", ctypes.c_int64),
+                ("n_owned_buckets", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("dock_launches", ctypes.c_int64), ("evals_alg", ctypes.c_double), ("prep_ms", ctypes.c_float),
+                ("dock_ms", ctypes.c_float), ("topk_ms", ctypes.c_float)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libvsdock.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(SO_PATH):
+        raise ImportError(f"{SO_PATH} is missing; run __graft_entry__.build() (nvcc, sm_100a)")
+    lib = ctypes.CDLL(SO_PATH)
+    P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    sig = {
+        "vs_create": [ctypes.POINTER(vs_config), ctypes.POINTER(P)],
+        "vs_destroy": [P],
+        "vs_last_error": [P],
+        "vs_workspace_size": [P, I64, I64, I64, I32, I32, ctypes.POINTER(SZ)],
+        "vs_set_workspace": [P, P, SZ],
+        "vs_load_pocket": [P, ctypes.POINTER(vs_pocket_desc), P, I32, ctypes.POINTER(I32)],
+        "vs_set_pose_table": [P, I32, P, P],
+        "vs_set_angle_table": [P, I32, P],
+        "vs_submit": [P, ctypes.POINTER(vs_ligand_batch), P, I32],
+        "vs_wait": [P],
+        "vs_get_results": [P, I32, P, P, P, I32],
+        "vs_get_coords": [P, I32, P, I32],
+        "vs_get_pose_debug": [P, I32, P, P],
+        "vs_local_topk": [P, I32, I32, P, ctypes.POINTER(I32)],
+        "vs_merge_topk": [P, P, I64, I32, P, P, ctypes.POINTER(I32)],
+        "vs_get_manifest": [P, I32, P, ctypes.POINTER(I32), P],
+        "vs_query_classes": [P, I32, P, ctypes.POINTER(I32)],
+        "vs_score_points": [P, I32, I64, P, P],
+        "vs_get_stats": [P, ctypes.POINTER(vs_stats)],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = None if name == "vs_destroy" else (ctypes.c_char_p if name == "vs_last_error" else I32)
+    _lib = lib
+    return lib
+
+
+def _ptr(x):
+    """Pointer of a numpy array or torch tensor (None passes through)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return ctypes.c_void_p(x.ctypes.data)
+    assert x.is_contiguous()
+    return ctypes.c_void_p(x.data_ptr())
+
+
+@dataclass
+class Results:
+    best_score: np.ndarray   # float32 [n]
+    best_pose: np.ndarray    # int32 [n]
+    angles: np.ndarray       # uint8 [S_w * sum R]
+
+
+class Engine:
+    """One context per GPU (include/vsdock.h).  Device memory and the stream come from torch."""
+
+    def __init__(self, device: int = 0, n_sweeps: int = 1, atom_clusters: int = 6, rot_clusters: int = 23,
+                 atom_upper_bound: int = 0, rot_upper_bound: int = 0, bucket_multiple: int = 16, n_streams: int = 4,
+                 rank: int = 0, world_size: int = 1, debug_poses: bool = False, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("vsdock needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+        self._torch = torch
+        self.lib = load_library()
+        self.device = device
+        self.n_sweeps = n_sweeps
+        torch.cuda.set_device(device)
+        st = stream if stream is not None else torch.cuda.current_stream(device)
+        self._stream = st
+        cfg = vs_config(device, n_sweeps, atom_clusters, rot_clusters, atom_upper_bound, rot_upper_bound,
+                        bucket_multiple, n_streams, rank, world_size, int(debug_poses), ctypes.c_void_p(st.cuda_stream))
+        h = ctypes.c_void_p()
+        self._check(self.lib.vs_create(ctypes.byref(cfg), ctypes.byref(h)), None)
+        self.h = h
+        self.ws = None
+        self.P = self.K = None
+        self._n = 0
+        self._batch_keep = None
+
+    def _check(self, rc, h="self"):
+        if rc != VS_OK:
+            hh = self.h if h == "self" else None
+            msg = self.lib.vs_last_error(hh).decode() if hh else ""
+            raise VsError(rc, msg)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- tables and pockets
+    def set_poses(self, rot, trans):
+        rot = np.ascontiguousarray(rot, np.float32).reshape(-1, 9)
+        trans = np.ascontiguousarray(trans, np.float32).reshape(-1, 3)
+        self._check(self.lib.vs_set_pose_table(self.h, rot.shape[0], _ptr(rot), _ptr(trans)))
+        self.P = rot.shape[0]
+
+    def set_angles(self, cs):
+        cs = np.ascontiguousarray(cs, np.float32).reshape(-1, 2)
+        self._check(self.lib.vs_set_angle_table(self.h, cs.shape[0], _ptr(cs)))
+        self.K = cs.shape[0]
+
+    def load_pocket(self, pocket) -> int:
+        g = np.ascontiguousarray(pocket.grid, np.float32)
+        nz, ny, nx = g.shape
+        d = vs_pocket_desc(nx, ny, nz, (ctypes.c_float * 3)(*pocket.origin), pocket.spacing,
+                           (ctypes.c_float * 3)(*pocket.center), pocket.out_slope)
+        pid = ctypes.c_int32()
+        self._check(self.lib.vs_load_pocket(self.h, ctypes.byref(d), _ptr(g), 0, ctypes.byref(pid)))
+        return pid.value
+
+    # ---- workspace
+    def reserve(self, n_lig, n_atoms, n_frags, max_atoms, n_pockets):
+        nbytes = ctypes.c_size_t()
+        self._check(self.lib.vs_workspace_size(self.h, n_lig, n_atoms, n_frags, max_atoms, n_pockets,
+                                               ctypes.byref(nbytes)))
+        if self.ws is None or self.ws.numel() < nbytes.value:
+            self.ws = None
+            self.ws = self._torch.empty(nbytes.value, dtype=self._torch.uint8, device=f"cuda:{self.device}")
+            self._check(self.lib.vs_set_workspace(self.h, ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()))
+        return nbytes.value
+
+    # ---- the hot path
+    def submit(self, atom_off, xyz, frag_off, frags, pockets, on_device=None, max_atoms=None):
+        """Submit a CSR ligand batch (numpy host arrays, pinned torch CPU tensors, or CUDA tensors)."""
+        n = int(atom_off.shape[0]) - 1
+        if on_device is None:
+            on_device = hasattr(xyz, "is_cuda") and xyz.is_cuda
+        if max_atoms is None:
+            if on_device:
+                max_atoms = int((atom_off[1:] - atom_off[:-1]).max().item()) if n > 0 else 1
+            else:
+                max_atoms = int(np.diff(np.asarray(atom_off)).max()) if n > 0 else 1
+        nA = int(xyz.shape[0])
+        nR = int(frags.shape[0])
+        pockets = np.ascontiguousarray(pockets, np.int32).reshape(-1)
+        self.reserve(n, nA, nR, max(1, min(256, max_atoms)), len(pockets))
+        b = vs_ligand_batch(n, _ptr(atom_off), _ptr(xyz), _ptr(frag_off), _ptr(frags), int(bool(on_device)))
+        self._batch_keep = (atom_off, xyz, frag_off, frags)
+        self._check(self.lib.vs_submit(self.h, ctypes.byref(b), _ptr(pockets), len(pockets)))
+        self._n, self._nA, self._nR = n, nA, nR
+        self._npk = len(pockets)
+
+    def submit_library(self, lib, pockets, **kw):
+        return self.submit(lib.atom_off, lib.xyz, lib.frag_off, lib.frags, pockets, **kw)
+
+    def wait(self):
+        self._check(self.lib.vs_wait(self.h))
+
+    def results(self, slot=0) -> Results:
+        s = np.empty(self._n, np.float32)
+        p = np.empty(self._n, np.int32)
+        a = np.empty(max(1, self.n_sweeps * self._nR), np.uint8)
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(s), _ptr(p), _ptr(a), 0))
+        return Results(s, p, a[: self.n_sweeps * self._nR])
+
+    def results_device(self, slot, best_score, best_pose, angles=None):
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(best_score), _ptr(best_pose), _ptr(angles), 1))
+
+    def coords(self, slot=0) -> np.ndarray:
+        out = np.empty((max(1, self._nA), 3), np.float32)
+        self._check(self.lib.vs_get_coords(self.h, slot, _ptr(out), 0))
+        return out[: self._nA]
+
+    def pose_debug(self, slot=0):
+        s = np.empty((self._n, self.P), np.float32)
+        a = np.empty(max(1, self.P * self.n_sweeps * self._nR), np.uint8)
+        self._check(self.lib.vs_get_pose_debug(self.h, slot, _ptr(s), _ptr(a)))
+        return s, a[: self.P * self.n_sweeps * self._nR]
+
+    def local_topk(self, slot, k):
+        """Device tensor [k] of uint64 keys (as int64) and the number of valid entries."""
+        t = self._torch.empty(k, dtype=self._torch.int64, device=f"cuda:{self.device}")
+        nv = ctypes.c_int32()
+        self._check(self.lib.vs_local_topk(self.h, slot, k, _ptr(t), ctypes.byref(nv)))
+        return t, nv.value
+
+    def merge_topk(self, keys_dev, k):
+        idx = np.empty(k, np.int64)
+        sc = np.empty(k, np.float32)
+        m = ctypes.c_int32()
+        self._check(self.lib.vs_merge_topk(self.h, _ptr(keys_dev), int(keys_dev.numel()), k, _ptr(idx), _ptr(sc),
+                                           ctypes.byref(m)))
+        return idx[: m.value], sc[: m.value]
+
+    def manifest(self, want_perm=True):
+        nb = ctypes.c_int32()
+        self._check(self.lib.vs_get_manifest(self.h, 0, None, ctypes.byref(nb), None))
+        arr = (vs_bucket * max(1, nb.value))()
+        perm = np.empty(max(1, self._n), np.uint32) if want_perm else None
+        self._check(self.lib.vs_get_manifest(self.h, nb.value, arr, ctypes.byref(nb), _ptr(perm)))
+        keys = [f[0] for f in vs_bucket._fields_]
+        buckets = [{k: getattr(arr[i], k) for k in keys} for i in range(nb.value)]
+        return buckets, (perm[: self._n] if want_perm else None)
+
+    def classes(self):
+        n = ctypes.c_int32()
+        self._check(self.lib.vs_query_classes(self.h, 0, None, ctypes.byref(n)))
+        arr = (vs_class_info * max(1, n.value))()
+        self._check(self.lib.vs_query_classes(self.h, n.value, arr, ctypes.byref(n)))
+        keys = [f[0] for f in vs_class_info._fields_]
+        return [{k: getattr(arr[i], k) for k in keys} for i in range(n.value)]
+
+    def stats(self):
+        s = vs_stats()
+        self._check(self.lib.vs_get_stats(self.h, ctypes.byref(s)))
+        return {f[0]: getattr(s, f[0]) for f in vs_stats._fields_}
+
+    def score_points(self, pocket_id, pts):
+        pts = np.ascontiguousarray(pts, np.float32).reshape(-1, 3)
+        out = np.empty(pts.shape[0], np.float32)
+        self._check(self.lib.vs_score_points(self.h, pocket_id, pts.shape[0], _ptr(pts), _ptr(out)))
+        return out
