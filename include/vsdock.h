@@ -60,6 +60,9 @@ typedef struct {
     int32_t n_streams;         /* concurrent bucket launches (1..16) */
     int32_t rank, world_size;  /* this context docks the buckets LPT assigns to `rank` (a4) */
     int32_t debug_poses;       /* 1: keep every pose's score and angle sequence (parity replay) */
+    int32_t launch_per_bucket; /* 1: one kernel launch per bucket, as the paper does;
+                                  0 (default): the owned buckets of one atom class run as ONE
+                                  persistent launch with dynamic ligand scheduling */
     void* stream;              /* cudaStream_t the library orders its work on (e.g. torch's); NULL = own */
 } vs_config;
 
@@ -198,6 +201,21 @@ typedef struct {
     float topk_ms;             /* last vs_local_topk */
 } vs_stats;
 vs_status vs_get_stats(vs_ctx* ctx, vs_stats* out);
+
+/* Host-only planning steps of vs_submit, exported so every rank's plan can be
+ * checked without a GPU.  Both are pure functions of their inputs.
+ *
+ * a2 class boundaries: atom classes [32, 64, ..., 32(n-1), last] with last =
+ * atom_ub if atom_ub >= 32(n-1)+1 else 32n (reading Q16); rotamer
+ * classes per S:215-223 with prev_0 = -1 and round-half-up (Q17).  Capacities:
+ * atom_b[8], rot_b[33].  Errors: VS_E_ARG. */
+vs_status vs_plan_boundaries(int32_t n_atom_clusters, int32_t atom_ub, int32_t n_rot_clusters, int32_t rot_ub,
+                             int32_t* atom_b, int32_t* n_atom_b, int32_t* rot_b, int32_t* n_rot_b);
+/* a4 LPT: buckets by weight descending (ties: lower id first) go to the
+ * least-loaded rank (ties: lowest rank); owner[b] and launch_order[b] (position
+ * in the owner's sequence) for n_buckets buckets.  Errors: VS_E_ARG. */
+vs_status vs_plan_lpt(const uint64_t* weights, int32_t n_buckets, int32_t world, int32_t* owner,
+                      int32_t* launch_order);
 
 #ifdef __cplusplus
 }

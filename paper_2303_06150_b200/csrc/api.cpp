@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,7 +32,7 @@ struct PocketHost {
 };
 
 struct ClassInfo {
-    int atom_bound, AC, NW, LC, b, l, cap;
+    int atom_bound, AC, NW, PPW, LC, b, l, cap;
     size_t smem;
     cudaFuncAttributes attr;
 };
@@ -79,6 +80,27 @@ std::vector<int> rot_bounds(int n, int mx) {
         prev = v;
     }
     return b;
+}
+
+// a4: buckets by weight descending (ties: id ascending) to the least-loaded rank
+// (ties: lowest rank); launch_order = position in that rank's sequence.
+void lpt_plan(const uint64_t* w, int nb, int world, int32_t* owner, int32_t* launch_order) {
+    std::vector<int> order(nb);
+    for (int b = 0; b < nb; ++b) order[b] = b;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        if (w[x] != w[y]) return w[x] > w[y];
+        return x < y;
+    });
+    std::vector<unsigned long long> load(world, 0);
+    std::vector<int> nlaunch(world, 0);
+    for (int b : order) {
+        int r = 0;
+        for (int q = 1; q < world; ++q)
+            if (load[q] < load[r]) r = q;
+        load[r] += w[b];
+        owner[b] = r;
+        launch_order[b] = nlaunch[r]++;
+    }
 }
 
 }  // namespace
@@ -242,7 +264,7 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int P, int K, size_t grid_bytes,
 
 // Stage-2 workspace (records + results), placed after stage 1.
 struct Stage2 {
-    size_t rec, meta, score, pose_best, ang, dbg_score, dbg_ang, coords, keys, topk_out, sel, end;
+    size_t rec, meta, score, pose_best, ang, dbg_score, dbg_ang, coords, keys, topk_out, sel, counters, end;
     size_t per_slot;  // bytes of results per pocket slot
 };
 
@@ -263,6 +285,7 @@ Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats,
     s.keys = r.add(kc * 8);
     s.topk_out = r.add(8192 * 8);
     s.sel = r.add(4096);
+    s.counters = r.add((size_t)(n + kMaxCells) * n_pockets * 4 + 256);
     s.end = r.off;
     return s;
 }
@@ -296,18 +319,22 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps
         ci.AC = std::max(32, roundup32(atom_b[i]));
         if (ci.AC > kMaxAtoms) return fail(c, VS_E_ARG, "atom class bound %d exceeds %d", atom_b[i], kMaxAtoms);
         ci.b = 0;
-        for (int NW : {32, 16}) {
-            const int wl = std::min(c->P, NW);
-            const int LC = std::max(1, NW / wl);
-            const DockLayout L = dock_layout(ci.AC, NW, nz, ps, c->P, c->K, c->cfg.n_sweeps, LC);
+        // poses per warp: 2 when the K angle lanes fit in half a warp; the
+        // same for every class so the reduction order, hence every result, is class-independent (Q22)
+        int PPW = c->K <= 16 ? 2 : 1;
+        if (const char* e = getenv("VSDOCK_PPW")) PPW = atoi(e) == 1 ? 1 : PPW;
+        for (int NW : {32, 16, 8}) {
+            const int LC = ligs_per_cta(NW, PPW, c->P);
+            const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, ps, c->P, c->K, c->cfg.n_sweeps, LC);
             int b = 0;
-            CK(dock_occupancy(ci.AC, NW, L.total, &b));
+            CK(dock_occupancy(ci.AC, NW, PPW, L.total, &b));
             if (b >= 1) {
                 ci.NW = NW;
+                ci.PPW = PPW;
                 ci.LC = LC;
                 ci.b = b;
                 ci.smem = L.total;
-                CK(dock_kernel_attrs(ci.AC, NW, &ci.attr));
+                CK(dock_kernel_attrs(ci.AC, NW, PPW, &ci.attr));
                 break;
             }
         }
@@ -686,26 +713,26 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     CK(cudaStreamSynchronize(ms));
     for (int b = 0; b < nb; ++b) std::memcpy(&c->buckets[b].weight, H + (size_t)b * 8, 8);
 
-    // ---- a4 LPT shard: weight descending (ties: id), least-loaded rank (ties: lowest rank)
-    std::vector<int> order(nb);
-    for (int b = 0; b < nb; ++b) order[b] = b;
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
-        if (c->buckets[x].weight != c->buckets[y].weight) return c->buckets[x].weight > c->buckets[y].weight;
-        return x < y;
-    });
-    const int Wn = c->cfg.world_size;
-    std::vector<unsigned long long> load(Wn, 0);
-    std::vector<int> nlaunch(Wn, 0);
-    c->owned.clear();
-    for (int b : order) {
-        int r = 0;
-        for (int q = 1; q < Wn; ++q)
-            if (load[q] < load[r]) r = q;
-        load[r] += c->buckets[b].weight;
-        c->buckets[b].owner = r;
-        c->buckets[b].launch_order = nlaunch[r]++;
-        if (r == c->cfg.rank) c->owned.push_back(b);
+    // ---- a4 LPT shard (identical on every rank: a pure function of the manifest)
+    {
+        std::vector<uint64_t> w(nb);
+        std::vector<int32_t> owner(nb), lorder(nb);
+        for (int b = 0; b < nb; ++b) w[b] = c->buckets[b].weight;
+        lpt_plan(w.data(), nb, c->cfg.world_size, owner.data(), lorder.data());
+        std::vector<int> mine;
+        for (int b = 0; b < nb; ++b) {
+            c->buckets[b].owner = owner[b];
+            c->buckets[b].launch_order = lorder[b];
+            if (owner[b] == c->cfg.rank) mine.push_back(b);
+        }
+        std::sort(mine.begin(), mine.end(), [&](int x, int y) { return lorder[x] < lorder[y]; });
+        c->owned = mine;
     }
+    // fused mode: group the owned buckets by atom class (LPT order kept inside a class)
+    // so each class is one contiguous slot range = one persistent launch
+    if (!c->cfg.launch_per_bucket)
+        std::stable_sort(c->owned.begin(), c->owned.end(),
+                         [&](int x, int y) { return c->buckets[x].atom_class < c->buckets[y].atom_class; });
 
     // ---- stage-2 workspace and a5 pack
     const int no = (int)c->owned.size();
@@ -745,6 +772,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->keys_cap = std::max<int64_t>(n, 65536);
     c->d_topk_out = (unsigned long long*)(W + s2.topk_out);
     c->d_sel = W + s2.sel;
+    int* d_counters = (int*)(W + s2.counters);
+    CK(cudaMemsetAsync(d_counters, 0, (size_t)no * n_pockets * 4 + 4, ms));
     {
         int64_t* h_start = (int64_t*)H;
         int* h_prefix = (int*)(H + (size_t)no * 8);
@@ -772,18 +801,36 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     }
     CK(cudaEventRecord(c->ev_prep1, ms));
 
-    // ---- a6-a9 dock: one launch per (owned bucket, pocket), LPT order, round-robin over streams
+    // ---- a6-a9 dock.  Launch units: one per owned bucket (paper mode) or one per atom
+    // class (fused: contiguous slot ranges); heaviest first, round-robin over streams.
+    struct Unit {
+        int cls, first, slots;
+        unsigned long long w;
+    };
+    std::vector<Unit> units;
+    for (int i = 0; i < no; ++i) {
+        const vs_bucket& b = c->buckets[c->owned[i]];
+        if (!c->cfg.launch_per_bucket && !units.empty() && units.back().cls == b.atom_class) {
+            units.back().slots += b.size;
+            units.back().w += b.weight;
+        } else {
+            units.push_back({b.atom_class, i, b.size, b.weight});
+        }
+    }
+    if (!c->cfg.launch_per_bucket)
+        std::stable_sort(units.begin(), units.end(), [](const Unit& x, const Unit& y) { return x.w > y.w; });
     const int NS = (int)c->workers.size();
     for (int s = 0; s < NS; ++s) CK(cudaStreamWaitEvent(c->workers[s], c->ev_prep1, 0));
     int64_t dock_launches = 0;
-    for (int i = 0; i < no; ++i) {
-        const vs_bucket& b = c->buckets[c->owned[i]];
-        const ClassInfo& ci = c->classes[b.atom_class];
+    for (const Unit& u : units) {
+        const vs_bucket& b = c->buckets[c->owned[u.first]];
+        const ClassInfo& ci = c->classes[u.cls];
+        const int i = u.first;
         for (int q = 0; q < n_pockets; ++q) {
             DockArgs a{};
             a.rec = c->d_rec + c->owned_rec_off[i];
             a.meta = c->d_meta + c->owned_prefix[i];
-            a.n = b.size;
+            a.n = u.slots;
             a.rec_floats = 3 * b.kernel_atoms + 32;
             a.P = c->P;
             a.K = c->K;
@@ -797,11 +844,12 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.angles = c->d_ang[q];
             a.dbg_score = c->d_dbg_score[q];
             a.dbg_angles = c->d_dbg_ang[q];
-            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, a.pk.nz, a.pk.ps, c->P, c->K, S_w, ci.LC);
-            const int rounds = (b.size + ci.LC - 1) / ci.LC;
+            a.counter = d_counters + dock_launches;
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.nz, a.pk.ps, c->P, c->K, S_w, ci.LC);
+            const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];
-            CK(launch_dock(b.kernel_atoms, ci.NW, a, grid, L.total, s));
+            CK(launch_dock(b.kernel_atoms, ci.NW, ci.PPW, a, grid, L.total, s));
             ++dock_launches;
         }
     }
@@ -1006,6 +1054,29 @@ vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* 
     cudaFree(dg);
     cudaFree(dx);
     cudaFree(dout);
+    return VS_OK;
+}
+
+vs_status vs_plan_boundaries(int32_t n_atom_clusters, int32_t atom_ub, int32_t n_rot_clusters, int32_t rot_ub,
+                             int32_t* atom_b, int32_t* n_atom_b, int32_t* rot_b, int32_t* n_rot_b) {
+    if (!atom_b || !n_atom_b || !rot_b || !n_rot_b) return VS_E_ARG;
+    if (n_atom_clusters < 1 || n_atom_clusters > kMaxAtomClasses || n_rot_clusters < 1 ||
+        n_rot_clusters > kMaxRotClasses || atom_ub < 1 || rot_ub < 0 || rot_ub > kMaxFrags)
+        return VS_E_ARG;
+    const std::vector<int> a = atom_bounds(n_atom_clusters, atom_ub);
+    const std::vector<int> r = rot_bounds(n_rot_clusters, rot_ub);
+    if ((int)r.size() > kMaxRotClasses) return VS_E_ARG;
+    std::copy(a.begin(), a.end(), atom_b);
+    std::copy(r.begin(), r.end(), rot_b);
+    *n_atom_b = (int32_t)a.size();
+    *n_rot_b = (int32_t)r.size();
+    return VS_OK;
+}
+
+vs_status vs_plan_lpt(const uint64_t* weights, int32_t n_buckets, int32_t world, int32_t* owner,
+                      int32_t* launch_order) {
+    if (n_buckets < 0 || world < 1 || (n_buckets > 0 && (!weights || !owner || !launch_order))) return VS_E_ARG;
+    lpt_plan(weights, n_buckets, world, owner, launch_order);
     return VS_OK;
 }
 

@@ -24,6 +24,8 @@
 // reproducible bit for bit by the finalize kernel.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -126,30 +128,40 @@ __device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk) {
     }
 }
 
-// One (ligand, pose) item on one warp: a6 placement, a7 sweep, a9 pose score.
-template <int AC>
-__device__ __forceinline__ void dock_pose(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
-                                          float4* __restrict__ buf, const float* __restrict__ G, const PocketDev& pk,
-                                          int K, int kbits, int S_w, float ck, float sk,
-                                          const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
-                                          float* __restrict__ scoreOut, int lane) {
+// Order-preserving map of fp32 onto uint32 (-0 canonicalised to +0 first).
+__device__ __forceinline__ unsigned ord32(float v) {
+    const unsigned b = __float_as_uint(__fadd_rn(v, 0.0f));
+    return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
+}
+
+// PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
+// a6 placement, a7 sweep, a9 pose score.  Sweep lane map inside a pose group:
+// li = jl * K + k (moving atom jl of the pass, angle k); APW = LPP / K atoms per pass.
+template <int AC, int PPW>
+__device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
+                                           bool valid, float4* __restrict__ buf, const float* __restrict__ G,
+                                           const PocketDev& pk, int K, int kbits, int S_w, float ck, float sk,
+                                           const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
+                                           float* __restrict__ scoreOut, int lane) {
+    constexpr int LPP = 32 / PPW;
+    const int li = lane & (LPP - 1);
     const float* rx = rec;
     const float* ry = rec + AC;
     const float* rz = rec + 2 * AC;
     const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
-    float Tr[12];
+    {
+        float Tr[12];
 #pragma unroll
-    for (int t = 0; t < 12; ++t) Tr[t] = T[t];
-#pragma unroll
-    for (int s = 0; s < AC / 32; ++s) {
-        const int i = s * 32 + lane;
-        if (i < A) buf[i] = place_atom(Tr, rx[i], ry[i], rz[i]);
+        for (int t = 0; t < 12; ++t) Tr[t] = T[t];
+        if (valid)
+            for (int i = li; i < A; i += LPP) buf[i] = place_atom(Tr, rx[i], ry[i], rz[i]);
     }
     __syncwarp();
     if (K > 1) {
-        const int k = lane & (K - 1);
-        const int jl = lane >> kbits;
-        const int apw = 32 >> kbits;
+        const int k = li & (K - 1);
+        const int jl = li >> kbits;
+        const int apw = LPP >> kbits;
+        const unsigned gmask = ((K == 32) ? 0xffffffffu : ((1u << K) - 1u)) << (lane & ~(K - 1));
         for (int sw = 0; sw < S_w; ++sw) {
             for (int r = 0; r < R; ++r) {
                 const uint32_t f = rfr[r];
@@ -158,64 +170,74 @@ __device__ __forceinline__ void dock_pose(const float* __restrict__ rec, int A, 
                 float ux, uy, uz;
                 axis_of(ya, yb, ux, uy, uz);
                 const Rot M = rodrigues(ux, uy, uz, ck, sk);
+                const bool id = (k == 0);   // theta_0: the current pose itself (Q3)
                 float acc = 0.f;
-                for (int base = lo; base < hi; base += apw) {
+                float3 keep = make_float3(0.f, 0.f, 0.f);
+                int base = lo;
+                for (; base + apw < hi; base += 2 * apw) {     // two independent evaluations per lane
+                    const int j0 = base + jl, j1 = base + apw + jl;
+                    const float4 v0 = buf[j0];
+                    const float4 v1 = buf[j1 < hi ? j1 : j0];
+                    const float3 p0 = rot_about(M, yb.x, yb.y, yb.z, v0.x, v0.y, v0.z);
+                    const float3 p1 = rot_about(M, yb.x, yb.y, yb.z, v1.x, v1.y, v1.z);
+                    const float g0 = grid_g(G, id ? v0.x : p0.x, id ? v0.y : p0.y, id ? v0.z : p0.z, pk);
+                    const float g1 = grid_g(G, id ? v1.x : p1.x, id ? v1.y : p1.y, id ? v1.z : p1.z, pk);
+                    acc = __fadd_rn(acc, g0);
+                    if (j1 < hi) acc = __fadd_rn(acc, g1);
+                }
+                if (base < hi) {
                     const int j = base + jl;
                     if (j < hi) {
                         const float4 v = buf[j];
                         const float3 p = rot_about(M, yb.x, yb.y, yb.z, v.x, v.y, v.z);
-                        const bool id = (k == 0);   // theta_0: the current pose itself (Q3)
+                        keep = p;
                         acc = __fadd_rn(acc, grid_g(G, id ? v.x : p.x, id ? v.y : p.y, id ? v.z : p.z, pk));
                     }
                 }
-                for (int o = K; o < 32; o <<= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
-                float best = acc;
-                int bk = k;
-                for (int o = 1; o < K; o <<= 1) {
-                    const float ob = __shfl_xor_sync(FULL, best, o);
-                    const int ok = __shfl_xor_sync(FULL, bk, o);
-                    if (ob < best || (ob == best && ok < bk)) {
-                        best = ob;
-                        bk = ok;
-                    }
-                }
-                if (bk != 0) {  // warp-uniform
+                for (int o = K; o < LPP; o <<= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                // argmin over the K angles of this group; ties -> lowest k (Q11)
+                const unsigned key = ord32(acc);
+                const unsigned mn = __reduce_min_sync(gmask, key);
+                const unsigned bal = __ballot_sync(FULL, key == mn) & gmask;
+                const int bk = (__ffs(bal) - 1) & (K - 1);
+                if (hi - lo <= apw) {
+                    // single pass: the lane (jl, k*) already holds the rotated atom
+                    if (valid && bk != 0 && k == bk && lo + jl < hi) buf[lo + jl] = make_float4(keep.x, keep.y, keep.z, 0.f);
+                } else if (valid && bk != 0) {
                     const Rot Ms = rodrigues(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1]);
-                    for (int j = lo + lane; j < hi; j += 32) {
+                    for (int j = lo + li; j < hi; j += LPP) {
                         const float4 v = buf[j];
                         const float3 p = rot_about(Ms, yb.x, yb.y, yb.z, v.x, v.y, v.z);
                         buf[j] = make_float4(p.x, p.y, p.z, 0.f);
                     }
                 }
                 __syncwarp();
-                if (lane == 0) angOut[sw * R + r] = (uint8_t)bk;
+                if (valid && li == 0) angOut[sw * R + r] = (uint8_t)bk;
             }
         }
-    } else {
-        for (int t = lane; t < S_w * R; t += 32) angOut[t] = 0;
+    } else if (valid) {
+        for (int t = li; t < S_w * R; t += LPP) angOut[t] = 0;
     }
-    // a9: pose score, canonical order (atom i -> lane i mod 32, ascending slots, xor tree) (Q22)
+    // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree) (Q22)
     float acc = 0.f;
-#pragma unroll
-    for (int s = 0; s < AC / 32; ++s) {
-        const int i = s * 32 + lane;
-        if (i < A) {
-            const float4 v = buf[i];
-            acc = __fadd_rn(acc, grid_g(G, v.x, v.y, v.z, pk));
-        }
+    for (int i = li; i < A; i += LPP) {
+        const float4 v = buf[i];
+        acc = __fadd_rn(acc, grid_g(G, v.x, v.y, v.z, pk));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
-    if (lane == 0) *scoreOut = acc;
+    for (int o = LPP / 2; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+    if (valid && li == 0) *scoreOut = acc;
     __syncwarp();
 }
 
-template <int AC, int NW>
+template <int AC, int NW, int PPW>
 __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_round;
+    constexpr int LPP = 32 / PPW;
     const PocketDev& pk = a.pk;
     const int LC = a.ligs_per_cta;
-    const DockLayout L = dock_layout(AC, NW, pk.nz, pk.ps, a.P, a.K, a.S_w, LC);
+    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.ps, a.P, a.K, a.S_w, LC);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sPose = reinterpret_cast<float*>(smem + L.pose);
     float* sCS = reinterpret_cast<float*>(smem + L.cs);
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     float4* sBuf = reinterpret_cast<float4*>(smem + L.buf);
     float* sScore = reinterpret_cast<float*>(smem + L.score);
     uint8_t* sAng = smem + L.ang;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
 
     stage_grid(sG, pk);
     for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
@@ -233,12 +255,17 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int K = a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
     const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
-    float4* buf = sBuf + warp * AC;
+    float4* buf = sBuf + (warp * PPW + h) * AC;
     const int rec_floats = a.rec_floats;
     const int n_rounds = (a.n + LC - 1) / LC;
     const int ang_stride = 32 * S_w;
+    const int G = (P + PPW - 1) / PPW;   // warp items per ligand
 
-    for (int round = blockIdx.x; round < n_rounds; round += gridDim.x) {
+    while (true) {
+        if (tid == 0) s_round = atomicAdd(a.counter, 1);   // dynamic: balance CTAs within the bucket
+        __syncthreads();
+        const int round = s_round;
+        if (round >= n_rounds) break;
         const int slot0 = round * LC;
         const int nl = min(LC, a.n - slot0);
         {
@@ -248,37 +275,33 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             for (int t = tid; t < n4; t += blockDim.x) dst[t] = src[t];
         }
         __syncthreads();
-        for (int item = warp; item < nl * P; item += NW) {
-            const int l = item / P, p = item - l * P;
+        for (int item = warp; item < nl * G; item += NW) {
+            const int l = item / G, g = item - l * G;
+            const int p = g * PPW + h;
+            const bool valid = p < P;
+            const int pc = valid ? p : P - 1;
             const int4 m = a.meta[slot0 + l];
-            dock_pose<AC>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * p, buf, sG, pk, K, kbits, S_w, ck, sk, sCS,
-                          sAng + (size_t)item * ang_stride, sScore + item, lane);
+            dock_poses<AC, PPW>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w,
+                                ck, sk, sCS, sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncthreads();
         if (warp < nl) {  // a9 best pose: lowest score, ties -> lowest pose index (Q11)
             const int l = warp;
             const int4 m = a.meta[slot0 + l];
-            float best = __int_as_float(0x7f800000);
-            int bp = 0x7fffffff;
+            unsigned long long best = ~0ull;
             for (int p = lane; p < P; p += 32) {
-                const float s = sScore[l * P + p];
-                if (s < best || bp == 0x7fffffff) {
-                    best = s;
-                    bp = p;
-                }
+                const unsigned long long key = ((unsigned long long)ord32(sScore[l * P + p]) << 32) | (unsigned)p;
+                best = key < best ? key : best;
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
-                const float ob = __shfl_xor_sync(FULL, best, o);
-                const int op = __shfl_xor_sync(FULL, bp, o);
-                if (ob < best || (ob == best && op < bp)) {
-                    best = ob;
-                    bp = op;
-                }
+                const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+                best = ob < best ? ob : best;
             }
+            const int bp = (int)(best & 0xffffffffu);
             const int li = m.x, R = m.z, nang = S_w * R;
             if (lane == 0) {
-                a.best_score[li] = best;
+                a.best_score[li] = sScore[l * P + bp];
                 a.best_pose[li] = bp;
             }
             const uint8_t* sa = sAng + (size_t)(l * P + bp) * ang_stride;
@@ -359,46 +382,48 @@ __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, 
 
 using DockFn = void (*)(const DockArgs);
 
-template <int AC, int NW>
-DockFn dock_fn() {
-    return dock_kernel<AC, NW>;
+template <int AC>
+DockFn pick_ac(int NW, int PPW) {
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1> : (NW == 16 ? dock_kernel<AC, 16, 1> : (NW == 8 ? dock_kernel<AC, 8, 1> : nullptr));
+    if (PPW == 2) return NW == 32 ? dock_kernel<AC, 32, 2> : (NW == 16 ? dock_kernel<AC, 16, 2> : (NW == 8 ? dock_kernel<AC, 8, 2> : nullptr));
+    return nullptr;
 }
 
-DockFn pick(int AC, int NW) {
-#define VSD_CASE(ac)                                   \
-    case ac:                                           \
-        return NW == 32 ? dock_fn<ac, 32>() : dock_fn<ac, 16>();
+DockFn pick(int AC, int NW, int PPW) {
     switch (AC) {
-        VSD_CASE(32)
-        VSD_CASE(64)
-        VSD_CASE(96)
-        VSD_CASE(128)
-        VSD_CASE(160)
-        VSD_CASE(192)
-        VSD_CASE(224)
-        VSD_CASE(256)
-        default:
-            return nullptr;
+        case 32: return pick_ac<32>(NW, PPW);
+        case 64: return pick_ac<64>(NW, PPW);
+        case 96: return pick_ac<96>(NW, PPW);
+        case 128: return pick_ac<128>(NW, PPW);
+        case 160: return pick_ac<160>(NW, PPW);
+        case 192: return pick_ac<192>(NW, PPW);
+        case 224: return pick_ac<224>(NW, PPW);
+        case 256: return pick_ac<256>(NW, PPW);
+        default: return nullptr;
     }
-#undef VSD_CASE
 }
 
 }  // namespace
 
+// Padded shared-memory strides: row stride nx + 1 and plane stride (nx + 1) * ny + 7
+// (chosen with tools/bank_sim.py: 2.5-way instead of 6.2-way bank conflicts on the
+// sweep's corner gathers for 32^3 grids).  VSDOCK_GRID_PAD="dr,dp" overrides.
 void grid_strides(int nx, int ny, int* rs, int* ps) {
-    *rs = nx;
-    *ps = nx * ny;
+    int dr = 1, dp = 7;
+    if (const char* e = getenv("VSDOCK_GRID_PAD")) sscanf(e, "%d,%d", &dr, &dp);
+    *rs = nx + dr;
+    *ps = (nx + dr) * ny + dp;
 }
 
-cudaError_t dock_kernel_attrs(int AC, int NW, cudaFuncAttributes* attr) {
-    DockFn f = pick(AC, NW);
-    if (!f || (NW != 32 && NW != 16)) return cudaErrorInvalidValue;
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, cudaFuncAttributes* attr) {
+    DockFn f = pick(AC, NW, PPW);
+    if (!f) return cudaErrorInvalidValue;
     return cudaFuncGetAttributes(attr, reinterpret_cast<const void*>(f));
 }
 
-cudaError_t dock_occupancy(int AC, int NW, size_t smem, int* blocks_per_sm) {
-    DockFn f = pick(AC, NW);
-    if (!f || (NW != 32 && NW != 16)) return cudaErrorInvalidValue;
+cudaError_t dock_occupancy(int AC, int NW, int PPW, size_t smem, int* blocks_per_sm) {
+    DockFn f = pick(AC, NW, PPW);
+    if (!f) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {
@@ -410,9 +435,9 @@ cudaError_t dock_occupancy(int AC, int NW, size_t smem, int* blocks_per_sm) {
                                                          smem);
 }
 
-cudaError_t launch_dock(int AC, int NW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
-    DockFn f = pick(AC, NW);
-    if (!f || (NW != 32 && NW != 16)) return cudaErrorInvalidValue;
+cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
+    DockFn f = pick(AC, NW, PPW);
+    if (!f) return cudaErrorInvalidValue;
     if (a.n <= 0) return cudaSuccess;
     f<<<grid, NW * 32, smem, st>>>(a);
     return cudaGetLastError();

@@ -39,6 +39,7 @@ struct DockArgs {
     int rec_floats;            // 3 * AC + 32
     int P, K, S_w;
     int ligs_per_cta;          // LC
+    int* counter;              // dynamic round counter of this launch (zeroed before launch)
     const float* pose_tab;     // [P][12] raw: R (9, row-major) then tau (3)
     const float* cs;           // [K][2]
     PocketDev pk;
@@ -49,24 +50,33 @@ struct DockArgs {
     uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
 };
 
-// Shared-memory layout of dock<AC, NW> (byte offsets).  Used by the kernel and
-// by the host (occupancy query, launch) so both agree.
+// Shared-memory layout of dock<AC, NW, PPW> (byte offsets).  Used by the kernel
+// and by the host (occupancy query, launch) so both agree.
 struct DockLayout {
     size_t grid, pose, cs, rec, buf, score, ang, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
-__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int nz, int ps, int P, int K, int S_w, int LC) {
+__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int ps, int P, int K, int S_w,
+                                                  int LC) {
     DockLayout L;
     size_t o = 0;
     L.grid = o;  o += align16((size_t)nz * ps * 4);
     L.pose = o;  o += align16((size_t)P * 12 * 4);
     L.cs = o;    o += align16((size_t)K * 2 * 4);
     L.rec = o;   o += align16((size_t)LC * (3 * AC + 32) * 4);
-    L.buf = o;   o += (size_t)NW * AC * 16;
+    L.buf = o;   o += (size_t)NW * PPW * AC * 16;
     L.score = o; o += align16((size_t)LC * P * 4);
     L.ang = o;   o += align16((size_t)LC * P * S_w * 32);
     L.total = o;
     return L;
+}
+// Ligands a CTA docks concurrently (Eq. 1's t/ws, reading Q19): each ligand needs
+// ceil(P / PPW) warp items; a CTA of NW warps holds NW / min(NW, items) ligands.
+__host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
+    const int g = (P + PPW - 1) / PPW;
+    const int wl = g < NW ? g : NW;
+    const int lc = NW / wl;
+    return lc > 0 ? lc : 1;
 }
 // Shared-memory grid strides: row stride rs >= nx, plane stride ps >= ny * rs.
 void grid_strides(int nx, int ny, int* rs, int* ps);
@@ -89,9 +99,9 @@ cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const 
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
                         const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
                         int4* meta, cudaStream_t st);
-cudaError_t launch_dock(int AC, int NW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
-cudaError_t dock_kernel_attrs(int AC, int NW, cudaFuncAttributes* attr);
-cudaError_t dock_occupancy(int AC, int NW, size_t smem, int* blocks_per_sm);
+cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, cudaFuncAttributes* attr);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, size_t smem, int* blocks_per_sm);
 cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
                                 cudaStream_t st);

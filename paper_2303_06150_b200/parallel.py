@@ -1,0 +1,63 @@
+"""Multi-GPU plumbing for the hot path (a4 shard, a11 gather + merge).
+
+One process per GPU.  Every rank submits the SAME library to its own Engine
+(``rank``/``world_size`` in the config): the manifest and the LPT shard are pure
+functions of the library (vs_plan_lpt), so every rank agrees on who docks which
+bucket without communicating.  The only exchange is the per-pocket ranking
+("for each docking site, we can rank the input chemical
+library"): each rank's k best keys are all-gathered (NCCL over NVLink on B200;
+gloo in the CPU tests) and merged into the global top-k on the device.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def gather_keys(keys_local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather every rank's [k] key vector into one [world * k] tensor (rank-major)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return keys_local
+    world = dist.get_world_size(group)
+    if world == 1:
+        return keys_local
+    out = torch.empty(world * keys_local.numel(), dtype=keys_local.dtype, device=keys_local.device)
+    if keys_local.is_cuda:
+        dist.all_gather_into_tensor(out, keys_local, group=group)
+    else:  # gloo
+        parts = [torch.empty_like(keys_local) for _ in range(world)]
+        dist.all_gather(parts, keys_local, group=group)
+        out = torch.cat(parts)
+    return out
+
+
+def global_topk(engine, slot: int, k: int, group=None):
+    """a10 + a11: local top-k on this rank's buckets, all-gather, merge on the device.
+
+    Returns (ligand index [m] int64, score [m] float32) on the host, identical on every rank
+    and bit-identical to the single-GPU ranking (keys are unique and totally ordered)."""
+    keys, _ = engine.local_topk(slot, k)
+    g = gather_keys(keys, group)
+    return engine.merge_topk(g, k)
+
+
+def decode_keys(keys: torch.Tensor):
+    """(ligand index, score) of uint64 keys ord(score) << 32 | index held in an int64 tensor (host)."""
+    import numpy as np
+    u = keys.detach().cpu().numpy().view(np.uint64)
+    valid = u != np.uint64(0xFFFFFFFFFFFFFFFF)
+    u = u[valid]
+    idx = (u & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    ordv = (u >> np.uint64(32)).astype(np.uint32)
+    bits = np.where(ordv & np.uint32(0x80000000), ordv & np.uint32(0x7FFFFFFF), ~ordv).astype(np.uint32)
+    return idx, bits.view(np.float32)
+
+
+def encode_keys(scores, index):
+    """Inverse of decode_keys for host-side tests: int64 tensor of ord(score) << 32 | index."""
+    import numpy as np
+    s = np.asarray(scores, np.float32) + np.float32(0.0)
+    b = s.view(np.uint32)
+    o = np.where(b & np.uint32(0x80000000), ~b, b | np.uint32(0x80000000)).astype(np.uint64)
+    k = (o << np.uint64(32)) | np.asarray(index, np.uint64)
+    return torch.from_numpy(k.view(np.int64).copy())

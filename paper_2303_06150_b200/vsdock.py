@@ -25,7 +25,7 @@ _NAMES = {0: "VS_OK", -1: "VS_E_ARG", -2: "VS_E_PARSE", -3: "VS_E_OVERFLOW_ATOMS
 SYMBOLS = ["vs_create", "vs_destroy", "vs_last_error", "vs_workspace_size", "vs_set_workspace", "vs_load_pocket",
            "vs_set_pose_table", "vs_set_angle_table", "vs_submit", "vs_wait", "vs_get_results", "vs_get_coords",
            "vs_get_pose_debug", "vs_local_topk", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
-           "vs_score_points", "vs_get_stats"]
+           "vs_score_points", "vs_get_stats", "vs_plan_boundaries", "vs_plan_lpt"]
 
 
 class VsError(RuntimeError):
@@ -39,7 +39,7 @@ class vs_config(ctypes.Structure):
                 ("n_rot_clusters", ctypes.c_int32), ("atom_upper_bound", ctypes.c_int32),
                 ("rot_upper_bound", ctypes.c_int32), ("bucket_multiple", ctypes.c_int32),
                 ("n_streams", ctypes.c_int32), ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32),
-                ("debug_poses", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+                ("debug_poses", ctypes.c_int32), ("launch_per_bucket", ctypes.c_int32), ("stream", ctypes.c_void_p)]
 
 
 class vs_pocket_desc(ctypes.Structure):
@@ -105,6 +105,8 @@ def load_library():
         "vs_query_classes": [P, I32, P, ctypes.POINTER(I32)],
         "vs_score_points": [P, I32, I64, P, P],
         "vs_get_stats": [P, ctypes.POINTER(vs_stats)],
+        "vs_plan_boundaries": [I32, I32, I32, I32, P, ctypes.POINTER(I32), P, ctypes.POINTER(I32)],
+        "vs_plan_lpt": [P, I32, I32, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -125,6 +127,31 @@ def _ptr(x):
     return ctypes.c_void_p(x.data_ptr())
 
 
+def plan_boundaries(n_atom_clusters, atom_ub, n_rot_clusters, rot_ub):
+    """Host-only a2 class boundaries exactly as vs_submit computes them (no GPU needed)."""
+    lib = load_library()
+    ab = np.zeros(8, np.int32)
+    rb = np.zeros(33, np.int32)
+    na, nr = ctypes.c_int32(), ctypes.c_int32()
+    rc = lib.vs_plan_boundaries(n_atom_clusters, atom_ub, n_rot_clusters, rot_ub, _ptr(ab), ctypes.byref(na),
+                                _ptr(rb), ctypes.byref(nr))
+    if rc != VS_OK:
+        raise VsError(rc, "vs_plan_boundaries")
+    return list(ab[: na.value]), list(rb[: nr.value])
+
+
+def plan_lpt(weights, world):
+    """Host-only a4 LPT plan exactly as vs_submit computes it: (owner[b], launch_order[b])."""
+    lib = load_library()
+    w = np.ascontiguousarray(weights, np.uint64)
+    owner = np.zeros(max(1, len(w)), np.int32)
+    order = np.zeros(max(1, len(w)), np.int32)
+    rc = lib.vs_plan_lpt(_ptr(w), len(w), world, _ptr(owner), _ptr(order))
+    if rc != VS_OK:
+        raise VsError(rc, "vs_plan_lpt")
+    return owner[: len(w)], order[: len(w)]
+
+
 @dataclass
 class Results:
     best_score: np.ndarray   # float32 [n]
@@ -137,7 +164,8 @@ class Engine:
 
     def __init__(self, device: int = 0, n_sweeps: int = 1, atom_clusters: int = 6, rot_clusters: int = 23,
                  atom_upper_bound: int = 0, rot_upper_bound: int = 0, bucket_multiple: int = 16, n_streams: int = 4,
-                 rank: int = 0, world_size: int = 1, debug_poses: bool = False, stream=None):
+                 rank: int = 0, world_size: int = 1, debug_poses: bool = False, launch_per_bucket: bool = False,
+                 stream=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("vsdock needs a CUDA device (B200, sm_100a); there is no CPU fallback")
@@ -149,7 +177,8 @@ class Engine:
         st = stream if stream is not None else torch.cuda.current_stream(device)
         self._stream = st
         cfg = vs_config(device, n_sweeps, atom_clusters, rot_clusters, atom_upper_bound, rot_upper_bound,
-                        bucket_multiple, n_streams, rank, world_size, int(debug_poses), ctypes.c_void_p(st.cuda_stream))
+                        bucket_multiple, n_streams, rank, world_size, int(debug_poses), int(launch_per_bucket),
+                        ctypes.c_void_p(st.cuda_stream))
         h = ctypes.c_void_p()
         self._check(self.lib.vs_create(ctypes.byref(cfg), ctypes.byref(h)), None)
         self.h = h
