@@ -170,7 +170,7 @@ def main():
         return run_reference(args)
     import torch
     import torch.distributed as dist
-    from paper_2303_06150_b200 import Engine
+    from paper_2303_06150_b200 import Engine, parallel
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -202,12 +202,7 @@ def main():
         e.wait()
         tops = []
         for s in range(len(ids)):
-            keys, nv = e.local_topk(s, K_TOP)
-            if world > 1:
-                g = torch.empty(world * K_TOP, dtype=torch.int64, device=dev)
-                dist.all_gather_into_tensor(g, keys)
-                keys = g
-            tops.append(e.merge_topk(keys, K_TOP))
+            tops.append(parallel.global_topk(e, s, K_TOP))   # a10 local top-k, a11 NCCL all_gather + merge
             if host_out is not None:     # D2H of the step's per-ligand result (score, pose)
                 e.results_device(s, host_out[0], host_out[1])
         return tops

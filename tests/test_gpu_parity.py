@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path through the C-ABI (libvsdock.so) against the fp64 oracle.
+
+Contract (BASELINE.json north_star): bucketing, ordering and
+angle indices bit-exact outside near-ties (band 1e-5 * max(1, |S|)); final scores
+within 1e-4 * max(1, |S|); best-pose coordinates within 1e-3 A.  Every GPU angle
+choice is replayed in fp64 (oracle.parity).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import vsgen
+from oracle import parity
+
+pytestmark = pytest.mark.gpu
+
+BAND, TOL_S, TOL_X = 1e-5, 1e-4, 1e-3
+
+
+def engine(**kw):
+    from paper_2303_06150_b200 import Engine
+    return Engine(**kw)
+
+
+def setup(e, pockets, P, K, seed=7):
+    rot, tr = vsgen.pose_table(P, seed)
+    cs = vsgen.angle_table(K)
+    e.set_poses(rot, tr)
+    e.set_angles(cs)
+    ids = [e.load_pocket(p) for p in pockets]
+    return rot, tr, cs, ids
+
+
+def run(lib, pockets, P=8, K=8, debug=True, **kw):
+    e = engine(debug_poses=debug, **kw)
+    rot, tr, cs, ids = setup(e, pockets, P, K)
+    e.submit_library(lib, ids)
+    e.wait()
+    return e, rot, tr, cs
+
+
+def check(e, lib, idx, pk, rot, tr, cs, slot=0, debug=True, S_w=1):
+    r = e.results(slot)
+    xyz = e.coords(slot)
+    ps, pa = e.pose_debug(slot) if debug else (None, None)
+    rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, xyz, ps, pa, S_w=S_w,
+                       band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + "\n" + "\n".join(map(str, rep.failures[:10]))
+    return rep, r
+
+
+# ----------------------------------------------------------------------------- a8
+
+def test_grid_score_hook_vs_oracle():
+    pk = vsgen.pocket(101)
+    e = engine()
+    pid = e.load_pocket(pk)
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(-5, 36, size=(20000, 3)).astype(np.float32)
+    g = e.score_points(pid, pts)
+    ref = oracle.grid_score(pk, pts.astype(np.float64))
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < 2e-6
+    # node exactness: integer coordinates (h = 1, origin 0) hit nodes exactly
+    nodes = rng.integers(0, 32, size=(2000, 3)).astype(np.float32)
+    g = e.score_points(pid, nodes)
+    want = pk.grid[nodes[:, 2].astype(int), nodes[:, 1].astype(int), nodes[:, 0].astype(int)]
+    assert np.array_equal(g, want)
+
+
+# ----------------------------------------------------------------------------- C1 full
+
+def test_c1_full_parity_every_pose():
+    c = vsgen.CONFIGS["C1"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
+    rep, r = check(e, lib, range(lib.n), pk, rot, tr, cs)
+    assert rep.independent_checked >= lib.n // 2 and rep.independent_equal == rep.independent_checked
+
+
+# ----------------------------------------------------------------------------- C2 / C3 samples
+
+@pytest.fixture(scope="module")
+def c2():
+    c = vsgen.CONFIGS["C2"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    return c, lib, vsgen.pocket(101)
+
+
+def test_c2_sample_parity_and_bucketing_invariance(c2):
+    c, lib, pk = c2
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
+    rng = np.random.default_rng(2)
+    idx = rng.choice(lib.n, 120, replace=False)
+    rep, r = check(e, lib, idx, pk, rot, tr, cs)
+    assert rep.independent_equal == rep.independent_checked > 30
+    # Q22: results are bit-identical for the unsorted baseline and for one launch per bucket
+    for kw in (dict(atom_clusters=1, rot_clusters=1), dict(launch_per_bucket=True, bucket_multiple=1),
+               dict(atom_clusters=3, rot_clusters=3, n_streams=1)):
+        e2, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, **kw)
+        r2 = e2.results(0)
+        assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.best_pose, r2.best_pose)
+        assert np.array_equal(r.angles, r2.angles)
+        assert np.array_equal(e.coords(0), e2.coords(0))
+
+
+def test_c3_large_ligand_sample_parity():
+    c = vsgen.CONFIGS["C3"]
+    lib = vsgen.ligands(2048, c["seed"], c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
+    assert {cl["kernel_atoms"] for cl in e.classes()} >= {96, 128, 160}
+    rng = np.random.default_rng(3)
+    check(e, lib, rng.choice(lib.n, 40, replace=False), pk, rot, tr, cs)
+
+
+# ----------------------------------------------------------------------------- a2-a4 bit-exact
+
+@pytest.mark.parametrize("grid", [(6, 23), (1, 1), (3, 3), (4, 5)])
+def test_manifest_bit_exact_vs_oracle(c2, grid):
+    c, lib, pk = c2
+    e, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, atom_clusters=grid[0], rot_clusters=grid[1],
+                bucket_multiple=1)
+    buckets, perm = e.manifest()
+    cls = e.classes()
+    ab, rb = oracle.atom_boundaries(grid[0], 32, int(lib.n_atoms.max())), oracle.rotamer_boundaries(grid[1], int(lib.n_frags.max()))
+    assert [cl["atom_bound"] for cl in cls] == ab
+    ref = oracle.bucketize(lib.n_atoms, lib.n_frags, ab, rb, [cl["capacity"] for cl in cls])
+    assert len(ref) == len(buckets)
+    assert np.array_equal(perm, np.concatenate([b.ligands for b in ref]).astype(np.uint32))
+    for b, rbk in zip(buckets, ref):
+        assert (b["atom_class"], b["rot_class"]) == rbk.cell
+        assert b["size"] == len(rbk.ligands) and b["capacity"] == rbk.capacity
+    # exact work weights and the LPT shard
+    E = oracle.ligand_work(lib.n_atoms, lib.n_moving, c["P"], c["K"])
+    w = [int(E[rbk.ligands].sum()) for rbk in ref]
+    assert [b["weight"] for b in buckets] == w
+    for W in (2, 4, 8):
+        sh = oracle.lpt_shards(w, W)
+        owners = {bb: r for r, bl in enumerate(sh) for bb in bl}
+        eW, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, atom_clusters=grid[0], rot_clusters=grid[1],
+                     bucket_multiple=1, rank=W - 1, world_size=W)
+        bW, _ = eW.manifest(want_perm=False)
+        assert [b["owner"] for b in bW] == [owners[i] for i in range(len(bW))]
+
+
+def test_eq1_class_table_matches_occupancy_model(c2):
+    c, lib, pk = c2
+    e, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    for cl in e.classes():
+        # S:109 min-of-limits with B200 limits: 64K regs, 2048 threads, 32 CTAs, 228 KB smem (1 KB/CTA reserved)
+        b = oracle.active_blocks_per_sm(65536, 2048, 32, 233472, 256, cl["regs_per_thread"], cl["threads_per_cta"],
+                                        cl["dyn_smem"] + cl["static_smem"] + 1024)
+        assert cl["blocks_per_sm"] == b
+        assert cl["l"] == oracle.bucket_capacity_native(b, cl["sm_count"], 32 * cl["ligands_per_cta"], 32)
+        assert cl["sm_count"] == 148
+
+
+# ----------------------------------------------------------------------------- a10/a11 bit-exact
+
+def test_topk_and_virtual_rank_merge_bit_exact(c2):
+    import torch
+    c, lib, pk = c2
+    e, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    r = e.results(0)
+    for k in (1, 10, 1000, 4096):
+        keys, nv = e.local_topk(0, k)
+        idx, sc = e.merge_topk(keys[:nv], k)
+        want = oracle.topk(r.best_score, k)
+        assert list(idx) == list(want)
+        assert np.array_equal(sc, r.best_score[want])
+    # W virtual ranks on one GPU: each docks its LPT shard; gather + merge == single GPU
+    for W in (2, 4):
+        parts = []
+        for rank in range(W):
+            eR, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, rank=rank, world_size=W)
+            rr = eR.results(0)
+            own = ~np.isnan(rr.best_score)
+            assert np.array_equal(rr.best_score[own], r.best_score[own])
+            keys, _ = eR.local_topk(0, 1000)
+            parts.append(keys)
+            merger = eR
+        gathered = torch.cat(parts)
+        idx, sc = merger.merge_topk(gathered, 1000)
+        assert list(idx) == list(oracle.topk(r.best_score, 1000))
+
+
+def test_topk_vs_oracle_scores_outside_ties(c2):
+    """The GPU ranking equals the fp64 oracle's ranking except where scores are within the band."""
+    c, lib, pk = c2
+    sub = lib.subset(np.arange(400))
+    e, rot, tr, cs = run(sub, [pk], P=c["P"], K=c["K"], debug=False)
+    r = e.results(0)
+    ref = oracle.dock_batch(sub, pk, rot, tr, cs, want_xyz=False, want_debug=False)
+    g = oracle.topk(r.best_score, 50)
+    o = oracle.topk(ref.best_score, 50)
+    for a, b in zip(g, o):
+        if a != b:
+            assert abs(ref.best_score[a] - ref.best_score[b]) <= 2 * TOL_S * max(1, abs(ref.best_score[b]))
+
+
+# ----------------------------------------------------------------------------- edge cases
+
+def mk_lib(ligs):
+    A = [len(x) for x, _ in ligs]
+    R = [len(f) for _, f in ligs]
+    ao = np.zeros(len(ligs) + 1, np.int64); ao[1:] = np.cumsum(A)
+    fo = np.zeros(len(ligs) + 1, np.int64); fo[1:] = np.cumsum(R)
+    xyz = np.concatenate([np.asarray(x, np.float32).reshape(-1, 3) for x, _ in ligs]) if ligs else np.zeros((0, 3), np.float32)
+    fr = np.concatenate([np.asarray(f, np.int32).reshape(-1, 4) for _, f in ligs]) if sum(R) else np.zeros((0, 4), np.int32)
+    return vsgen.Library(np.arange(len(ligs), dtype=np.uint64), ao, xyz, fo, fr)
+
+
+def test_edge_cases_tiny_ligands_and_tables():
+    pk = vsgen.pocket(102)
+    base = vsgen.ligands(40, 9, (20, 40), (0, 4))
+    ligs = [base.ligand(i) for i in range(base.n)]
+    ligs += [(np.array([[1.0, 2.0, 3.0]]), np.zeros((0, 4))),                       # A = 1
+             (np.array([[0, 0, 0], [1.5, 0, 0]], np.float32), np.zeros((0, 4)))]     # A = 2, R = 0
+    lib = mk_lib(ligs)
+    for P, K in [(1, 8), (7, 8), (8, 1), (8, 2), (4, 16), (4, 32), (33, 4)]:
+        e, rot, tr, cs = run(lib, [pk], P=P, K=K)
+        check(e, lib, range(lib.n), pk, rot, tr, cs)
+
+
+def test_two_sweeps_and_two_pockets_with_different_grids():
+    lib = vsgen.ligands(30, 12, (20, 60), (1, 6))
+    pk1 = vsgen.pocket(103)
+    pk2 = vsgen.pocket(104, n=28, spacing=1.25)
+    e = engine(debug_poses=True, n_sweeps=2)
+    rot, tr, cs, ids = setup(e, [pk1, pk2], 8, 8)
+    e.submit_library(lib, ids)
+    e.wait()
+    for slot, pk in enumerate([pk1, pk2]):
+        check(e, lib, range(lib.n), pk, rot, tr, cs, slot=slot, S_w=2)
+
+
+def test_empty_batch():
+    e = engine()
+    setup(e, [vsgen.pocket(101)], 8, 8)
+    e.submit_library(mk_lib([]), [0])
+    e.wait()
+    assert e.results(0).best_score.size == 0
+
+
+def test_validation_errors_name_the_ligand():
+    from paper_2303_06150_b200 import VsError
+    from paper_2303_06150_b200 import vsdock
+    base = vsgen.ligands(10, 5, (20, 40), (1, 4))
+    e = engine()
+    setup(e, [vsgen.pocket(101)], 8, 8)
+
+    def bad(mutate, code):
+        ligs = [tuple(np.array(a, copy=True) for a in base.ligand(i)) for i in range(base.n)]
+        mutate(ligs)
+        with pytest.raises(VsError) as ei:
+            e.submit_library(mk_lib(ligs), [0])
+        assert ei.value.code == code
+        assert "ligand 3" in str(ei.value)
+
+    def nan(l): l[3][0][2, 1] = np.nan
+    def axis_eq(l): l[3][1][0, 1] = l[3][1][0, 0]
+    def rng_bad(l): l[3][1][0, 3] = 1000
+    def axis_in(l): l[3][1][0, 2] = l[3][1][0, 1]
+    def too_big(l): l[3] = (np.zeros((300, 3), np.float32), np.zeros((0, 4), np.int32))
+    bad(nan, vsdock.VS_E_PARSE)
+    bad(axis_eq, vsdock.VS_E_PARSE)
+    bad(rng_bad, vsdock.VS_E_PARSE)
+    bad(axis_in, vsdock.VS_E_PARSE)
+    bad(too_big, vsdock.VS_E_PARSE)
+    # overflow names the axis: user upper bounds below the data
+    e2 = engine(atom_upper_bound=30, rot_upper_bound=2, atom_clusters=1, rot_clusters=1)
+    setup(e2, [vsgen.pocket(101)], 8, 8)
+    with pytest.raises(VsError) as ei:
+        e2.submit_library(base, [0])
+    assert ei.value.code in (vsdock.VS_E_OVERFLOW_ATOMS, vsdock.VS_E_OVERFLOW_ROTAMERS)
+    assert "axis" in str(ei.value)
+
+
+# ----------------------------------------------------------------------------- full size (bench config)
+
+def test_c4_full_size_sampled_parity():
+    """BASELINE configs[3] at full size in bench.py's launch configuration; sampled ligands
+    against the oracle one by one, plus properties over all 1M outputs."""
+    import torch
+    c = vsgen.CONFIGS["C4"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    e = engine(bucket_multiple=16, n_streams=4)
+    rot, tr, cs, ids = setup(e, [pk], c["P"], c["K"])
+    d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    e.submit(*d, ids, on_device=True)
+    e.wait()
+    r = e.results(0)
+    assert np.isfinite(r.best_score).all()
+    assert ((r.best_pose >= 0) & (r.best_pose < c["P"])).all()
+    assert (r.angles < c["K"]).all()
+    rng = np.random.default_rng(4)
+    idx = rng.choice(lib.n, 30, replace=False)
+    xyz = e.coords(0)
+    rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, xyz, band=BAND,
+                       tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + str(rep.failures[:5])
