@@ -323,7 +323,10 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps
         // same for every class so the reduction order, hence every result, is class-independent (Q22)
         int PPW = c->K <= 16 ? 2 : 1;
         if (const char* e = getenv("VSDOCK_PPW")) PPW = atoi(e) == 1 ? 1 : PPW;
+        int max_nw = 32;
+        if (const char* e = getenv("VSDOCK_MAXNW")) max_nw = atoi(e);
         for (int NW : {32, 16, 8}) {
+            if (NW > max_nw) continue;
             const int LC = ligs_per_cta(NW, PPW, c->P);
             const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, ps, c->P, c->K, c->cfg.n_sweeps, LC);
             int b = 0;

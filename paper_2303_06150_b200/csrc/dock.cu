@@ -194,10 +194,16 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                         acc = __fadd_rn(acc, grid_g(G, id ? v.x : p.x, id ? v.y : p.y, id ? v.z : p.z, pk));
                     }
                 }
-                for (int o = K; o < LPP; o <<= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
-                // argmin over the K angles of this group; ties -> lowest k (Q11)
+                // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+                    if (o >= K) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                // argmin over the K angles of this group (xor offsets 1 .. K/2); ties -> lowest k (Q11)
                 const unsigned key = ord32(acc);
-                const unsigned mn = __reduce_min_sync(gmask, key);
+                unsigned mn = key;
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+                    if (o < K) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
                 const unsigned bal = __ballot_sync(FULL, key == mn) & gmask;
                 const int bk = (__ffs(bal) - 1) & (K - 1);
                 if (hi - lo <= apw) {
