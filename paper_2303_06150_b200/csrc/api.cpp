@@ -319,14 +319,23 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps
         ci.AC = std::max(32, roundup32(atom_b[i]));
         if (ci.AC > kMaxAtoms) return fail(c, VS_E_ARG, "atom class bound %d exceeds %d", atom_b[i], kMaxAtoms);
         ci.b = 0;
-        // poses per warp: 2 when the K angle lanes fit in half a warp; the
-        // same for every class so the reduction order, hence every result, is class-independent (Q22)
-        int PPW = c->K <= 16 ? 2 : 1;
-        if (const char* e = getenv("VSDOCK_PPW")) PPW = atoi(e) == 1 ? 1 : PPW;
-        int max_nw = 32;
-        if (const char* e = getenv("VSDOCK_MAXNW")) max_nw = atoi(e);
-        for (int NW : {32, 16, 8}) {
-            if (NW > max_nw) continue;
+        // (poses per warp, warps per CTA): the first candidate of the policy whose shared
+        // memory fits one CTA per SM and whose pose group holds the K angle lanes
+        // (PPW poses x 32/PPW lanes).  VSDOCK_POLICY="4:16,2:16,..." overrides.
+        std::vector<std::pair<int, int>> cand = {{4, 16}, {2, 16}, {4, 8}, {2, 8}, {4, 4}, {1, 32}, {1, 16}};
+        if (const char* e = getenv("VSDOCK_POLICY")) {
+            cand.clear();
+            int a = 0, b2 = 0, n = 0;
+            const char* s = e;
+            while (sscanf(s, "%d:%d%n", &a, &b2, &n) == 2) {
+                cand.push_back({a, b2});
+                s += n;
+                if (*s == ',') ++s;
+            }
+        }
+        for (auto pr : cand) {
+            const int PPW = pr.first, NW = pr.second;
+            if (c->K > 32 / PPW) continue;
             const int LC = ligs_per_cta(NW, PPW, c->P);
             const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, ps, c->P, c->K, c->cfg.n_sweeps, LC);
             int b = 0;

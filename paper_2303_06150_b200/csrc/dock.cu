@@ -4,24 +4,26 @@
 // contraction, BJ: "no tensor cores").
 //
 // B200 design:
-//  * one CTA per SM (persistent over the bucket's ligands, grid <= b * 148);
-//    the pocket grid (32^3 fp32 = 128 KB) lives in SHARED memory for the whole
-//    launch -- the 8 corner gathers of every evaluation hit smem, not L1/L2;
-//  * a CTA docks `LC` ligands at a time; its NW warps split the LC x P
-//    (ligand, pose) items, so one ligand's 64 poses run on 32 warps at once and
-//    every warp of the CTA runs the same control flow (same A, R, M_r);
-//  * sweep lane map: lane = j * K + k -- (moving atom j, angle k).  Each lane
-//    holds its angle's Rodrigues matrix in registers, lanes of equal k reduce
-//    their partial sums with xor shuffles K..16, the argmin over k takes log2 K
-//    more shuffle rounds (ties -> lowest k, Q11), and the chosen rotation is
-//    applied with atoms across lanes;
-//  * template<int AC, int NW> per atom class = the paper's "non-type template
-//    parameter for the kernel maximum number of atoms": AC sizes
-//    the per-warp pose buffers in shared memory and therefore the occupancy.
+//  * one CTA per SM, persistent over a launch's ligands with a dynamic round
+//    counter; the pocket grid (32^3 fp32 = 128 KB, padded strides) lives in
+//    SHARED memory for the whole launch -- the 8 corner gathers of every
+//    evaluation are shared-memory loads, never L1/L2;
+//  * a CTA docks LC ligands at a time; its NW warps split the ligand's poses,
+//    PPW poses per warp (lane groups of 32/PPW), so all warps of a CTA run the
+//    same control flow (same A, R, M_r: poses of one ligand differ only in data);
+//  * sweep lane map inside a pose group: li = jl * K + k -- (moving atom jl of
+//    the pass, angle k).  Each lane holds its angle's rotation in registers,
+//    lanes of equal k sum with xor shuffles, the argmin over k takes log2 K
+//    shuffle rounds (ties -> lowest k, Q11), and the winner is applied;
+//  * (x, y) arithmetic is packed in Blackwell's FFMA2/FADD2 (per-element IEEE
+//    fma/add, so every result is bit-identical to the scalar form);
+//  * template<int AC, int NW, int PPW> per atom class = the paper's "non-type
+//    template parameter for the kernel maximum number of atoms":
+//    AC sizes the per-pose buffers in shared memory, hence the occupancy.
 //
 // All arithmetic that decides an angle or is replayed (placement, Rodrigues,
-// rotation, interpolation) uses explicit _rn intrinsics, so the trajectory is
-// reproducible bit for bit by the finalize kernel.
+// rotation, interpolation) uses explicit _rn intrinsics in shared helpers, so
+// the finalize kernel reproduces the trajectory bit for bit.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
@@ -34,37 +36,47 @@ namespace vsd {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr float kMagic = 8388608.f;              // 2^23: floor via round-down add
+constexpr int kMagicBits = 0x4B000000;
 
-struct Rot {
-    float m00, m01, m02, m10, m11, m12, m20, m21, m22;
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+// Rotation about a pivot in "M v + t" form: p = M v + t with t = q - M q.
+// Rows 0 and 1 are packed column-wise: c0 = (m00, m10), c1 = (m01, m11), c2 = (m02, m12).
+struct RotT {
+    float2 c0, c1, c2, txy;
+    float m20, m21, m22, tz;
 };
 
-// M = c I + s [u]x + (1 - c) u u^T (a7; Q3, Q6)
-__device__ __forceinline__ Rot rodrigues(float ux, float uy, float uz, float c, float s) {
+// M = c I + s [u]x + (1 - c) u u^T (a7; Q3, Q6), pivot q = y_b.  For (c, s) = (1, 0)
+// this is exactly I and t = 0, so the identity candidate leaves coordinates bit-unchanged.
+__device__ __forceinline__ RotT rodrigues_t(float ux, float uy, float uz, float c, float s, float qx, float qy,
+                                            float qz) {
     const float omc = __fsub_rn(1.f, c);
     const float a = __fmul_rn(omc, ux), b = __fmul_rn(omc, uy), d = __fmul_rn(omc, uz);
     const float sx = __fmul_rn(s, ux), sy = __fmul_rn(s, uy), sz = __fmul_rn(s, uz);
-    Rot M;
-    M.m00 = __fmaf_rn(a, ux, c);
-    M.m01 = __fmaf_rn(a, uy, -sz);
-    M.m02 = __fmaf_rn(a, uz, sy);
-    M.m10 = __fmaf_rn(b, ux, sz);
-    M.m11 = __fmaf_rn(b, uy, c);
-    M.m12 = __fmaf_rn(b, uz, -sx);
+    RotT M;
+    const float m00 = __fmaf_rn(a, ux, c), m01 = __fmaf_rn(a, uy, -sz), m02 = __fmaf_rn(a, uz, sy);
+    const float m10 = __fmaf_rn(b, ux, sz), m11 = __fmaf_rn(b, uy, c), m12 = __fmaf_rn(b, uz, -sx);
     M.m20 = __fmaf_rn(d, ux, -sy);
     M.m21 = __fmaf_rn(d, uy, sx);
     M.m22 = __fmaf_rn(d, uz, c);
+    M.c0 = make_float2(m00, m10);
+    M.c1 = make_float2(m01, m11);
+    M.c2 = make_float2(m02, m12);
+    // t = q - M q
+    M.txy = make_float2(__fmaf_rn(-m00, qx, __fmaf_rn(-m01, qy, __fmaf_rn(-m02, qz, qx))),
+                        __fmaf_rn(-m10, qx, __fmaf_rn(-m11, qy, __fmaf_rn(-m12, qz, qy))));
+    M.tz = __fmaf_rn(-M.m20, qx, __fmaf_rn(-M.m21, qy, __fmaf_rn(-M.m22, qz, qz)));
     return M;
 }
 
-// y' = M (y - q) + q
-__device__ __forceinline__ float3 rot_about(const Rot& M, float qx, float qy, float qz, float vx, float vy, float vz) {
-    const float dx = __fsub_rn(vx, qx), dy = __fsub_rn(vy, qy), dz = __fsub_rn(vz, qz);
-    float3 r;
-    r.x = __fmaf_rn(M.m00, dx, __fmaf_rn(M.m01, dy, __fmaf_rn(M.m02, dz, qx)));
-    r.y = __fmaf_rn(M.m10, dx, __fmaf_rn(M.m11, dy, __fmaf_rn(M.m12, dz, qy)));
-    r.z = __fmaf_rn(M.m20, dx, __fmaf_rn(M.m21, dy, __fmaf_rn(M.m22, dz, qz)));
-    return r;
+// p = M v + t; (x, y) in one FFMA2 chain, z scalar
+__device__ __forceinline__ float4 apply_rot(const RotT& M, float vx, float vy, float vz) {
+    const float2 pxy = __ffma2_rn(M.c0, f2(vx), __ffma2_rn(M.c1, f2(vy), __ffma2_rn(M.c2, f2(vz), M.txy)));
+    const float pz = __fmaf_rn(M.m20, vx, __fmaf_rn(M.m21, vy, __fmaf_rn(M.m22, vz, M.tz)));
+    return make_float4(pxy.x, pxy.y, pz, 0.f);
 }
 
 // unit axis a -> b
@@ -78,43 +90,61 @@ __device__ __forceinline__ void axis_of(const float4& ya, const float4& yb, floa
 }
 
 __device__ __forceinline__ float lerp(float a, float b, float t) { return __fmaf_rn(t, b, __fmaf_rn(-t, a, a)); }
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float t) {
+    return __ffma2_rn(f2(t), b, __ffma2_rn(f2(-t), a, a));
+}
 
-// a8: g(u), u in grid units (Q9, Q10).  G is the shared-memory copy with row
-// stride rs and plane stride ps.
+// a8: g(u), u in grid units (Q9, Q10): clamp, L1 excess, i0 = min(floor(u_c), n-2),
+// lerps x then y then z, + kappa*h*excess.  G is the shared-memory copy (strides rs, ps).
+// floor(m) for 0 <= m < 2^23 is the round-down sum m + 2^23 (its bits also give the
+// integer); identical values to floorf.  The x-lerps run on (z0, z1) pairs, the
+// y-lerp on the (l0, l1) pair: per element the same fma sequence as the scalar form.
 __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
     const float cx = fminf(fmaxf(ux, 0.f), pk.top_x);
     const float cy = fminf(fmaxf(uy, 0.f), pk.top_y);
     const float cz = fminf(fmaxf(uz, 0.f), pk.top_z);
-    const float e = __fadd_rn(__fadd_rn(fabsf(__fsub_rn(ux, cx)), fabsf(__fsub_rn(uy, cy))), fabsf(__fsub_rn(uz, cz)));
-    const float fx = fminf(floorf(cx), pk.top2_x);
-    const float fy = fminf(floorf(cy), pk.top2_y);
-    const float fz = fminf(floorf(cz), pk.top2_z);
-    const float tx = __fsub_rn(cx, fx), ty = __fsub_rn(cy, fy), tz = __fsub_rn(cz, fz);
-    const int idx = __float2int_rn(__fmaf_rn(fz, (float)pk.ps, __fmaf_rn(fy, (float)pk.rs, fx)));
+    const float2 dxy = __fadd2_rn(make_float2(ux, uy), make_float2(-cx, -cy));
+    const float e = __fadd_rn(__fadd_rn(fabsf(dxy.x), fabsf(dxy.y)), fabsf(__fsub_rn(uz, cz)));
+    const float2 bxy = __fadd2_rd(make_float2(fminf(cx, pk.top2_x), fminf(cy, pk.top2_y)), f2(kMagic));
+    const float bz = __fadd_rd(fminf(cz, pk.top2_z), kMagic);
+    const float2 fxy = __fadd2_rn(make_float2(cx, cy), neg2(__fadd2_rn(bxy, f2(-kMagic))));
+    const float fz = __fsub_rn(cz, __fsub_rn(bz, kMagic));
+    const int idx = (__float_as_int(bxy.x) - kMagicBits) + (__float_as_int(bxy.y) - kMagicBits) * pk.rs +
+                    (__float_as_int(bz) - kMagicBits) * pk.ps;
     const float* p = G + idx;
-    const float c000 = p[0], c100 = p[1];
-    const float c010 = p[pk.rs], c110 = p[pk.rs + 1];
-    const float c001 = p[pk.ps], c101 = p[pk.ps + 1];
-    const float c011 = p[pk.ps + pk.rs], c111 = p[pk.ps + pk.rs + 1];
-    const float l00 = lerp(c000, c100, tx), l10 = lerp(c010, c110, tx);
-    const float l01 = lerp(c001, c101, tx), l11 = lerp(c011, c111, tx);
-    const float l0 = lerp(l00, l10, ty), l1 = lerp(l01, l11, ty);
-    return __fmaf_rn(pk.kh, e, lerp(l0, l1, tz));
+    const float2 c00 = make_float2(p[0], p[pk.ps]);                    // (c000, c001)
+    const float2 c10 = make_float2(p[1], p[pk.ps + 1]);                // (c100, c101)
+    const float2 c01 = make_float2(p[pk.rs], p[pk.ps + pk.rs]);        // (c010, c011)
+    const float2 c11 = make_float2(p[pk.rs + 1], p[pk.ps + pk.rs + 1]);// (c110, c111)
+    const float2 l_0 = lerp2(c00, c10, fxy.x);     // (l00, l01): y0, z0/z1
+    const float2 l_1 = lerp2(c01, c11, fxy.x);     // (l10, l11): y1, z0/z1
+    const float2 l = lerp2(l_0, l_1, fxy.y);       // (l0, l1)
+    return __fmaf_rn(pk.kh, e, lerp(l.x, l.y, fz));
 }
 
 // Pose p in grid units: R' = R / h, t' = (c + tau - o) / h, u = R' x + t'.
+// Stored as 12 floats: (R'00, R'10), (R'01, R'11), (R'02, R'12), (t'x, t'y), R'20, R'21, R'22, t'z.
 __device__ __forceinline__ void scaled_pose(const float* raw, const PocketDev& pk, float* out) {
+    float r[9];
 #pragma unroll
-    for (int t = 0; t < 9; ++t) out[t] = __fmul_rn(raw[t], pk.inv_h);
-    out[9] =__fadd_rn(pk.tx, __fmul_rn(raw[9], pk.inv_h));
-    out[10] = __fadd_rn(pk.ty, __fmul_rn(raw[10], pk.inv_h));
+    for (int t = 0; t < 9; ++t) r[t] = __fmul_rn(raw[t], pk.inv_h);
+    out[0] = r[0]; out[1] = r[3];
+    out[2] = r[1]; out[3] = r[4];
+    out[4] = r[2]; out[5] = r[5];
+    out[6] = __fadd_rn(pk.tx, __fmul_rn(raw[9], pk.inv_h));
+    out[7] = __fadd_rn(pk.ty, __fmul_rn(raw[10], pk.inv_h));
+    out[8] = r[6]; out[9] = r[7]; out[10] = r[8];
     out[11] = __fadd_rn(pk.tz, __fmul_rn(raw[11], pk.inv_h));
 }
 
-__device__ __forceinline__ float4 place_atom(const float* T, float x, float y, float z) {
-    return make_float4(__fmaf_rn(T[0], x, __fmaf_rn(T[1], y, __fmaf_rn(T[2], z, T[9]))),
-                       __fmaf_rn(T[3], x, __fmaf_rn(T[4], y, __fmaf_rn(T[5], z, T[10]))),
-                       __fmaf_rn(T[6], x, __fmaf_rn(T[7], y, __fmaf_rn(T[8], z, T[11]))), 0.f);
+__device__ __forceinline__ RotT load_pose(const float* T) {
+    RotT M;
+    M.c0 = make_float2(T[0], T[1]);
+    M.c1 = make_float2(T[2], T[3]);
+    M.c2 = make_float2(T[4], T[5]);
+    M.txy = make_float2(T[6], T[7]);
+    M.m20 = T[8]; M.m21 = T[9]; M.m22 = T[10]; M.tz = T[11];
+    return M;
 }
 
 // Stage the pocket grid into shared memory with padded strides.
@@ -134,9 +164,13 @@ __device__ __forceinline__ unsigned ord32(float v) {
     return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
 }
 
+// Per-pose buffer stride in float4: AC + 1 so that the PPW pose groups of a warp
+// read their buffers from different banks.
+template <int AC>
+__host__ __device__ constexpr int pose_stride() { return AC + 1; }
+
 // PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
-// a6 placement, a7 sweep, a9 pose score.  Sweep lane map inside a pose group:
-// li = jl * K + k (moving atom jl of the pass, angle k); APW = LPP / K atoms per pass.
+// a6 placement, a7 sweep, a9 pose score.
 template <int AC, int PPW>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, float4* __restrict__ buf, const float* __restrict__ G,
@@ -150,11 +184,9 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     const float* rz = rec + 2 * AC;
     const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
     {
-        float Tr[12];
-#pragma unroll
-        for (int t = 0; t < 12; ++t) Tr[t] = T[t];
+        const RotT Pz = load_pose(T);
         if (valid)
-            for (int i = li; i < A; i += LPP) buf[i] = place_atom(Tr, rx[i], ry[i], rz[i]);
+            for (int i = li; i < A; i += LPP) buf[i] = apply_rot(Pz, rx[i], ry[i], rz[i]);
     }
     __syncwarp();
     if (K > 1) {
@@ -169,19 +201,18 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 const float4 ya = buf[fa], yb = buf[fb];
                 float ux, uy, uz;
                 axis_of(ya, yb, ux, uy, uz);
-                const Rot M = rodrigues(ux, uy, uz, ck, sk);
-                const bool id = (k == 0);   // theta_0: the current pose itself (Q3)
+                const RotT M = rodrigues_t(ux, uy, uz, ck, sk, yb.x, yb.y, yb.z);
                 float acc = 0.f;
-                float3 keep = make_float3(0.f, 0.f, 0.f);
+                float4 keep = make_float4(0.f, 0.f, 0.f, 0.f);
                 int base = lo;
                 for (; base + apw < hi; base += 2 * apw) {     // two independent evaluations per lane
                     const int j0 = base + jl, j1 = base + apw + jl;
                     const float4 v0 = buf[j0];
                     const float4 v1 = buf[j1 < hi ? j1 : j0];
-                    const float3 p0 = rot_about(M, yb.x, yb.y, yb.z, v0.x, v0.y, v0.z);
-                    const float3 p1 = rot_about(M, yb.x, yb.y, yb.z, v1.x, v1.y, v1.z);
-                    const float g0 = grid_g(G, id ? v0.x : p0.x, id ? v0.y : p0.y, id ? v0.z : p0.z, pk);
-                    const float g1 = grid_g(G, id ? v1.x : p1.x, id ? v1.y : p1.y, id ? v1.z : p1.z, pk);
+                    const float4 p0 = apply_rot(M, v0.x, v0.y, v0.z);
+                    const float4 p1 = apply_rot(M, v1.x, v1.y, v1.z);
+                    const float g0 = grid_g(G, p0.x, p0.y, p0.z, pk);
+                    const float g1 = grid_g(G, p1.x, p1.y, p1.z, pk);
                     acc = __fadd_rn(acc, g0);
                     if (j1 < hi) acc = __fadd_rn(acc, g1);
                 }
@@ -189,9 +220,8 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                     const int j = base + jl;
                     if (j < hi) {
                         const float4 v = buf[j];
-                        const float3 p = rot_about(M, yb.x, yb.y, yb.z, v.x, v.y, v.z);
-                        keep = p;
-                        acc = __fadd_rn(acc, grid_g(G, id ? v.x : p.x, id ? v.y : p.y, id ? v.z : p.z, pk));
+                        keep = apply_rot(M, v.x, v.y, v.z);
+                        acc = __fadd_rn(acc, grid_g(G, keep.x, keep.y, keep.z, pk));
                     }
                 }
                 // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
@@ -208,13 +238,12 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 const int bk = (__ffs(bal) - 1) & (K - 1);
                 if (hi - lo <= apw) {
                     // single pass: the lane (jl, k*) already holds the rotated atom
-                    if (valid && bk != 0 && k == bk && lo + jl < hi) buf[lo + jl] = make_float4(keep.x, keep.y, keep.z, 0.f);
+                    if (valid && bk != 0 && k == bk && lo + jl < hi) buf[lo + jl] = keep;
                 } else if (valid && bk != 0) {
-                    const Rot Ms = rodrigues(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1]);
+                    const RotT Ms = rodrigues_t(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1], yb.x, yb.y, yb.z);
                     for (int j = lo + li; j < hi; j += LPP) {
                         const float4 v = buf[j];
-                        const float3 p = rot_about(Ms, yb.x, yb.y, yb.z, v.x, v.y, v.z);
-                        buf[j] = make_float4(p.x, p.y, p.z, 0.f);
+                        buf[j] = apply_rot(Ms, v.x, v.y, v.z);
                     }
                 }
                 __syncwarp();
@@ -261,14 +290,14 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int K = a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
     const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
-    float4* buf = sBuf + (warp * PPW + h) * AC;
+    float4* buf = sBuf + (warp * PPW + h) * pose_stride<AC>();
     const int rec_floats = a.rec_floats;
     const int n_rounds = (a.n + LC - 1) / LC;
     const int ang_stride = 32 * S_w;
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
 
     while (true) {
-        if (tid == 0) s_round = atomicAdd(a.counter, 1);   // dynamic: balance CTAs within the bucket
+        if (tid == 0) s_round = atomicAdd(a.counter, 1);   // dynamic: balance CTAs within the launch
         __syncthreads();
         const int round = s_round;
         if (round >= n_rounds) break;
@@ -324,8 +353,8 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
 }
 
 // a9 coordinates: replay p* with the recorded angles, bit-identical to the
-// dock kernel (same placement, axis, Rodrigues and rotation code); one warp per
-// ligand; output in Angstrom, input atom order.
+// dock kernel (same placement, axis, Rodrigues and rotation helpers); one warp
+// per ligand; output in Angstrom, input atom order.
 template <int AC>
 __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const int64_t* __restrict__ atom_off,
                                                        float* __restrict__ xyz_out) {
@@ -341,8 +370,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const i
     const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
     float T[12];
     scaled_pose(a.pose_tab + 12 * p, pk, T);
+    const RotT Pz = load_pose(T);
     float4* buf = sb[w];
-    for (int i = lane; i < A; i += 32) buf[i] = place_atom(T, rec[i], rec[AC + i], rec[2 * AC + i]);
+    for (int i = lane; i < A; i += 32) buf[i] = apply_rot(Pz, rec[i], rec[AC + i], rec[2 * AC + i]);
     __syncwarp();
     for (int sw = 0; sw < a.S_w; ++sw) {
         for (int r = 0; r < R; ++r) {
@@ -353,11 +383,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const i
                 const float4 ya = buf[fa], yb = buf[fb];
                 float ux, uy, uz;
                 axis_of(ya, yb, ux, uy, uz);
-                const Rot Ms = rodrigues(ux, uy, uz, a.cs[2 * bk], a.cs[2 * bk + 1]);
+                const RotT Ms = rodrigues_t(ux, uy, uz, a.cs[2 * bk], a.cs[2 * bk + 1], yb.x, yb.y, yb.z);
                 for (int j = lo + lane; j < hi; j += 32) {
                     const float4 v = buf[j];
-                    const float3 q = rot_about(Ms, yb.x, yb.y, yb.z, v.x, v.y, v.z);
-                    buf[j] = make_float4(q.x, q.y, q.z, 0.f);
+                    buf[j] = apply_rot(Ms, v.x, v.y, v.z);
                 }
             }
             __syncwarp();
@@ -390,8 +419,9 @@ using DockFn = void (*)(const DockArgs);
 
 template <int AC>
 DockFn pick_ac(int NW, int PPW) {
-    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1> : (NW == 16 ? dock_kernel<AC, 16, 1> : (NW == 8 ? dock_kernel<AC, 8, 1> : nullptr));
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1> : (NW == 16 ? dock_kernel<AC, 16, 1> : nullptr);
     if (PPW == 2) return NW == 32 ? dock_kernel<AC, 32, 2> : (NW == 16 ? dock_kernel<AC, 16, 2> : (NW == 8 ? dock_kernel<AC, 8, 2> : nullptr));
+    if (PPW == 4) return NW == 16 ? dock_kernel<AC, 16, 4> : (NW == 8 ? dock_kernel<AC, 8, 4> : (NW == 4 ? dock_kernel<AC, 4, 4> : nullptr));
     return nullptr;
 }
 

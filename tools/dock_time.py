@@ -6,7 +6,8 @@ import vsgen
 from paper_2303_06150_b200 import Engine
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200000
 na, nr = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (6, 23)
-lib = vsgen.ligands(n, 4)
+ATOMS = tuple(int(x) for x in os.environ.get("ATOMS", "20,120").split(","))
+lib = vsgen.ligands(n, 4, ATOMS)
 e = Engine(atom_clusters=na, rot_clusters=nr, launch_per_bucket=bool(int(os.environ.get("LPB", "0"))), bucket_multiple=int(os.environ.get("BM", "16")), n_streams=int(os.environ.get("NS", "4")))
 e.set_poses(*vsgen.pose_table(64)); e.set_angles(vsgen.angle_table(8)); pid = e.load_pocket(vsgen.pocket(101))
 import torch

@@ -1,8 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()"
-for n in 200000; do
-  TAG=base python tools/dock_time.py $n
-  TAG=nw16 VSDOCK_MAXNW=16 python tools/dock_time.py $n
-  TAG=unsorted python tools/dock_time.py $n 1 1
-done
+n=200000
+TAG=default python tools/dock_time.py $n
+TAG=p2 VSDOCK_POLICY="2:32,2:16,2:8" python tools/dock_time.py $n
+TAG=unsorted_default python tools/dock_time.py $n 1 1
+python -m pytest tests -m gpu -x -q 2>&1 | tail -3
