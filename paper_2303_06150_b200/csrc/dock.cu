@@ -205,18 +205,22 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 float acc = 0.f;
                 float4 keep = make_float4(0.f, 0.f, 0.f, 0.f);
                 int base = lo;
-                if (PPW == 4) {   // APW = 1: four independent evaluations in flight per lane
-                    for (; base + 3 < hi; base += 4) {
+                if (PPW == 4) {   // four independent evaluations in flight per lane (passes of apw atoms)
+                    for (; base + 3 * apw < hi; base += 4 * apw) {
                         float4 v[4], q[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) v[u] = buf[base + u];
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = base + u * apw + jl;
+                            v[u] = buf[j < hi ? j : base + jl];
+                        }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) q[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
                         float g[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) g[u] = grid_g(G, q[u].x, q[u].y, q[u].z, pk);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, g[u]);
+                        for (int u = 0; u < 4; ++u)
+                            if (base + u * apw + jl < hi) acc = __fadd_rn(acc, g[u]);
                     }
                 }
                 for (; base + apw < hi; base += 2 * apw) {     // two independent evaluations per lane
