@@ -166,14 +166,26 @@ __device__ __forceinline__ unsigned ord32(float v) {
 
 // Per-pose buffer stride in float4: AC + 1 so that the PPW pose groups of a warp
 // read their buffers from different banks.
+// Per-pose coordinate buffer in shared memory, SoA: x[AC] | y[AC] | z[AC] (12 B per atom),
+// pose buffers 3*AC + 4 floats apart so the PPW pose groups of a warp hit different banks.
 template <int AC>
-__host__ __device__ constexpr int pose_stride() { return AC + 1; }
+__host__ __device__ constexpr int pose_stride() { return 3 * AC + 4; }
+template <int AC>
+struct PoseBuf {
+    float* b;
+    __device__ __forceinline__ float4 get(int j) const { return make_float4(b[j], b[AC + j], b[2 * AC + j], 0.f); }
+    __device__ __forceinline__ void set(int j, float4 v) const {
+        b[j] = v.x;
+        b[AC + j] = v.y;
+        b[2 * AC + j] = v.z;
+    }
+};
 
 // PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
 // a6 placement, a7 sweep, a9 pose score.
 template <int AC, int PPW>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
-                                           bool valid, float4* __restrict__ buf, const float* __restrict__ G,
+                                           bool valid, PoseBuf<AC> B, const float* __restrict__ G,
                                            const PocketDev& pk, int K, int kbits, int S_w, float ck, float sk,
                                            const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
                                            float* __restrict__ scoreOut, int lane) {
@@ -186,7 +198,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     {
         const RotT Pz = load_pose(T);
         if (valid)
-            for (int i = li; i < A; i += LPP) buf[i] = apply_rot(Pz, rx[i], ry[i], rz[i]);
+            for (int i = li; i < A; i += LPP) B.set(i, apply_rot(Pz, rx[i], ry[i], rz[i]));
     }
     __syncwarp();
     if (K > 1) {
@@ -198,7 +210,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
             for (int r = 0; r < R; ++r) {
                 const uint32_t f = rfr[r];
                 const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
-                const float4 ya = buf[fa], yb = buf[fb];
+                const float4 ya = B.get(fa), yb = B.get(fb);
                 float ux, uy, uz;
                 axis_of(ya, yb, ux, uy, uz);
                 const RotT M = rodrigues_t(ux, uy, uz, ck, sk, yb.x, yb.y, yb.z);
@@ -211,7 +223,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int j = base + u * apw + jl;
-                            v[u] = buf[j < hi ? j : base + jl];
+                            v[u] = B.get(j < hi ? j : base + jl);
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) q[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
@@ -225,8 +237,8 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 }
                 for (; base + apw < hi; base += 2 * apw) {     // two independent evaluations per lane
                     const int j0 = base + jl, j1 = base + apw + jl;
-                    const float4 v0 = buf[j0];
-                    const float4 v1 = buf[j1 < hi ? j1 : j0];
+                    const float4 v0 = B.get(j0);
+                    const float4 v1 = B.get(j1 < hi ? j1 : j0);
                     const float4 p0 = apply_rot(M, v0.x, v0.y, v0.z);
                     const float4 p1 = apply_rot(M, v1.x, v1.y, v1.z);
                     const float g0 = grid_g(G, p0.x, p0.y, p0.z, pk);
@@ -237,7 +249,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 if (base < hi) {
                     const int j = base + jl;
                     if (j < hi) {
-                        const float4 v = buf[j];
+                        const float4 v = B.get(j);
                         keep = apply_rot(M, v.x, v.y, v.z);
                         acc = __fadd_rn(acc, grid_g(G, keep.x, keep.y, keep.z, pk));
                     }
@@ -256,12 +268,12 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 const int bk = (__ffs(bal) - 1) & (K - 1);
                 if (hi - lo <= apw) {
                     // single pass: the lane (jl, k*) already holds the rotated atom
-                    if (valid && bk != 0 && k == bk && lo + jl < hi) buf[lo + jl] = keep;
+                    if (valid && bk != 0 && k == bk && lo + jl < hi) B.set(lo + jl, keep);
                 } else if (valid && bk != 0) {
                     const RotT Ms = rodrigues_t(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1], yb.x, yb.y, yb.z);
                     for (int j = lo + li; j < hi; j += LPP) {
-                        const float4 v = buf[j];
-                        buf[j] = apply_rot(Ms, v.x, v.y, v.z);
+                        const float4 v = B.get(j);
+                        B.set(j, apply_rot(Ms, v.x, v.y, v.z));
                     }
                 }
                 __syncwarp();
@@ -274,7 +286,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree) (Q22)
     float acc = 0.f;
     for (int i = li; i < A; i += LPP) {
-        const float4 v = buf[i];
+        const float4 v = B.get(i);
         acc = __fadd_rn(acc, grid_g(G, v.x, v.y, v.z, pk));
     }
 #pragma unroll
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     float* sPose = reinterpret_cast<float*>(smem + L.pose);
     float* sCS = reinterpret_cast<float*>(smem + L.cs);
     float* sRec = reinterpret_cast<float*>(smem + L.rec);
-    float4* sBuf = reinterpret_cast<float4*>(smem + L.buf);
+    float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     float* sScore = reinterpret_cast<float*>(smem + L.score);
     uint8_t* sAng = smem + L.ang;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int K = a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
     const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
-    float4* buf = sBuf + (warp * PPW + h) * pose_stride<AC>();
+    const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride<AC>()};
     const int rec_floats = a.rec_floats;
     const int n_rounds = (a.n + LC - 1) / LC;
     const int ang_stride = 32 * S_w;

@@ -64,7 +64,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     L.pose = o;  o += align16((size_t)P * 12 * 4);
     L.cs = o;    o += align16((size_t)K * 2 * 4);
     L.rec = o;   o += align16((size_t)LC * (3 * AC + 32) * 4);
-    L.buf = o;   o += (size_t)NW * PPW * (AC + 1) * 16;   // float4 per atom, stride AC + 1 per pose
+    L.buf = o;   o += (size_t)NW * PPW * (3 * AC + 4) * 4;   // SoA x|y|z per pose, stride 3 AC + 4 floats
     L.score = o; o += align16((size_t)LC * P * 4);
     L.ang = o;   o += align16((size_t)LC * P * S_w * 32);
     L.total = o;
