@@ -63,7 +63,9 @@ typedef struct {
     int32_t launch_per_bucket; /* 1: one kernel launch per bucket, as the paper does;
                                   0 (default): the owned buckets of one atom class run as ONE
                                   persistent launch with dynamic ligand scheduling */
-    void* stream;              /* cudaStream_t the library orders its work on (e.g. torch's); NULL = own */
+    int32_t bucket_capacity;   /* > 0: every bucket holds this many ligands instead of m * l_c
+                                  (the bucket-size sweep of P:283-333); 0 = Eq. 1 */
+    void* stream;             /* cudaStream_t the library orders its work on (e.g. torch's); NULL = own */
 } vs_config;
 
 /* Create a context on cfg->device.  Fills the kernel class table (registers,

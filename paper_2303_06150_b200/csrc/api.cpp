@@ -354,7 +354,7 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps
             return fail(c, VS_E_NOFIT, "kernel class %d (A_c = %d) does not fit: occupancy is 0 (grid %dx%d planes)",
                         (int)i, ci.AC, nz, ps);
         ci.l = ci.b * c->sm_count * ci.LC;       // Eq. 1: l = b * SM * t/ws  (Q19)
-        ci.cap = ci.l * std::max(1, c->cfg.bucket_multiple);
+        ci.cap = c->cfg.bucket_capacity > 0 ? c->cfg.bucket_capacity : ci.l * std::max(1, c->cfg.bucket_multiple);
         c->classes.push_back(ci);
     }
     return VS_OK;
@@ -380,6 +380,7 @@ vs_status vs_create(const vs_config* cfg, vs_ctx** out) {
     else if (c->cfg.atom_upper_bound < 0 || c->cfg.atom_upper_bound > kMaxAtoms) st = bad("atom_upper_bound must be in [0, 256]");
     else if (c->cfg.rot_upper_bound < 0 || c->cfg.rot_upper_bound > kMaxFrags) st = bad("rot_upper_bound must be in [0, 32]");
     else if (c->cfg.world_size < 1 || c->cfg.rank < 0 || c->cfg.rank >= c->cfg.world_size) st = bad("bad rank / world_size");
+    else if (c->cfg.bucket_capacity < 0) st = bad("bucket_capacity must be >= 0");
     if (st != VS_OK) {
         delete c;
         return st;

@@ -129,6 +129,20 @@ def ligands(n: int, seed: int, atoms=(20, 120), rot=(0, 20), first: int = 0, nth
     return Library(ids, ao, xyz, fo, frags, M)
 
 
+def replicate(lib: Library, i: int, n: int) -> Library:
+    """n copies of ligand i of `lib`, differing only in id."""
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    x, f = lib.ligand(i)
+    A, R = len(x), len(f)
+    ao = np.arange(n + 1, dtype=np.int64) * A
+    fo = np.arange(n + 1, dtype=np.int64) * R
+    xyz = np.tile(x, (n, 1)).astype(np.float32)
+    fr = np.tile(f, (n, 1)).astype(np.int32).reshape(-1, 4)
+    nm = None if lib.n_moving is None else np.full(n, lib.n_moving[i], np.int32)
+    return Library(np.arange(n, dtype=np.uint64), ao, xyz, fo, fr, nm)
+
+
 # ----------------------------------------------------------------------------- pocket
 
 @dataclass
