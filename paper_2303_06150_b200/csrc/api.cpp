@@ -311,7 +311,7 @@ const char* vcode_msg(int code) {
 }
 
 // Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1.
-vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps) {
+vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs, int ps) {
     c->classes.clear();
     for (size_t i = 0; i < atom_b.size(); ++i) {
         ClassInfo ci{};
@@ -337,16 +337,16 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int ps
             const int PPW = pr.first, NW = pr.second;
             if (c->K > 32 / PPW) continue;
             const int LC = ligs_per_cta(NW, PPW, c->P);
-            const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, ps, c->P, c->K, c->cfg.n_sweeps, LC);
+            const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC);
             int b = 0;
-            CK(dock_occupancy(ci.AC, NW, PPW, L.total, &b));
+            CK(dock_occupancy(ci.AC, NW, PPW, grid_fixed(rs, ps), L.total, &b));
             if (b >= 1) {
                 ci.NW = NW;
                 ci.PPW = PPW;
                 ci.LC = LC;
                 ci.b = b;
                 ci.smem = L.total;
-                CK(dock_kernel_attrs(ci.AC, NW, PPW, &ci.attr));
+                CK(dock_kernel_attrs(ci.AC, NW, PPW, grid_fixed(rs, ps), &ci.attr));
                 break;
             }
         }
@@ -653,14 +653,15 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->atom_b = atom_bounds(c->cfg.n_atom_clusters, ubA);
     c->rot_b = rot_bounds(c->cfg.n_rot_clusters, ubR);
     if ((int)c->rot_b.size() > kMaxRotClasses) return fail(c, VS_E_ARG, "too many rotamer classes");
-    int nz_max = 0, ps_max = 0;
+    int nz_max = 0, rs_max = 0, ps_max = 0;
     for (auto& pk : c->pkdev) {
         if ((int64_t)pk.nz * pk.ps > (int64_t)nz_max * ps_max) {
             nz_max = pk.nz;
             ps_max = pk.ps;
+            rs_max = pk.rs;
         }
     }
-    st = plan_classes(c, c->atom_b, nz_max, ps_max);
+    st = plan_classes(c, c->atom_b, nz_max, rs_max, ps_max);
     if (st) return st;
     const int nRc = (int)c->rot_b.size();
     const int n_cells = (int)c->atom_b.size() * nRc;
@@ -858,7 +859,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.dbg_score = c->d_dbg_score[q];
             a.dbg_angles = c->d_dbg_ang[q];
             a.counter = d_counters + dock_launches;
-            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.nz, a.pk.ps, c->P, c->K, S_w, ci.LC);
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.nz, a.pk.rs, a.pk.ps, c->P, c->K, S_w, ci.LC);
             const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];
@@ -1060,7 +1061,7 @@ vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* 
     CK(cudaMemcpy(dg, ph.grid.data(), gb, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dx, xyz, (size_t)n * 12, cudaMemcpyHostToDevice));
     PocketDev pk = make_pocket_dev(ph.d, dg);
-    const size_t smem = align16((size_t)pk.nz * pk.ps * 4);
+    const size_t smem = align16(((size_t)(pk.nz + 1) * pk.ps + pk.rs + 2) * 4);
     CK(launch_score_points(pk, dx, n, dout, smem, c->main));
     CK(cudaMemcpyAsync(g_out, dout, (size_t)n * 4, cudaMemcpyDeviceToHost, c->main));
     CK(cudaStreamSynchronize(c->main));

@@ -99,23 +99,32 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float t) {
 // floor(m) for 0 <= m < 2^23 is the round-down sum m + 2^23 (its bits also give the
 // integer); identical values to floorf.  The x-lerps run on (z0, z1) pairs, the
 // y-lerp on the (l0, l1) pair: per element the same fma sequence as the scalar form.
+//
+// The upper edge (u_c = n-1) takes i0 = n-1 with f = 0 instead of i0 = n-2 with f = 1:
+// both reduce exactly to the node value (lerp(a, b, 0) = a, lerp(a, b, 1) = b bitwise),
+// and the corner at n is a finite zero pad of the shared-memory copy, so no clamp of
+// i0 is needed.  FIX: the 32x32-plane layout with compile-time strides (33, 1063)
+// that lets every corner load use an immediate offset.
+constexpr int kFixRS = 33, kFixPS = 1063;
+template <bool FIX>
 __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
+    const int RS = FIX ? kFixRS : pk.rs, PS = FIX ? kFixPS : pk.ps;
     const float cx = fminf(fmaxf(ux, 0.f), pk.top_x);
     const float cy = fminf(fmaxf(uy, 0.f), pk.top_y);
     const float cz = fminf(fmaxf(uz, 0.f), pk.top_z);
     const float2 dxy = __fadd2_rn(make_float2(ux, uy), make_float2(-cx, -cy));
     const float e = __fadd_rn(__fadd_rn(fabsf(dxy.x), fabsf(dxy.y)), fabsf(__fsub_rn(uz, cz)));
-    const float2 bxy = __fadd2_rd(make_float2(fminf(cx, pk.top2_x), fminf(cy, pk.top2_y)), f2(kMagic));
-    const float bz = __fadd_rd(fminf(cz, pk.top2_z), kMagic);
+    const float2 bxy = __fadd2_rd(make_float2(cx, cy), f2(kMagic));
+    const float bz = __fadd_rd(cz, kMagic);
     const float2 fxy = __fadd2_rn(make_float2(cx, cy), neg2(__fadd2_rn(bxy, f2(-kMagic))));
     const float fz = __fsub_rn(cz, __fsub_rn(bz, kMagic));
-    const int idx = (__float_as_int(bxy.x) - kMagicBits) + (__float_as_int(bxy.y) - kMagicBits) * pk.rs +
-                    (__float_as_int(bz) - kMagicBits) * pk.ps;
+    const int idx = (__float_as_int(bxy.x) - kMagicBits) + (__float_as_int(bxy.y) - kMagicBits) * RS +
+                    (__float_as_int(bz) - kMagicBits) * PS;
     const float* p = G + idx;
-    const float2 c00 = make_float2(p[0], p[pk.ps]);                    // (c000, c001)
-    const float2 c10 = make_float2(p[1], p[pk.ps + 1]);                // (c100, c101)
-    const float2 c01 = make_float2(p[pk.rs], p[pk.ps + pk.rs]);        // (c010, c011)
-    const float2 c11 = make_float2(p[pk.rs + 1], p[pk.ps + pk.rs + 1]);// (c110, c111)
+    const float2 c00 = make_float2(p[0], p[PS]);                 // (c000, c001)
+    const float2 c10 = make_float2(p[1], p[PS + 1]);             // (c100, c101)
+    const float2 c01 = make_float2(p[RS], p[PS + RS]);           // (c010, c011)
+    const float2 c11 = make_float2(p[RS + 1], p[PS + RS + 1]);   // (c110, c111)
     const float2 l_0 = lerp2(c00, c10, fxy.x);     // (l00, l01): y0, z0/z1
     const float2 l_1 = lerp2(c01, c11, fxy.x);     // (l10, l11): y1, z0/z1
     const float2 l = lerp2(l_0, l_1, fxy.y);       // (l0, l1)
@@ -147,9 +156,13 @@ __device__ __forceinline__ RotT load_pose(const float* T) {
     return M;
 }
 
-// Stage the pocket grid into shared memory with padded strides.
+// Stage the pocket grid into shared memory with padded strides; the padding (and
+// the zero plane/row above the grid) is zero-filled first.  Ends with a barrier.
 __device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int n4 = (int)(align16(((size_t)(pk.nz + 1) * pk.ps + pk.rs + 2) * 4) / 16);
+    for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
     for (int row = w; row < pk.ny * pk.nz; row += nw) {
         const int z = row / pk.ny, y = row - z * pk.ny;
         const float* src = pk.grid + (size_t)row * pk.nx;
@@ -183,7 +196,7 @@ struct PoseBuf {
 
 // PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
 // a6 placement, a7 sweep, a9 pose score.
-template <int AC, int PPW>
+template <int AC, int PPW, bool FIX>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, PoseBuf<AC> B, const float* __restrict__ G,
                                            const PocketDev& pk, int K, int kbits, int S_w, float ck, float sk,
@@ -229,7 +242,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                         for (int u = 0; u < 4; ++u) q[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
                         float g[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) g[u] = grid_g(G, q[u].x, q[u].y, q[u].z, pk);
+                        for (int u = 0; u < 4; ++u) g[u] = grid_g<FIX>(G, q[u].x, q[u].y, q[u].z, pk);
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
                             if (base + u * apw + jl < hi) acc = __fadd_rn(acc, g[u]);
@@ -241,8 +254,8 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                     const float4 v1 = B.get(j1 < hi ? j1 : j0);
                     const float4 p0 = apply_rot(M, v0.x, v0.y, v0.z);
                     const float4 p1 = apply_rot(M, v1.x, v1.y, v1.z);
-                    const float g0 = grid_g(G, p0.x, p0.y, p0.z, pk);
-                    const float g1 = grid_g(G, p1.x, p1.y, p1.z, pk);
+                    const float g0 = grid_g<FIX>(G, p0.x, p0.y, p0.z, pk);
+                    const float g1 = grid_g<FIX>(G, p1.x, p1.y, p1.z, pk);
                     acc = __fadd_rn(acc, g0);
                     if (j1 < hi) acc = __fadd_rn(acc, g1);
                 }
@@ -251,7 +264,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                     if (j < hi) {
                         const float4 v = B.get(j);
                         keep = apply_rot(M, v.x, v.y, v.z);
-                        acc = __fadd_rn(acc, grid_g(G, keep.x, keep.y, keep.z, pk));
+                        acc = __fadd_rn(acc, grid_g<FIX>(G, keep.x, keep.y, keep.z, pk));
                     }
                 }
                 // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
@@ -287,7 +300,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     float acc = 0.f;
     for (int i = li; i < A; i += LPP) {
         const float4 v = B.get(i);
-        acc = __fadd_rn(acc, grid_g(G, v.x, v.y, v.z, pk));
+        acc = __fadd_rn(acc, grid_g<FIX>(G, v.x, v.y, v.z, pk));
     }
 #pragma unroll
     for (int o = LPP / 2; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
@@ -295,14 +308,14 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     __syncwarp();
 }
 
-template <int AC, int NW, int PPW>
+template <int AC, int NW, int PPW, bool FIX>
 __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_round;
     constexpr int LPP = 32 / PPW;
     const PocketDev& pk = a.pk;
     const int LC = a.ligs_per_cta;
-    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.ps, a.P, a.K, a.S_w, LC);
+    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sPose = reinterpret_cast<float*>(smem + L.pose);
     float* sCS = reinterpret_cast<float*>(smem + L.cs);
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             const bool valid = p < P;
             const int pc = valid ? p : P - 1;
             const int4 m = a.meta[slot0 + l];
-            dock_poses<AC, PPW>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w,
+            dock_poses<AC, PPW, FIX>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w,
                                 ck, sk, sCS, sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncthreads();
@@ -431,6 +444,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const i
     }
 }
 
+template <bool FIX>
 __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, const float* __restrict__ xyz,
                                                             int64_t n, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -441,54 +455,67 @@ __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, 
         const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
         const float uy = __fmul_rn(__fsub_rn(xyz[3 * i + 1], pk.oy), pk.inv_h);
         const float uz = __fmul_rn(__fsub_rn(xyz[3 * i + 2], pk.oz), pk.inv_h);
-        out[i] = grid_g(sG, ux, uy, uz, pk);
+        out[i] = grid_g<FIX>(sG, ux, uy, uz, pk);
     }
 }
 
 using DockFn = void (*)(const DockArgs);
 
-template <int AC>
+template <int AC, bool FIX>
 DockFn pick_ac(int NW, int PPW) {
-    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1> : (NW == 16 ? dock_kernel<AC, 16, 1> : nullptr);
-    if (PPW == 2) return NW == 32 ? dock_kernel<AC, 32, 2> : (NW == 16 ? dock_kernel<AC, 16, 2> : (NW == 8 ? dock_kernel<AC, 8, 2> : nullptr));
-    if (PPW == 4) return NW == 16 ? dock_kernel<AC, 16, 4> : (NW == 8 ? dock_kernel<AC, 8, 4> : (NW == 4 ? dock_kernel<AC, 4, 4> : nullptr));
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, FIX> : (NW == 16 ? dock_kernel<AC, 16, 1, FIX> : nullptr);
+    if (PPW == 2)
+        return NW == 32 ? dock_kernel<AC, 32, 2, FIX>
+                        : (NW == 16 ? dock_kernel<AC, 16, 2, FIX> : (NW == 8 ? dock_kernel<AC, 8, 2, FIX> : nullptr));
+    if (PPW == 4)
+        return NW == 16 ? dock_kernel<AC, 16, 4, FIX>
+                        : (NW == 8 ? dock_kernel<AC, 8, 4, FIX> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX> : nullptr));
     return nullptr;
 }
 
-DockFn pick(int AC, int NW, int PPW) {
+template <bool FIX>
+DockFn pick_fix(int AC, int NW, int PPW) {
     switch (AC) {
-        case 32: return pick_ac<32>(NW, PPW);
-        case 64: return pick_ac<64>(NW, PPW);
-        case 96: return pick_ac<96>(NW, PPW);
-        case 128: return pick_ac<128>(NW, PPW);
-        case 160: return pick_ac<160>(NW, PPW);
-        case 192: return pick_ac<192>(NW, PPW);
-        case 224: return pick_ac<224>(NW, PPW);
-        case 256: return pick_ac<256>(NW, PPW);
+        case 32: return pick_ac<32, FIX>(NW, PPW);
+        case 64: return pick_ac<64, FIX>(NW, PPW);
+        case 96: return pick_ac<96, FIX>(NW, PPW);
+        case 128: return pick_ac<128, FIX>(NW, PPW);
+        case 160: return pick_ac<160, FIX>(NW, PPW);
+        case 192: return pick_ac<192, FIX>(NW, PPW);
+        case 224: return pick_ac<224, FIX>(NW, PPW);
+        case 256: return pick_ac<256, FIX>(NW, PPW);
         default: return nullptr;
     }
 }
 
+DockFn pick(int AC, int NW, int PPW, int fix) { return fix ? pick_fix<true>(AC, NW, PPW) : pick_fix<false>(AC, NW, PPW); }
+
 }  // namespace
 
-// Padded shared-memory strides: row stride nx + 1 and plane stride (nx + 1) * ny + 7
-// (chosen with tools/bank_sim.py: 2.5-way instead of 6.2-way bank conflicts on the
-// sweep's corner gathers for 32^3 grids).  VSDOCK_GRID_PAD="dr,dp" overrides.
+// Padded shared-memory strides (tools/bank_sim.py: 2.5-way instead of 6.2-way bank
+// conflicts on the sweep's corner gathers).  Grids of at most 32 x 32 per plane use
+// the fixed layout (33, 1063) with compile-time strides; larger planes use
+// (nx + 1, (nx + 1) * ny + 7).
 void grid_strides(int nx, int ny, int* rs, int* ps) {
-    int dr = 1, dp = 7;
-    if (const char* e = getenv("VSDOCK_GRID_PAD")) sscanf(e, "%d,%d", &dr, &dp);
-    *rs = nx + dr;
-    *ps = (nx + dr) * ny + dp;
+    if (nx <= 32 && ny <= 32) {
+        *rs = kFixRS;
+        *ps = kFixPS;
+    } else {
+        *rs = nx + 1;
+        *ps = (nx + 1) * ny + 7;
+    }
 }
 
-cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, cudaFuncAttributes* attr) {
-    DockFn f = pick(AC, NW, PPW);
+bool grid_fixed(int rs, int ps) { return rs == kFixRS && ps == kFixPS; }
+
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, cudaFuncAttributes* attr) {
+    DockFn f = pick(AC, NW, PPW, fix);
     if (!f) return cudaErrorInvalidValue;
     return cudaFuncGetAttributes(attr, reinterpret_cast<const void*>(f));
 }
 
-cudaError_t dock_occupancy(int AC, int NW, int PPW, size_t smem, int* blocks_per_sm) {
-    DockFn f = pick(AC, NW, PPW);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, size_t smem, int* blocks_per_sm) {
+    DockFn f = pick(AC, NW, PPW, fix);
     if (!f) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -502,7 +529,7 @@ cudaError_t dock_occupancy(int AC, int NW, int PPW, size_t smem, int* blocks_per
 }
 
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
-    DockFn f = pick(AC, NW, PPW);
+    DockFn f = pick(AC, NW, PPW, grid_fixed(a.pk.rs, a.pk.ps));
     if (!f) return cudaErrorInvalidValue;
     if (a.n <= 0) return cudaSuccess;
     f<<<grid, NW * 32, smem, st>>>(a);
@@ -534,10 +561,13 @@ cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, 
 
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
                                 cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(score_points_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool fix = grid_fixed(pk.rs, pk.ps);
+    const void* f = fix ? reinterpret_cast<const void*>(score_points_kernel<true>)
+                        : reinterpret_cast<const void*>(score_points_kernel<false>);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    score_points_kernel<<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    if (fix) score_points_kernel<true><<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    else score_points_kernel<false><<<148, 1024, smem, st>>>(pk, xyz, n, out);
     return cudaGetLastError();
 }
 

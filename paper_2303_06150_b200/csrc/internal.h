@@ -56,11 +56,12 @@ struct DockLayout {
     size_t grid, pose, cs, rec, buf, score, ang, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
-__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int ps, int P, int K, int S_w,
-                                                  int LC) {
+__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int rs, int ps, int P, int K,
+                                                  int S_w, int LC) {
     DockLayout L;
     size_t o = 0;
-    L.grid = o;  o += align16((size_t)nz * ps * 4);
+    // grid planes + one zero plane and row above: corner reads at i0 + 1 = n (weight 0) stay in bounds
+    L.grid = o;  o += align16(((size_t)(nz + 1) * ps + rs + 2) * 4);
     L.pose = o;  o += align16((size_t)P * 12 * 4);
     L.cs = o;    o += align16((size_t)K * 2 * 4);
     L.rec = o;   o += align16((size_t)LC * (3 * AC + 32) * 4);
@@ -100,8 +101,9 @@ cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const 
                         const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
                         int4* meta, cudaStream_t st);
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
-cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, cudaFuncAttributes* attr);
-cudaError_t dock_occupancy(int AC, int NW, int PPW, size_t smem, int* blocks_per_sm);
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, cudaFuncAttributes* attr);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, size_t smem, int* blocks_per_sm);
+bool grid_fixed(int rs, int ps);
 cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
                                 cudaStream_t st);
