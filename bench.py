@@ -252,12 +252,15 @@ def main():
 
     e2e = None
     if not args.no_e2e:
+        # the public host-to-results call (Engine.submit from pinned host buffers): H2D of the
+        # library inside the step, D2H of every ligand's best score and pose at its end
         hs = torch.empty(n, dtype=torch.float32).pin_memory()
         hp = torch.empty(n, dtype=torch.int32).pin_memory()
         t_e, _, _, _ = timed(eng, ids, h_lib, False, host_out=(hs, hp))
         d2h = len(pockets) * (n * 8 + K_TOP * 8)
         e2e = {"value": n * len(pockets) / (t_e / args.steps / 1e3), "unit": "ligands/s",
-               "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h}
+               "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
+               "api": "Engine.submit(host pinned CSR) + results D2H, CUDA events"}
     unsorted = None
     if not args.no_unsorted:
         eng.close()

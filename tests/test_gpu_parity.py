@@ -306,3 +306,20 @@ def test_c4_full_size_sampled_parity():
     rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, xyz, band=BAND,
                        tol_score=TOL_S, tol_xyz=TOL_X)
     assert rep.ok, rep.summary() + str(rep.failures[:5])
+
+
+def test_pipelined_docker_matches_single_submit(c2):
+    """Double-buffered chunks give the single-submit results and ranking."""
+    import torch
+    from paper_2303_06150_b200.pipeline import PipelinedDocker
+    c, lib, pk = c2
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    r = e.results(0)
+    pd = PipelinedDocker(n_buffers=2)
+    pd.setup(rot, tr, cs, [pk])
+    h = [torch.from_numpy(a).pin_memory() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    best, pose, tops = pd.run(*h, k=100, chunks=3)
+    assert np.max(np.abs(best[0] - r.best_score) / np.maximum(1, np.abs(r.best_score))) < 2 * TOL_S
+    assert list(tops[0][0]) == list(oracle.topk(best[0], 100))
+    assert np.array_equal(tops[0][1], best[0][tops[0][0]])
+    pd.close()
