@@ -1,0 +1,72 @@
+"""Input generators (SPEC dataset invariants) and the bench.py contract of the reference arm."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import vsgen
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_generator_ranges_determinism_and_prefix_stability():
+    a = vsgen.ligands(300, 9, (20, 120), (0, 20))
+    b = vsgen.ligands(300, 9, (20, 120), (0, 20))
+    for f in ("atom_off", "xyz", "frag_off", "frags"):
+        assert np.array_equal(getattr(a, f), getattr(b, f))          # S:68 determinism
+    assert ((a.n_atoms >= 20) & (a.n_atoms <= 120)).all()             # S:39 in range
+    assert ((a.n_frags >= 0) & (a.n_frags <= 20)).all()
+    tail = vsgen.ligands(100, 9, (20, 120), (0, 20), first=200)       # ligand i depends only on (seed, i)
+    for i in range(100):
+        x1, f1 = a.ligand(200 + i)
+        x2, f2 = tail.ligand(i)
+        assert np.array_equal(x1, x2) and np.array_equal(f1, f2)
+    assert vsgen.ligands(0, 1).n == 0
+    d = vsgen.ligands(3, 5, (5, 5), (0, 0))                            # S:44 degenerate ranges
+    assert list(d.n_atoms) == [5, 5, 5] and list(d.n_frags) == [0, 0, 0]
+    with pytest.raises(ValueError):
+        vsgen.ligands(3, 1, (10, 5), (0, 1))                           # S:40 inverted range
+
+
+def test_generated_fragments_are_valid_rotatable_bonds():
+    lib = vsgen.ligands(200, 3, (20, 120), (0, 20))
+    for i in range(lib.n):
+        x, fr = lib.ligand(i)
+        A = len(x)
+        for a, b, lo, hi in fr:
+            assert 0 <= a < A and 0 <= b < A and a != b
+            assert 0 <= lo < hi <= A and not (lo <= a < hi) and not (lo <= b < hi)
+            assert abs(np.linalg.norm(x[b] - x[a]) - 1.5) < 1e-4     # a -> b is a bond
+        assert int(np.sum(fr[:, 3] - fr[:, 2])) == int(lib.n_moving[i])
+
+
+def test_replicate():
+    lib = vsgen.ligands(2, 4, (53, 53), (4, 4))
+    r = vsgen.replicate(lib, 1, 4)
+    assert r.n == 4 and len(set(r.ligand_id.tolist())) == 4
+    for i in range(4):
+        assert np.array_equal(r.ligand(i)[0], lib.ligand(1)[0]) and np.array_equal(r.ligand(i)[1], lib.ligand(1)[1])
+    assert vsgen.replicate(lib, 0, 1).n == 1
+
+
+def test_tables():
+    rot, tr = vsgen.pose_table(16, 7)
+    assert np.array_equal(rot[0], np.eye(3, dtype=np.float32)) and not tr.any()
+    cs = vsgen.angle_table(8)
+    assert cs[0, 0] == 1.0 and cs[0, 1] == 0.0
+    assert np.allclose(np.hypot(cs[:, 0], cs[:, 1]), 1.0, atol=1e-7)
+
+
+def test_bench_reference_arm_json_contract():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "config",
+              "cpu_baseline", "e2e", "impl"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
