@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--n", type=int, default=0, help="override the ligand count (not a bench value)")
+    ap.add_argument("--ligands", type=int, default=0, help="override the ligand count (not a bench value)")
     ap.add_argument("--no-unsorted", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -96,8 +96,8 @@ class Clocks:
 def workload(args):
     import vsgen
     c = dict(vsgen.CONFIGS[args.config])
-    if args.n:
-        c["n"] = args.n
+    if args.ligands:
+        c["n"] = args.ligands
     lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
     pockets = [vsgen.pocket(s) for s in c["pockets"]]
     rot, tr = vsgen.pose_table(c["P"])
@@ -175,10 +175,24 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook for the multi-rank path on a one-GPU box: every rank on device 0 over gloo
+    # (NCCL refuses two ranks on one GPU).  Never set for a measurement.
+    single_box = os.environ.get("VSDOCK_BENCH_SAME_DEVICE") == "1"
+    if single_box:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if single_box:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
+
+    def reduce_scalar(v, op):
+        x = torch.tensor([float(v)], device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(x, op=op)
+        return float(x.item())
+
     c, lib, pockets, rot, tr, cs = workload(args)
     K_TOP = 1000
     n = lib.n
@@ -230,9 +244,7 @@ def main():
             torch.cuda.synchronize()
         t = ev0.elapsed_time(ev1)
         if world > 1:
-            x = torch.tensor([t], device=dev)
-            dist.all_reduce(x, op=dist.ReduceOp.MAX)
-            t = float(x.item())
+            t = reduce_scalar(t, dist.ReduceOp.MAX)
         return t, dock_ms, launches, evals
 
     eng, ids = make_engine(6, 23)
@@ -245,9 +257,7 @@ def main():
     evals_step = evals / args.steps
     achieved = FLOPS_PER_EVAL * evals_step / (dock_avg / 1e3) / 1e12
     if world > 1:
-        x = torch.tensor([achieved], device=dev)
-        dist.all_reduce(x, op=dist.ReduceOp.MIN)
-        achieved = float(x.item())
+        achieved = reduce_scalar(achieved, dist.ReduceOp.MIN)
     classes = eng.classes()
 
     e2e = None

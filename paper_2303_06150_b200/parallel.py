@@ -21,14 +21,15 @@ def gather_keys(keys_local: torch.Tensor, group=None) -> torch.Tensor:
     world = dist.get_world_size(group)
     if world == 1:
         return keys_local
-    out = torch.empty(world * keys_local.numel(), dtype=keys_local.dtype, device=keys_local.device)
-    if keys_local.is_cuda:
-        dist.all_gather_into_tensor(out, keys_local, group=group)
-    else:  # gloo
-        parts = [torch.empty_like(keys_local) for _ in range(world)]
-        dist.all_gather(parts, keys_local, group=group)
-        out = torch.cat(parts)
-    return out
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(world * keys_local.numel(), dtype=keys_local.dtype, device=keys_local.device)
+        dist.all_gather_into_tensor(out, keys_local, group=group)   # NVLink / NVSwitch
+        return out
+    # gloo (CPU tests, single-GPU test hook): host staging
+    host = keys_local.detach().cpu()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    return torch.cat(parts).to(keys_local.device)
 
 
 def global_topk(engine, slot: int, k: int, group=None):
