@@ -1,0 +1,527 @@
+// dock_impl.cuh -- the docking kernel (a6-a9): rigid roto-translation from P initial
+// poses, greedy rotatable-bond sweep over K discrete angle steps, trilinear
+// pocket-grid score, best-pose reduction.  fp32 on CUDA cores (not a dense
+// contraction, BJ: "no tensor cores").
+//
+// B200 design:
+//  * one CTA per SM, persistent over a launch's ligands with a dynamic round
+//    counter; the pocket grid (32^3 fp32 = 128 KB, padded strides) lives in
+//    SHARED memory for the whole launch -- the 8 corner gathers of every
+//    evaluation are shared-memory loads, never L1/L2;
+//  * a CTA docks LC ligands at a time; its NW warps split the ligand's poses,
+//    PPW poses per warp (lane groups of 32/PPW), so all warps of a CTA run the
+//    same control flow (same A, R, M_r: poses of one ligand differ only in data);
+//  * sweep lane map inside a pose group: li = jl * K + k -- (moving atom jl of
+//    the pass, angle k).  Each lane holds its angle's rotation in registers,
+//    lanes of equal k sum with xor shuffles, the argmin over k takes log2 K
+//    shuffle rounds (ties -> lowest k, Q11), and the winner is applied;
+//  * (x, y) arithmetic is packed in Blackwell's FFMA2/FADD2 (per-element IEEE
+//    fma/add, so every result is bit-identical to the scalar form);
+//  * template<int AC, int NW, int PPW> per atom class = the paper's "non-type
+//    template parameter for the kernel maximum number of atoms":
+//    AC sizes the per-pose buffers in shared memory, hence the occupancy.
+//
+// All arithmetic that decides an angle or is replayed (placement, Rodrigues,
+// rotation, interpolation) uses explicit _rn intrinsics in shared helpers, so
+// the finalize kernel reproduces the trajectory bit for bit.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace vsd {
+
+namespace dk {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr float kMagic = 8388608.f;              // 2^23: floor via round-down add
+constexpr int kMagicBits = 0x4B000000;
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+// Rotation about a pivot in "M v + t" form: p = M v + t with t = q - M q.
+// Rows 0 and 1 are packed column-wise: c0 = (m00, m10), c1 = (m01, m11), c2 = (m02, m12).
+struct RotT {
+    float2 c0, c1, c2, txy;
+    float m20, m21, m22, tz;
+};
+
+// M = c I + s [u]x + (1 - c) u u^T (a7; Q3, Q6), pivot q = y_b.  For (c, s) = (1, 0)
+// this is exactly I and t = 0, so the identity candidate leaves coordinates bit-unchanged.
+// Rows 0 and 1 run as FFMA2/FMUL2 pairs (per element the same IEEE op as the scalar form).
+__device__ __forceinline__ RotT rodrigues_t(float ux, float uy, float uz, float c, float s, float qx, float qy,
+                                            float qz) {
+    const float omc = __fsub_rn(1.f, c);
+    const float2 ab = __fmul2_rn(f2(omc), make_float2(ux, uy));          // (a, b) = (1 - c) (ux, uy)
+    const float d = __fmul_rn(omc, uz);
+    const float2 sxy = __fmul2_rn(f2(s), make_float2(ux, uy));           // (sx, sy)
+    const float sz = __fmul_rn(s, uz);
+    RotT M;
+    M.c0 = __ffma2_rn(ab, f2(ux), make_float2(c, sz));                   // (m00, m10)
+    M.c1 = __ffma2_rn(ab, f2(uy), make_float2(-sz, c));                  // (m01, m11)
+    M.c2 = __ffma2_rn(ab, f2(uz), make_float2(sxy.y, -sxy.x));           // (m02, m12)
+    M.m20 = __fmaf_rn(d, ux, -sxy.y);
+    M.m21 = __fmaf_rn(d, uy, sxy.x);
+    M.m22 = __fmaf_rn(d, uz, c);
+    // t = q - M q
+    M.txy = __ffma2_rn(neg2(M.c0), f2(qx), __ffma2_rn(neg2(M.c1), f2(qy), __ffma2_rn(neg2(M.c2), f2(qz),
+                                                                                      make_float2(qx, qy))));
+    M.tz = __fmaf_rn(-M.m20, qx, __fmaf_rn(-M.m21, qy, __fmaf_rn(-M.m22, qz, qz)));
+    return M;
+}
+
+// p = M v + t; (x, y) in one FFMA2 chain, z scalar
+__device__ __forceinline__ float4 apply_rot(const RotT& M, float vx, float vy, float vz) {
+    const float2 pxy = __ffma2_rn(M.c0, f2(vx), __ffma2_rn(M.c1, f2(vy), __ffma2_rn(M.c2, f2(vz), M.txy)));
+    const float pz = __fmaf_rn(M.m20, vx, __fmaf_rn(M.m21, vy, __fmaf_rn(M.m22, vz, M.tz)));
+    return make_float4(pxy.x, pxy.y, pz, 0.f);
+}
+
+// unit axis a -> b
+__device__ __forceinline__ void axis_of(const float4& ya, const float4& yb, float& ux, float& uy, float& uz) {
+    const float dx = __fsub_rn(yb.x, ya.x), dy = __fsub_rn(yb.y, ya.y), dz = __fsub_rn(yb.z, ya.z);
+    const float n2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+    const float inv = rsqrtf(n2);
+    ux = __fmul_rn(dx, inv);
+    uy = __fmul_rn(dy, inv);
+    uz = __fmul_rn(dz, inv);
+}
+
+__device__ __forceinline__ float lerp(float a, float b, float t) { return __fmaf_rn(t, b, __fmaf_rn(-t, a, a)); }
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float t) {
+    return __ffma2_rn(f2(t), b, __ffma2_rn(f2(-t), a, a));
+}
+
+// a8: g(u), u in grid units (Q9, Q10): clamp, L1 excess, i0 = min(floor(u_c), n-2),
+// lerps x then y then z, + kappa*h*excess.  G is the shared-memory copy (strides rs, ps).
+// floor(m) for 0 <= m < 2^23 is the round-down sum m + 2^23 (its bits also give the
+// integer); identical values to floorf.  The x-lerps run on (z0, z1) pairs, the
+// y-lerp on the (l0, l1) pair: per element the same fma sequence as the scalar form.
+//
+// The upper edge (u_c = n-1) takes i0 = n-1 with f = 0 instead of i0 = n-2 with f = 1:
+// both reduce exactly to the node value (lerp(a, b, 0) = a, lerp(a, b, 1) = b bitwise),
+// and the corner at n is a finite zero pad of the shared-memory copy, so no clamp of
+// i0 is needed.  FIX: the 32x32-plane layout with compile-time strides (33, 1063)
+// that lets every corner load use an immediate offset.
+constexpr int kFixRS = 33, kFixPS = 1063;
+template <bool FIX>
+__device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
+    const int RS = FIX ? kFixRS : pk.rs, PS = FIX ? kFixPS : pk.ps;
+    const float cx = fminf(fmaxf(ux, 0.f), pk.top_x);
+    const float cy = fminf(fmaxf(uy, 0.f), pk.top_y);
+    const float cz = fminf(fmaxf(uz, 0.f), pk.top_z);
+    const float2 dxy = __fadd2_rn(make_float2(ux, uy), make_float2(-cx, -cy));
+    const float e = __fadd_rn(__fadd_rn(fabsf(dxy.x), fabsf(dxy.y)), fabsf(__fsub_rn(uz, cz)));
+    const float2 bxy = __fadd2_rd(make_float2(cx, cy), f2(kMagic));
+    const float bz = __fadd_rd(cz, kMagic);
+    const float2 fxy = __fadd2_rn(make_float2(cx, cy), neg2(__fadd2_rn(bxy, f2(-kMagic))));
+    const float fz = __fsub_rn(cz, __fsub_rn(bz, kMagic));
+    const int idx = (__float_as_int(bxy.x) - kMagicBits) + (__float_as_int(bxy.y) - kMagicBits) * RS +
+                    (__float_as_int(bz) - kMagicBits) * PS;
+    const float* p = G + idx;
+    const float2 c00 = make_float2(p[0], p[PS]);                 // (c000, c001)
+    const float2 c10 = make_float2(p[1], p[PS + 1]);             // (c100, c101)
+    const float2 c01 = make_float2(p[RS], p[PS + RS]);           // (c010, c011)
+    const float2 c11 = make_float2(p[RS + 1], p[PS + RS + 1]);   // (c110, c111)
+    const float2 l_0 = lerp2(c00, c10, fxy.x);     // (l00, l01): y0, z0/z1
+    const float2 l_1 = lerp2(c01, c11, fxy.x);     // (l10, l11): y1, z0/z1
+    const float2 l = lerp2(l_0, l_1, fxy.y);       // (l0, l1)
+    return __fmaf_rn(pk.kh, e, lerp(l.x, l.y, fz));
+}
+
+// Pose p in grid units: R' = R / h, t' = (c + tau - o) / h, u = R' x + t'.
+// Stored as 12 floats: (R'00, R'10), (R'01, R'11), (R'02, R'12), (t'x, t'y), R'20, R'21, R'22, t'z.
+__device__ __forceinline__ void scaled_pose(const float* raw, const PocketDev& pk, float* out) {
+    float r[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) r[t] = __fmul_rn(raw[t], pk.inv_h);
+    out[0] = r[0]; out[1] = r[3];
+    out[2] = r[1]; out[3] = r[4];
+    out[4] = r[2]; out[5] = r[5];
+    out[6] = __fadd_rn(pk.tx, __fmul_rn(raw[9], pk.inv_h));
+    out[7] = __fadd_rn(pk.ty, __fmul_rn(raw[10], pk.inv_h));
+    out[8] = r[6]; out[9] = r[7]; out[10] = r[8];
+    out[11] = __fadd_rn(pk.tz, __fmul_rn(raw[11], pk.inv_h));
+}
+
+__device__ __forceinline__ RotT load_pose(const float* T) {
+    RotT M;
+    M.c0 = make_float2(T[0], T[1]);
+    M.c1 = make_float2(T[2], T[3]);
+    M.c2 = make_float2(T[4], T[5]);
+    M.txy = make_float2(T[6], T[7]);
+    M.m20 = T[8]; M.m21 = T[9]; M.m22 = T[10]; M.tz = T[11];
+    return M;
+}
+
+// Stage the pocket grid into shared memory with padded strides; the padding (and
+// the zero plane/row above the grid) is zero-filled first.  Ends with a barrier.
+__device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int n4 = (int)(align16(((size_t)(pk.nz + 1) * pk.ps + pk.rs + 2) * 4) / 16);
+    for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    for (int row = w; row < pk.ny * pk.nz; row += nw) {
+        const int z = row / pk.ny, y = row - z * pk.ny;
+        const float* src = pk.grid + (size_t)row * pk.nx;
+        float* dst = sG + z * pk.ps + y * pk.rs;
+        for (int x = lane; x < pk.nx; x += 32) dst[x] = src[x];
+    }
+}
+
+// Order-preserving map of fp32 onto uint32 (-0 canonicalised to +0 first).
+__device__ __forceinline__ unsigned ord32(float v) {
+    const unsigned b = __float_as_uint(__fadd_rn(v, 0.0f));
+    return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
+}
+
+// Per-pose buffer stride in float4: AC + 1 so that the PPW pose groups of a warp
+// read their buffers from different banks.
+// Per-pose coordinate buffer in shared memory, SoA: x[AC] | y[AC] | z[AC] (12 B per atom),
+// pose buffers 3*AC + 4 floats apart so the PPW pose groups of a warp hit different banks.
+template <int AC>
+__host__ __device__ constexpr int pose_stride() { return 3 * AC + 4; }
+template <int AC>
+struct PoseBuf {
+    float* b;
+    __device__ __forceinline__ float4 get(int j) const { return make_float4(b[j], b[AC + j], b[2 * AC + j], 0.f); }
+    __device__ __forceinline__ void set(int j, float4 v) const {
+        b[j] = v.x;
+        b[AC + j] = v.y;
+        b[2 * AC + j] = v.z;
+    }
+};
+
+// U independent sweep evaluations per lane: atoms j0, j0 + apw, ... (j < hi), rotated by M,
+// scored, summed into acc in ascending order; the rotated atoms stay in kp[0..U).
+template <int U, bool FIX, int AC>
+__device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, const float* __restrict__ G,
+                                           const PocketDev& pk, int j0, int apw, int hi, float& acc, float4 (&kp)[4]) {
+    float4 v[U];
+    float g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = j0 + u * apw;
+        v[u] = B.get(j < hi ? j : j0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) kp[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
+#pragma unroll
+    for (int u = 0; u < U; ++u) g[u] = grid_g<FIX>(G, kp[u].x, kp[u].y, kp[u].z, pk);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (j0 + u * apw < hi) acc = __fadd_rn(acc, g[u]);
+}
+
+// PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
+// a6 placement, a7 sweep, a9 pose score.
+template <int AC, int PPW, bool FIX>
+__device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
+                                           bool valid, PoseBuf<AC> B, const float* __restrict__ G,
+                                           const PocketDev& pk, int K, int kbits, int S_w, float ck, float sk,
+                                           const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
+                                           float* __restrict__ scoreOut, int lane) {
+    constexpr int LPP = 32 / PPW;
+    const int li = lane & (LPP - 1);
+    const float* rx = rec;
+    const float* ry = rec + AC;
+    const float* rz = rec + 2 * AC;
+    const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
+    {
+        const RotT Pz = load_pose(T);
+        if (valid)
+            for (int i = li; i < A; i += LPP) B.set(i, apply_rot(Pz, rx[i], ry[i], rz[i]));
+    }
+    __syncwarp();
+    if (K > 1) {
+        const int k = li & (K - 1);
+        const int jl = li >> kbits;
+        const int abits = __ffs(LPP) - 1 - kbits;     // log2(apw)
+        const int apw = 1 << abits;                   // moving atoms per step of a pose group
+        const unsigned gmask = ((K == 32) ? 0xffffffffu : ((1u << K) - 1u)) << (lane & ~(K - 1));
+        for (int sw = 0; sw < S_w; ++sw) {
+            for (int r = 0; r < R; ++r) {
+                const uint32_t f = rfr[r];
+                const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
+                const float4 ya = B.get(fa), yb = B.get(fb);
+                float ux, uy, uz;
+                axis_of(ya, yb, ux, uy, uz);
+                const RotT M = rodrigues_t(ux, uy, uz, ck, sk, yb.x, yb.y, yb.z);
+                // steps of apw atoms; the step count is warp-uniform (all pose groups of a
+                // warp dock the same ligand), so the batch dispatch below never diverges.
+                // Every lane sums its atoms in ascending order (the canonical order).
+                const int nst = (hi - lo + apw - 1) >> abits;
+                float acc = 0.f;
+                float4 kp[4];
+                int st = 0;
+                for (; st + 4 <= nst; st += 4) eval_batch<4, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp);
+                switch (nst - st) {
+                    case 3: eval_batch<3, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    case 2: eval_batch<2, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    case 1: eval_batch<1, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    default: break;
+                }
+                // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+                    if (o >= K) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                // argmin over the K angles of this group (xor offsets 1 .. K/2); ties -> lowest k (Q11)
+                const unsigned key = ord32(acc);
+                unsigned mn = key;
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+                    if (o < K) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
+                const unsigned bal = __ballot_sync(FULL, key == mn) & gmask;
+                const int bk = (__ffs(bal) - 1) & (K - 1);
+                if (nst <= 4) {
+                    // one batch: the lanes (jl, k*) still hold the rotated atoms in registers
+                    if (valid && bk != 0 && k == bk) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = lo + u * apw + jl;
+                            if (u < nst && j < hi) B.set(j, kp[u]);
+                        }
+                    }
+                } else if (valid && bk != 0) {
+                    const RotT Ms = rodrigues_t(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1], yb.x, yb.y, yb.z);
+                    for (int j = lo + li; j < hi; j += LPP) {
+                        const float4 v = B.get(j);
+                        B.set(j, apply_rot(Ms, v.x, v.y, v.z));
+                    }
+                }
+                __syncwarp();
+                if (valid && li == 0) angOut[sw * R + r] = (uint8_t)bk;
+            }
+        }
+    } else if (valid) {
+        for (int t = li; t < S_w * R; t += LPP) angOut[t] = 0;
+    }
+    // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree) (Q22)
+    float acc = 0.f;
+    for (int i = li; i < A; i += LPP) {
+        const float4 v = B.get(i);
+        acc = __fadd_rn(acc, grid_g<FIX>(G, v.x, v.y, v.z, pk));
+    }
+#pragma unroll
+    for (int o = LPP / 2; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+    if (valid && li == 0) *scoreOut = acc;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stage round `round` (LC ligand records + meta) into buffer b with cp.async (no wait).
+__device__ __forceinline__ void prefetch_round(const DockArgs& a, int round, int LC, float* sRec, int4* sMeta) {
+    const int slot0 = round * LC;
+    const int nl = min(LC, a.n - slot0);
+    const float4* src = reinterpret_cast<const float4*>(a.rec + (size_t)slot0 * a.rec_floats);
+    float4* dst = reinterpret_cast<float4*>(sRec);
+    const int n4 = nl * a.rec_floats / 4;
+    for (int t = threadIdx.x; t < n4; t += blockDim.x) cp_async16(dst + t, src + t);
+    for (int t = threadIdx.x; t < nl; t += blockDim.x) cp_async16(sMeta + t, a.meta + slot0 + t);
+}
+
+template <int AC, int NW, int PPW, bool FIX>
+__global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_rounds[3];
+    constexpr int LPP = 32 / PPW;
+    const PocketDev& pk = a.pk;
+    const int LC = a.ligs_per_cta;
+    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC);
+    float* sG = reinterpret_cast<float*>(smem + L.grid);
+    float* sPose = reinterpret_cast<float*>(smem + L.pose);
+    float* sCS = reinterpret_cast<float*>(smem + L.cs);
+    float* sBuf = reinterpret_cast<float*>(smem + L.buf);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
+    auto rec_buf = [&](int b) { return reinterpret_cast<float*>(smem + L.rec + b * L.rec_b); };
+    auto meta_buf = [&](int b) { return reinterpret_cast<int4*>(smem + L.meta + b * L.meta_b); };
+    auto score_buf = [&](int b) { return reinterpret_cast<float*>(smem + L.score + b * L.score_b); };
+    auto ang_buf = [&](int b) { return smem + L.ang + b * L.ang_b; };
+
+    const int rec_floats = a.rec_floats;
+    const int n_rounds = (a.n + LC - 1) / LC;
+    // dynamic scheduling (balances CTAs within the launch): round indices are claimed two
+    // rounds ahead, so neither the counter atomic nor the record fetch is on the critical path
+    if (tid == 0) {
+        s_rounds[0] = atomicAdd(a.counter, 1);
+        s_rounds[1] = atomicAdd(a.counter, 1);
+    }
+    stage_grid(sG, pk);
+    for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
+    for (int t = tid; t < 2 * a.K; t += blockDim.x) sCS[t] = a.cs[t];
+    __syncthreads();
+    int cur = s_rounds[0];
+    if (cur < n_rounds) prefetch_round(a, cur, LC, rec_buf(0), meta_buf(0));
+    cp_async_wait_all();
+    __syncthreads();
+
+    const int K = a.K, S_w = a.S_w, P = a.P;
+    const int kbits = 31 - __clz(K);
+    const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
+    const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride<AC>()};
+    const int ang_stride = 32 * S_w;
+    const int G = (P + PPW - 1) / PPW;   // warp items per ligand
+
+    for (int i = 0; cur < n_rounds; ++i) {
+        const int b = i & 1;
+        const int nxt = s_rounds[(i + 1) % 3];
+        // rec[b ^ 1] was last read by round i - 1, which ended at the previous barrier; meta is
+        // triple-buffered because the a9 warps of round i - 1 may still read it
+        if (nxt < n_rounds) prefetch_round(a, nxt, LC, rec_buf(b ^ 1), meta_buf((i + 1) % 3));
+        if (tid == 0) s_rounds[(i + 2) % 3] = atomicAdd(a.counter, 1);   // slot last read in round i - 1
+        const int slot0 = cur * LC;
+        const int nl = min(LC, a.n - slot0);
+        const float* sRec = rec_buf(b);
+        const int4* sMeta = meta_buf(i % 3);   // triple-buffered: read by the a9 warps after the barrier
+        float* sScore = score_buf(b);
+        uint8_t* sAng = ang_buf(b);
+        for (int item = warp; item < nl * G; item += NW) {
+            const int l = item / G, g = item - l * G;
+            const int p = g * PPW + h;
+            const bool valid = p < P;
+            const int pc = valid ? p : P - 1;
+            const int4 m = sMeta[l];
+            dock_poses<AC, PPW, FIX>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w,
+                                ck, sk, sCS, sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
+        }
+        cp_async_wait_all();
+        __syncthreads();   // scores of round i complete; record of round i + 1 and s_rounds visible
+        // a9 best pose of round i (its score / angle buffers are rewritten only after the
+        // next barrier, which these warps reach after finishing)
+        if (warp >= NW - nl) {
+            const int l = NW - 1 - warp;
+            const int4 m = sMeta[l];
+            unsigned long long best = ~0ull;
+            for (int p = lane; p < P; p += 32) {
+                const unsigned long long key = ((unsigned long long)ord32(sScore[l * P + p]) << 32) | (unsigned)p;
+                best = key < best ? key : best;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+                best = ob < best ? ob : best;
+            }
+            const int bp = (int)(best & 0xffffffffu);
+            const int li = m.x, R = m.z, nang = S_w * R;
+            if (lane == 0) {
+                a.best_score[li] = sScore[l * P + bp];
+                a.best_pose[li] = bp;
+            }
+            const uint8_t* sa = sAng + (size_t)(l * P + bp) * ang_stride;
+            for (int t = lane; t < nang; t += 32) a.angles[m.w + t] = sa[t];
+            if (a.dbg_score)
+                for (int p = lane; p < P; p += 32) a.dbg_score[(size_t)li * P + p] = sScore[l * P + p];
+            if (a.dbg_angles)
+                for (int t = lane; t < P * nang; t += 32) {
+                    const int p = t / nang, q = t - p * nang;
+                    a.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
+                }
+        }
+        cur = nxt;
+    }
+}
+
+// a9 coordinates: replay p* with the recorded angles, bit-identical to the
+// dock kernel (same placement, axis, Rodrigues and rotation helpers); one warp
+// per ligand; output in Angstrom, input atom order.
+template <int AC>
+__global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const int64_t* __restrict__ atom_off,
+                                                       float* __restrict__ xyz_out) {
+    __shared__ __align__(16) float4 sb[8][AC];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int s = blockIdx.x * 8 + w;
+    if (s >= a.n) return;
+    const PocketDev& pk = a.pk;
+    const int4 m = a.meta[s];
+    const int li = m.x, A = m.y, R = m.z;
+    const int p = a.best_pose[li];
+    const float* rec = a.rec + (size_t)s * a.rec_floats;
+    const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
+    float T[12];
+    scaled_pose(a.pose_tab + 12 * p, pk, T);
+    const RotT Pz = load_pose(T);
+    float4* buf = sb[w];
+    for (int i = lane; i < A; i += 32) buf[i] = apply_rot(Pz, rec[i], rec[AC + i], rec[2 * AC + i]);
+    __syncwarp();
+    for (int sw = 0; sw < a.S_w; ++sw) {
+        for (int r = 0; r < R; ++r) {
+            const int bk = a.angles[m.w + sw * R + r];
+            if (bk != 0) {
+                const uint32_t f = rfr[r];
+                const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
+                const float4 ya = buf[fa], yb = buf[fb];
+                float ux, uy, uz;
+                axis_of(ya, yb, ux, uy, uz);
+                const RotT Ms = rodrigues_t(ux, uy, uz, a.cs[2 * bk], a.cs[2 * bk + 1], yb.x, yb.y, yb.z);
+                for (int j = lo + lane; j < hi; j += 32) {
+                    const float4 v = buf[j];
+                    buf[j] = apply_rot(Ms, v.x, v.y, v.z);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    float* out = xyz_out + 3 * atom_off[li];
+    for (int i = lane; i < A; i += 32) {
+        const float4 v = buf[i];
+        out[3 * i] = __fmaf_rn(pk.h, v.x, pk.ox);
+        out[3 * i + 1] = __fmaf_rn(pk.h, v.y, pk.oy);
+        out[3 * i + 2] = __fmaf_rn(pk.h, v.z, pk.oz);
+    }
+}
+
+template <bool FIX>
+__global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, const float* __restrict__ xyz,
+                                                            int64_t n, float* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* sG = reinterpret_cast<float*>(smem);
+    stage_grid(sG, pk);
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
+        const float uy = __fmul_rn(__fsub_rn(xyz[3 * i + 1], pk.oy), pk.inv_h);
+        const float uz = __fmul_rn(__fsub_rn(xyz[3 * i + 2], pk.oz), pk.inv_h);
+        out[i] = grid_g<FIX>(sG, ux, uy, uz, pk);
+    }
+}
+
+using DockFn = void (*)(const DockArgs);
+
+template <int AC, bool FIX>
+DockFn pick_ac(int NW, int PPW) {
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, FIX> : (NW == 16 ? dock_kernel<AC, 16, 1, FIX> : nullptr);
+    if (PPW == 2)
+        return NW == 32 ? dock_kernel<AC, 32, 2, FIX>
+                        : (NW == 16 ? dock_kernel<AC, 16, 2, FIX> : (NW == 8 ? dock_kernel<AC, 8, 2, FIX> : nullptr));
+    if (PPW == 4)
+        return NW == 16 ? dock_kernel<AC, 16, 4, FIX>
+                        : (NW == 8 ? dock_kernel<AC, 8, 4, FIX> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX> : nullptr));
+    return nullptr;
+}
+
+// Per-atom-class entry points, each compiled in its own translation unit
+// (dock_inst.cu with -DVSD_AC=<AC>) so the 8 classes build in parallel.
+#define VSD_DECL_CLASS(ac)                                                                                     \
+    DockFn dock_pick_##ac(int fix, int NW, int PPW);                                                           \
+    cudaError_t launch_finalize_##ac(const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
+VSD_DECL_CLASS(32)
+VSD_DECL_CLASS(64)
+VSD_DECL_CLASS(96)
+VSD_DECL_CLASS(128)
+VSD_DECL_CLASS(160)
+VSD_DECL_CLASS(192)
+VSD_DECL_CLASS(224)
+VSD_DECL_CLASS(256)
+#undef VSD_DECL_CLASS
+
+}  // namespace dk
+}  // namespace vsd

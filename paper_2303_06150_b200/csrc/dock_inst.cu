@@ -1,0 +1,25 @@
+// dock_inst.cu -- instantiates the dock and finalize kernels of ONE atom class
+// (compiled once per class with -DVSD_AC=<AC>; see build.py).
+#include "dock_impl.cuh"
+
+#ifndef VSD_AC
+#error "compile with -DVSD_AC=<atom class capacity>"
+#endif
+#define VSD_CAT2(a, b) a##b
+#define VSD_CAT(a, b) VSD_CAT2(a, b)
+
+namespace vsd {
+namespace dk {
+
+DockFn VSD_CAT(dock_pick_, VSD_AC)(int fix, int NW, int PPW) {
+    return fix ? pick_ac<VSD_AC, true>(NW, PPW) : pick_ac<VSD_AC, false>(NW, PPW);
+}
+
+cudaError_t VSD_CAT(launch_finalize_, VSD_AC)(const DockArgs& a, const int64_t* atom_off, float* xyz_out,
+                                              cudaStream_t st) {
+    finalize_kernel<VSD_AC><<<(a.n + 7) / 8, 256, 0, st>>>(a, atom_off, xyz_out);
+    return cudaGetLastError();
+}
+
+}  // namespace dk
+}  // namespace vsd

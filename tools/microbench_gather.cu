@@ -20,7 +20,7 @@ __device__ __forceinline__ float3 next_point(unsigned& s) {
 }
 
 template <int RS, int PS>
-__global__ void __launch_bounds__(512, 1) k_smem(const float* __restrict__ G, int iters, float* out) {
+__global__ void __launch_bounds__(1024, 1) k_smem(const float* __restrict__ G, int iters, float* out) {
     extern __shared__ float sG[];
     for (int i = threadIdx.x; i < 33 * PS + RS + 2; i += blockDim.x) sG[i] = 0.f;
     __syncthreads();
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(512, 1) k_smem(const float* __restrict__ G, in
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
-__global__ void __launch_bounds__(512, 1) k_tex(cudaTextureObject_t tex, int iters, float* out) {
+__global__ void __launch_bounds__(1024, 1) k_tex(cudaTextureObject_t tex, int iters, float* out) {
     unsigned s = blockIdx.x * 1024 + threadIdx.x;
     float acc = 0.f;
     for (int it = 0; it < iters; ++it) {
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(512, 1) k_tex(cudaTextureObject_t tex, int ite
 
 // (c) mixed: z0 plane from shared memory (4 LDS), z1 plane by one tex2Dgather
 template <int RS, int PS>
-__global__ void __launch_bounds__(512, 1) k_mixed(const float* __restrict__ G, cudaTextureObject_t tex, int iters, float* out) {
+__global__ void __launch_bounds__(1024, 1) k_mixed(const float* __restrict__ G, cudaTextureObject_t tex, int iters, float* out) {
     extern __shared__ float sG[];
     for (int i = threadIdx.x; i < 33 * PS + RS + 2; i += blockDim.x) sG[i] = 0.f;
     __syncthreads();
