@@ -312,27 +312,106 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     __syncwarp();
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// Stage round `round` (LC ligand records + meta) into buffer b with cp.async (no wait).
-__device__ __forceinline__ void prefetch_round(const DockArgs& a, int round, int LC, float* sRec, int4* sMeta) {
-    const int slot0 = round * LC;
-    const int nl = min(LC, a.n - slot0);
-    const float4* src = reinterpret_cast<const float4*>(a.rec + (size_t)slot0 * a.rec_floats);
-    float4* dst = reinterpret_cast<float4*>(sRec);
-    const int n4 = nl * a.rec_floats / 4;
-    for (int t = threadIdx.x; t < n4; t += blockDim.x) cp_async16(dst + t, src + t);
-    for (int t = threadIdx.x; t < nl; t += blockDim.x) cp_async16(sMeta + t, a.meta + slot0 + t);
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
+// Ring control in static shared memory (one entry per slot).
+struct DockRing {
+    int ready[kDockSlots];   // round sequence number whose record this slot holds
+    int round[kDockSlots];   // global round index held (-1: the launch is exhausted)
+    int done[kDockSlots];    // warp items of the slot's round completed
+    int free_seq[kDockSlots];// next sequence number allowed into the slot
+    int item;                // CTA-local item counter
+    int end_seq;             // first sequence number that found the launch exhausted (INT_MAX: none yet)
+};
+
+// Claim the next global round and stage its LC records + meta into `slot` (one warp,
+// plain 16-byte loads); publish it as sequence `seq` with a release store.
+template <int AC>
+__device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, unsigned char* slot, const DockLayout& L,
+                                           int seq, int n_rounds, int lane) {
+    const int sl = seq % kDockSlots;
+    if (lane == 0)
+        while (ld_acquire_cta(&ring.free_seq[sl]) != seq) __nanosleep(64);
+    int round = 0;
+    if (lane == 0) round = atomicAdd(a.counter, 1);   // dynamic scheduling across the CTAs of the launch
+    round = __shfl_sync(FULL, round, 0);
+    const int LC = a.ligs_per_cta;
+    if (round < n_rounds) {
+        const int slot0 = round * LC;
+        const int nl = min(LC, a.n - slot0);
+        const float4* src = reinterpret_cast<const float4*>(a.rec + (size_t)slot0 * a.rec_floats);
+        float4* dst = reinterpret_cast<float4*>(slot + L.rec_o);
+        const int n4 = nl * a.rec_floats / 4;
+        for (int t = lane; t < n4; t += 32) dst[t] = __ldg(src + t);
+        int4* md = reinterpret_cast<int4*>(slot + L.meta_o);
+        for (int t = lane; t < nl; t += 32) md[t] = __ldg(a.meta + slot0 + t);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        ring.round[sl] = round < n_rounds ? round : -1;
+        if (round >= n_rounds) atomicMin(&ring.end_seq, seq);
+        st_release_cta(&ring.ready[sl], seq);
+    }
+}
+
+// a9 best pose of one round (run by the warp that completes the round's last item).
+__device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned char* slot, const DockLayout& L, int round,
+                                             int lane) {
+    const int LC = a.ligs_per_cta, P = a.P, S_w = a.S_w;
+    const int nl = min(LC, a.n - round * LC);
+    const int4* sMeta = reinterpret_cast<const int4*>(slot + L.meta_o);
+    const float* sScore = reinterpret_cast<const float*>(slot + L.score_o);
+    const uint8_t* sAng = slot + L.ang_o;
+    const int ang_stride = 32 * S_w;
+    for (int l = 0; l < nl; ++l) {   // lowest score, ties -> lowest pose index (Q11)
+        const int4 m = sMeta[l];
+        unsigned long long best = ~0ull;
+        for (int p = lane; p < P; p += 32) {
+            const unsigned long long key = ((unsigned long long)ord32(sScore[l * P + p]) << 32) | (unsigned)p;
+            best = key < best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
+            best = ob < best ? ob : best;
+        }
+        const int bp = (int)(best & 0xffffffffu);
+        const int li = m.x, R = m.z, nang = S_w * R;
+        if (lane == 0) {
+            a.best_score[li] = sScore[l * P + bp];
+            a.best_pose[li] = bp;
+        }
+        const uint8_t* sa = sAng + (size_t)(l * P + bp) * ang_stride;
+        for (int t = lane; t < nang; t += 32) a.angles[m.w + t] = sa[t];
+        if (a.dbg_score)
+            for (int p = lane; p < P; p += 32) a.dbg_score[(size_t)li * P + p] = sScore[l * P + p];
+        if (a.dbg_angles)
+            for (int t = lane; t < P * nang; t += 32) {
+                const int p = t / nang, q = t - p * nang;
+                a.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
+            }
+    }
+}
+
+// Persistent CTA per SM.  Warps run independently (no CTA barrier after the prologue):
+// each claims warp items (round sequence, ligand of the round, PPW-pose group) from a
+// CTA-local counter; rounds sit in a ring of kDockSlots slots.  The warp that claims the
+// middle item of round s loads round s + 1 once round s is staged (so records are staged
+// long before use and global rounds are claimed in sequence order), the
+// warp that completes the last item of a round reduces its best pose (a9) and frees the
+// slot.  NW is therefore free of P / PPW (e.g. 12 warps of 4 poses for 64 poses).
 template <int AC, int NW, int PPW, bool FIX>
 __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int s_rounds[3];
+    __shared__ DockRing ring;
     constexpr int LPP = 32 / PPW;
     const PocketDev& pk = a.pk;
     const int LC = a.ligs_per_cta;
@@ -342,27 +421,23 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     float* sCS = reinterpret_cast<float*>(smem + L.cs);
     float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
-    auto rec_buf = [&](int b) { return reinterpret_cast<float*>(smem + L.rec + b * L.rec_b); };
-    auto meta_buf = [&](int b) { return reinterpret_cast<int4*>(smem + L.meta + b * L.meta_b); };
-    auto score_buf = [&](int b) { return reinterpret_cast<float*>(smem + L.score + b * L.score_b); };
-    auto ang_buf = [&](int b) { return smem + L.ang + b * L.ang_b; };
+    auto slot_ptr = [&](int seq) { return smem + L.slots + (size_t)(seq % kDockSlots) * L.slot_b; };
 
-    const int rec_floats = a.rec_floats;
     const int n_rounds = (a.n + LC - 1) / LC;
-    // dynamic scheduling (balances CTAs within the launch): round indices are claimed two
-    // rounds ahead, so neither the counter atomic nor the record fetch is on the critical path
+    if (tid < kDockSlots) {
+        ring.ready[tid] = -1;
+        ring.done[tid] = 0;
+        ring.free_seq[tid] = tid;
+    }
     if (tid == 0) {
-        s_rounds[0] = atomicAdd(a.counter, 1);
-        s_rounds[1] = atomicAdd(a.counter, 1);
+        ring.item = 0;
+        ring.end_seq = 0x7fffffff;
     }
     stage_grid(sG, pk);
     for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
     for (int t = tid; t < 2 * a.K; t += blockDim.x) sCS[t] = a.cs[t];
     __syncthreads();
-    int cur = s_rounds[0];
-    if (cur < n_rounds) prefetch_round(a, cur, LC, rec_buf(0), meta_buf(0));
-    cp_async_wait_all();
-    __syncthreads();
+    if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
     const int K = a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
@@ -370,63 +445,64 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride<AC>()};
     const int ang_stride = 32 * S_w;
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
+    const int IG = LC * G;               // warp items per round
+    const int loader_item = IG / 2;
 
-    for (int i = 0; cur < n_rounds; ++i) {
-        const int b = i & 1;
-        const int nxt = s_rounds[(i + 1) % 3];
-        // rec[b ^ 1] was last read by round i - 1, which ended at the previous barrier; meta is
-        // triple-buffered because the a9 warps of round i - 1 may still read it
-        if (nxt < n_rounds) prefetch_round(a, nxt, LC, rec_buf(b ^ 1), meta_buf((i + 1) % 3));
-        if (tid == 0) s_rounds[(i + 2) % 3] = atomicAdd(a.counter, 1);   // slot last read in round i - 1
-        const int slot0 = cur * LC;
-        const int nl = min(LC, a.n - slot0);
-        const float* sRec = rec_buf(b);
-        const int4* sMeta = meta_buf(i % 3);   // triple-buffered: read by the a9 warps after the barrier
-        float* sScore = score_buf(b);
-        uint8_t* sAng = ang_buf(b);
-        for (int item = warp; item < nl * G; item += NW) {
-            const int l = item / G, g = item - l * G;
+    while (true) {
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&ring.item, 1);
+        t = __shfl_sync(FULL, t, 0);
+        const int seq = t / IG, it = t - seq * IG;
+        // wait for the round's record (or for the launch to be exhausted)
+        int ok = 0;
+        if (lane == 0) {
+            const int sl = seq % kDockSlots;
+            while (true) {
+                if (ld_acquire_cta(&ring.ready[sl]) == seq) {
+                    ok = ring.round[sl] >= 0;
+                    break;
+                }
+                if (*(volatile int*)&ring.end_seq <= seq) break;
+                __nanosleep(64);
+            }
+        }
+        ok = __shfl_sync(FULL, ok, 0);
+        __syncwarp();   // lane 0's acquire orders the slot reads of the whole warp
+        if (!ok) break;
+        // round s + 1 is claimed only once round s is (claims follow the sequence order, so
+        // the first exhausted sequence bounds all later ones: end_seq is exact)
+        if (it == loader_item) load_round<AC>(a, ring, slot_ptr(seq + 1), L, seq + 1, n_rounds, lane);
+        unsigned char* slot = slot_ptr(seq);
+        const int round = ring.round[seq % kDockSlots];
+        const int nl = min(LC, a.n - round * LC);
+        const int l = it / G, g = it - l * G;
+        if (l < nl) {
             const int p = g * PPW + h;
             const bool valid = p < P;
             const int pc = valid ? p : P - 1;
-            const int4 m = sMeta[l];
-            dock_poses<AC, PPW, FIX>(sRec + l * rec_floats, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w,
-                                ck, sk, sCS, sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
+            const int4 m = reinterpret_cast<const int4*>(slot + L.meta_o)[l];
+            const float* rec = reinterpret_cast<const float*>(slot + L.rec_o) + l * a.rec_floats;
+            float* sScore = reinterpret_cast<float*>(slot + L.score_o);
+            uint8_t* sAng = slot + L.ang_o;
+            dock_poses<AC, PPW, FIX>(rec, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w, ck, sk, sCS,
+                                     sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
-        cp_async_wait_all();
-        __syncthreads();   // scores of round i complete; record of round i + 1 and s_rounds visible
-        // a9 best pose of round i (its score / angle buffers are rewritten only after the
-        // next barrier, which these warps reach after finishing)
-        if (warp >= NW - nl) {
-            const int l = NW - 1 - warp;
-            const int4 m = sMeta[l];
-            unsigned long long best = ~0ull;
-            for (int p = lane; p < P; p += 32) {
-                const unsigned long long key = ((unsigned long long)ord32(sScore[l * P + p]) << 32) | (unsigned)p;
-                best = key < best ? key : best;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long ob = __shfl_xor_sync(FULL, best, o);
-                best = ob < best ? ob : best;
-            }
-            const int bp = (int)(best & 0xffffffffu);
-            const int li = m.x, R = m.z, nang = S_w * R;
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = atomicAdd(&ring.done[seq % kDockSlots], 1) == IG - 1;
+            if (last) __threadfence_block();
+        }
+        last = __shfl_sync(FULL, last, 0);
+        if (last) {
+            finish_round(a, slot, L, round, lane);
+            __syncwarp();
             if (lane == 0) {
-                a.best_score[li] = sScore[l * P + bp];
-                a.best_pose[li] = bp;
+                ring.done[seq % kDockSlots] = 0;
+                st_release_cta(&ring.free_seq[seq % kDockSlots], seq + kDockSlots);
             }
-            const uint8_t* sa = sAng + (size_t)(l * P + bp) * ang_stride;
-            for (int t = lane; t < nang; t += 32) a.angles[m.w + t] = sa[t];
-            if (a.dbg_score)
-                for (int p = lane; p < P; p += 32) a.dbg_score[(size_t)li * P + p] = sScore[l * P + p];
-            if (a.dbg_angles)
-                for (int t = lane; t < P * nang; t += 32) {
-                    const int p = t / nang, q = t - p * nang;
-                    a.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
-                }
         }
-        cur = nxt;
     }
 }
 
@@ -504,7 +580,8 @@ DockFn pick_ac(int NW, int PPW) {
                         : (NW == 16 ? dock_kernel<AC, 16, 2, FIX> : (NW == 8 ? dock_kernel<AC, 8, 2, FIX> : nullptr));
     if (PPW == 4)
         return NW == 16 ? dock_kernel<AC, 16, 4, FIX>
-                        : (NW == 8 ? dock_kernel<AC, 8, 4, FIX> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX> : nullptr));
+                        : NW == 12 ? dock_kernel<AC, 12, 4, FIX>
+                                   : (NW == 8 ? dock_kernel<AC, 8, 4, FIX> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX> : nullptr));
     return nullptr;
 }
 

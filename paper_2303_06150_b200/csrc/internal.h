@@ -51,12 +51,12 @@ struct DockArgs {
 };
 
 // Shared-memory layout of dock<AC, NW, PPW> (byte offsets).  Used by the kernel
-// and by the host (occupancy query, launch) so both agree.
-// rec / score / ang are double-buffered by round parity, meta triple-buffered (the next
-// round's record is fetched with cp.async while the current one docks); *_b = one buffer.
+// and by the host (occupancy query, launch) so both agree.  Rounds (LC ligands each)
+// live in a ring of kDockSlots slots: record, meta, pose scores, angle choices.
+constexpr int kDockSlots = 3;
 struct DockLayout {
-    size_t grid, pose, cs, rec, meta, buf, score, ang, total;
-    size_t rec_b, meta_b, score_b, ang_b;
+    size_t grid, pose, cs, slots, buf, total;
+    size_t rec_o, meta_o, score_o, ang_o, slot_b;   // offsets inside one slot, slot size
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int rs, int ps, int P, int K,
@@ -67,15 +67,14 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     L.grid = o;  o += align16(((size_t)(nz + 1) * ps + rs + 2) * 4);
     L.pose = o;  o += align16((size_t)P * 12 * 4);
     L.cs = o;    o += align16((size_t)K * 2 * 4);
-    L.rec_b = align16((size_t)LC * (3 * AC + 32) * 4);
-    L.meta_b = (size_t)LC * 16;
-    L.score_b = align16((size_t)LC * P * 4);
-    L.ang_b = align16((size_t)LC * P * S_w * 32);
-    L.rec = o;   o += 2 * L.rec_b;
-    L.meta = o;  o += 3 * L.meta_b;
+    size_t q = 0;
+    L.rec_o = q;   q += align16((size_t)LC * (3 * AC + 32) * 4);
+    L.meta_o = q;  q += (size_t)LC * 16;
+    L.score_o = q; q += align16((size_t)LC * P * 4);
+    L.ang_o = q;   q += align16((size_t)LC * P * S_w * 32);
+    L.slot_b = q;
+    L.slots = o; o += kDockSlots * q;
     L.buf = o;   o += (size_t)NW * PPW * (3 * AC + 4) * 4;   // SoA x|y|z per pose, stride 3 AC + 4 floats
-    L.score = o; o += 2 * L.score_b;
-    L.ang = o;   o += 2 * L.ang_b;
     L.total = o;
     return L;
 }
