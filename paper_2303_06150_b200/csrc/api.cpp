@@ -116,6 +116,7 @@ struct vs_ctx {
     std::string err;
 
     int P = 0, K = 0;
+    int frag_cap = 0;             // max fragments per ligand of the submitted library (sizes angle buffers)
     std::vector<float> pose_tab;  // P * 12
     std::vector<float> cs;        // K * 2
     std::vector<PocketHost> pockets;
@@ -311,7 +312,7 @@ const char* vcode_msg(int code) {
 }
 
 // Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1.
-vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs, int ps) {
+vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs, int ps, int RC) {
     c->classes.clear();
     for (size_t i = 0; i < atom_b.size(); ++i) {
         ClassInfo ci{};
@@ -337,7 +338,7 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs
             const int PPW = pr.first, NW = pr.second;
             if (c->K > 32 / PPW) continue;
             const int LC = ligs_per_cta(NW, PPW, c->P);
-            const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC);
+            const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
             int b = 0;
             CK(dock_occupancy(ci.AC, NW, PPW, grid_fixed(rs, ps), L.total, &b));
             if (b >= 1) {
@@ -661,7 +662,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             rs_max = pk.rs;
         }
     }
-    st = plan_classes(c, c->atom_b, nz_max, rs_max, ps_max);
+    c->frag_cap = maxAR[1];
+    st = plan_classes(c, c->atom_b, nz_max, rs_max, ps_max, c->frag_cap);
     if (st) return st;
     const int nRc = (int)c->rot_b.size();
     const int n_cells = (int)c->atom_b.size() * nRc;
@@ -850,6 +852,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.K = c->K;
             a.S_w = S_w;
             a.ligs_per_cta = ci.LC;
+            a.frag_cap = c->frag_cap;
             a.pose_tab = c->d_pose;
             a.cs = c->d_cs;
             a.pk = c->pkdev[q];
@@ -859,7 +862,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.dbg_score = c->d_dbg_score[q];
             a.dbg_angles = c->d_dbg_ang[q];
             a.counter = d_counters + dock_launches;
-            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.nz, a.pk.rs, a.pk.ps, c->P, c->K, S_w, ci.LC);
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.nz, a.pk.rs, a.pk.ps, c->P, c->K, S_w, ci.LC, c->frag_cap);
             const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];

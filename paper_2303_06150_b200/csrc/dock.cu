@@ -25,9 +25,10 @@ DockFn pick(int AC, int NW, int PPW, int fix) {
 
 }  // namespace
 
-// Padded shared-memory strides (tools/bank_sim.py: 2.5-way instead of 6.2-way bank
-// conflicts on the sweep's corner gathers).  Grids of at most 32 x 32 per plane use
-// the fixed layout (33, 1063) with compile-time strides; larger planes use
+// Padded shared-memory strides (tools/bank_sim3.py, the lane map of 4 poses x 8 angles:
+// 3.06-way bank conflicts on the sweep's corner gathers instead of 3.21 at (33, 1063) and
+// 7.5 unpadded; uniform random gathers give 3.5).  Grids of at most 32 x 32 per plane use
+// the fixed layout (34, 1097) with compile-time strides; larger planes use
 // (nx + 1, (nx + 1) * ny + 7).
 void grid_strides(int nx, int ny, int* rs, int* ps) {
     if (nx <= 32 && ny <= 32) {

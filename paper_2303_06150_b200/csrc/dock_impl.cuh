@@ -105,9 +105,9 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float t) {
 // The upper edge (u_c = n-1) takes i0 = n-1 with f = 0 instead of i0 = n-2 with f = 1:
 // both reduce exactly to the node value (lerp(a, b, 0) = a, lerp(a, b, 1) = b bitwise),
 // and the corner at n is a finite zero pad of the shared-memory copy, so no clamp of
-// i0 is needed.  FIX: the 32x32-plane layout with compile-time strides (33, 1063)
+// i0 is needed.  FIX: the 32x32-plane layout with compile-time strides (34, 1097)
 // that lets every corner load use an immediate offset.
-constexpr int kFixRS = 33, kFixPS = 1063;
+constexpr int kFixRS = 34, kFixPS = 1097;
 template <bool FIX>
 __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
     const int RS = FIX ? kFixRS : pk.rs, PS = FIX ? kFixPS : pk.ps;
@@ -179,19 +179,19 @@ __device__ __forceinline__ unsigned ord32(float v) {
     return b ^ ((unsigned)((int)b >> 31) | 0x80000000u);
 }
 
-// Per-pose buffer stride in float4: AC + 1 so that the PPW pose groups of a warp
-// read their buffers from different banks.
-// Per-pose coordinate buffer in shared memory, SoA: x[AC] | y[AC] | z[AC] (12 B per atom),
-// pose buffers 3*AC + 4 floats apart so the PPW pose groups of a warp hit different banks.
+// Per-pose coordinate buffer in shared memory: (x, y) pairs then z (12 B per atom), pose
+// buffers 3*AC + 4 floats apart so the PPW pose groups of a warp hit different banks.
 template <int AC>
 __host__ __device__ constexpr int pose_stride() { return 3 * AC + 4; }
 template <int AC>
 struct PoseBuf {
-    float* b;
-    __device__ __forceinline__ float4 get(int j) const { return make_float4(b[j], b[AC + j], b[2 * AC + j], 0.f); }
+    float* b;   // (x, y) pairs [2 AC] | z [AC]: one 8-byte and one 4-byte load per atom
+    __device__ __forceinline__ float4 get(int j) const {
+        const float2 xy = *reinterpret_cast<const float2*>(b + 2 * j);
+        return make_float4(xy.x, xy.y, b[2 * AC + j], 0.f);
+    }
     __device__ __forceinline__ void set(int j, float4 v) const {
-        b[j] = v.x;
-        b[AC + j] = v.y;
+        *reinterpret_cast<float2*>(b + 2 * j) = make_float2(v.x, v.y);
         b[2 * AC + j] = v.z;
     }
 };
@@ -370,7 +370,7 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned c
     const int4* sMeta = reinterpret_cast<const int4*>(slot + L.meta_o);
     const float* sScore = reinterpret_cast<const float*>(slot + L.score_o);
     const uint8_t* sAng = slot + L.ang_o;
-    const int ang_stride = 32 * S_w;
+    const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
     for (int l = 0; l < nl; ++l) {   // lowest score, ties -> lowest pose index (Q11)
         const int4 m = sMeta[l];
         unsigned long long best = ~0ull;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     constexpr int LPP = 32 / PPW;
     const PocketDev& pk = a.pk;
     const int LC = a.ligs_per_cta;
-    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC);
+    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sPose = reinterpret_cast<float*>(smem + L.pose);
     float* sCS = reinterpret_cast<float*>(smem + L.cs);
@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int kbits = 31 - __clz(K);
     const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
     const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride<AC>()};
-    const int ang_stride = 32 * S_w;
+    const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
     const int IG = LC * G;               // warp items per round
     const int loader_item = IG / 2;

@@ -39,6 +39,7 @@ struct DockArgs {
     int rec_floats;            // 3 * AC + 32
     int P, K, S_w;
     int ligs_per_cta;          // LC
+    int frag_cap;              // RC: no ligand of the launch has more fragments
     int* counter;              // dynamic round counter of this launch (zeroed before launch)
     const float* pose_tab;     // [P][12] raw: R (9, row-major) then tau (3)
     const float* cs;           // [K][2]
@@ -59,8 +60,10 @@ struct DockLayout {
     size_t rec_o, meta_o, score_o, ang_o, slot_b;   // offsets inside one slot, slot size
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+// Angle choices kept per pose: S_w * RC bytes (RC = the launch's fragment cap), 4-aligned.
+__host__ __device__ inline int dock_ang_stride(int S_w, int RC) { return ((S_w * (RC > 0 ? RC : 1)) + 3) & ~3; }
 __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int rs, int ps, int P, int K,
-                                                  int S_w, int LC) {
+                                                  int S_w, int LC, int RC) {
     DockLayout L;
     size_t o = 0;
     // grid planes + one zero plane and row above: corner reads at i0 + 1 = n (weight 0) stay in bounds
@@ -71,7 +74,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     L.rec_o = q;   q += align16((size_t)LC * (3 * AC + 32) * 4);
     L.meta_o = q;  q += (size_t)LC * 16;
     L.score_o = q; q += align16((size_t)LC * P * 4);
-    L.ang_o = q;   q += align16((size_t)LC * P * S_w * 32);
+    L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC));
     L.slot_b = q;
     L.slots = o; o += kDockSlots * q;
     L.buf = o;   o += (size_t)NW * PPW * (3 * AC + 4) * 4;   // SoA x|y|z per pose, stride 3 AC + 4 floats
