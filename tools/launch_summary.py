@@ -16,7 +16,7 @@ for r in rows:
     per.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for (i, name), m in per.items():
-    short = name.split("(")[0].replace("void ", "").replace("unnamed>::", "")
+    short = name.split("(")[0].replace("void ", "").replace("unnamed>::", "").replace("dk::", "").replace("vsd::", "")
     a = agg[short]
     a[0] += 1
     a[1] += m.get("gpu__time_duration.sum", 0.0)
