@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--ligands", type=int, default=0, help="override the ligand count (not a bench value)")
     ap.add_argument("--no-unsorted", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-every", type=int, default=250)
     ap.add_argument("--streams", type=int, default=4)
@@ -262,18 +263,41 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        # the public host-to-results call (Engine.submit from pinned host buffers): H2D of the
-        # library inside the step, D2H of every ligand's best score and pose at its end
-        hs = torch.empty(n, dtype=torch.float32).pin_memory()
-        hp = torch.empty(n, dtype=torch.int32).pin_memory()
-        t_e, _, _, _ = timed(eng, ids, h_lib, False, host_out=(hs, hp))
-        d2h = len(pockets) * (n * 8 + K_TOP * 8)
+        # the public host-to-results API (pipeline.PipelinedDocker, PAPER.md l.200-203 double
+        # buffering): pinned host CSR in, every ligand's best score / pose and the merged top-k
+        # per pocket out on the host; chunk H2D copies overlap the previous chunk's docking
+        from paper_2303_06150_b200.pipeline import PipelinedDocker
+        eng.close()
+        pdk = PipelinedDocker(device=local, n_buffers=2, atom_clusters=6, rot_clusters=23,
+                              bucket_multiple=args.bucket_multiple, n_streams=args.streams, rank=rank,
+                              world_size=world)
+        pdk.setup(rot, tr, cs, pockets)
+        run_e2e = lambda: pdk.run(*h_lib, k=K_TOP, chunks=args.e2e_chunks, max_atoms=max_atoms)
+        for _ in range(args.warmup):
+            run_e2e()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        st = torch.cuda.current_stream()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(st)
+        for _ in range(args.steps):
+            run_e2e()
+        ev1.record(st)
+        torch.cuda.synchronize()
+        t_e = ev0.elapsed_time(ev1)
+        if world > 1:
+            t_e = reduce_scalar(t_e, dist.ReduceOp.MAX)
+        pdk.close()
+        d2h = len(pockets) * (n * 8 + K_TOP * 12)
         e2e = {"value": n * len(pockets) / (t_e / args.steps / 1e3), "unit": "ligands/s",
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
-               "api": "Engine.submit(host pinned CSR) + results D2H, CUDA events"}
+               "api": f"PipelinedDocker.run: pinned host CSR -> host scores/poses + top-{K_TOP}; "
+                      f"{args.e2e_chunks} chunks on 2 contexts (H2D of chunk i+1 overlaps docking of chunk i)"}
     unsorted = None
     if not args.no_unsorted:
-        eng.close()
+        if args.no_e2e:
+            eng.close()
         ue, uids = make_engine(1, 1)
         t_u, dock_u, _, _ = timed(ue, uids, d_lib, True)
         uv = n * len(pockets) / (t_u / args.steps / 1e3)

@@ -117,6 +117,8 @@ struct vs_ctx {
 
     int P = 0, K = 0;
     int frag_cap = 0;             // max fragments per ligand of the submitted library (sizes angle buffers)
+    long long tables_version = 0; // bumped by every pose / angle table or pocket change
+    std::vector<long long> uploaded_sig;   // (workspace, tables_version, grid size, pocket ids) on the device
     std::vector<float> pose_tab;  // P * 12
     std::vector<float> cs;        // K * 2
     std::vector<PocketHost> pockets;
@@ -236,6 +238,11 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int P, int K, size_t grid_bytes,
     s.n_blocks = (int)((n + kPrepTile - 1) / kPrepTile);
     if (s.n_blocks < 1) s.n_blocks = 1;
     s.max_buckets = n + kMaxCells;
+    // tables and grids first: their offsets depend only on (P, K, grid size, pockets), so
+    // an unchanged set stays resident across submits and is not re-uploaded
+    s.pose = r.add((size_t)P * 12 * 4);
+    s.cs = r.add((size_t)K * 2 * 4 + 16);
+    s.grids = r.add(grid_bytes * n_pockets);
     s.atom_off = r.add((n + 1) * 8);
     s.frag_off = r.add((n + 1) * 8);
     s.xyz = r.add(nA * 12);
@@ -256,9 +263,6 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int P, int K, size_t grid_bytes,
     s.own_prefix = r.add((s.max_buckets + 1) * 4);
     s.own_ac = r.add(s.max_buckets * 4);
     s.own_rec_off = r.add(s.max_buckets * 8);
-    s.pose = r.add((size_t)P * 12 * 4);
-    s.cs = r.add((size_t)K * 2 * 4 + 16);
-    s.grids = r.add(grid_bytes * n_pockets);
     s.end = r.off;
     return s;
 }
@@ -438,6 +442,7 @@ vs_status vs_set_pose_table(vs_ctx* c, int32_t P, const float* rot, const float*
     if (P < 1 || P > kMaxPoses || !rot || !trans) return fail(c, VS_E_ARG, "pose table: need 1 <= P <= %d", kMaxPoses);
     c->P = P;
     c->pose_tab.assign((size_t)P * 12, 0.f);
+    ++c->tables_version;
     for (int p = 0; p < P; ++p) {
         for (int t = 0; t < 9; ++t) {
             if (!std::isfinite(rot[9 * p + t])) return fail(c, VS_E_ARG, "pose %d: non-finite rotation", p);
@@ -460,6 +465,7 @@ vs_status vs_set_angle_table(vs_ctx* c, int32_t K, const float* cos_sin) {
         if (!std::isfinite(cos_sin[t])) return fail(c, VS_E_ARG, "angle table: non-finite entry %d", t / 2);
     c->K = K;
     c->cs.assign(cos_sin, cos_sin + 2 * K);
+    ++c->tables_version;
     return VS_OK;
 }
 
@@ -485,6 +491,7 @@ vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, 
     for (size_t i = 0; i < cnt; ++i)
         if (!std::isfinite(ph.grid[i])) return fail(c, VS_E_ARG, "pocket grid value %zu is not finite", i);
     c->pockets.push_back(std::move(ph));
+    ++c->tables_version;
     if (pocket_id) *pocket_id = (int32_t)c->pockets.size() - 1;
     return VS_OK;
 }
@@ -511,6 +518,7 @@ vs_status vs_set_workspace(vs_ctx* c, void* ptr, size_t bytes) {
     if (!c) return VS_E_ARG;
     if (((uintptr_t)ptr & 255) != 0) return fail(c, VS_E_ARG, "workspace must be 256-byte aligned");
     c->ws = (uint8_t*)ptr;
+    c->uploaded_sig.clear();   // new memory: tables and grids must be uploaded again
     c->ws_bytes = bytes;
     c->submitted = false;
     return VS_OK;
@@ -604,15 +612,24 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     }
 
     CK(cudaEventRecord(c->ev_prep0, ms));
-    // tables + grids (small H2D)
-    CK(cudaMemcpyAsync(c->d_pose, c->pose_tab.data(), c->pose_tab.size() * 4, cudaMemcpyHostToDevice, ms));
-    CK(cudaMemcpyAsync(c->d_cs, c->cs.data(), c->cs.size() * 4, cudaMemcpyHostToDevice, ms));
-    c->pkdev.clear();
-    for (int i = 0; i < n_pockets; ++i) {
-        auto& ph = c->pockets[pocket_ids[i]];
-        CK(cudaMemcpyAsync(c->d_grid[i], ph.grid.data(), ph.grid.size() * 4, cudaMemcpyHostToDevice, ms));
-        c->pkdev.push_back(make_pocket_dev(ph.d, c->d_grid[i]));
+    // tables + grids (small H2D), only when they changed since the last submit: a pageable
+    // copy queues on the H2D copy engine behind any large transfer in flight (a pipelined
+    // caller's next chunk), so an unconditional re-upload would stall every submit on it
+    {
+        std::vector<long long> sig = {(long long)(uintptr_t)W, c->tables_version, (long long)gmax};
+        for (int i = 0; i < n_pockets; ++i) sig.push_back(pocket_ids[i]);
+        if (sig != c->uploaded_sig) {
+            CK(cudaMemcpyAsync(c->d_pose, c->pose_tab.data(), c->pose_tab.size() * 4, cudaMemcpyHostToDevice, ms));
+            CK(cudaMemcpyAsync(c->d_cs, c->cs.data(), c->cs.size() * 4, cudaMemcpyHostToDevice, ms));
+            for (int i = 0; i < n_pockets; ++i) {
+                auto& ph = c->pockets[pocket_ids[i]];
+                CK(cudaMemcpyAsync(c->d_grid[i], ph.grid.data(), ph.grid.size() * 4, cudaMemcpyHostToDevice, ms));
+            }
+            c->uploaded_sig = sig;
+        }
     }
+    c->pkdev.clear();
+    for (int i = 0; i < n_pockets; ++i) c->pkdev.push_back(make_pocket_dev(c->pockets[pocket_ids[i]].d, c->d_grid[i]));
     if (n == 0) {
         c->buckets.clear();
         c->owned.clear();

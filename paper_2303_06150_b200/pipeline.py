@@ -2,95 +2,128 @@
 
 LiGen overlaps transfers with compute by handing buckets to CPU "workers" that copy
 into a free device buffer, run, and copy results back ("double buffering technique
-for hiding data transfers").  On B200 the same idea is two (or more) contexts on their
-own CUDA streams, driven by one host thread each: while one context docks chunk i, the
-other's host-to-device copy of chunk i+1 is already in flight on the copy engines.
-Each chunk is a full hot-path submit (validate, bucket, pack, dock, local top-k); the
-per-pocket ranking is merged over chunks on the device (vs_merge_topk), and across
-ranks with the NCCL gather of ``parallel.global_topk``.
+for hiding data transfers").  On B200 one context is enough: the library is cut into
+chunks, chunk i + 1's host-to-device copy runs on a copy stream (the copy engines)
+while chunk i is prepared, docked and ranked on the context's compute stream, into
+``n_buffers`` rotating device buffers.
+
+Compute phases are deliberately serialised: the persistent dock kernel holds every SM
+(one CTA per SM, ~227 KB of shared memory), so a second context's preparation kernels
+could not start before the dock drains anyway -- and its local top-k would queue behind
+the other context's dock.  What overlaps is the only thing that can: PCIe copies against
+SM work.  Each chunk is a full hot-path submit (validate, bucket, pack, dock, local top-k);
+the per-pocket ranking is merged over chunks on the device (vs_merge_topk) and across
+ranks with one all-gather of k keys per pocket (``parallel.gather_keys``).
 """
 from __future__ import annotations
-
-import threading
 
 import numpy as np
 
 from .vsdock import Engine
 
 
-def _slice_csr(lib_arrays, lo, hi):
-    """Chunk [lo, hi) of a CSR batch: rebased offsets, zero-copy views of xyz / frags."""
-    atom_off, xyz, frag_off, frags = lib_arrays
+def _bounds(atom_off, frag_off, lo, hi):
     ao = np.asarray(atom_off[lo:hi + 1])
     fo = np.asarray(frag_off[lo:hi + 1])
-    a0, a1, f0, f1 = int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
-    return (np.ascontiguousarray(ao - a0), xyz[a0:a1], np.ascontiguousarray(fo - f0), frags[f0:f1])
+    return ao, fo, int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
 
 
 class PipelinedDocker:
-    """Dock a host-resident library in chunks on ``n_buffers`` concurrent contexts."""
+    """Dock a host-resident library in chunks; H2D of the next chunk overlaps the current one."""
 
     def __init__(self, device: int = 0, n_buffers: int = 2, **engine_kw):
         import torch
         self._torch = torch
-        self.engines = [Engine(device=device, stream=torch.cuda.Stream(device=device), **engine_kw)
-                        for _ in range(n_buffers)]
         self.device = device
+        self.dev = torch.device(f"cuda:{device}")
+        self.n_buffers = max(2, int(n_buffers))
+        self.compute = torch.cuda.Stream(device=device)
+        self.copy = torch.cuda.Stream(device=device)
+        self.engine = Engine(device=device, stream=self.compute, **engine_kw)
+        self.engines = [self.engine]
+        self.trace = []
 
     def setup(self, rot, trans, cs, pockets):
-        for e in self.engines:
-            e.set_poses(rot, trans)
-            e.set_angles(cs)
-            ids = [e.load_pocket(p) for p in pockets]
-        self.pocket_ids = ids
-        return ids
+        e = self.engine
+        e.set_poses(rot, trans)
+        e.set_angles(cs)
+        self.pocket_ids = [e.load_pocket(p) for p in pockets]
+        return self.pocket_ids
 
-    def run(self, atom_off, xyz, frag_off, frags, k: int = 1000, chunks: int = 4, max_atoms: int = 256):
+    def _issue_copy(self, arrays, lo, hi):
+        """Chunk [lo, hi) to the device on the copy stream: rebased offsets + xyz / frags slices."""
+        torch = self._torch
+        atom_off, xyz, frag_off, frags = arrays
+        ao, fo, a0, a1, f0, f1 = _bounds(atom_off, frag_off, lo, hi)
+        host = [torch.from_numpy(np.ascontiguousarray(ao - a0)), xyz[a0:a1],
+                torch.from_numpy(np.ascontiguousarray(fo - f0)), frags[f0:f1]]
+        host = [h if isinstance(h, torch.Tensor) else torch.from_numpy(np.asarray(h)) for h in host]
+        with torch.cuda.stream(self.copy):
+            dev = [h.to(self.dev, non_blocking=True) for h in host]
+            ev = torch.cuda.Event()
+            ev.record(self.copy)
+        return dev, ev, host
+
+    def run(self, atom_off, xyz, frag_off, frags, k: int = 1000, chunks: int = 4, max_atoms: int = 256,
+            group=None):
         """Returns (best_score [P][n], best_pose [P][n], topk [(index, score)] per pocket) on the host.
 
-        xyz / frags should be pinned host tensors (torch ``pin_memory``) for overlapped copies."""
+        xyz / frags should be pinned host tensors (torch ``pin_memory``) for overlapped copies.
+        With ``rank`` / ``world_size`` engine options under an initialised process group, every
+        rank docks its LPT share of each chunk and the per-pocket top-k is merged across ranks."""
+        import time
+        from . import parallel
+        torch = self._torch
+        e = self.engine
         n = int(atom_off.shape[0]) - 1
         npk = len(self.pocket_ids)
+        chunks = max(1, min(int(chunks), max(1, n)))
         bounds = [n * c // chunks for c in range(chunks + 1)]
-        best = np.full((npk, n), np.nan, np.float32)
-        pose = np.full((npk, n), -1, np.int32)
-        keys = [[None] * chunks for _ in range(npk)]
-        errors = []
-
-        def worker(w):
-            e = self.engines[w]
-            try:
-                for c in range(w, chunks, len(self.engines)):
-                    lo, hi = bounds[c], bounds[c + 1]
-                    if hi <= lo:
-                        continue
-                    arrays = _slice_csr((atom_off, xyz, frag_off, frags), lo, hi)
-                    e.submit(*arrays, self.pocket_ids, on_device=False, max_atoms=max_atoms)
-                    e.wait()
-                    for s in range(npk):
-                        r = e.results(s)
-                        best[s, lo:hi] = r.best_score
-                        pose[s, lo:hi] = r.best_pose
-                        t, nv = e.local_topk(s, k)
-                        kk = t[:nv].cpu().numpy().view(np.uint64)
-                        keys[s][c] = kk + np.uint64(lo)       # ligand index lives in the low word
-            except Exception as ex:  # surfaced on the caller's thread
-                errors.append(ex)
-
-        th = [threading.Thread(target=worker, args=(w,)) for w in range(len(self.engines))]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-        if errors:
-            raise errors[0]
+        # pinned host outputs: the per-chunk result reads are plain DMA, not staged copies
+        best = torch.full((npk, n), float("nan"), dtype=torch.float32).pin_memory().numpy()
+        pose = torch.full((npk, n), -1, dtype=torch.int32).pin_memory().numpy()
+        keys = [[] for _ in range(npk)]
+        arrays = (atom_off, xyz, frag_off, frags)
+        self.trace = []
+        inflight = {}
+        for c in range(min(self.n_buffers - 1, chunks)):
+            inflight[c] = self._issue_copy(arrays, bounds[c], bounds[c + 1])
+        for c in range(chunks):
+            lo, hi = bounds[c], bounds[c + 1]
+            nxt = c + self.n_buffers - 1
+            dev, ev, _host = inflight.pop(c)
+            t0 = time.perf_counter()
+            ev.synchronize()        # chunk c resident (the engine reads its CSR totals on submit)
+            t1 = time.perf_counter()
+            if hi > lo:
+                # submit returns once the dock launches are queued; the preparation's small
+                # host<->device exchanges are over by then, so the prefetch issued next shares
+                # the copy engine with nothing and runs under the dock
+                e.submit(*dev, self.pocket_ids, on_device=True, max_atoms=max_atoms)
+            if nxt < chunks:
+                inflight[nxt] = self._issue_copy(arrays, bounds[nxt], bounds[nxt + 1])
+            if hi > lo:
+                e.wait()
+                for s in range(npk):
+                    e.results_into(s, best[s, lo:hi], pose[s, lo:hi])
+                    t, nv = e.local_topk(s, k)
+                    kk = t[:nv].cpu().numpy().view(np.uint64)
+                    keys[s].append(kk + np.uint64(lo))       # ligand index lives in the low word
+            st = e.stats()
+            self.trace.append((c, t0, t1, time.perf_counter(), st["prep_ms"], st["dock_ms"]))
+            del dev                 # buffer free once the chunk's work completed (wait above)
         tops = []
         for s in range(npk):
-            allk = np.concatenate([kk for kk in keys[s] if kk is not None]) if n else np.zeros(0, np.uint64)
-            dk = self._torch.from_numpy(allk.view(np.int64).copy()).to(f"cuda:{self.device}")
-            tops.append(self.engines[0].merge_topk(dk, k))
+            allk = np.concatenate(keys[s]) if keys[s] else np.zeros(0, np.uint64)
+            dk = torch.from_numpy(allk.view(np.int64).copy()).to(self.dev)
+            idx, sc = e.merge_topk(dk, k)
+            mine = torch.full((k,), -1, dtype=torch.int64)   # UINT64_MAX pads, as local_topk
+            mine[: len(idx)] = parallel.encode_keys(sc, idx)
+            g = parallel.gather_keys(mine.to(self.dev), group)
+            if g.numel() > k:                  # more than one rank: merge the gathered rankings
+                idx, sc = e.merge_topk(g, k)
+            tops.append((idx, sc))
         return best, pose, tops
 
     def close(self):
-        for e in self.engines:
-            e.close()
+        self.engine.close()

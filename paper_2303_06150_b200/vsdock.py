@@ -271,6 +271,10 @@ class Engine:
         self._check(self.lib.vs_get_results(self.h, slot, _ptr(s), _ptr(p), _ptr(a), 0))
         return Results(s, p, a[: self.n_sweeps * self._nR])
 
+    def results_into(self, slot, best_score, best_pose, angles=None):
+        """Copy the results into caller-owned HOST arrays (pinned for full-speed DMA)."""
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(best_score), _ptr(best_pose), _ptr(angles), 0))
+
     def results_device(self, slot, best_score, best_pose, angles=None):
         self._check(self.lib.vs_get_results(self.h, slot, _ptr(best_score), _ptr(best_pose), _ptr(angles), 1))
 
