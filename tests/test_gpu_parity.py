@@ -109,6 +109,25 @@ def test_c2_sample_parity_and_bucketing_invariance(c2):
     check(e3, lib, idx[:40], pk, rot, tr, cs)
 
 
+def test_round_ring_many_tiny_launches_bit_identical(c2):
+    """The dock kernel's round ring: launches of 1..5 rounds on up to 148 CTAs
+    (exhaustion at the first, second or a later sequence, CTAs with no round at all), P not a
+    multiple of the poses per warp, several ligands per round, many streams -- all bit-identical
+    to one fused launch per class."""
+    c, lib, pk = c2
+    sub = lib.subset(np.arange(1500))
+    for P in (64, 30, 6):
+        e, *_ = run(sub, [pk], P=P, K=c["K"], debug=False)
+        ref, ref_xyz = e.results(0), e.coords(0)
+        for cap in (1, 2, 5):
+            e2, *_ = run(sub, [pk], P=P, K=c["K"], debug=False, launch_per_bucket=True, bucket_capacity=cap,
+                         n_streams=8)
+            r2 = e2.results(0)
+            assert np.array_equal(ref.best_score, r2.best_score), (P, cap)
+            assert np.array_equal(ref.best_pose, r2.best_pose) and np.array_equal(ref.angles, r2.angles)
+            assert np.array_equal(ref_xyz, e2.coords(0))
+
+
 def test_c3_large_ligand_sample_parity():
     c = vsgen.CONFIGS["C3"]
     lib = vsgen.ligands(2048, c["seed"], c["atoms"], c["rot"])
