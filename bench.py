@@ -27,6 +27,10 @@ sys.path.insert(0, ROOT)
 
 FLOPS_PER_EVAL = 43          # rotation 18 + fractions 3 + 7 lerps x 3 + accumulate 1
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 (SMs x FP32 lanes x FMA x max clock)
+SMEM_PEAK_TBPS = 148 * 128 * 1.965e9 / 1e12          # 37.2: 128 B / clk / SM shared-memory crossbar (guide)
+# measured ceiling of random 8-corner trilinear gathers from a shared-memory 32^3 grid on this
+# B200 (tools/microbench_gather.cu, profiles/r01_gather_microbench.txt): 337 G evaluations / s
+GATHER_CEILING_EVALS = 337.4e9
 
 
 def parse():
@@ -257,8 +261,19 @@ def main():
     dock_avg = float(np.mean(dock_ms))
     evals_step = evals / args.steps
     achieved = FLOPS_PER_EVAL * evals_step / (dock_avg / 1e3) / 1e12
+    # executed evaluations: the kernel also scores the identity angle (k = 0) of every moving
+    # atom; algorithmic: E_alg = P (A + (K - 1) sum|M_r|)
+    a_i = np.diff(lib.atom_off).astype(np.float64)
+    m_i = np.zeros(n)
+    if lib.frags.shape[0]:
+        owner = np.repeat(np.arange(n), np.diff(lib.frag_off))
+        np.add.at(m_i, owner, (lib.frags[:, 3] - lib.frags[:, 2]).astype(np.float64))
+    K_ = c["K"]
+    exec_ratio = float((a_i + K_ * m_i).sum() / max(1.0, (a_i + (K_ - 1) * m_i).sum())) if K_ > 1 else 1.0
+    exec_rate = evals_step * exec_ratio / (dock_avg / 1e3)
     if world > 1:
         achieved = reduce_scalar(achieved, dist.ReduceOp.MIN)
+        exec_rate = reduce_scalar(exec_rate, dist.ReduceOp.MIN)
     classes = eng.classes()
 
     e2e = None
@@ -272,7 +287,9 @@ def main():
                               bucket_multiple=args.bucket_multiple, n_streams=args.streams, rank=rank,
                               world_size=world)
         pdk.setup(rot, tr, cs, pockets)
-        run_e2e = lambda: pdk.run(*h_lib, k=K_TOP, chunks=args.e2e_chunks, max_atoms=max_atoms)
+        # chunks of >= 125k ligands: below that the per-chunk fixed cost outweighs the overlap
+        chunks = max(1, min(args.e2e_chunks, n // 125000))
+        run_e2e = lambda: pdk.run(*h_lib, k=K_TOP, chunks=chunks, max_atoms=max_atoms)
         for _ in range(args.warmup):
             run_e2e()
         torch.cuda.synchronize()
@@ -293,7 +310,7 @@ def main():
         e2e = {"value": n * len(pockets) / (t_e / args.steps / 1e3), "unit": "ligands/s",
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
                "api": f"PipelinedDocker.run: pinned host CSR -> host scores/poses + top-{K_TOP}; "
-                      f"{args.e2e_chunks} chunks on 2 contexts (H2D of chunk i+1 overlaps docking of chunk i)"}
+                      f"{chunks} chunk(s), H2D of chunk i+1 on a copy stream under the docking of chunk i"}
     unsorted = None
     if not args.no_unsorted:
         if args.no_e2e:
@@ -327,6 +344,17 @@ def main():
                          "kernel": "dock_kernel<AC,NW> (all launches of the dock phase)",
                          "dock_ms_per_step": dock_avg, "evals_per_step": evals_step,
                          "flops_per_eval": FLOPS_PER_EVAL,
+                         "smem": {"bound": "smem", "unit": "TB/s",
+                                  "achieved": achieved / FLOPS_PER_EVAL * 32,
+                                  "peak": SMEM_PEAK_TBPS,
+                                  "frac": achieved / FLOPS_PER_EVAL * 32 / SMEM_PEAK_TBPS,
+                                  "bytes_per_eval": 32,
+                                  "executed_evals_per_s": exec_rate,
+                                  "random_gather_ceiling_evals_per_s": GATHER_CEILING_EVALS,
+                                  "frac_of_gather_ceiling": exec_rate / GATHER_CEILING_EVALS,
+                                  "note": "8 fp32 corner gathers per evaluation from the shared-memory grid; random "
+                                          "4-byte gathers run ~3.1-way bank-conflicted, so the measured ceiling "
+                                          "(microbenchmark) is ~1/3.2 of the crossbar peak"},
                          "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (guide unit counts, max clock)"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
             "cpu_baseline": cpu, "unsorted": unsorted,
