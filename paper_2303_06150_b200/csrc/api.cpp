@@ -344,14 +344,14 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs
             const int LC = ligs_per_cta(NW, PPW, c->P);
             const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
             int b = 0;
-            CK(dock_occupancy(ci.AC, NW, PPW, grid_fixed(rs, ps), L.total, &b));
+            CK(dock_occupancy(ci.AC, NW, PPW, grid_fixed(rs, ps), c->K, L.total, &b));
             if (b >= 1) {
                 ci.NW = NW;
                 ci.PPW = PPW;
                 ci.LC = LC;
                 ci.b = b;
                 ci.smem = L.total;
-                CK(dock_kernel_attrs(ci.AC, NW, PPW, grid_fixed(rs, ps), &ci.attr));
+                CK(dock_kernel_attrs(ci.AC, NW, PPW, grid_fixed(rs, ps), c->K, &ci.attr));
                 break;
             }
         }

@@ -9,16 +9,16 @@ using dk::DockFn;
 
 namespace {
 
-DockFn pick(int AC, int NW, int PPW, int fix) {
+DockFn pick(int AC, int NW, int PPW, int fix, int K) {
     switch (AC) {
-        case 32: return dk::dock_pick_32(fix, NW, PPW);
-        case 64: return dk::dock_pick_64(fix, NW, PPW);
-        case 96: return dk::dock_pick_96(fix, NW, PPW);
-        case 128: return dk::dock_pick_128(fix, NW, PPW);
-        case 160: return dk::dock_pick_160(fix, NW, PPW);
-        case 192: return dk::dock_pick_192(fix, NW, PPW);
-        case 224: return dk::dock_pick_224(fix, NW, PPW);
-        case 256: return dk::dock_pick_256(fix, NW, PPW);
+        case 32: return dk::dock_pick_32(fix, NW, PPW, K);
+        case 64: return dk::dock_pick_64(fix, NW, PPW, K);
+        case 96: return dk::dock_pick_96(fix, NW, PPW, K);
+        case 128: return dk::dock_pick_128(fix, NW, PPW, K);
+        case 160: return dk::dock_pick_160(fix, NW, PPW, K);
+        case 192: return dk::dock_pick_192(fix, NW, PPW, K);
+        case 224: return dk::dock_pick_224(fix, NW, PPW, K);
+        case 256: return dk::dock_pick_256(fix, NW, PPW, K);
         default: return nullptr;
     }
 }
@@ -42,14 +42,14 @@ void grid_strides(int nx, int ny, int* rs, int* ps) {
 
 bool grid_fixed(int rs, int ps) { return rs == dk::kFixRS && ps == dk::kFixPS; }
 
-cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, cudaFuncAttributes* attr) {
-    DockFn f = pick(AC, NW, PPW, fix);
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, int K, cudaFuncAttributes* attr) {
+    DockFn f = pick(AC, NW, PPW, fix, K);
     if (!f) return cudaErrorInvalidValue;
     return cudaFuncGetAttributes(attr, reinterpret_cast<const void*>(f));
 }
 
-cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, size_t smem, int* blocks_per_sm) {
-    DockFn f = pick(AC, NW, PPW, fix);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem, int* blocks_per_sm) {
+    DockFn f = pick(AC, NW, PPW, fix, K);
     if (!f) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -63,7 +63,7 @@ cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, size_t smem, int* b
 }
 
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
-    DockFn f = pick(AC, NW, PPW, grid_fixed(a.pk.rs, a.pk.ps));
+    DockFn f = pick(AC, NW, PPW, grid_fixed(a.pk.rs, a.pk.ps), a.K);
     if (!f) return cudaErrorInvalidValue;
     if (a.n <= 0) return cudaSuccess;
     f<<<grid, NW * 32, smem, st>>>(a);

@@ -219,13 +219,17 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
 
 // PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
 // a6 placement, a7 sweep, a9 pose score.
-template <int AC, int PPW, bool FIX>
+// KT = the angle count when known at compile time (8: the production path, every lane-map
+// constant folds), 0 = runtime K.
+template <int AC, int PPW, bool FIX, int KT>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, PoseBuf<AC> B, const float* __restrict__ G,
-                                           const PocketDev& pk, int K, int kbits, int S_w, float ck, float sk,
+                                           const PocketDev& pk, int K_rt, int kbits_rt, int S_w, float ck, float sk,
                                            const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
                                            float* __restrict__ scoreOut, int lane) {
     constexpr int LPP = 32 / PPW;
+    const int K = KT ? KT : K_rt;
+    const int kbits = KT ? (KT == 1 ? 0 : KT == 2 ? 1 : KT == 4 ? 2 : KT == 8 ? 3 : KT == 16 ? 4 : 5) : kbits_rt;
     const int li = lane & (LPP - 1);
     const float* rx = rec;
     const float* ry = rec + AC;
@@ -408,7 +412,7 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned c
 // long before use and global rounds are claimed in sequence order), the
 // warp that completes the last item of a round reduces its best pose (a9) and frees the
 // slot.  NW is therefore free of P / PPW (e.g. 12 warps of 4 poses for 64 poses).
-template <int AC, int NW, int PPW, bool FIX>
+template <int AC, int NW, int PPW, bool FIX, int KT>
 __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DockRing ring;
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     __syncthreads();
     if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
-    const int K = a.K, S_w = a.S_w, P = a.P;
+    const int K = KT ? KT : a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
     const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
     const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride<AC>()};
@@ -484,7 +488,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             const float* rec = reinterpret_cast<const float*>(slot + L.rec_o) + l * a.rec_floats;
             float* sScore = reinterpret_cast<float*>(slot + L.score_o);
             uint8_t* sAng = slot + L.ang_o;
-            dock_poses<AC, PPW, FIX>(rec, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w, ck, sk, sCS,
+            dock_poses<AC, PPW, FIX, KT>(rec, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w, ck, sk, sCS,
                                      sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncwarp();
@@ -573,22 +577,26 @@ __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, 
 using DockFn = void (*)(const DockArgs);
 
 template <int AC, bool FIX>
-DockFn pick_ac(int NW, int PPW) {
-    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, FIX> : (NW == 16 ? dock_kernel<AC, 16, 1, FIX> : nullptr);
+DockFn pick_ac(int NW, int PPW, int K) {
+    if (PPW == 4 && K == 8 && FIX)   // production path: compile-time K = 8
+        return NW == 16 ? dock_kernel<AC, 16, 4, FIX, 8>
+               : NW == 12 ? dock_kernel<AC, 12, 4, FIX, 8>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, FIX, 8> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX, 8> : nullptr));
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, FIX, 0> : (NW == 16 ? dock_kernel<AC, 16, 1, FIX, 0> : nullptr);
     if (PPW == 2)
-        return NW == 32 ? dock_kernel<AC, 32, 2, FIX>
-                        : (NW == 16 ? dock_kernel<AC, 16, 2, FIX> : (NW == 8 ? dock_kernel<AC, 8, 2, FIX> : nullptr));
+        return NW == 32 ? dock_kernel<AC, 32, 2, FIX, 0>
+                        : (NW == 16 ? dock_kernel<AC, 16, 2, FIX, 0> : (NW == 8 ? dock_kernel<AC, 8, 2, FIX, 0> : nullptr));
     if (PPW == 4)
-        return NW == 16 ? dock_kernel<AC, 16, 4, FIX>
-                        : NW == 12 ? dock_kernel<AC, 12, 4, FIX>
-                                   : (NW == 8 ? dock_kernel<AC, 8, 4, FIX> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX> : nullptr));
+        return NW == 16 ? dock_kernel<AC, 16, 4, FIX, 0>
+               : NW == 12 ? dock_kernel<AC, 12, 4, FIX, 0>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, FIX, 0> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX, 0> : nullptr));
     return nullptr;
 }
 
 // Per-atom-class entry points, each compiled in its own translation unit
 // (dock_inst.cu with -DVSD_AC=<AC>) so the 8 classes build in parallel.
 #define VSD_DECL_CLASS(ac)                                                                                     \
-    DockFn dock_pick_##ac(int fix, int NW, int PPW);                                                           \
+    DockFn dock_pick_##ac(int fix, int NW, int PPW, int K);                                                           \
     cudaError_t launch_finalize_##ac(const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 VSD_DECL_CLASS(32)
 VSD_DECL_CLASS(64)

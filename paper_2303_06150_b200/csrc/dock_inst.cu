@@ -11,8 +11,8 @@
 namespace vsd {
 namespace dk {
 
-DockFn VSD_CAT(dock_pick_, VSD_AC)(int fix, int NW, int PPW) {
-    return fix ? pick_ac<VSD_AC, true>(NW, PPW) : pick_ac<VSD_AC, false>(NW, PPW);
+DockFn VSD_CAT(dock_pick_, VSD_AC)(int fix, int NW, int PPW, int K) {
+    return fix ? pick_ac<VSD_AC, true>(NW, PPW, K) : pick_ac<VSD_AC, false>(NW, PPW, K);
 }
 
 cudaError_t VSD_CAT(launch_finalize_, VSD_AC)(const DockArgs& a, const int64_t* atom_off, float* xyz_out,

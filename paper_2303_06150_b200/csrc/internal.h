@@ -111,8 +111,8 @@ cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const 
                         const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
                         int4* meta, cudaStream_t st);
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
-cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, cudaFuncAttributes* attr);
-cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, size_t smem, int* blocks_per_sm);
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, int K, cudaFuncAttributes* attr);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem, int* blocks_per_sm);
 bool grid_fixed(int rs, int ps);
 cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
