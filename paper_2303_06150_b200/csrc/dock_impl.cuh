@@ -305,8 +305,20 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
         for (int t = li; t < S_w * R; t += LPP) angOut[t] = 0;
     }
     // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree) (Q22)
+    // four independent evaluations in flight, summed in the same ascending order
     float acc = 0.f;
-    for (int i = li; i < A; i += LPP) {
+    int i = li;
+    for (; i + 3 * LPP < A; i += 4 * LPP) {
+        float g[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float4 v = B.get(i + u * LPP);
+            g[u] = grid_g<FIX>(G, v.x, v.y, v.z, pk);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, g[u]);
+    }
+    for (; i < A; i += LPP) {
         const float4 v = B.get(i);
         acc = __fadd_rn(acc, grid_g<FIX>(G, v.x, v.y, v.z, pk));
     }
