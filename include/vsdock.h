@@ -127,7 +127,10 @@ typedef struct {
 /* Run the hot path a1..a9 for the batch against pockets pocket_ids[0..n_pockets):
  * validate, classify, bucket (stable), LPT-shard, pack, and dock this rank's
  * buckets into every pocket.  Asynchronous after the three small host syncs of
- * the preparation phase; results are valid after vs_wait.
+ * the preparation phase; results are valid after vs_wait.  The pose / angle
+ * tables and pocket grids are uploaded into the workspace only when they (or the
+ * workspace) changed since the previous submit, so a submit of a device batch
+ * issues no host-to-device copy of its own besides the bucket tables.
  * Errors: VS_E_PARSE (first invalid ligand), VS_E_OVERFLOW_*, VS_E_NOFIT,
  * VS_E_WORKSPACE, VS_E_STATE (tables/pockets/workspace missing), VS_E_CUDA. */
 vs_status vs_submit(vs_ctx* ctx, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets);
