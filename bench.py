@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--ligands", type=int, default=0, help="override the ligand count (not a bench value)")
     ap.add_argument("--no-unsorted", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--e2e-chunks", type=int, default=0, help="0: geometric schedule (pipeline.chunk_bounds)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-every", type=int, default=250)
     ap.add_argument("--streams", type=int, default=4)
@@ -287,8 +287,11 @@ def main():
                               bucket_multiple=args.bucket_multiple, n_streams=args.streams, rank=rank,
                               world_size=world)
         pdk.setup(rot, tr, cs, pockets)
-        # chunks of >= 125k ligands: below that the per-chunk fixed cost outweighs the overlap
-        chunks = max(1, min(args.e2e_chunks, n // 125000))
+        # geometric chunk schedule (pipeline.chunk_bounds): a small first chunk, each next one
+        # up to 4x larger; a single chunk below 250k ligands (fixed per-chunk cost)
+        from paper_2303_06150_b200.pipeline import chunk_bounds
+        chunks = args.e2e_chunks if args.e2e_chunks > 0 else (0 if n >= 250000 else 1)
+        n_chunks = len(chunk_bounds(n, chunks)) - 1
         run_e2e = lambda: pdk.run(*h_lib, k=K_TOP, chunks=chunks, max_atoms=max_atoms)
         for _ in range(args.warmup):
             run_e2e()
@@ -310,7 +313,8 @@ def main():
         e2e = {"value": n * len(pockets) / (t_e / args.steps / 1e3), "unit": "ligands/s",
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
                "api": f"PipelinedDocker.run: pinned host CSR -> host scores/poses + top-{K_TOP}; "
-                      f"{chunks} chunk(s), H2D of chunk i+1 on a copy stream under the docking of chunk i"}
+                      f"{n_chunks} chunk(s) {chunk_bounds(n, chunks)[1:]}, H2D of chunk i+1 on a copy stream under "
+                      f"the docking of chunk i"}
     unsorted = None
     if not args.no_unsorted:
         if args.no_e2e:

@@ -28,6 +28,25 @@ def _bounds(atom_off, frag_off, lo, hi):
     return ao, fo, int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
 
 
+def chunk_bounds(n: int, chunks: int = 0, first: int = 32, growth: int = 4):
+    """Chunk boundaries of an n-ligand library.  chunks > 0: equal chunks.  chunks = 0: a
+    geometric schedule -- first chunk n / first, each next one at most `growth` times the
+    previous -- so only a small first copy is exposed while every later copy (~7x faster
+    than docking the same ligands on B200) still hides under the previous chunk's dock."""
+    if n <= 0:
+        return [0, 0]
+    if chunks > 0:
+        chunks = min(int(chunks), n)
+        return [n * c // chunks for c in range(chunks + 1)]
+    b, size = [0], max(1, n // first)
+    while b[-1] < n:
+        b.append(min(n, b[-1] + size))
+        size *= growth
+    if len(b) > 2 and (b[-1] - b[-2]) < (b[-2] - b[-3]) // 4:   # fold a tiny tail into its predecessor
+        b.pop(-2)
+    return b
+
+
 class PipelinedDocker:
     """Dock a host-resident library in chunks; H2D of the next chunk overlaps the current one."""
 
@@ -64,12 +83,12 @@ class PipelinedDocker:
             ev.record(self.copy)
         return dev, ev, host
 
-    def run(self, atom_off, xyz, frag_off, frags, k: int = 1000, chunks: int = 4, max_atoms: int = 256,
+    def run(self, atom_off, xyz, frag_off, frags, k: int = 1000, chunks: int = 0, max_atoms: int = 256,
             group=None):
         """Returns (best_score [P][n], best_pose [P][n], topk [(index, score)] per pocket) on the host.
 
         xyz / frags should be pinned host tensors (torch ``pin_memory``) for overlapped copies.
-        With ``rank`` / ``world_size`` engine options under an initialised process group, every
+        ``chunks``: see ``chunk_bounds`` (0 = geometric schedule).  With ``rank`` / ``world_size`` engine options under an initialised process group, every
         rank docks its LPT share of each chunk and the per-pocket top-k is merged across ranks."""
         import time
         from . import parallel
@@ -77,8 +96,8 @@ class PipelinedDocker:
         e = self.engine
         n = int(atom_off.shape[0]) - 1
         npk = len(self.pocket_ids)
-        chunks = max(1, min(int(chunks), max(1, n)))
-        bounds = [n * c // chunks for c in range(chunks + 1)]
+        bounds = chunk_bounds(n, chunks)
+        chunks = len(bounds) - 1
         # pinned host outputs: the per-chunk result reads are plain DMA, not staged copies
         best = torch.full((npk, n), float("nan"), dtype=torch.float32).pin_memory().numpy()
         pose = torch.full((npk, n), -1, dtype=torch.int32).pin_memory().numpy()

@@ -70,3 +70,17 @@ def test_bench_reference_arm_json_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0 and line["higher_is_better"] is True
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_pipeline_chunk_schedule():
+    """Host-only chunk planning of the double-buffered path (pipeline.chunk_bounds)."""
+    from paper_2303_06150_b200.pipeline import chunk_bounds
+    for n in (0, 1, 5, 31, 32, 1000, 250_000, 1_000_000):
+        b = chunk_bounds(n)
+        assert b[0] == 0 and b[-1] == n and all(x < y for x, y in zip(b, b[1:])) or n == 0
+        sizes = [y - x for x, y in zip(b, b[1:])]
+        if n >= 32 and len(sizes) > 1:
+            assert sizes[0] == n // 32
+            assert all(s2 <= 4 * s1 for s1, s2 in zip(sizes, sizes[1:-1]))
+    assert chunk_bounds(100, 3) == [0, 33, 66, 100]
+    assert chunk_bounds(1_000_000) == [0, 31250, 156250, 656250, 1_000_000]
