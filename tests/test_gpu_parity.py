@@ -259,6 +259,29 @@ def test_two_sweeps_and_two_pockets_with_different_grids():
         check(e, lib, range(lib.n), pk, rot, tr, cs, slot=slot, S_w=2)
 
 
+def test_non_cubic_grid_runtime_strides():
+    """A 36 x 30 x 26 grid (nx > 32: the runtime-stride layout, not the fixed 32 x 32-plane
+    one), off-centre origin, h = 0.8 A: the score hook and full docking parity."""
+    rng = np.random.default_rng(11)
+    base = vsgen.pocket(105, n=36, spacing=0.8)
+    G = np.ascontiguousarray(base.grid[:26, :30, :36]) + rng.normal(0, 0.05, (26, 30, 36)).astype(np.float32)
+    origin = (-1.5, 0.25, 2.0)
+    h = 0.8
+    center = tuple(o + h * (n - 1) / 2 for o, n in zip(origin, (36, 30, 26)))
+    pk = vsgen.Pocket(G.astype(np.float32), origin, h, center, 0.7)
+    e = engine()
+    pid = e.load_pocket(pk)
+    pts = rng.uniform(-4, 32, size=(20000, 3)).astype(np.float32)
+    g = e.score_points(pid, pts)
+    ref = oracle.grid_score(pk, pts.astype(np.float64))
+    # fp32 u = (x - o) * (1/h) with h = 0.8 (1/h inexact): |du| <~ 2 ulp(40) ~ 8e-6 grid units,
+    # times |grad g| <~ 2 per grid unit -> 2e-5 (the h = 1 hook test above is exact to 2e-6)
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < 2e-5
+    lib = vsgen.ligands(24, 13, (20, 60), (0, 6))
+    e2, rot, tr, cs = run(lib, [pk], P=8, K=8)
+    check(e2, lib, range(lib.n), pk, rot, tr, cs)
+
+
 def test_empty_batch():
     e = engine()
     setup(e, [vsgen.pocket(101)], 8, 8)
