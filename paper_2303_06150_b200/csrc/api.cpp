@@ -209,9 +209,6 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.top_x = (float)(d.nx - 1);
     p.top_y = (float)(d.ny - 1);
     p.top_z = (float)(d.nz - 1);
-    p.top2_x = (float)(d.nx - 2);
-    p.top2_y = (float)(d.ny - 2);
-    p.top2_z = (float)(d.nz - 2);
     p.kh = (float)((double)d.out_slope * (double)d.spacing);
     p.h = d.spacing;
     p.inv_h = (float)(1.0 / (double)d.spacing);

@@ -4,22 +4,24 @@
 // contraction, BJ: "no tensor cores").
 //
 // B200 design:
-//  * one CTA per SM, persistent over a launch's ligands with a dynamic round
-//    counter; the pocket grid (32^3 fp32 = 128 KB, padded strides) lives in
-//    SHARED memory for the whole launch -- the 8 corner gathers of every
-//    evaluation are shared-memory loads, never L1/L2;
-//  * a CTA docks LC ligands at a time; its NW warps split the ligand's poses,
-//    PPW poses per warp (lane groups of 32/PPW), so all warps of a CTA run the
-//    same control flow (same A, R, M_r: poses of one ligand differ only in data);
+//  * one CTA per SM, persistent over a launch's ligands; the pocket grid (32^3 fp32
+//    = 128 KB, padded strides) lives in SHARED memory for the whole launch -- the 8
+//    corner gathers of every evaluation are shared-memory loads, never L1/L2;
+//  * warps run independently over a 3-slot ring of staged rounds (LC ligands each):
+//    a warp item is PPW poses of one ligand (lane groups of 32/PPW), items are claimed
+//    from a CTA-local counter, rounds from the launch's global counter (dynamic
+//    balancing across CTAs); no CTA barrier after the prologue (dock_kernel below);
 //  * sweep lane map inside a pose group: li = jl * K + k -- (moving atom jl of
-//    the pass, angle k).  Each lane holds its angle's rotation in registers,
-//    lanes of equal k sum with xor shuffles, the argmin over k takes log2 K
-//    shuffle rounds (ties -> lowest k, Q11), and the winner is applied;
-//  * (x, y) arithmetic is packed in Blackwell's FFMA2/FADD2 (per-element IEEE
-//    fma/add, so every result is bit-identical to the scalar form);
-//  * template<int AC, int NW, int PPW> per atom class = the paper's "non-type
-//    template parameter for the kernel maximum number of atoms":
-//    AC sizes the per-pose buffers in shared memory, hence the occupancy.
+//    the step, angle k).  Each lane holds its angle's rotation in registers and
+//    scores the fragment's atoms in warp-uniform batches of up to 4; lanes of equal
+//    k sum with xor shuffles, the argmin over k takes log2 K shuffle rounds (ties ->
+//    lowest k, Q11), and the winner is applied (from registers when it fits);
+//  * (x, y) arithmetic is packed in Blackwell's FFMA2/FADD2/FMUL2 (per-element IEEE
+//    ops, so every result is bit-identical to the scalar form);
+//  * template<int AC, int NW, int PPW, bool FIX, int KT> per atom class = the paper's
+//    "non-type template parameter for the kernel maximum number of atoms":
+//    AC sizes the per-pose buffers in shared memory, hence the warps per CTA;
+//    FIX = compile-time grid strides (<= 32 x 32 planes), KT = compile-time K (8).
 //
 // All arithmetic that decides an angle or is replayed (placement, Rodrigues,
 // rotation, interpolation) uses explicit _rn intrinsics in shared helpers, so

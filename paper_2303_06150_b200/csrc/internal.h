@@ -23,7 +23,6 @@ struct PocketDev {
     int nx, ny, nz;
     int rs, ps;            // shared-memory row stride and plane stride (floats)
     float top_x, top_y, top_z;    // n - 1
-    float top2_x, top2_y, top2_z; // n - 2
     float kh;              // kappa * h  (penalty per grid unit of excess)
     float h;
     float ox, oy, oz;      // origin
