@@ -350,6 +350,37 @@ def test_c4_full_size_sampled_parity():
     assert rep.ok, rep.summary() + str(rep.failures[:5])
 
 
+def test_c5_full_size_campaign_sampled_parity_and_topk():
+    """BASELINE configs[4]: the C4 library x 4 pockets in one submit (bench launch
+    configuration); per pocket, sampled ligands against the oracle and the top-1000 equal to
+    the sorted ranking of the GPU scores; pockets differ (scores are not copies)."""
+    import torch
+    c = vsgen.CONFIGS["C5"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    pks = [vsgen.pocket(s) for s in c["pockets"]]
+    e = engine(bucket_multiple=16, n_streams=4)
+    rot, tr, cs, ids = setup(e, pks, c["P"], c["K"])
+    d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    e.submit(*d, ids, on_device=True)
+    e.wait()
+    rng = np.random.default_rng(5)
+    prev = None
+    for slot, pk in enumerate(pks):
+        r = e.results(slot)
+        assert np.isfinite(r.best_score).all()
+        if prev is not None:
+            assert not np.array_equal(prev, r.best_score)
+        prev = r.best_score
+        idx = rng.choice(lib.n, 8, replace=False)
+        rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, e.coords(slot),
+                           band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+        assert rep.ok, rep.summary() + str(rep.failures[:5])
+        keys, _ = e.local_topk(slot, 1000)
+        ti, ts = e.merge_topk(keys, 1000)
+        assert list(ti) == list(oracle.topk(r.best_score, 1000))
+        assert np.array_equal(ts, r.best_score[ti])
+
+
 def test_pipelined_docker_matches_single_submit(c2):
     """Double-buffered chunks give the single-submit results and ranking."""
     import torch
