@@ -31,6 +31,9 @@ SMEM_PEAK_TBPS = 148 * 128 * 1.965e9 / 1e12          # 37.2: 128 B / clk / SM sh
 # measured ceiling of random 8-corner trilinear gathers from a shared-memory 32^3 grid on this
 # B200 (tools/microbench_gather.cu, profiles/r01_gather_microbench.txt): 337 G evaluations / s
 GATHER_CEILING_EVALS = 337.4e9
+# measured L2 read bandwidth of this B200 (tools/microbench_l2.cu, 48-96 MB L2-resident buffer,
+# ld.global.cg; profiles/r01_l2_microbench.txt): BJ's "FP32/L2" roof = min(FP32, AI x BW_L2)
+L2_READ_TBPS = 16.6
 
 
 def parse():
@@ -348,6 +351,13 @@ def main():
                          "kernel": "dock_kernel<AC,NW> (all launches of the dock phase)",
                          "dock_ms_per_step": dock_avg, "evals_per_step": evals_step,
                          "flops_per_eval": FLOPS_PER_EVAL,
+                         "fp32_l2": {"peak": min(FP32_PEAK_TFLOPS, FLOPS_PER_EVAL / 32 * L2_READ_TBPS),
+                                     "unit": "TFLOP/s", "l2_read_TBps": L2_READ_TBPS,
+                                     "ai_flop_per_byte": FLOPS_PER_EVAL / 32,
+                                     "frac": achieved / min(FP32_PEAK_TFLOPS, FLOPS_PER_EVAL / 32 * L2_READ_TBPS),
+                                     "note": "BASELINE.json's 'FP32/L2 roofline' (SURVEY 8(d)): achieved / "
+                                             "min(FP32 peak, algorithmic intensity x measured L2 bandwidth); the "
+                                             "grid itself is served from shared memory"},
                          "smem": {"bound": "smem", "unit": "TB/s",
                                   "achieved": achieved / FLOPS_PER_EVAL * 32,
                                   "peak": SMEM_PEAK_TBPS,
