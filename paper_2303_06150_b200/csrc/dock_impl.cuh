@@ -340,26 +340,42 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
+// Bounded back-off for the ring's spin-waits: a legitimate wait lasts microseconds; a
+// wait of seconds can only be a broken invariant, and trapping turns it into a launch
+// error (VS_E_CUDA from vs_wait) instead of a hung GPU.
+__device__ __forceinline__ void ring_backoff(unsigned& spins) {
+    __nanosleep(64);
+    if (++spins > (1u << 26)) __trap();
+}
+
 // Ring control in static shared memory (one entry per slot).
 struct DockRing {
     int ready[kDockSlots];   // round sequence number whose record this slot holds
     int round[kDockSlots];   // global round index held (-1: the launch is exhausted)
     int done[kDockSlots];    // warp items of the slot's round completed
     int free_seq[kDockSlots];// next sequence number allowed into the slot
+    int claim[kDockSlots];   // global round index claimed for sequence s (at s % kDockSlots), one ahead
     int item;                // CTA-local item counter
     int end_seq;             // first sequence number that found the launch exhausted (INT_MAX: none yet)
 };
 
-// Claim the next global round and stage its LC records + meta into `slot` (one warp,
-// plain 16-byte loads); publish it as sequence `seq` with a release store.
+// Stage sequence `seq` into `slot` (one warp, plain 16-byte loads) and publish it with a
+// release store.  Its global round index was claimed one sequence earlier; the claim for
+// seq + 1 (the launch's global counter: dynamic scheduling across CTAs) is issued here and
+// its latency overlaps the record loads.  Claims stay in sequence order.
 template <int AC>
 __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, unsigned char* slot, const DockLayout& L,
                                            int seq, int n_rounds, int lane) {
     const int sl = seq % kDockSlots;
-    if (lane == 0)
-        while (ld_acquire_cta(&ring.free_seq[sl]) != seq) __nanosleep(64);
-    int round = 0;
-    if (lane == 0) round = atomicAdd(a.counter, 1);   // dynamic scheduling across the CTAs of the launch
+    if (lane == 0) {
+        unsigned spins = 0;
+        while (ld_acquire_cta(&ring.free_seq[sl]) != seq) ring_backoff(spins);
+    }
+    int round = 0, next = 0;
+    if (lane == 0) {
+        round = ring.claim[sl];
+        next = atomicAdd(a.counter, 1);
+    }
     round = __shfl_sync(FULL, round, 0);
     const int LC = a.ligs_per_cta;
     if (round < n_rounds) {
@@ -374,6 +390,7 @@ __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, un
     }
     __syncwarp();
     if (lane == 0) {
+        ring.claim[(seq + 1) % kDockSlots] = next;
         ring.round[sl] = round < n_rounds ? round : -1;
         if (round >= n_rounds) atomicMin(&ring.end_seq, seq);
         st_release_cta(&ring.ready[sl], seq);
@@ -450,6 +467,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     if (tid == 0) {
         ring.item = 0;
         ring.end_seq = 0x7fffffff;
+        ring.claim[0] = atomicAdd(a.counter, 1);
     }
     stage_grid(sG, pk);
     for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
@@ -475,13 +493,14 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         int ok = 0;
         if (lane == 0) {
             const int sl = seq % kDockSlots;
+            unsigned spins = 0;
             while (true) {
                 if (ld_acquire_cta(&ring.ready[sl]) == seq) {
                     ok = ring.round[sl] >= 0;
                     break;
                 }
                 if (*(volatile int*)&ring.end_seq <= seq) break;
-                __nanosleep(64);
+                ring_backoff(spins);
             }
         }
         ok = __shfl_sync(FULL, ok, 0);
