@@ -1,4 +1,5 @@
 // Microbenchmark (not product code): L2 read bandwidth of this B200, for the "FP32/L2"
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_l2 tools/microbench_l2.cu
 // roofline of BASELINE.json (achieved / min(FP32, AI x BW_L2)).
 // A 48 MB buffer (L2 is 126 MB) is read repeatedly by every SM with 16-byte ld.global.cg
 // (L1 bypassed), after one warm-up pass that makes it L2-resident; bytes / CUDA-event time.
