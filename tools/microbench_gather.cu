@@ -1,5 +1,5 @@
 // Microbenchmark (not product code): trilinear evaluations per second on B200 with the
-# build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_gather tools/microbench_gather.cu
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench_gather tools/microbench_gather.cu
 // 32^3 grid (a) in shared memory, 8 corner LDS per evaluation (the dock kernel's path),
 // (b) behind a texture object over pitch-linear memory, 2 tex2Dgather per evaluation
 // (z0 and z1 planes of a 32 x (32*33) 2D texture), raw texels, same lerp arithmetic.
