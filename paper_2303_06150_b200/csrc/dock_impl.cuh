@@ -182,9 +182,7 @@ __device__ __forceinline__ unsigned ord32(float v) {
 }
 
 // Per-pose coordinate buffer in shared memory: (x, y) pairs then z (12 B per atom), pose
-// buffers 3*AC + 4 floats apart so the PPW pose groups of a warp hit different banks.
-template <int AC>
-__host__ __device__ constexpr int pose_stride() { return 3 * AC + 4; }
+// buffers pose_stride_of(AC, NW, PPW) floats apart (internal.h).
 template <int AC>
 struct PoseBuf {
     float* b;   // (x, y) pairs [2 AC] | z [AC]: one 8-byte and one 4-byte load per atom
@@ -478,7 +476,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int K = KT ? KT : a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
     const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
-    const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride<AC>()};
+    const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride_of(AC, NW, PPW)};
     const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
     const int IG = LC * G;               // warp items per round

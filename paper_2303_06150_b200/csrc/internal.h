@@ -50,6 +50,14 @@ struct DockArgs {
     uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
 };
 
+// Per-pose coordinate buffer stride (floats): 3 AC + 8, i.e. 8 banks apart, so the 4 pose
+// groups of a warp write 8-atom blocks of (x, y) pairs in 2 wavefronts and of z in 1 (the
+// sweep's broadcast loads stay conflict-free).  The 12-warp 128-atom class has no room for
+// it and keeps 3 AC + 4 (4 banks apart).
+__host__ __device__ constexpr int pose_stride_of(int AC, int NW, int PPW) {
+    return 3 * AC + ((AC == 128 && NW * PPW == 48) ? 4 : 8);
+}
+
 // Shared-memory layout of dock<AC, NW, PPW> (byte offsets).  Used by the kernel
 // and by the host (occupancy query, launch) so both agree.  Rounds (LC ligands each)
 // live in a ring of kDockSlots slots: record, meta, pose scores, angle choices.
@@ -76,7 +84,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC));
     L.slot_b = q;
     L.slots = o; o += kDockSlots * q;
-    L.buf = o;   o += (size_t)NW * PPW * (3 * AC + 4) * 4;   // SoA x|y|z per pose, stride 3 AC + 4 floats
+    L.buf = o;   o += (size_t)NW * PPW * pose_stride_of(AC, NW, PPW) * 4;   // (x,y)|z per pose
     L.total = o;
     return L;
 }
