@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C4")
     ap.add_argument("--ligands", type=int, default=0, help="override the ligand count (not a bench value)")
+    ap.add_argument("--poses", type=int, default=0, help="override P (sensitivity row, not a bench value)")
     ap.add_argument("--no-unsorted", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=0, help="0: geometric schedule (pipeline.chunk_bounds)")
@@ -106,6 +107,8 @@ def workload(args):
     c = dict(vsgen.CONFIGS[args.config])
     if args.ligands:
         c["n"] = args.ligands
+    if args.poses:
+        c["P"] = args.poses
     lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
     pockets = [vsgen.pocket(s) for s in c["pockets"]]
     rot, tr = vsgen.pose_table(c["P"])
