@@ -225,7 +225,7 @@ template <int AC, int PPW, bool FIX, int KT>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, PoseBuf<AC> B, const float* __restrict__ G,
                                            const PocketDev& pk, int K_rt, int kbits_rt, int S_w, float ck, float sk,
-                                           const float* __restrict__ sCS, uint8_t* __restrict__ angOut,
+                                           uint8_t* __restrict__ angOut,
                                            float* __restrict__ scoreOut, int lane) {
     constexpr int LPP = 32 / PPW;
     const int K = KT ? KT : K_rt;
@@ -290,11 +290,17 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                             if (u < nst && j < hi) B.set(j, kp[u]);
                         }
                     }
-                } else if (valid && bk != 0) {
-                    const RotT Ms = rodrigues_t(ux, uy, uz, sCS[2 * bk], sCS[2 * bk + 1], yb.x, yb.y, yb.z);
-                    for (int j = lo + li; j < hi; j += LPP) {
-                        const float4 v = B.get(j);
-                        B.set(j, apply_rot(Ms, v.x, v.y, v.z));
+                } else {
+                    // the winner's (cos, sin) from its lane (warp-uniform branch: nst is);
+                    // bit-identical rotation (same axis, same table entry)
+                    const int wl = (lane & ~(LPP - 1)) | bk;
+                    const float cw = __shfl_sync(FULL, ck, wl), sw2 = __shfl_sync(FULL, sk, wl);
+                    if (valid && bk != 0) {
+                        const RotT Ms = rodrigues_t(ux, uy, uz, cw, sw2, yb.x, yb.y, yb.z);
+                        for (int j = lo + li; j < hi; j += LPP) {
+                            const float4 v = B.get(j);
+                            B.set(j, apply_rot(Ms, v.x, v.y, v.z));
+                        }
                     }
                 }
                 __syncwarp();
@@ -338,6 +344,33 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
     asm volatile("st.release.cta.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
+// mbarrier + TMA bulk copy (cp.async.bulk, 1-D): the round loader issues the record copy
+// and moves on; consumers wait on the slot's mbarrier phase (one phase per use of the slot).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, unsigned parity) {
+    unsigned done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // Bounded back-off for the ring's spin-waits: a legitimate wait lasts microseconds; a
 // wait of seconds can only be a broken invariant, and trapping turns it into a launch
 // error (VS_E_CUDA from vs_wait) instead of a hung GPU.
@@ -355,12 +388,14 @@ struct DockRing {
     int claim[kDockSlots];   // global round index claimed for sequence s (at s % kDockSlots), one ahead
     int item;                // CTA-local item counter
     int end_seq;             // first sequence number that found the launch exhausted (INT_MAX: none yet)
+    uint64_t bar[kDockSlots];// record arrival (TMA complete_tx), phase (s / kDockSlots) & 1 for sequence s
 };
 
-// Stage sequence `seq` into `slot` (one warp, plain 16-byte loads) and publish it with a
-// release store.  Its global round index was claimed one sequence earlier; the claim for
-// seq + 1 (the launch's global counter: dynamic scheduling across CTAs) is issued here and
-// its latency overlaps the record loads.  Claims stay in sequence order.
+// Stage sequence `seq` into `slot` and publish it: lane 0 issues TMA bulk copies of the
+// round's LC records + meta (arrival on the slot's mbarrier) and a release store of the
+// round index.  The round was claimed one sequence earlier; the claim for seq + 1 (the
+// launch's global counter: dynamic scheduling across CTAs) is issued here, claims stay in
+// sequence order.
 template <int AC>
 __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, unsigned char* slot, const DockLayout& L,
                                            int seq, int n_rounds, int lane) {
@@ -368,31 +403,25 @@ __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, un
     if (lane == 0) {
         unsigned spins = 0;
         while (ld_acquire_cta(&ring.free_seq[sl]) != seq) ring_backoff(spins);
-    }
-    int round = 0, next = 0;
-    if (lane == 0) {
-        round = ring.claim[sl];
-        next = atomicAdd(a.counter, 1);
-    }
-    round = __shfl_sync(FULL, round, 0);
-    const int LC = a.ligs_per_cta;
-    if (round < n_rounds) {
-        const int slot0 = round * LC;
-        const int nl = min(LC, a.n - slot0);
-        const float4* src = reinterpret_cast<const float4*>(a.rec + (size_t)slot0 * a.rec_floats);
-        float4* dst = reinterpret_cast<float4*>(slot + L.rec_o);
-        const int n4 = nl * a.rec_floats / 4;
-        for (int t = lane; t < n4; t += 32) dst[t] = __ldg(src + t);
-        int4* md = reinterpret_cast<int4*>(slot + L.meta_o);
-        for (int t = lane; t < nl; t += 32) md[t] = __ldg(a.meta + slot0 + t);
-    }
-    __syncwarp();
-    if (lane == 0) {
+        const int round = ring.claim[sl];
+        const int next = atomicAdd(a.counter, 1);
+        if (round < n_rounds) {
+            const int LC = a.ligs_per_cta;
+            const int slot0 = round * LC;
+            const int nl = min(LC, a.n - slot0);
+            const unsigned rb = (unsigned)(nl * a.rec_floats * 4), mb = (unsigned)(nl * 16);
+            mbar_arrive_expect_tx(&ring.bar[sl], rb + mb);
+            bulk_g2s(slot + L.rec_o, a.rec + (size_t)slot0 * a.rec_floats, rb, &ring.bar[sl]);
+            bulk_g2s(slot + L.meta_o, a.meta + slot0, mb, &ring.bar[sl]);
+        } else {
+            mbar_arrive(&ring.bar[sl]);   // the phase completes without data
+        }
         ring.claim[(seq + 1) % kDockSlots] = next;
         ring.round[sl] = round < n_rounds ? round : -1;
         if (round >= n_rounds) atomicMin(&ring.end_seq, seq);
         st_release_cta(&ring.ready[sl], seq);
     }
+    __syncwarp();
 }
 
 // a9 best pose of one round (run by the warp that completes the round's last item).
@@ -451,7 +480,6 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sPose = reinterpret_cast<float*>(smem + L.pose);
-    float* sCS = reinterpret_cast<float*>(smem + L.cs);
     float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
     auto slot_ptr = [&](int seq) { return smem + L.slots + (size_t)(seq % kDockSlots) * L.slot_b; };
@@ -461,6 +489,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         ring.ready[tid] = -1;
         ring.done[tid] = 0;
         ring.free_seq[tid] = tid;
+        mbar_init(&ring.bar[tid], 1);
     }
     if (tid == 0) {
         ring.item = 0;
@@ -469,13 +498,12 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     }
     stage_grid(sG, pk);
     for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
-    for (int t = tid; t < 2 * a.K; t += blockDim.x) sCS[t] = a.cs[t];
     __syncthreads();
     if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
     const int K = KT ? KT : a.K, S_w = a.S_w, P = a.P;
     const int kbits = 31 - __clz(K);
-    const float ck = sCS[2 * (lane & (K - 1))], sk = sCS[2 * (lane & (K - 1)) + 1];
+    const float ck = a.cs[2 * (lane & (K - 1))], sk = a.cs[2 * (lane & (K - 1)) + 1];   // this lane's angle
     const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride_of(AC, NW, PPW)};
     const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
@@ -504,6 +532,10 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         ok = __shfl_sync(FULL, ok, 0);
         __syncwarp();   // lane 0's acquire orders the slot reads of the whole warp
         if (!ok) break;
+        {   // the record itself: TMA arrival on the slot's mbarrier (every lane acquires)
+            unsigned spins = 0;
+            while (!mbar_try_wait(&ring.bar[seq % kDockSlots], (unsigned)(seq / kDockSlots) & 1u)) ring_backoff(spins);
+        }
         // round s + 1 is claimed only once round s is (claims follow the sequence order, so
         // the first exhausted sequence bounds all later ones: end_seq is exact)
         if (it == loader_item) load_round<AC>(a, ring, slot_ptr(seq + 1), L, seq + 1, n_rounds, lane);
@@ -519,7 +551,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             const float* rec = reinterpret_cast<const float*>(slot + L.rec_o) + l * a.rec_floats;
             float* sScore = reinterpret_cast<float*>(slot + L.score_o);
             uint8_t* sAng = slot + L.ang_o;
-            dock_poses<AC, PPW, FIX, KT>(rec, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w, ck, sk, sCS,
+            dock_poses<AC, PPW, FIX, KT>(rec, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
                                      sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncwarp();

@@ -76,7 +76,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     // grid planes + one zero plane and row above: corner reads at i0 + 1 = n (weight 0) stay in bounds
     L.grid = o;  o += align16(((size_t)(nz + 1) * ps + rs + 2) * 4);
     L.pose = o;  o += align16((size_t)P * 12 * 4);
-    L.cs = o;    o += align16((size_t)K * 2 * 4);
+    L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
     size_t q = 0;
     L.rec_o = q;   q += align16((size_t)LC * (3 * AC + 32) * 4);
     L.meta_o = q;  q += (size_t)LC * 16;
