@@ -479,7 +479,6 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int LC = a.ligs_per_cta;
     const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
-    float* sPose = reinterpret_cast<float*>(smem + L.pose);
     float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
     auto slot_ptr = [&](int seq) { return smem + L.slots + (size_t)(seq % kDockSlots) * L.slot_b; };
@@ -497,7 +496,6 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         ring.claim[0] = atomicAdd(a.counter, 1);
     }
     stage_grid(sG, pk);
-    for (int p = tid; p < a.P; p += blockDim.x) scaled_pose(a.pose_tab + 12 * p, pk, sPose + 12 * p);
     __syncthreads();
     if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
@@ -551,7 +549,9 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             const float* rec = reinterpret_cast<const float*>(slot + L.rec_o) + l * a.rec_floats;
             float* sScore = reinterpret_cast<float*>(slot + L.score_o);
             uint8_t* sAng = slot + L.ang_o;
-            dock_poses<AC, PPW, FIX, KT>(rec, m.y, m.z, sPose + 12 * pc, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
+            float T[12];   // pose p in grid units, from the raw table (48 B, L1-resident)
+            scaled_pose(a.pose_tab + 12 * pc, pk, T);
+            dock_poses<AC, PPW, FIX, KT>(rec, m.y, m.z, T, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
                                      sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncwarp();

@@ -52,10 +52,9 @@ struct DockArgs {
 
 // Per-pose coordinate buffer stride (floats): 3 AC + 8, i.e. 8 banks apart, so the 4 pose
 // groups of a warp write 8-atom blocks of (x, y) pairs in 2 wavefronts and of z in 1 (the
-// sweep's broadcast loads stay conflict-free).  The 12-warp 128-atom class has no room for
-// it and keeps 3 AC + 4 (4 banks apart).
+// sweep's broadcast loads stay conflict-free).
 __host__ __device__ constexpr int pose_stride_of(int AC, int NW, int PPW) {
-    return 3 * AC + ((AC == 128 && NW * PPW == 48) ? 4 : 8);
+    return 3 * AC + 8;
 }
 
 // Shared-memory layout of dock<AC, NW, PPW> (byte offsets).  Used by the kernel
@@ -75,7 +74,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     size_t o = 0;
     // grid planes + one zero plane and row above: corner reads at i0 + 1 = n (weight 0) stay in bounds
     L.grid = o;  o += align16(((size_t)(nz + 1) * ps + rs + 2) * 4);
-    L.pose = o;  o += align16((size_t)P * 12 * 4);
+    L.pose = o;   // pose table: read per warp item from global (L1-resident), no shared copy
     L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
     size_t q = 0;
     L.rec_o = q;   q += align16((size_t)LC * (3 * AC + 32) * 4);
