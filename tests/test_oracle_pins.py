@@ -310,3 +310,27 @@ def test_brute_force_general_ligands_greedy_upper_bounds(c1):
         x, fr = L.ligand(i)
         bf = _brute_force(pk, x, fr, rot[:3], cs)
         assert r.best_score[j] >= bf - 1e-9 * max(1.0, abs(bf))
+
+
+# ----------------------------------------------------------------------------- S_w > 1 sweeps (Q13)
+
+def test_second_sweep_extends_the_first_and_never_raises_the_score(c1):
+    """The greedy is deterministic, so the first sweep of S_w = 2 replays S_w = 1 exactly
+    (identical angle choices) and the second sweep -- angle 0 is always a candidate -- can
+    only keep or lower every pose's score; a constant grid keeps every choice at 0."""
+    L, pk, (rot, tr), cs = c1
+    r1 = oracle.dock_batch(L, pk, rot, tr, cs, S_w=1)
+    r2 = oracle.dock_batch(L, pk, rot, tr, cs, S_w=2)
+    P = rot.shape[0]
+    for i in range(L.n):
+        R = int(L.frag_off[i + 1] - L.frag_off[i])
+        f0 = int(L.frag_off[i])
+        for p in range(P):
+            a1 = r1.pose_angles[P * f0 + p * R: P * f0 + (p + 1) * R]
+            a2 = r2.pose_angles[P * 2 * f0 + p * 2 * R: P * 2 * f0 + (p + 1) * 2 * R]
+            assert np.array_equal(a2[:R], a1)
+        assert np.all(r2.pose_score[i] <= r1.pose_score[i] + 1e-12)
+    assert np.all(r2.best_score <= r1.best_score + 1e-12)
+    flat = mkpocket(np.full((32, 32, 32), 0.25, np.float32), kappa=0.0)
+    r3 = oracle.dock_batch(L, flat, rot, tr, cs, S_w=3)
+    assert not r3.angles.any() and not r3.best_pose.any()
