@@ -206,18 +206,28 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.ny = d.ny;
     p.nz = d.nz;
     grid_strides(d.nx, d.ny, &p.rs, &p.ps);
-    p.top_x = (float)(d.nx - 1);
-    p.top_y = (float)(d.ny - 1);
-    p.top_z = (float)(d.nz - 1);
+    // centring shift (PocketDev): 16 on every axis for the fixed-stride layout (planes of at
+    // most 32 x 32; the dock kernel then folds -Z and 2^23 + Z into immediates), n / 2 otherwise
+    const bool fix = grid_fixed(p.rs, p.ps);
+    const int Z[3] = {fix ? 16 : d.nx / 2, fix ? 16 : d.ny / 2, fix ? 16 : d.nz / 2};
+    p.lo_x = (float)-Z[0];
+    p.lo_y = (float)-Z[1];
+    p.lo_z = (float)-Z[2];
+    p.top_x = (float)(d.nx - 1 - Z[0]);
+    p.top_y = (float)(d.ny - 1 - Z[1]);
+    p.top_z = (float)(d.nz - 1 - Z[2]);
+    p.mx = 8388608.f + (float)Z[0];
+    p.my = 8388608.f + (float)Z[1];
+    p.mz = 8388608.f + (float)Z[2];
     p.kh = (float)((double)d.out_slope * (double)d.spacing);
     p.h = d.spacing;
     p.inv_h = (float)(1.0 / (double)d.spacing);
-    p.ox = d.origin[0];
-    p.oy = d.origin[1];
-    p.oz = d.origin[2];
-    p.tx = (float)(((double)d.center[0] - d.origin[0]) / d.spacing);
-    p.ty = (float)(((double)d.center[1] - d.origin[1]) / d.spacing);
-    p.tz = (float)(((double)d.center[2] - d.origin[2]) / d.spacing);
+    p.ox = (float)((double)d.origin[0] + (double)d.spacing * Z[0]);
+    p.oy = (float)((double)d.origin[1] + (double)d.spacing * Z[1]);
+    p.oz = (float)((double)d.origin[2] + (double)d.spacing * Z[2]);
+    p.tx = (float)(((double)d.center[0] - d.origin[0]) / d.spacing - Z[0]);
+    p.ty = (float)(((double)d.center[1] - d.origin[1]) / d.spacing - Z[1]);
+    p.tz = (float)(((double)d.center[2] - d.origin[2]) / d.spacing - Z[2]);
     return p;
 }
 

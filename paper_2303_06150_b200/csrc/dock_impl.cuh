@@ -113,15 +113,21 @@ constexpr int kFixRS = 34, kFixPS = 1097;
 template <bool FIX>
 __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
     const int RS = FIX ? kFixRS : pk.rs, PS = FIX ? kFixPS : pk.ps;
-    const float cx = fminf(fmaxf(ux, 0.f), pk.top_x);
-    const float cy = fminf(fmaxf(uy, 0.f), pk.top_y);
-    const float cz = fminf(fmaxf(uz, 0.f), pk.top_z);
+    // centred coordinates (PocketDev): clamp to [-Z, n-1-Z]; floor(u_c) = bits of the
+    // round-down sum c + (2^23 + Z) minus the bits of 2^23; f = c - (floor(u_c) - Z)
+    // (FIX: Z = 16 on every axis, so -Z and 2^23 + Z are immediates)
+    const float lox = FIX ? -16.f : pk.lo_x, loy = FIX ? -16.f : pk.lo_y, loz = FIX ? -16.f : pk.lo_z;
+    const float mx = FIX ? 8388624.f : pk.mx, my = FIX ? 8388624.f : pk.my, mz = FIX ? 8388624.f : pk.mz;
+    const float cx = fminf(fmaxf(ux, lox), pk.top_x);
+    const float cy = fminf(fmaxf(uy, loy), pk.top_y);
+    const float cz = fminf(fmaxf(uz, loz), pk.top_z);
     const float2 dxy = __fadd2_rn(make_float2(ux, uy), make_float2(-cx, -cy));
     const float e = __fadd_rn(__fadd_rn(fabsf(dxy.x), fabsf(dxy.y)), fabsf(__fsub_rn(uz, cz)));
-    const float2 bxy = __fadd2_rd(make_float2(cx, cy), f2(kMagic));
-    const float bz = __fadd_rd(cz, kMagic);
-    const float2 fxy = __fadd2_rn(make_float2(cx, cy), neg2(__fadd2_rn(bxy, f2(-kMagic))));
-    const float fz = __fsub_rn(cz, __fsub_rn(bz, kMagic));
+    const float2 mxy = make_float2(mx, my);
+    const float2 bxy = __fadd2_rd(make_float2(cx, cy), mxy);
+    const float bz = __fadd_rd(cz, mz);
+    const float2 fxy = __fadd2_rn(make_float2(cx, cy), neg2(__fadd2_rn(bxy, neg2(mxy))));
+    const float fz = __fsub_rn(cz, __fsub_rn(bz, mz));
     const int idx = (__float_as_int(bxy.x) - kMagicBits) + (__float_as_int(bxy.y) - kMagicBits) * RS +
                     (__float_as_int(bz) - kMagicBits) * PS;
     const float* p = G + idx;
@@ -135,7 +141,7 @@ __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, f
     return __fmaf_rn(pk.kh, e, lerp(l.x, l.y, fz));
 }
 
-// Pose p in grid units: R' = R / h, t' = (c + tau - o) / h, u = R' x + t'.
+// Pose p in centred grid units: R' = R / h, t' = (c + tau - o) / h - Z, v = R' x + t'.
 // Stored as 12 floats: (R'00, R'10), (R'01, R'11), (R'02, R'12), (t'x, t'y), R'20, R'21, R'22, t'z.
 __device__ __forceinline__ void scaled_pose(const float* raw, const PocketDev& pk, float* out) {
     float r[9];

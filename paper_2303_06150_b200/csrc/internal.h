@@ -17,16 +17,21 @@ constexpr int kMaxPoses = 1024;
 constexpr int kMaxSweeps = 4;
 
 // Pocket as the dock kernel sees it: grid staged in shared memory with padded
-// row / plane strides (floats), coordinates in grid units u = (y - o)/h.
+// row / plane strides (floats).  Coordinates are kept in CENTRED grid units
+// v = (y - o)/h - Z with the integer shift Z = floor(n/2) per axis: |v| <= n/2 halves the
+// fp32 rounding of every placement / rotation step against u = v + Z in [0, n-1], and the
+// shift costs nothing -- it is folded into the clamp bounds and the floor constant 2^23 + Z.
 struct PocketDev {
     const float* grid;     // global copy [nz][ny][nx]
     int nx, ny, nz;
     int rs, ps;            // shared-memory row stride and plane stride (floats)
-    float top_x, top_y, top_z;    // n - 1
+    float lo_x, lo_y, lo_z;       // -Z          (u = 0)
+    float top_x, top_y, top_z;    // n - 1 - Z   (u = n - 1)
+    float mx, my, mz;             // 2^23 + Z    (exact)
     float kh;              // kappa * h  (penalty per grid unit of excess)
     float h;
-    float ox, oy, oz;      // origin
-    float tx, ty, tz;      // (center - origin) / h
+    float ox, oy, oz;      // origin of the centred frame: o + h Z (Angstrom)
+    float tx, ty, tz;      // (center - origin) / h - Z
     float inv_h;
 };
 
