@@ -91,9 +91,9 @@ def test_c2_sample_parity_and_bucketing_invariance(c2):
     c, lib, pk = c2
     e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
     rng = np.random.default_rng(2)
-    idx = rng.choice(lib.n, 120, replace=False)
+    idx = rng.choice(lib.n, 1000, replace=False)
     rep, r = check(e, lib, idx, pk, rot, tr, cs)
-    assert rep.independent_equal == rep.independent_checked > 30
+    assert rep.independent_equal == rep.independent_checked > 300
     # Q22: bit-identical whatever the launch structure (one launch per bucket, bucket multiple, streams)
     for kw in (dict(launch_per_bucket=True, bucket_multiple=1), dict(bucket_multiple=3, n_streams=1)):
         e2, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, **kw)
