@@ -84,7 +84,7 @@ class PipelinedDocker:
         return dev, ev, host
 
     def run(self, atom_off, xyz, frag_off, frags, k: int = 1000, chunks: int = 0, max_atoms: int = 256,
-            group=None):
+            group=None, first: int = 32, growth: int = 4):
         """Returns (best_score [P][n], best_pose [P][n], topk [(index, score)] per pocket) on the host.
 
         xyz / frags should be pinned host tensors (torch ``pin_memory``) for overlapped copies.
@@ -96,7 +96,7 @@ class PipelinedDocker:
         e = self.engine
         n = int(atom_off.shape[0]) - 1
         npk = len(self.pocket_ids)
-        bounds = chunk_bounds(n, chunks)
+        bounds = chunk_bounds(n, chunks, first, growth)
         chunks = len(bounds) - 1
         # pinned host outputs: the per-chunk result reads are plain DMA, not staged copies
         best = torch.full((npk, n), float("nan"), dtype=torch.float32).pin_memory().numpy()
