@@ -50,7 +50,10 @@ cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, int K, cudaFuncA
 
 cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem, int* blocks_per_sm) {
     DockFn f = pick(AC, NW, PPW, fix, K);
-    if (!f) return cudaErrorInvalidValue;
+    if (!f) {   // no instantiation for this (class, warps, poses per warp, K): the policy skips it
+        *blocks_per_sm = 0;
+        return cudaSuccess;
+    }
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {

@@ -168,9 +168,11 @@ __device__ __forceinline__ RotT load_pose(const float* T) {
 
 // Stage the pocket grid into shared memory with padded strides; the padding (and
 // the zero plane/row above the grid) is zero-filled first.  Ends with a barrier.
-__device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk) {
+// zero_floats: how much to zero first (the grid region, plus -- for the dock kernel -- the
+// pose buffers behind it, see dock_grid_floats).
+__device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk, size_t zero_floats) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int n4 = (int)(align16(((size_t)(pk.nz + 1) * pk.ps + pk.rs + 2) * 4) / 16);
+    const int n4 = (int)(align16(zero_floats * 4) / 16);
     for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     for (int row = w; row < pk.ny * pk.nz; row += nw) {
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         ring.end_seq = 0x7fffffff;
         ring.claim[0] = atomicAdd(a.counter, 1);
     }
-    stage_grid(sG, pk);
+    stage_grid(sG, pk, (L.buf - L.grid) / 4 + (size_t)NW * PPW * pose_stride_of(AC, NW, PPW));   // grid + pose buffers
     __syncthreads();
     if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
@@ -633,7 +635,7 @@ __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, 
                                                             int64_t n, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* sG = reinterpret_cast<float*>(smem);
-    stage_grid(sG, pk);
+    stage_grid(sG, pk, (size_t)(pk.nz + 1) * pk.ps + pk.rs + 2);
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
@@ -649,7 +651,9 @@ template <int AC, bool FIX>
 DockFn pick_ac(int NW, int PPW, int K) {
     if (PPW == 4 && K == 8 && FIX)   // production path: compile-time K = 8
         return NW == 16 ? dock_kernel<AC, 16, 4, FIX, 8>
+               : NW == 13 ? dock_kernel<AC, 13, 4, FIX, 8>
                : NW == 12 ? dock_kernel<AC, 12, 4, FIX, 8>
+               : NW == 10 ? dock_kernel<AC, 10, 4, FIX, 8>
                           : (NW == 8 ? dock_kernel<AC, 8, 4, FIX, 8> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX, 8> : nullptr));
     if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, FIX, 0> : (NW == 16 ? dock_kernel<AC, 16, 1, FIX, 0> : nullptr);
     if (PPW == 2)

@@ -73,12 +73,20 @@ struct DockLayout {
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 // Angle choices kept per pose: S_w * RC bytes (RC = the launch's fragment cap), 4-aligned.
 __host__ __device__ inline int dock_ang_stride(int S_w, int RC) { return ((S_w * (RC > 0 ? RC : 1)) + 3) & ~3; }
+// Grid region of the dock kernel (floats).  Corner reads at i0 + 1 = n carry weight 0 but
+// must read FINITE values.  Fixed-stride grids (rs, ps) = (34, 1097): the region is the nz
+// planes only and those reads land in the pose buffers placed right behind it (zeroed at
+// kernel start, only ever holding coordinates; <= ny rs + nx + 2 = 1122 floats, less than
+// any pose-buffer area).  Other strides keep a zero plane + row.
+__host__ __device__ inline size_t dock_grid_floats(int nz, int rs, int ps) {
+    return (rs == 34 && ps == 1097) ? (size_t)nz * ps : (size_t)(nz + 1) * ps + rs + 2;
+}
 __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int rs, int ps, int P, int K,
                                                   int S_w, int LC, int RC) {
     DockLayout L;
     size_t o = 0;
-    // grid planes + one zero plane and row above: corner reads at i0 + 1 = n (weight 0) stay in bounds
-    L.grid = o;  o += align16(((size_t)(nz + 1) * ps + rs + 2) * 4);
+    L.grid = o;  o += align16(dock_grid_floats(nz, rs, ps) * 4);
+    L.buf = o;   o += (size_t)NW * PPW * pose_stride_of(AC, NW, PPW) * 4;   // (x,y)|z per pose
     L.pose = o;   // pose table: read per warp item from global (L1-resident), no shared copy
     L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
     size_t q = 0;
@@ -88,7 +96,6 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int n
     L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC));
     L.slot_b = q;
     L.slots = o; o += kDockSlots * q;
-    L.buf = o;   o += (size_t)NW * PPW * pose_stride_of(AC, NW, PPW) * 4;   // (x,y)|z per pose
     L.total = o;
     return L;
 }
