@@ -1081,6 +1081,13 @@ vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* 
     // test hook: temporary device buffers (not on the product path)
     const PocketHost& ph = c->pockets[pocket_id];
     float *dg = nullptr, *dx = nullptr, *dout = nullptr;
+    struct Free {   // released on every return path
+        float** p[3];
+        ~Free() {
+            for (float** q : p)
+                if (*q) cudaFree(*q);
+        }
+    } guard{{&dg, &dx, &dout}};
     const size_t gb = ph.grid.size() * 4;
     CK(cudaMalloc(&dg, gb));
     CK(cudaMalloc(&dx, (size_t)n * 12));
@@ -1092,9 +1099,6 @@ vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* 
     CK(launch_score_points(pk, dx, n, dout, smem, c->main));
     CK(cudaMemcpyAsync(g_out, dout, (size_t)n * 4, cudaMemcpyDeviceToHost, c->main));
     CK(cudaStreamSynchronize(c->main));
-    cudaFree(dg);
-    cudaFree(dx);
-    cudaFree(dout);
     return VS_OK;
 }
 
