@@ -155,6 +155,13 @@ vs_status vs_get_pose_debug(vs_ctx* ctx, int32_t slot, float* pose_score, uint8_
  * entries (fewer than k ligands) are UINT64_MAX.  *n_valid = min(k, owned).
  * ord maps fp32 to unsigned order (sign-flip), -0 is canonicalised to +0. */
 vs_status vs_local_topk(vs_ctx* ctx, int32_t slot, int32_t k, uint64_t* keys_dev, int32_t* n_valid);
+/* a10 for streamed libraries: the keys (ord(score) << 32 | (ligand index + index_offset))
+ * of every ligand this rank docked for pocket slot s, in slot order (unsorted), written
+ * asynchronously on the context's stream into keys_dev (DEVICE, capacity >= the owned
+ * ligand count, returned in *n_keys).  A caller docking a library in chunks collects each
+ * chunk's keys (index_offset = the chunk's first ligand) and ranks them all at once with
+ * vs_merge_topk.  Errors: VS_E_ARG (index_offset + n >= 2^32), VS_E_STATE. */
+vs_status vs_keys(vs_ctx* ctx, int32_t slot, uint32_t index_offset, uint64_t* keys_dev, int64_t* n_keys);
 /* a11: merge n_keys gathered keys (DEVICE, e.g. after an NCCL all_gather of W
  * local top-k lists) into the global top-k: ligand index and score (HOST). */
 vs_status vs_merge_topk(vs_ctx* ctx, const uint64_t* keys_dev, int64_t n_keys, int32_t k, int64_t* index_out,

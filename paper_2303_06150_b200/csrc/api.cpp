@@ -1006,6 +1006,21 @@ vs_status vs_local_topk(vs_ctx* c, int32_t slot, int32_t k, uint64_t* keys_dev, 
     return VS_OK;
 }
 
+vs_status vs_keys(vs_ctx* c, int32_t slot, uint32_t index_offset, uint64_t* keys_dev, int64_t* n_keys) {
+    if (!c || !n_keys) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (c->total_slots > 0 && !keys_dev) return VS_E_ARG;
+    if ((uint64_t)index_offset + (uint64_t)c->n > 0xffffffffull) return fail(c, VS_E_ARG, "index_offset + n exceeds 2^32");
+    if (c->total_slots > 0) {
+        CK(launch_make_keys(c->d_meta, c->total_slots, c->d_score[slot], (unsigned long long*)keys_dev, c->main,
+                            index_offset));
+        ++c->stats.kernel_launches;
+    }
+    *n_keys = c->total_slots;
+    return VS_OK;
+}
+
 vs_status vs_merge_topk(vs_ctx* c, const uint64_t* keys_dev, int64_t n_keys, int32_t k, int64_t* index_out,
                         float* score_out, int32_t* n_out) {
     if (!c || (!keys_dev && n_keys > 0)) return VS_E_ARG;

@@ -139,7 +139,7 @@ cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n
                                 cudaStream_t st);
 // top-k
 cudaError_t launch_make_keys(const int4* meta, int n_slots, const float* best_score, unsigned long long* keys,
-                             cudaStream_t st);
+                             cudaStream_t st, uint32_t index_offset = 0);
 // Select the k smallest of keys[n] (unique), write them sorted to out[k] (UINT64_MAX padded).
 // scratch: >= (n + 2048) u64 + 4 KB.  Returns the number of kernels launched in *launches.
 cudaError_t topk_select_sort(const unsigned long long* keys, int64_t n, int k, unsigned long long* out,

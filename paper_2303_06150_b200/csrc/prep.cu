@@ -311,14 +311,14 @@ __global__ void fill_results_kernel(float* best_score, int* best_pose, int64_t n
 // a10 keys: ord(score) << 32 | ligand index; ord is the order-preserving map of
 // fp32 onto uint32 (sign-magnitude flip); -0 is canonicalised to +0.
 __global__ void make_keys_kernel(const int4* __restrict__ meta, int n_slots, const float* __restrict__ best_score,
-                                 unsigned long long* __restrict__ keys) {
+                                 unsigned long long* __restrict__ keys, uint32_t index_offset) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n_slots) return;
     const int li = meta[s].x;
     const float v = __fadd_rn(best_score[li], 0.0f);
     const uint32_t bits = __float_as_uint(v);
     const uint32_t ord = (bits & 0x80000000u) ? ~bits : (bits | 0x80000000u);
-    keys[s] = ((unsigned long long)ord << 32) | (uint32_t)li;
+    keys[s] = ((unsigned long long)ord << 32) | ((uint32_t)li + index_offset);
 }
 
 }  // namespace
@@ -383,9 +383,9 @@ cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, ui
 }
 
 cudaError_t launch_make_keys(const int4* meta, int n_slots, const float* best_score, unsigned long long* keys,
-                             cudaStream_t st) {
+                             cudaStream_t st, uint32_t index_offset) {
     if (n_slots <= 0) return cudaSuccess;
-    make_keys_kernel<<<(n_slots + 255) / 256, 256, 0, st>>>(meta, n_slots, best_score, keys);
+    make_keys_kernel<<<(n_slots + 255) / 256, 256, 0, st>>>(meta, n_slots, best_score, keys, index_offset);
     return cudaGetLastError();
 }
 

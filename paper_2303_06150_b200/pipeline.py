@@ -12,8 +12,9 @@ Compute phases are deliberately serialised: the persistent dock kernel holds eve
 could not start before the dock drains anyway -- and its local top-k would queue behind
 the other context's dock.  What overlaps is the only thing that can: PCIe copies against
 SM work.  Each chunk is a full hot-path submit (validate, bucket, pack, dock, local top-k);
-the per-pocket ranking is merged over chunks on the device (vs_merge_topk) and across
-ranks with one all-gather of k keys per pocket (``parallel.gather_keys``).
+every chunk's ranking keys are collected on the device (vs_keys) and ranked once at the end
+(vs_merge_topk), then across ranks with one all-gather of k keys per pocket
+(``parallel.gather_keys``).
 """
 from __future__ import annotations
 
@@ -101,7 +102,10 @@ class PipelinedDocker:
         # pinned host outputs: the per-chunk result reads are plain DMA, not staged copies
         best = torch.full((npk, n), float("nan"), dtype=torch.float32).pin_memory().numpy()
         pose = torch.full((npk, n), -1, dtype=torch.int32).pin_memory().numpy()
-        keys = [[] for _ in range(npk)]
+        # every chunk's keys land in one device array per pocket (index + chunk offset); the
+        # ranking is one selection at the end (no per-chunk top-k round trip)
+        all_keys = [torch.empty(max(1, n), dtype=torch.int64, device=self.dev) for _ in range(npk)]
+        nkeys = [0] * npk
         arrays = (atom_off, xyz, frag_off, frags)
         self.trace = []
         inflight = {}
@@ -125,17 +129,13 @@ class PipelinedDocker:
                 e.wait()
                 for s in range(npk):
                     e.results_into(s, best[s, lo:hi], pose[s, lo:hi])
-                    t, nv = e.local_topk(s, k)
-                    kk = t[:nv].cpu().numpy().view(np.uint64)
-                    keys[s].append(kk + np.uint64(lo))       # ligand index lives in the low word
+                    nkeys[s] += e.keys_into(s, all_keys[s][nkeys[s]:], lo)
             st = e.stats()
             self.trace.append((c, t0, t1, time.perf_counter(), st["prep_ms"], st["dock_ms"]))
             del dev                 # buffer free once the chunk's work completed (wait above)
         tops = []
         for s in range(npk):
-            allk = np.concatenate(keys[s]) if keys[s] else np.zeros(0, np.uint64)
-            dk = torch.from_numpy(allk.view(np.int64).copy()).to(self.dev)
-            idx, sc = e.merge_topk(dk, k)
+            idx, sc = e.merge_topk(all_keys[s][:nkeys[s]], k)
             mine = torch.full((k,), -1, dtype=torch.int64)   # UINT64_MAX pads, as local_topk
             mine[: len(idx)] = parallel.encode_keys(sc, idx)
             g = parallel.gather_keys(mine.to(self.dev), group)

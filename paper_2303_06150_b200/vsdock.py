@@ -24,7 +24,7 @@ _NAMES = {0: "VS_OK", -1: "VS_E_ARG", -2: "VS_E_PARSE", -3: "VS_E_OVERFLOW_ATOMS
 
 SYMBOLS = ["vs_create", "vs_destroy", "vs_last_error", "vs_workspace_size", "vs_set_workspace", "vs_load_pocket",
            "vs_set_pose_table", "vs_set_angle_table", "vs_submit", "vs_wait", "vs_get_results", "vs_get_coords",
-           "vs_get_pose_debug", "vs_local_topk", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
+           "vs_get_pose_debug", "vs_local_topk", "vs_keys", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
            "vs_score_points", "vs_get_stats", "vs_plan_boundaries", "vs_plan_lpt"]
 
 
@@ -101,6 +101,7 @@ def load_library():
         "vs_get_coords": [P, I32, P, I32],
         "vs_get_pose_debug": [P, I32, P, P],
         "vs_local_topk": [P, I32, I32, P, ctypes.POINTER(I32)],
+        "vs_keys": [P, I32, ctypes.c_uint32, P, ctypes.POINTER(I64)],
         "vs_merge_topk": [P, P, I64, I32, P, P, ctypes.POINTER(I32)],
         "vs_get_manifest": [P, I32, P, ctypes.POINTER(I32), P],
         "vs_query_classes": [P, I32, P, ctypes.POINTER(I32)],
@@ -295,6 +296,13 @@ class Engine:
         nv = ctypes.c_int32()
         self._check(self.lib.vs_local_topk(self.h, slot, k, _ptr(t), ctypes.byref(nv)))
         return t, nv.value
+
+    def keys_into(self, slot, out, index_offset=0):
+        """Write this rank's (score, ligand index + index_offset) keys for ``slot`` into the
+        DEVICE int64 tensor ``out`` (asynchronous); returns how many were written."""
+        nk = ctypes.c_int64()
+        self._check(self.lib.vs_keys(self.h, slot, int(index_offset), _ptr(out), ctypes.byref(nk)))
+        return nk.value
 
     def merge_topk(self, keys_dev, k):
         idx = np.empty(k, np.int64)

@@ -381,6 +381,23 @@ def test_c5_full_size_campaign_sampled_parity_and_topk():
         assert np.array_equal(ts, r.best_score[ti])
 
 
+def test_keys_with_offset_rank_like_local_topk(c2):
+    """vs_keys: every owned ligand's key with a ligand-index offset; ranking them with
+    vs_merge_topk equals the local top-k shifted by the offset (streamed-library path)."""
+    import torch
+    c, lib, pk = c2
+    sub = lib.subset(np.arange(3000))
+    e, *_ = run(sub, [pk], P=c["P"], K=c["K"], debug=False)
+    r = e.results(0)
+    out = torch.empty(sub.n, dtype=torch.int64, device="cuda")
+    n = e.keys_into(0, out, 123456)
+    assert n == sub.n
+    idx, sc = e.merge_topk(out[:n], 500)
+    want = oracle.topk(r.best_score, 500)
+    assert list(idx - 123456) == list(want)
+    assert np.array_equal(sc, r.best_score[want])
+
+
 def test_pipelined_docker_matches_single_submit(c2):
     """Double-buffered chunks give the single-submit results and ranking."""
     import torch
