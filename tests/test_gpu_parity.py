@@ -282,6 +282,26 @@ def test_non_cubic_grid_runtime_strides():
     check(e2, lib, range(lib.n), pk, rot, tr, cs)
 
 
+def test_small_grid_atoms_outside_the_box():
+    """A 14^3 grid at 1 A around ligands of 40-90 atoms: many atoms sit on or beyond the
+    faces (clamped, penalised), so the weight-0 top-edge corner reads that land past the last
+    plane (into the zeroed pose buffers on the fixed-stride layout) are exercised; full parity
+    against the oracle, every pose replayed."""
+    base = vsgen.pocket(106, n=14, spacing=1.0)
+    lib = vsgen.ligands(24, 17, (40, 90), (2, 10))
+    e, rot, tr, cs = run(lib, [base], P=8, K=8)
+    check(e, lib, range(lib.n), base, rot, tr, cs)
+    # score hook on points all around and outside the box, including exact top-face points
+    e2 = engine()
+    pid = e2.load_pocket(base)
+    rng = np.random.default_rng(6)
+    pts = rng.uniform(-6, 20, size=(20000, 3)).astype(np.float32)
+    pts[:2000, rng.integers(0, 3, 2000)] = 13.0          # exactly on the top faces
+    g = e2.score_points(pid, pts)
+    ref = oracle.grid_score(base, pts.astype(np.float64))
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < 2e-6
+
+
 def test_empty_batch():
     e = engine()
     setup(e, [vsgen.pocket(101)], 8, 8)
