@@ -50,7 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return SO
     os.makedirs(OBJ, exist_ok=True)
     us = units()
-    with ThreadPoolExecutor(max_workers=max(1, min(len(us), os.cpu_count() or 4))) as ex:
+    # at most 8 concurrent nvcc processes (each dock class unit needs ~1-2 GB of host memory)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(us), os.cpu_count() or 4, 8))) as ex:
         results = list(ex.map(_compile, us))
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
