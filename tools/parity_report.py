@@ -4,6 +4,7 @@ oracle (oracle/parity.py) on every BASELINE config, far beyond the pytest sample
   C1: all 16 ligands, every pose replayed         C2: all 10,000 ligands, every pose replayed
   C3: all 8,192 ligands (best pose + independent) C4: every 100th of 1M (10,000 ligands)
   C5: every 500th of 1M for each of the 4 pockets
+  (DENSE=1: C3 every pose replayed, C4 every 10th ligand, C5 every 100th per pocket)
 
 Writes gpurun_out/parity_report.json (one summary per config)."""
 import json
@@ -58,12 +59,14 @@ def run(name, every, debug):
 
 
 if __name__ == "__main__":
+    # DENSE=1: C3 with every pose replayed, C4 every 10th ligand, C5 every 100th per pocket
+    dense = os.environ.get("DENSE") == "1"
     rows = []
     rows += run("C1", 1, True)
     rows += run("C2", 1, True)
-    rows += run("C3", 1, False)
-    rows += run("C4", 100, False)
-    rows += run("C5", 500, False)
+    rows += run("C3", 1, dense)
+    rows += run("C4", 10 if dense else 100, False)
+    rows += run("C5", 100 if dense else 500, False)
     os.makedirs("gpurun_out", exist_ok=True)
     json.dump({"band": BAND, "tol_score": TOL_S, "tol_xyz": TOL_X, "rows": rows},
               open("gpurun_out/parity_report.json", "w"), indent=1)
