@@ -5,6 +5,7 @@
                 structures (fused per class, and one launch per bucket as the paper).
   sweep  N      Fig. 2: three ligands (17/53/99 atoms) replicated N times,
                 one launch per bucket, bucket size k/3 * l for k = 1..12 plus "All".
+  tail   N      tail effect: 6 x 23 over 1 x 1 for libraries of 3k .. N ligands.
 Timing: CUDA events of the library (dock phase) and wall time of the whole submit (step);
 device-resident library; median of 3 after 1 warm-up.  Not bench values.
 """
@@ -103,7 +104,36 @@ def sweep(n):
     out.close()
 
 
+def tail(n_max):
+    """Tail-effect study: bucketed (6 x 23) over unsorted (1 x 1) as
+    the library grows, for both launch structures."""
+    pk = [vsgen.pocket(101)]
+    out = open("gpurun_out/tail_effect.csv", "w", newline="")
+    w = csv.writer(out)
+    w.writerow(["ligands", "mode", "buckets_6x23", "step_ms_1x1", "step_ms_6x23", "ligands_per_s_6x23", "speedup"])
+    full = vsgen.ligands(n_max, 4)
+    for n in (3000, 10000, 30000, 100000, 300000, 1000000):
+        if n > n_max:
+            break
+        lib = full.subset(np.arange(n)) if n < n_max else full
+        d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+        for mode in ("fused", "per_bucket"):
+            res = {}
+            for na, nr in ((1, 1), (6, 23)):
+                e = Engine(atom_clusters=na, rot_clusters=nr, launch_per_bucket=(mode == "per_bucket"),
+                           bucket_multiple=1 if mode == "per_bucket" else 16, n_streams=4)
+                ids = setup(e, pk)
+                step, dock, s = timed(e, d, ids)
+                res[(na, nr)] = (step, s["n_buckets"])
+                e.close()
+            s11, s623 = res[(1, 1)][0], res[(6, 23)][0]
+            w.writerow([n, mode, res[(6, 23)][1], f"{s11:.3f}", f"{s623:.3f}", f"{n / (s623 / 1e3):.1f}", f"{s11 / s623:.4f}"])
+            out.flush()
+            print(n, mode, f"{s11:.2f} ms vs {s623:.2f} ms", f"{s11 / s623:.3f}x", flush=True)
+    out.close()
+
+
 if __name__ == "__main__":
     os.makedirs("gpurun_out", exist_ok=True)
     what, n = sys.argv[1], int(sys.argv[2])
-    {"heatmap": heatmap, "sweep": sweep}[what](n)
+    {"heatmap": heatmap, "sweep": sweep, "tail": tail}[what](n)
