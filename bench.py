@@ -375,7 +375,7 @@ def main():
                          "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (guide unit counts, max clock)"},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
             "cpu_baseline": cpu, "unsorted": unsorted,
-            "classes": [{k: cl[k] for k in ("kernel_atoms", "regs_per_thread", "dyn_smem", "blocks_per_sm",
+            "classes": [{k: cl[k] for k in ("kernel_atoms", "warps_per_cta", "regs_per_thread", "dyn_smem", "blocks_per_sm",
                                             "ligands_per_cta", "l", "capacity")} for cl in classes],
         }
         print(json.dumps(line))
