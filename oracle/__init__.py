@@ -51,15 +51,16 @@ def _load():
         build()
         lib = ctypes.CDLL(_SO)
         p, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
-        lib.oracle_dock_batch.argtypes = [i64, p, p, p, p, p, p, p, i32, p, p, i32, p, i32, p, p, p, p, p, p, p, p, i32]
+        lib.oracle_dock_batch.argtypes = [i64, p, p, p, p, p, p, p, p, p, i32, p, p, i32, p, i32, p, p, p, p, p, p, p, p,
+                                          i32]
         lib.oracle_dock_batch.restype = i32
-        lib.oracle_replay_pose.argtypes = [p, p, p, i32, p, i32, p, p, p, i32, p, i32, p, p, p]
+        lib.oracle_replay_pose.argtypes = [p, p, p, i32, p, i32, p, p, p, p, p, i32, p, i32, p, p, p]
         lib.oracle_replay_pose.restype = f64
         lib.oracle_grid_score_points.argtypes = [p, p, p, i64, p, p]
         lib.oracle_grid_score_points.restype = i32
         lib.oracle_place.argtypes = [p, p, i32, p, p, p, p]
         lib.oracle_place.restype = i32
-        lib.oracle_rotate.argtypes = [i32, p, p, f64, f64]
+        lib.oracle_rotate.argtypes = [i32, p, i32, i32, p, i32, f64, f64]
         lib.oracle_rotate.restype = i32
         _lib = lib
     return _lib
@@ -101,7 +102,10 @@ def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_de
     P, K = int(rot.shape[0]), int(cs.shape[0])
     dims, prm, G = _pocket_args(pocket)
     ao, fo = _c(lib.atom_off, np.int64), _c(lib.frag_off, np.int64)
-    xyz, fr = _c(lib.xyz, np.float32), _c(lib.frags, np.int32)
+    xyz = _c(lib.xyz, np.float32)
+    fax, mo, ma = _c(lib.frag_axis, np.int32), _c(lib.move_off, np.int64), _c(lib.move_atoms, np.int32)
+    if ma.size == 0:
+        ma = np.zeros(1, np.int32)
     rot, trans, cs = _c(rot, np.float32), _c(trans, np.float32), _c(cs, np.float32)
     nA, nR = int(ao[-1]), int(fo[-1])
     bs = np.zeros(n, np.float64); bp = np.zeros(n, np.int32)
@@ -112,7 +116,7 @@ def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_de
     sm = np.zeros((n, P), np.float64) if want_debug else None
     pm = np.zeros(n, np.float64) if want_debug else None
     nthreads = nthreads or (os.cpu_count() or 1)
-    rc = L.oracle_dock_batch(n, _p(ao), _p(xyz), _p(fo), _p(fr), _p(dims), _p(prm), _p(G), P, _p(rot), _p(trans),
+    rc = L.oracle_dock_batch(n, _p(ao), _p(xyz), _p(fo), _p(fax), _p(mo), _p(ma), _p(dims), _p(prm), _p(G), P, _p(rot), _p(trans),
                              K, _p(cs), S_w, _p(bs), _p(bp), _p(ang), _p(xo), _p(ps), _p(pa), _p(sm), _p(pm), nthreads)
     if rc != 0:
         raise ValueError("oracle_dock_batch: invalid arguments")
@@ -120,19 +124,36 @@ def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_de
                       None if pa is None else pa[:P * S_w * nR], sm, pm)
 
 
+def _frags_csr(frags):
+    """(frag_axis [R,2] int32, move_off [R+1] int64, move_atoms int32) of a ligand's fragments, given in
+    the general form (vsgen.Frags, or a list of (a, b, moving atoms)) or the range form [R,4]."""
+    if isinstance(frags, np.ndarray) and frags.ndim == 2 and frags.shape[1] == 4:
+        items = [(int(a), int(b), np.arange(lo, hi)) for a, b, lo, hi in frags]
+    else:
+        items = [(int(a), int(b), np.asarray(m)) for a, b, m in frags]
+    ax = np.array([[a, b] for a, b, _ in items], np.int32).reshape(-1, 2)
+    mo = np.zeros(len(items) + 1, np.int64)
+    mo[1:] = np.cumsum([len(m) for _, _, m in items])
+    ma = np.concatenate([np.asarray(m, np.int32) for _, _, m in items]) if items else np.zeros(0, np.int32)
+    return ax, mo, (ma if ma.size else np.zeros(1, np.int32)).astype(np.int32)
+
+
 def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1):
-    """Replay a given angle sequence from pose (rot9, tr3).
+    """Replay a given angle sequence from pose (rot9, tr3).  ``frags``: general form (vsgen.Frags)
+    or range form [R,4].
 
     Returns (final_score, final_xyz [A,3] fp64, step_scores [S_w*R, K] fp64)."""
     L = _load()
     dims, prm, G = _pocket_args(pocket)
-    xyz = _c(xyz, np.float32); frags = _c(frags, np.int32).reshape(-1, 4)
-    A, R, K = int(xyz.shape[0]), int(frags.shape[0]), int(cs.shape[0])
+    xyz = _c(xyz, np.float32)
+    ax, mo, ma = _frags_csr(frags)
+    A, R, K = int(xyz.shape[0]), int(ax.shape[0]), int(cs.shape[0])
     kseq = _c(kseq, np.uint8)
     steps = np.zeros((max(1, S_w * R), K), np.float64)
     y = np.zeros((max(1, A), 3), np.float64)
-    s = L.oracle_replay_pose(_p(dims), _p(prm), _p(G), A, _p(xyz), R, _p(frags), _p(_c(rot9, np.float32)),
-                             _p(_c(tr3, np.float32)), K, _p(_c(cs, np.float32)), S_w, _p(kseq), _p(steps), _p(y))
+    s = L.oracle_replay_pose(_p(dims), _p(prm), _p(G), A, _p(xyz), R, _p(ax), _p(mo), _p(ma),
+                             _p(_c(rot9, np.float32)), _p(_c(tr3, np.float32)), K, _p(_c(cs, np.float32)), S_w,
+                             _p(kseq), _p(steps), _p(y))
     return float(s), y[:A], steps[:S_w * R]
 
 
@@ -157,10 +178,18 @@ def place(pocket, xyz, rot9, tr3) -> np.ndarray:
 
 
 def rotate(y, frag, ck, sk) -> np.ndarray:
-    """Rotate fragment frag=(a,b,lo,hi) of coordinates y by (cos, sin) (a7), fp64; returns a copy."""
+    """Rotate one fragment of coordinates y by (cos, sin) (a7), fp64; returns a copy.  ``frag`` is
+    (a, b, moving atoms) (general form) or (a, b, lo, hi) (range form, M = [lo, hi))."""
     L = _load()
     y = np.array(y, dtype=np.float64, order="C").reshape(-1, 3)
-    L.oracle_rotate(y.shape[0], _p(y), _p(_c(frag, np.int32)), float(ck), float(sk))
+    if len(frag) == 4 and np.isscalar(frag[2]):
+        a, b, lo, hi = (int(v) for v in frag)
+        mv = np.arange(lo, hi, dtype=np.int32)
+    else:
+        a, b, mv = int(frag[0]), int(frag[1]), np.asarray(frag[2], np.int32)
+    mv = np.ascontiguousarray(mv, np.int32)
+    L.oracle_rotate(y.shape[0], _p(y), a, b, _p(mv if mv.size else np.zeros(1, np.int32)), int(mv.size), float(ck),
+                    float(sk))
     return y
 
 

@@ -22,8 +22,14 @@
  * no delta trick, no caching), no blocking, no SIMD.  Threads only split the
  * ligand list.
  *
+ * Fragments come in the C-ABI's general form: axis (a, b) and the
+ * moving-atom set M_r as an index list (a rotamer is "a subset
+ * of the molecule atoms that can rotate"); the oracle rotates exactly the listed atoms
+ * and never renumbers them (the CUDA path's DFS renumbering is checked against it).
+ *
  * Pins: tests/test_oracle_pins.py (closed forms, invariants, brute force,
- * library routines scipy.ndimage.map_coordinates / scipy Rotation).
+ * library routines scipy.ndimage.map_coordinates / scipy Rotation, renumbering
+ * invariance, pose translations tau_p != 0 and a docking centre off the grid centre).
  */
 #include <math.h>
 #include <pthread.h>
@@ -105,15 +111,16 @@ void oracle_place_pose(const opocket* pk, const float* xyz, int A, const float* 
 }
 
 /*
- * a7: rotate fragment r (axis atoms a -> b, moving set [lo, hi)) by the angle
- * step with table entry (cos_k, sin_k) (P:215-216 rotamers; Q3, Q5, Q6):
+ * a7: rotate fragment r -- rotation axis a -> b, moving-atom set M_r (an arbitrary
+ * subset of the atoms, axis atoms excluded: "a subset of the
+ * molecule atoms that can rotate") -- by the angle step with table entry
+ * (cos_k, sin_k) (Q3, Q5, Q6):
  *   u = (y_b - y_a)/|y_b - y_a|,  q = y_b,
  *   M = c I + s [u]_x + (1 - c) u u^T   (Rodrigues),
- *   y_i <- q + M (y_i - q)   for i in [lo, hi).
+ *   y_i <- q + M (y_i - q)   for i in M_r  (mv[0..nm)).
  */
-void oracle_rotate_fragment(double* y, const int32_t* frag, double ck, double sk) {
+void oracle_rotate_fragment(double* y, int a, int b, const int32_t* mv, int nm, double ck, double sk) {
     if (ck == 1.0 && sk == 0.0) return;   /* theta = 0: M = I, the coordinates do not move (Q3) */
-    int a = frag[0], b = frag[1], lo = frag[2], hi = frag[3];
     double d[3], u[3], q[3];
     for (int t = 0; t < 3; ++t) d[t] = y[3 * b + t] - y[3 * a + t];
     double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
@@ -123,11 +130,20 @@ void oracle_rotate_fragment(double* y, const int32_t* frag, double ck, double sk
     for (int r = 0; r < 3; ++r)
         for (int s = 0; s < 3; ++s)
             M[r][s] = (r == s ? ck : 0.0) + sk * ux[r][s] + (1.0 - ck) * u[r] * u[s];
-    for (int i = lo; i < hi; ++i) {
+    for (int t = 0; t < nm; ++t) {
+        const int i = mv[t];
         double v[3];
-        for (int t = 0; t < 3; ++t) v[t] = y[3 * i + t] - q[t];
+        for (int c = 0; c < 3; ++c) v[c] = y[3 * i + c] - q[c];
         for (int r = 0; r < 3; ++r) y[3 * i + r] = q[r] + M[r][0] * v[0] + M[r][1] * v[1] + M[r][2] * v[2];
     }
+}
+
+/* Fragment f of a general-form CSR batch: axis (frag_axis[2f], frag_axis[2f+1]), M_f =
+ * move_atoms[move_off[f] .. move_off[f+1]). */
+static void rotate_frag_csr(double* y, const int32_t* frag_axis, const int64_t* move_off, const int32_t* move_atoms,
+                            int64_t f, double ck, double sk) {
+    oracle_rotate_fragment(y, frag_axis[2 * f], frag_axis[2 * f + 1], move_atoms + move_off[f],
+                           (int)(move_off[f + 1] - move_off[f]), ck, sk);
 }
 
 typedef struct {
@@ -136,9 +152,9 @@ typedef struct {
     int P, K, S_w;
     const float *rot, *tr, *cs;
     /* library (CSR) */
-    const int64_t *atom_off, *frag_off;
+    const int64_t *atom_off, *frag_off, *move_off;
     const float* xyz;
-    const int32_t* frags;
+    const int32_t *frag_axis, *move_atoms;
     /* outputs (any may be NULL except best_score/best_pose) */
     double* best_score;
     int32_t* best_pose;
@@ -162,7 +178,7 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
     int A = (int)(B->atom_off[li + 1] - B->atom_off[li]);
     int R = (int)(B->frag_off[li + 1] - B->frag_off[li]);
     const float* x = B->xyz + 3 * B->atom_off[li];
-    const int32_t* fr = B->frags + 4 * B->frag_off[li];
+    const int64_t f0 = B->frag_off[li];
     double best = INFINITY, second = INFINITY;
     int bestp = -1;
     for (int p = 0; p < B->P; ++p) {
@@ -174,7 +190,8 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
                 int kmin = 0;
                 for (int k = 0; k < B->K; ++k) {
                     memcpy(ytmp, y, sizeof(double) * 3 * (size_t)A);
-                    oracle_rotate_fragment(ytmp, fr + 4 * r, (double)B->cs[2 * k], (double)B->cs[2 * k + 1]);
+                    rotate_frag_csr(ytmp, B->frag_axis, B->move_off, B->move_atoms, f0 + r, (double)B->cs[2 * k],
+                                    (double)B->cs[2 * k + 1]);
                     double s = score(pk, ytmp, A);
                     if (s < smin) { s2 = smin; smin = s; kmin = k; }
                     else if (s < s2) { s2 = s; }
@@ -183,7 +200,8 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
                     double m = (s2 - smin) / fmax(1.0, fabs(smin));
                     if (m < margin) margin = m;
                 }
-                oracle_rotate_fragment(y, fr + 4 * r, (double)B->cs[2 * kmin], (double)B->cs[2 * kmin + 1]);
+                rotate_frag_csr(y, B->frag_axis, B->move_off, B->move_atoms, f0 + r, (double)B->cs[2 * kmin],
+                                (double)B->cs[2 * kmin + 1]);
                 kseq[sw * R + r] = (uint8_t)kmin;
             }
         }
@@ -239,7 +257,8 @@ static void make_pocket(opocket* pk, const int32_t* dims, const double* prm, con
  * Dock a batch.  dims = {nx, ny, nz}; prm = {ox, oy, oz, h, cx, cy, cz, kappa}.
  * Returns 0, or -1 on invalid arguments.
  */
-int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frags,
+int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, const int64_t* frag_off,
+                      const int32_t* frag_axis, const int64_t* move_off, const int32_t* move_atoms,
                       const int32_t* dims, const double* prm, const float* grid,
                       int P, const float* rot, const float* trans, int K, const float* cs, int S_w,
                       double* best_score, int32_t* best_pose, uint8_t* angles, double* xyz_out,
@@ -257,7 +276,8 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
         batch_t* B = &jobs[t];
         memset(B, 0, sizeof *B);
         B->pk = &pk; B->P = P; B->K = K; B->S_w = S_w; B->rot = rot; B->tr = trans; B->cs = cs;
-        B->atom_off = atom_off; B->frag_off = frag_off; B->xyz = xyz; B->frags = frags;
+        B->atom_off = atom_off; B->frag_off = frag_off; B->xyz = xyz;
+        B->frag_axis = frag_axis; B->move_off = move_off; B->move_atoms = move_atoms;
         B->best_score = best_score; B->best_pose = best_pose; B->angles = angles; B->xyz_out = xyz_out;
         B->pose_score = pose_score; B->pose_angles = pose_angles; B->step_margin = step_margin; B->pose_margin = pose_margin;
         B->lo = n * t / nthreads; B->hi = n * (t + 1) / nthreads;
@@ -269,14 +289,15 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
 
 /*
  * Replay checker primitive: place ligand (xyz,
- * frags) in pose p and apply the GIVEN angle sequence kseq[S_w*R] (e.g. the
+ * fragments frag_axis[2R] / move_off[R+1] / move_atoms) in pose p and apply the GIVEN angle sequence kseq[S_w*R] (e.g. the
  * one the GPU chose).  For every step it records the full-sum score of every
  * candidate k into step_scores[(sw*R + r)*K + k] before applying kseq's
  * choice, so a checker can verify each choice is within the near-tie band of
  * the fp64 minimum.  Final coordinates -> y_out[3A], final score returned.
  */
 double oracle_replay_pose(const int32_t* dims, const double* prm, const float* grid,
-                          int A, const float* xyz, int R, const int32_t* frags,
+                          int A, const float* xyz, int R, const int32_t* frag_axis, const int64_t* move_off,
+                          const int32_t* move_atoms,
                           const float* rot9, const float* tr3, int K, const float* cs, int S_w,
                           const uint8_t* kseq, double* step_scores, double* y_out) {
     opocket pk;
@@ -288,12 +309,12 @@ double oracle_replay_pose(const int32_t* dims, const double* prm, const float* g
             if (step_scores) {
                 for (int k = 0; k < K; ++k) {
                     memcpy(yt, y_out, sizeof(double) * 3 * (size_t)A);
-                    oracle_rotate_fragment(yt, frags + 4 * r, (double)cs[2 * k], (double)cs[2 * k + 1]);
+                    rotate_frag_csr(yt, frag_axis, move_off, move_atoms, r, (double)cs[2 * k], (double)cs[2 * k + 1]);
                     step_scores[(sw * R + r) * K + k] = score(&pk, yt, A);
                 }
             }
             int k = kseq[sw * R + r];
-            oracle_rotate_fragment(y_out, frags + 4 * r, (double)cs[2 * k], (double)cs[2 * k + 1]);
+            rotate_frag_csr(y_out, frag_axis, move_off, move_atoms, r, (double)cs[2 * k], (double)cs[2 * k + 1]);
         }
     }
     double s = score(&pk, y_out, A);
@@ -316,8 +337,8 @@ int oracle_place(const int32_t* dims, const double* prm, int A, const float* xyz
     return 0;
 }
 
-int oracle_rotate(int A, double* y, const int32_t* frag, double ck, double sk) {
+int oracle_rotate(int A, double* y, int a, int b, const int32_t* mv, int nm, double ck, double sk) {
     (void)A;
-    oracle_rotate_fragment(y, frag, ck, sk);
+    oracle_rotate_fragment(y, a, b, mv, nm, ck, sk);
     return 0;
 }

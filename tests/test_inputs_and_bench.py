@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_generator_ranges_determinism_and_prefix_stability():
     a = vsgen.ligands(300, 9, (20, 120), (0, 20))
     b = vsgen.ligands(300, 9, (20, 120), (0, 20))
-    for f in ("atom_off", "xyz", "frag_off", "frags"):
+    for f in ("atom_off", "xyz", "frag_off", "frags", "frag_axis", "move_off", "move_atoms"):
         assert np.array_equal(getattr(a, f), getattr(b, f))          # S:68 determinism
     assert ((a.n_atoms >= 20) & (a.n_atoms <= 120)).all()             # S:39 in range
     assert ((a.n_frags >= 0) & (a.n_frags <= 20)).all()
@@ -23,7 +23,7 @@ def test_generator_ranges_determinism_and_prefix_stability():
     for i in range(100):
         x1, f1 = a.ligand(200 + i)
         x2, f2 = tail.ligand(i)
-        assert np.array_equal(x1, x2) and np.array_equal(f1, f2)
+        assert np.array_equal(x1, x2) and f1 == f2
     assert vsgen.ligands(0, 1).n == 0
     d = vsgen.ligands(3, 5, (5, 5), (0, 0))                            # S:44 degenerate ranges
     assert list(d.n_atoms) == [5, 5, 5] and list(d.n_frags) == [0, 0, 0]
@@ -34,8 +34,9 @@ def test_generator_ranges_determinism_and_prefix_stability():
 def test_generated_fragments_are_valid_rotatable_bonds():
     lib = vsgen.ligands(200, 3, (20, 120), (0, 20))
     for i in range(lib.n):
-        x, fr = lib.ligand(i)
+        x, fr = lib.ligand_ranges(i)
         A = len(x)
+        assert lib.ligand(i)[1] == vsgen.Frags.from_ranges(fr)           # general form == range form
         for a, b, lo, hi in fr:
             assert 0 <= a < A and 0 <= b < A and a != b
             assert 0 <= lo < hi <= A and not (lo <= a < hi) and not (lo <= b < hi)
@@ -48,7 +49,7 @@ def test_replicate():
     r = vsgen.replicate(lib, 1, 4)
     assert r.n == 4 and len(set(r.ligand_id.tolist())) == 4
     for i in range(4):
-        assert np.array_equal(r.ligand(i)[0], lib.ligand(1)[0]) and np.array_equal(r.ligand(i)[1], lib.ligand(1)[1])
+        assert np.array_equal(r.ligand(i)[0], lib.ligand(1)[0]) and r.ligand(i)[1] == lib.ligand(1)[1]
     assert vsgen.replicate(lib, 0, 1).n == 1
 
 

@@ -138,13 +138,12 @@ def test_fragment_rotation_matches_scipy_rodrigues(c1):
         if len(fr) == 0:
             continue
         y = oracle.place(pk, x, rot[1], tr[1])
-        for f in fr:
-            a, b, lo, hi = (int(v) for v in f)
+        for a, b, mv in fr:
             theta = rng.uniform(-math.pi, math.pi)
-            got = oracle.rotate(y, f, math.cos(theta), math.sin(theta))
+            got = oracle.rotate(y, (a, b, mv), math.cos(theta), math.sin(theta))
             u = (y[b] - y[a]) / np.linalg.norm(y[b] - y[a])
             want = y.copy()
-            want[lo:hi] = Rotation.from_rotvec(theta * u).apply(y[lo:hi] - y[b]) + y[b]
+            want[mv] = Rotation.from_rotvec(theta * u).apply(y[mv] - y[b]) + y[b]
             assert np.max(np.abs(got - want)) < 1e-12          # sign convention: right-hand rule about a->b
 
 
@@ -153,20 +152,20 @@ def test_fragment_rotation_invariants(c1):
     for i in range(L.n):
         x, fr = L.ligand(i)
         y = oracle.place(pk, x, rot[2], tr[2])
-        for f in fr:
-            a, b, lo, hi = (int(v) for v in f)
+        for a, b, mv in fr:
+            f = (a, b, mv)
             y0 = oracle.rotate(y, f, cs[0, 0], cs[0, 1])
             assert np.array_equal(y0, y)                          # theta_0 = 0 -> identity, bitwise
             y1 = oracle.rotate(y, f, cs[1, 0], cs[1, 1])
             assert np.array_equal(y1[[a, b]], y[[a, b]])          # axis atoms fixed
-            mov = np.zeros(len(y), bool); mov[lo:hi] = True
+            mov = np.zeros(len(y), bool); mov[mv] = True
             for grp in (mov, ~mov):                               # both rigid bodies keep their shape
                 d0 = np.linalg.norm(y[grp][:, None] - y[grp][None], axis=-1)
                 d1 = np.linalg.norm(y1[grp][:, None] - y1[grp][None], axis=-1)
                 assert np.max(np.abs(d1 - d0)) < 1e-6
             # distances from the axis atoms to moving atoms are preserved (bond lengths across the axis)
             for ax in (a, b):
-                assert np.max(np.abs(np.linalg.norm(y1[lo:hi] - y1[ax], axis=1) - np.linalg.norm(y[lo:hi] - y[ax], axis=1))) < 1e-6
+                assert np.max(np.abs(np.linalg.norm(y1[mv] - y1[ax], axis=1) - np.linalg.norm(y[mv] - y[ax], axis=1))) < 1e-6
             yk = y
             for _ in range(cs.shape[0]):                          # K steps of 2 pi / K return to start
                 yk = oracle.rotate(yk, f, cs[1, 0], cs[1, 1])
@@ -217,38 +216,89 @@ def test_K1_or_R0_is_rigid_only(c1):
         assert abs(r.best_score[i] - min(s)) < 1e-9 and r.best_pose[i] == int(np.argmin(s))
 
 
-def test_linear_grid_closed_form():
-    """G = w.u + g0 with every atom inside the box: S = A*g0 + w.sum(u_i).  Every initial pose ties
-    (rigid rotation about the centroid keeps sum y), and each greedy step picks argmin_k w.M_k v_r with
-    v_r = sum_{i in M_r} (y_i - q) -- computed here with scipy's rotation."""
+@pytest.mark.parametrize("tau,offset", [(0.0, (0.0, 0.0, 0.0)), (1.5, (2.5, -3.0, 1.25))])
+def test_linear_grid_closed_form(tau, offset):
+    """G = w.u + g0 with every atom inside the box: S = A*g0 + w.sum(u_i).  Without translations every
+    initial pose ties (rigid rotation about the centroid keeps sum y), and each greedy step picks
+    argmin_k w.M_k v_r with v_r = sum_{i in M_r} (y_i - q) -- computed here with scipy's rotation.
+    The second case carries pose translations tau_p != 0 and a docking centre c off the grid centre:
+    y = R_p (x - xbar) + c + tau_p (a6)."""
     n, h = 32, 2.0
     w = np.array([0.7, -1.3, 0.4])
     Z, Y, X = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
     G = (w[0] * X + w[1] * Y + w[2] * Z + 5.0).astype(np.float64)
-    pk = mkpocket(G.astype(np.float32), h=h)
+    ctr = tuple(h * (n - 1) / 2 + o for o in offset)
+    pk = mkpocket(G.astype(np.float32), h=h, center=ctr)
     Gf = pk.grid.astype(np.float64)
     assert np.max(np.abs(Gf - G)) < 1e-5
     L = vsgen.ligands(12, 11, (20, 60), (2, 6))
-    rot, tr = vsgen.pose_table(6)
+    rot, tr = vsgen.pose_table(6, tau=tau)
+    assert (np.abs(tr[1:]).max() > 0.1) == (tau > 0)
     K = 8
     cs = vsgen.angle_table(K)
     r = oracle.dock_batch(L, pk, rot, tr, cs)
     for i in range(L.n):
         x, fr = L.ligand(i)
         p = int(r.best_pose[i])
-        y = (x.astype(np.float64) - x.astype(np.float64).mean(0)) @ rot[p].astype(np.float64).T + np.array(pk.center)
+        y = ((x.astype(np.float64) - x.astype(np.float64).mean(0)) @ rot[p].astype(np.float64).T + np.array(ctr)
+             + tr[p].astype(np.float64))
         init = [oracle.grid_score(pk, oracle.place(pk, x, rot[q], tr[q])).sum() for q in range(6)]
-        assert np.ptp(init) < 1e-6 * max(1.0, abs(init[0]))
+        if tau == 0:
+            assert np.ptp(init) < 1e-6 * max(1.0, abs(init[0]))
+        else:   # S_p^0 = A g0 + w.(A (c + tau_p - o) / h): the translation enters linearly
+            want0 = [x.shape[0] * (5.0 + w @ ((np.array(ctr) + tr[q] - np.array(pk.origin)) / h)) for q in range(6)]
+            assert np.max(np.abs(np.array(init) - want0)) < 1e-6 * max(1.0, abs(want0[0]))
         kseq = r.angles[r_off(L, i): r_off(L, i) + len(fr)]
-        for f, kg in zip(fr, kseq):
-            a, b, lo, hi = (int(v) for v in f)
+        for (a, b, mv), kg in zip(fr, kseq):
             u = (y[b] - y[a]) / np.linalg.norm(y[b] - y[a])
-            v = (y[lo:hi] - y[b]).sum(axis=0)
+            v = (y[mv] - y[b]).sum(axis=0)
             vals = [w @ Rotation.from_rotvec(math.atan2(cs[k, 1], cs[k, 0]) * u).apply(v) / h for k in range(K)]
             assert vals[kg] <= min(vals) + 1e-6 * max(1.0, abs(min(vals)))
-            y[lo:hi] = Rotation.from_rotvec(math.atan2(cs[kg, 1], cs[kg, 0]) * u).apply(y[lo:hi] - y[b]) + y[b]
+            y[mv] = Rotation.from_rotvec(math.atan2(cs[kg, 1], cs[kg, 0]) * u).apply(y[mv] - y[b]) + y[b]
         want = x.shape[0] * 5.0 + (w @ ((y - np.array(pk.origin)) / h).sum(axis=0))
         assert abs(r.best_score[i] - want) < 1e-4 * max(1.0, abs(want))
+
+
+def test_placement_with_translation_and_offcentre_pocket_closed_form():
+    """a6 with tau_p != 0 and c != grid centre: numpy R (x - xbar) + c + tau against oracle.place, and
+    a replay of the all-zero angle sequence (identity steps) ends at the same coordinates with the
+    scipy-trilinear score of them (independent of the oracle's loops)."""
+    pk = vsgen.pocket(101, center_offset=(1.75, -2.5, 3.0))
+    assert np.max(np.abs(np.array(pk.center) - 15.5 - np.array([1.75, -2.5, 3.0]))) < 1e-12
+    rot, tr = vsgen.pose_table(8, tau=2.0)
+    assert np.all(np.linalg.norm(tr[1:], axis=1) > 0) and np.all(np.linalg.norm(tr, axis=1) <= 2.0 + 1e-6)
+    cs = vsgen.angle_table(8)
+    L = vsgen.ligands(6, 1, (20, 40), (1, 4))
+    for i in range(L.n):
+        x, fr = L.ligand(i)
+        xc = x.astype(np.float64) - x.astype(np.float64).mean(0)
+        for p in range(rot.shape[0]):
+            want = xc @ rot[p].astype(np.float64).T + np.array(pk.center) + tr[p].astype(np.float64)
+            y = oracle.place(pk, x, rot[p], tr[p])
+            assert np.max(np.abs(y - want)) < 1e-9
+            assert np.max(np.abs(y.mean(0) - (np.array(pk.center) + tr[p]))) < 1e-9   # centroid = c + tau_p
+            s, yr, _ = oracle.replay_pose(pk, x, fr, rot[p], tr[p], cs, np.zeros(len(fr), np.uint8))
+            assert np.array_equal(yr, y)
+            assert abs(s - lib_ref_score(pk, want).sum()) < 1e-9 * max(1.0, abs(s))
+
+
+def test_oracle_invariant_under_atom_renumbering():
+    """The moving sets are atom SUBSETS: renumbering the atoms of every ligand (and
+    remapping axes and sets) must not change what is docked -- same best pose and angle sequence,
+    same score up to fp64 summation order, same coordinates (mapped back)."""
+    c = vsgen.CONFIGS["C1"]
+    L = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    Lp, perm = L.permuted(5)
+    assert any(not np.array_equal(m, np.arange(m.min(), m.max() + 1)) for _, _, m in Lp.ligand(0)[1]) or \
+        any(len(Lp.ligand(i)[1]) for i in range(L.n))
+    pk = vsgen.pocket(101, center_offset=(0.5, 1.0, -0.75))
+    rot, tr = vsgen.pose_table(c["P"], tau=1.0)
+    cs = vsgen.angle_table(c["K"])
+    a = oracle.dock_batch(L, pk, rot, tr, cs)
+    b = oracle.dock_batch(Lp, pk, rot, tr, cs)
+    assert np.array_equal(a.best_pose, b.best_pose) and np.array_equal(a.angles, b.angles)
+    assert np.max(np.abs(a.best_score - b.best_score) / np.maximum(1, np.abs(a.best_score))) < 1e-12
+    assert np.max(np.abs(a.xyz - b.xyz[perm])) < 1e-9      # new[perm[j]] = old[j]
 
 
 def _brute_force(pk, x, fr, rot, cs):
@@ -261,10 +311,9 @@ def _brute_force(pk, x, fr, rot, cs):
         y0 = xc @ rot[p].astype(np.float64).T + np.array(pk.center)
         for combo in itertools.product(range(K), repeat=len(fr)):
             y = y0.copy()
-            for f, k in zip(fr, combo):
-                a, b, lo, hi = (int(v) for v in f)
+            for (a, b, mv), k in zip(fr, combo):
                 u = (y[b] - y[a]) / np.linalg.norm(y[b] - y[a])
-                y[lo:hi] = Rotation.from_rotvec(thetas[k] * u).apply(y[lo:hi] - y[b]) + y[b]
+                y[mv] = Rotation.from_rotvec(thetas[k] * u).apply(y[mv] - y[b]) + y[b]
             best = min(best, float(lib_ref_score(pk, y).sum()))
     return best
 
@@ -284,7 +333,7 @@ def _star_ligand(rng, arms):
         pts.append(pts[-1] + 1.5 * d + rng.normal(scale=0.05, size=3))
         frags.append([0, b, b + 1, b + 3])
     x = (np.array(pts) + np.array([15.5, 15.5, 15.5])).astype(np.float32)
-    return x, np.array(frags, np.int32)
+    return x, vsgen.Frags.from_ranges(np.array(frags, np.int32))
 
 
 def test_brute_force_star_ligands_greedy_is_exact():
@@ -294,11 +343,17 @@ def test_brute_force_star_ligands_greedy_is_exact():
     cs = vsgen.angle_table(8)
     for arms in (1, 2, 3):
         x, fr = _star_ligand(rng, arms)
-        lib = vsgen.Library(np.arange(1, dtype=np.uint64), np.array([0, len(x)], np.int64), x,
-                            np.array([0, len(fr)], np.int64), fr)
+        lib = vsgen.Library.from_ligands([(x, fr)])
         r = oracle.dock_batch(lib, pk, rot, tr, cs)
         bf = _brute_force(pk, x, fr, rot, cs)
         assert abs(r.best_score[0] - bf) < 1e-9 * max(1.0, abs(bf))
+        # the same molecule with shuffled atom numbers: moving sets are arbitrary subsets now
+        lp, _ = lib.permuted(arms)
+        xp, frp = lp.ligand(0)
+        rp = oracle.dock_batch(lp, pk, rot, tr, cs)
+        bfp = _brute_force(pk, xp, frp, rot, cs)
+        assert abs(bfp - bf) < 1e-9 * max(1.0, abs(bf))
+        assert abs(rp.best_score[0] - bfp) < 1e-9 * max(1.0, abs(bfp))
 
 
 def test_brute_force_general_ligands_greedy_upper_bounds(c1):

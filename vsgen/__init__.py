@@ -62,15 +62,88 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
+class Frags:
+    """Fragments of ONE ligand in the C-ABI's general form (include/vsdock.h):
+    axis[r] = (a, b) (rotation axis a -> b, b on the moving side) and moves[r] = the
+    moving-atom set M_r (ligand-local indices, axis atoms excluded; "a
+    subset of the molecule atoms that can rotate")."""
+
+    def __init__(self, axis, moves):
+        self.axis = np.asarray(axis, np.int32).reshape(-1, 2)
+        self.moves = [np.asarray(m, np.int32).reshape(-1) for m in moves]
+
+    def __len__(self):
+        return int(self.axis.shape[0])
+
+    def __iter__(self):
+        for r in range(len(self)):
+            yield int(self.axis[r, 0]), int(self.axis[r, 1]), self.moves[r]
+
+    def __eq__(self, o):
+        return (isinstance(o, Frags) and np.array_equal(self.axis, o.axis) and len(self.moves) == len(o.moves)
+                and all(np.array_equal(a, b) for a, b in zip(self.moves, o.moves)))
+
+    @staticmethod
+    def from_ranges(fr):
+        fr = np.asarray(fr, np.int32).reshape(-1, 4)
+        return Frags(fr[:, :2], [np.arange(lo, hi, dtype=np.int32) for _, _, lo, hi in fr])
+
+
+def _csr_from_ranges(frags):
+    """General-form CSR (frag_axis, move_off, move_atoms) of range-form fragments {a, b, lo, hi}."""
+    frags = np.asarray(frags, np.int32).reshape(-1, 4)
+    cnt = (frags[:, 3] - frags[:, 2]).astype(np.int64)
+    move_off = np.zeros(len(frags) + 1, np.int64)
+    move_off[1:] = np.cumsum(cnt)
+    # concatenated aranges lo..hi-1 of every fragment
+    starts = np.repeat(frags[:, 2].astype(np.int64) - move_off[:-1], cnt)
+    move_atoms = (np.arange(int(move_off[-1]), dtype=np.int64) + starts).astype(np.int32)
+    return np.ascontiguousarray(frags[:, :2]), move_off, move_atoms
+
+
 @dataclass
 class Library:
-    """A ligand batch in the C-ABI's CSR layout (include/vsdock.h vs_ligand_batch)."""
+    """A ligand batch in the C-ABI's CSR layout (include/vsdock.h vs_ligand_batch).
+
+    Ligand i: atoms atom_off[i]..atom_off[i+1] (xyz, Angstrom), fragments
+    f = frag_off[i]..frag_off[i+1] with axis frag_axis[f] = (a, b) and moving set
+    move_atoms[move_off[f]..move_off[f+1]] (ligand-local indices).  ``frags`` keeps the
+    generator's range form {a, b, lo, hi} when every M_r is a contiguous range (the
+    generator numbers atoms in DFS preorder); it is None for a renumbered library."""
     ligand_id: np.ndarray   # uint64 [n]
     atom_off: np.ndarray    # int64 [n+1]
     xyz: np.ndarray         # float32 [sum A, 3], Angstrom, AoS
     frag_off: np.ndarray    # int64 [n+1]
-    frags: np.ndarray       # int32 [sum R, 4]: a, b, lo, hi (M_r = [lo, hi))
+    frag_axis: np.ndarray   # int32 [sum R, 2]
+    move_off: np.ndarray    # int64 [sum R + 1]
+    move_atoms: np.ndarray  # int32 [sum |M_r|]
     n_moving: np.ndarray = field(default=None)  # int32 [n]: sum_r |M_r| (generator metadata)
+    frags: np.ndarray = field(default=None)     # int32 [sum R, 4] range form, or None
+
+    @staticmethod
+    def from_ranges(ligand_id, atom_off, xyz, frag_off, frags, n_moving=None) -> "Library":
+        ax, mo, ma = _csr_from_ranges(frags)
+        return Library(np.asarray(ligand_id, np.uint64), np.asarray(atom_off, np.int64),
+                       np.ascontiguousarray(xyz, np.float32), np.asarray(frag_off, np.int64), ax, mo, ma,
+                       n_moving, np.ascontiguousarray(frags, np.int32).reshape(-1, 4))
+
+    @staticmethod
+    def from_ligands(ligs, ligand_id=None) -> "Library":
+        """Build from a list of (xyz [A,3], Frags) in the general form."""
+        n = len(ligs)
+        A = [len(x) for x, _ in ligs]
+        R = [len(f) for _, f in ligs]
+        ao = np.zeros(n + 1, np.int64); ao[1:] = np.cumsum(A)
+        fo = np.zeros(n + 1, np.int64); fo[1:] = np.cumsum(R)
+        xyz = np.concatenate([np.asarray(x, np.float32).reshape(-1, 3) for x, _ in ligs]) if n else np.zeros((0, 3), np.float32)
+        ax = np.concatenate([f.axis for _, f in ligs]) if n else np.zeros((0, 2), np.int32)
+        mv = [m for _, f in ligs for m in f.moves]
+        mo = np.zeros(len(mv) + 1, np.int64); mo[1:] = np.cumsum([len(m) for m in mv])
+        ma = np.concatenate(mv).astype(np.int32) if mv else np.zeros(0, np.int32)
+        nm = np.array([sum(len(m) for m in f.moves) for _, f in ligs], np.int32)
+        ids = np.arange(n, dtype=np.uint64) if ligand_id is None else np.asarray(ligand_id, np.uint64)
+        return Library(ids, ao, np.ascontiguousarray(xyz), fo, np.ascontiguousarray(ax, np.int32).reshape(-1, 2),
+                       mo, np.ascontiguousarray(ma), nm, None)
 
     @property
     def n(self) -> int:
@@ -84,26 +157,59 @@ class Library:
     def n_frags(self) -> np.ndarray:
         return np.diff(self.frag_off).astype(np.int32)
 
+    @property
+    def moving_per_ligand(self) -> np.ndarray:
+        """sum_r |M_r| per ligand (from the CSR itself)."""
+        per_frag = np.diff(self.move_off)
+        out = np.zeros(self.n, np.int64)
+        if per_frag.size:
+            np.add.at(out, np.repeat(np.arange(self.n), self.n_frags), per_frag)
+        return out
+
+    def arrays(self):
+        """The C-ABI batch arrays, in vs_ligand_batch order."""
+        return (self.ligand_id, self.atom_off, self.xyz, self.frag_off, self.frag_axis, self.move_off,
+                self.move_atoms)
+
     def ligand(self, i: int):
-        """(xyz [A,3] float32, frags [R,4] int32) of ligand i."""
+        """(xyz [A,3] float32, Frags) of ligand i (general form)."""
+        a0, a1 = int(self.atom_off[i]), int(self.atom_off[i + 1])
+        f0, f1 = int(self.frag_off[i]), int(self.frag_off[i + 1])
+        moves = [self.move_atoms[int(self.move_off[f]):int(self.move_off[f + 1])] for f in range(f0, f1)]
+        return self.xyz[a0:a1], Frags(self.frag_axis[f0:f1], moves)
+
+    def ligand_ranges(self, i: int):
+        """(xyz, range-form frags [R,4]) of a preordered (generator-numbered) library."""
+        assert self.frags is not None, "range form only exists for the generator's DFS-preordered libraries"
         a0, a1 = int(self.atom_off[i]), int(self.atom_off[i + 1])
         f0, f1 = int(self.frag_off[i]), int(self.frag_off[i + 1])
         return self.xyz[a0:a1], self.frags[f0:f1]
 
     def subset(self, idx) -> "Library":
         idx = np.asarray(idx, dtype=np.int64)
-        A = self.n_atoms[idx].astype(np.int64)
-        R = self.n_frags[idx].astype(np.int64)
-        ao = np.zeros(len(idx) + 1, np.int64); ao[1:] = np.cumsum(A)
-        fo = np.zeros(len(idx) + 1, np.int64); fo[1:] = np.cumsum(R)
-        xyz = np.empty((int(ao[-1]), 3), np.float32)
-        fr = np.empty((int(fo[-1]), 4), np.int32)
-        for j, i in enumerate(idx):
-            x, f = self.ligand(int(i))
-            xyz[ao[j]:ao[j + 1]] = x
-            fr[fo[j]:fo[j + 1]] = f
-        nm = None if self.n_moving is None else self.n_moving[idx]
-        return Library(self.ligand_id[idx].copy(), ao, xyz, fo, fr, nm)
+        ligs = [self.ligand(int(i)) for i in idx]
+        out = Library.from_ligands(ligs, self.ligand_id[idx].copy())
+        if self.frags is not None:
+            out.frags = (np.concatenate([self.ligand_ranges(int(i))[1] for i in idx]) if len(idx)
+                         else np.zeros((0, 4), np.int32)).astype(np.int32).reshape(-1, 4)
+        return out
+
+    def permuted(self, seed: int) -> "Library":
+        """The same molecules with the atoms of every ligand renumbered by a seeded random
+        permutation (coordinates, axes and moving sets remapped): the moving sets are then
+        arbitrary atom subsets, not ranges.  Returns (library, perm): perm[g] = the global index
+        in the new library of old global atom g (new.xyz[perm] == old.xyz)."""
+        rng = np.random.Generator(np.random.PCG64(seed))
+        ligs, perms = [], []
+        for i in range(self.n):
+            x, f = self.ligand(i)
+            p = rng.permutation(len(x)).astype(np.int32)        # old index j -> new index p[j]
+            nx = np.empty_like(x)
+            nx[p] = x
+            ligs.append((nx, Frags(p[f.axis] if len(f) else f.axis, [p[m] for m in f.moves])))
+            perms.append(p.astype(np.int64) + int(self.atom_off[i]))
+        out = Library.from_ligands(ligs, self.ligand_id.copy())
+        return out, (np.concatenate(perms) if perms else np.zeros(0, np.int64))
 
 
 def ligands(n: int, seed: int, atoms=(20, 120), rot=(0, 20), first: int = 0, nthreads: int | None = None) -> Library:
@@ -126,21 +232,21 @@ def ligands(n: int, seed: int, atoms=(20, 120), rot=(0, 20), first: int = 0, nth
     if rc != 0:
         raise RuntimeError("vsgen_ligand_fill failed")
     ids = np.arange(first, first + n, dtype=np.uint64)
-    return Library(ids, ao, xyz, fo, frags, M)
+    return Library.from_ranges(ids, ao, xyz, fo, frags, M)
 
 
 def replicate(lib: Library, i: int, n: int) -> Library:
     """n copies of ligand i of `lib`, differing only in id."""
     if n < 0:
         raise ValueError("n must be >= 0")
-    x, f = lib.ligand(i)
+    x, f = lib.ligand_ranges(i)
     A, R = len(x), len(f)
     ao = np.arange(n + 1, dtype=np.int64) * A
     fo = np.arange(n + 1, dtype=np.int64) * R
     xyz = np.tile(x, (n, 1)).astype(np.float32)
     fr = np.tile(f, (n, 1)).astype(np.int32).reshape(-1, 4)
     nm = None if lib.n_moving is None else np.full(n, lib.n_moving[i], np.int32)
-    return Library(np.arange(n, dtype=np.uint64), ao, xyz, fo, fr, nm)
+    return Library.from_ranges(np.arange(n, dtype=np.uint64), ao, xyz, fo, fr, nm)
 
 
 # ----------------------------------------------------------------------------- pocket
@@ -160,11 +266,15 @@ class Pocket:
         return nx, ny, nz
 
 
-def pocket(seed: int, n: int = 32, spacing: float = 1.0, n_receptor: int = 96,
-           shell=(9.0, 13.0), mouth_deg: float = 50.0, out_slope: float = 1.0) -> Pocket:
+def pocket(seed: int, n=32, spacing: float = 1.0, n_receptor: int = 96,
+           shell=(9.0, 13.0), mouth_deg: float = 50.0, out_slope: float = 1.0, center_offset=(0.0, 0.0, 0.0),
+           origin=(0.0, 0.0, 0.0)) -> Pocket:
+    """A synthetic pocket.  ``n`` = nx = ny = nz, or (nx, ny, nz).  The docking centre c is the
+    grid centre moved by ``center_offset`` (Angstrom); the receptor shell surrounds c."""
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else tuple(int(v) for v in n)
     rng = np.random.Generator(np.random.PCG64(seed))
-    origin = np.zeros(3)
-    c = origin + spacing * (n - 1) / 2.0
+    origin = np.asarray(origin, np.float64)
+    c = origin + spacing * (np.array([nx, ny, nz], np.float64) - 1) / 2.0 + np.asarray(center_offset, np.float64)
     pts = []
     cos_half = math.cos(math.radians(mouth_deg / 2.0))
     while len(pts) < n_receptor:
@@ -175,8 +285,8 @@ def pocket(seed: int, n: int = 32, spacing: float = 1.0, n_receptor: int = 96,
         r = rng.uniform(shell[0], shell[1])
         pts.append(c + r * v)
     P = np.array(pts)
-    ax = origin[0] + spacing * np.arange(n)
-    Z, Y, X = np.meshgrid(ax, ax, ax, indexing="ij")
+    Z, Y, X = np.meshgrid(origin[2] + spacing * np.arange(nz), origin[1] + spacing * np.arange(ny),
+                          origin[0] + spacing * np.arange(nx), indexing="ij")
     node = np.stack([X, Y, Z], axis=-1)                  # [nz, ny, nx, 3]
     G = 0.01 * np.sum((node - c) ** 2, axis=-1)
     for p in P:
@@ -199,8 +309,11 @@ def _splitmix64(state: int):
     return state, z ^ (z >> 31)
 
 
-def pose_table(P: int, seed: int = 7):
-    """(rot [P,3,3] float32 row-major, trans [P,3] float32).  p = 0 is the identity."""
+def pose_table(P: int, seed: int = 7, tau: float = 0.0):
+    """(rot [P,3,3] float32 row-major, trans [P,3] float32).  p = 0 is the identity.
+
+    tau > 0: every pose p >= 1 also carries a translation tau_p drawn uniformly in the ball of
+    radius tau (Angstrom) from the same splitmix64 stream (reading Q7 sets tau = 0 by default)."""
     rot = np.zeros((P, 3, 3), np.float64)
     for p in range(P):
         if p == 0:
@@ -218,7 +331,19 @@ def pose_table(P: int, seed: int = 7):
         rot[p] = [[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
                   [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
                   [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]]
-    return rot.astype(np.float32), np.zeros((P, 3), np.float32)
+    trans = np.zeros((P, 3), np.float64)
+    if tau > 0:
+        for p in range(1, P):
+            s = (seed * 0x9E3779B97F4A7C15 ^ (p * 0xD1B54A32D192ED03) ^ 0x5851F42D4C957F2D) & _M64
+            while True:
+                v = []
+                for _ in range(3):
+                    s, a = _splitmix64(s)
+                    v.append(2.0 * ((a >> 11) / 9007199254740992.0) - 1.0)
+                if v[0] * v[0] + v[1] * v[1] + v[2] * v[2] <= 1.0:
+                    break
+            trans[p] = tau * np.array(v)
+    return rot.astype(np.float32), trans.astype(np.float32)
 
 
 def angle_table(K: int) -> np.ndarray:
