@@ -209,8 +209,8 @@ def main():
     n = lib.n
 
     # library HBM-resident for `value`; pinned host copies for `e2e`
-    d_lib = [torch.from_numpy(a).to(dev) for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
-    h_lib = [torch.from_numpy(a).pin_memory() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    d_lib = [torch.from_numpy(a).to(dev) for a in lib.arrays()]
+    h_lib = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
     h2d_bytes = sum(t.numel() * t.element_size() for t in h_lib)
     max_atoms = int(lib.n_atoms.max())
 
@@ -270,10 +270,7 @@ def main():
     # executed evaluations: the kernel also scores the identity angle (k = 0) of every moving
     # atom; algorithmic: E_alg = P (A + (K - 1) sum|M_r|)
     a_i = np.diff(lib.atom_off).astype(np.float64)
-    m_i = np.zeros(n)
-    if lib.frags.shape[0]:
-        owner = np.repeat(np.arange(n), np.diff(lib.frag_off))
-        np.add.at(m_i, owner, (lib.frags[:, 3] - lib.frags[:, 2]).astype(np.float64))
+    m_i = lib.moving_per_ligand.astype(np.float64)
     K_ = c["K"]
     exec_ratio = float((a_i + K_ * m_i).sum() / max(1.0, (a_i + (K_ - 1) * m_i).sum())) if K_ > 1 else 1.0
     exec_rate = evals_step * exec_ratio / (dock_avg / 1e3)
@@ -289,7 +286,7 @@ def main():
         # per pocket out on the host; chunk H2D copies overlap the previous chunk's docking
         from paper_2303_06150_b200.pipeline import PipelinedDocker
         eng.close()
-        pdk = PipelinedDocker(device=local, n_buffers=2, atom_clusters=6, rot_clusters=23,
+        pdk = PipelinedDocker(device=local, n_engines=2, atom_clusters=6, rot_clusters=23,
                               bucket_multiple=args.bucket_multiple, n_streams=args.streams, rank=rank,
                               world_size=world)
         pdk.setup(rot, tr, cs, pockets)
@@ -315,12 +312,14 @@ def main():
         if world > 1:
             t_e = reduce_scalar(t_e, dist.ReduceOp.MAX)
         pdk.close()
-        d2h = len(pockets) * (n * 8 + K_TOP * 12)
+        nA_, nR_ = int(lib.atom_off[-1]), int(lib.frag_off[-1])
+        d2h = len(pockets) * (n * 8 + nR_ + nA_ * 12 + K_TOP * 12)
         e2e = {"value": n * len(pockets) / (t_e / args.steps / 1e3), "unit": "ligands/s",
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
-               "api": f"PipelinedDocker.run: pinned host CSR -> host scores/poses + top-{K_TOP}; "
-                      f"{n_chunks} chunk(s) {chunk_bounds(n, chunks)[1:]}, H2D of chunk i+1 on a copy stream under "
-                      f"the docking of chunk i"}
+               "api": f"PipelinedDocker.run: pinned host CSR (general form: axes + moving-atom lists) -> host "
+                      f"best scores, poses, angle indices, best-pose coordinates (input atom order) + top-{K_TOP} "
+                      f"per pocket; {n_chunks} chunk(s) {chunk_bounds(n, chunks)[1:]} over 2 engines: H2D of chunk "
+                      f"i+1 and the D2H of chunk i-1's outputs under the docking of chunk i"}
     unsorted = None
     if not args.no_unsorted:
         if args.no_e2e:

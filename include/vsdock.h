@@ -38,7 +38,7 @@ typedef int32_t vs_status;
 enum {
     VS_OK = 0,
     VS_E_ARG = -1,              /* invalid argument / configuration */
-    VS_E_PARSE = -2,            /* invalid ligand record (a1): message names ligand index and field */
+    VS_E_PARSE = -2,            /* invalid ligand record (a1): message names ligand index and check */
     VS_E_OVERFLOW_ATOMS = -3,   /* atoms above the last atom boundary (axis "atoms") */
     VS_E_OVERFLOW_ROTAMERS = -4,/* rotamers above the last rotamer boundary (axis "rotamers") */
     VS_E_NOFIT = -5,            /* occupancy query returned b = 0: kernel does not fit */
@@ -75,11 +75,12 @@ void vs_destroy(vs_ctx* ctx);
 const char* vs_last_error(const vs_ctx* ctx);
 
 /* Upper bound of the device workspace for a batch of n_lig ligands with
- * n_atoms atoms, n_frags fragments in total and at most max_atoms atoms per
- * ligand, docked into n_pockets pockets with the current pose table.
- * Requires the pose table.  Errors: VS_E_ARG, VS_E_STATE. */
-vs_status vs_workspace_size(vs_ctx* ctx, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int32_t max_atoms,
-                            int32_t n_pockets, size_t* bytes);
+ * n_atoms atoms, n_frags fragments and n_moving moving-atom entries in total
+ * (the lengths of xyz / 3, frag_axis / 2 and move_atoms of vs_ligand_batch) and at
+ * most max_atoms atoms per ligand, docked into n_pockets pockets with the current
+ * pose table.  Requires the pose table.  Errors: VS_E_ARG, VS_E_STATE. */
+vs_status vs_workspace_size(vs_ctx* ctx, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int64_t n_moving,
+                            int32_t max_atoms, int32_t n_pockets, size_t* bytes);
 /* Hand the library a device buffer (e.g. a torch uint8 tensor) of >= bytes; 256-B aligned. */
 vs_status vs_set_workspace(vs_ctx* ctx, void* dev_ptr, size_t bytes);
 
@@ -106,21 +107,34 @@ vs_status vs_load_pocket(vs_ctx* ctx, const vs_pocket_desc* desc, const float* g
 vs_status vs_set_pose_table(vs_ctx* ctx, int32_t P, const float* rot, const float* trans);
 
 /* a7 angle steps (Q3): cos_sin[K*2], host, fp32; entry 0 must be exactly (1, 0);
- * K must be a power of two, 1 <= K <= 32 (warp lane map). */
+ * 1 <= K <= 32 (theta_k = 2 pi k / K for any K; a K that is not a power of two runs on
+ * the lane map of the next power of two, the extra lanes idle -- DESIGN.md 6). */
 vs_status vs_set_angle_table(vs_ctx* ctx, int32_t K, const float* cos_sin);
 
-/* D1: a ligand batch in CSR form.  Ligand i has atoms atom_off[i]..atom_off[i+1]
- * (1 <= A <= 256) with coordinates xyz[3*atom] in Angstrom, and fragments
- * frag_off[i]..frag_off[i+1] (0 <= R <= 32).  Fragment r is frags[4*f] =
- * {a, b, lo, hi} in ligand-local atom indices: rotation axis a -> b, moving set
- * M_r = [lo, hi) with a, b outside it (Q5, Q6).  on_device = 1: all
- * pointers are device pointers (borrowed until vs_wait). */
+/* D1: a ligand batch in CSR form.  Ligand i has atoms atom_off[i] ..
+ * atom_off[i+1] (1 <= A <= 256) with coordinates xyz[3*atom] in Angstrom (finite,
+ * |x| <= 1e6), and fragments f = frag_off[i] .. frag_off[i+1] (0 <= R <= 32).
+ * Fragment f is a rotatable bond: axis frag_axis[2f] = a -> frag_axis[2f+1] = b
+ * (ligand-local atom indices, b on the moving side) and the moving-atom set
+ * M_f = move_atoms[move_off[f] .. move_off[f+1]) -- ANY subset of the ligand's atoms
+ * ("a subset of the molecule atoms that can rotate"), axis atoms
+ * excluded, 1 <= |M_f| <= A - 2, no repeats.  The moving sets of one ligand must form a
+ * laminar family (any two nested or disjoint: what the bonds of a tree give) -- a1
+ * checks it and renumbers the atoms on the device so that every set is one contiguous
+ * range ("a1 ingest"); results come back in the caller's atom order.
+ * Fragments are swept in input order (Q4).  ligand_id[n] (may be NULL: ids = batch
+ * indices) is passed through to vs_get_results and vs_merge_topk.  atom_off[0],
+ * frag_off[0] and move_off[0] must be 0.  on_device = 1: every pointer is a device
+ * pointer (borrowed until vs_wait); 0: host memory, copied during vs_submit. */
 typedef struct {
     int64_t n;
-    const int64_t* atom_off;
-    const float* xyz;
-    const int64_t* frag_off;
-    const int32_t* frags;
+    const uint64_t* ligand_id;   /* [n] or NULL */
+    const int64_t* atom_off;     /* [n + 1] */
+    const float* xyz;            /* [3 * atom_off[n]] */
+    const int64_t* frag_off;     /* [n + 1] */
+    const int32_t* frag_axis;    /* [2 * frag_off[n]] (a, b) */
+    const int64_t* move_off;     /* [frag_off[n] + 1] */
+    const int32_t* move_atoms;   /* [move_off[frag_off[n]]] */
     int32_t on_device;
 } vs_ligand_batch;
 
@@ -137,14 +151,19 @@ vs_status vs_submit(vs_ctx* ctx, const vs_ligand_batch* batch, const int32_t* po
 vs_status vs_wait(vs_ctx* ctx);
 
 /* a9 per-ligand results for pocket slot s (index into the submit's pocket_ids),
- * input order, length n: best score S_{p*}, best pose p*, and the angle index
- * sequence of p*, CSR by n_sweeps*frag_off (angle_idx[S_w*frag_off[i] + sw*R_i + r]).
+ * input order, length n: ligand id (the batch's, or the batch index when it gave
+ * none), best score S_{p*}, best pose p*, and the angle index sequence of p*, CSR by
+ * n_sweeps*frag_off (angle_idx[S_w*frag_off[i] + sw*R_i + r]).
  * Ligands docked by another rank: score NaN, pose -1, angles 0xFF.
- * Any output pointer may be NULL.  on_device: outputs are device pointers. */
-vs_status vs_get_results(vs_ctx* ctx, int32_t slot, float* best_score, int32_t* best_pose, uint8_t* angle_idx,
-                         int32_t on_device);
-/* a9 best-pose coordinates (Angstrom, input atom order, [3*n_atoms]); replays p*
- * on the GPU bit-identically to the dock kernel. */
+ * Any output pointer may be NULL.  on_device: 1 = outputs are device pointers (copied,
+ * synchronous); 0 = host memory (synchronous); 2 = host memory, copied ASYNCHRONOUSLY on
+ * the context's stream (pinned memory for overlap; complete after the next vs_wait) --
+ * the double-buffered result read-back of P:200-203. */
+vs_status vs_get_results(vs_ctx* ctx, int32_t slot, uint64_t* ligand_id, float* best_score, int32_t* best_pose,
+                         uint8_t* angle_idx, int32_t on_device);
+/* a9 best-pose coordinates (Angstrom, the caller's input atom order, [3*n_atoms]);
+ * replays p* on the GPU bit-identically to the dock kernel.  on_device as for
+ * vs_get_results (2: asynchronous into pinned host memory). */
 vs_status vs_get_coords(vs_ctx* ctx, int32_t slot, float* xyz_out, int32_t on_device);
 /* Parity hook (requires debug_poses): every pose's final score [n*P] and angle
  * sequence [P*S_w*frag_off ...] (pose p of ligand i at P*S_w*frag_off[i] + p*S_w*R_i). */
@@ -162,10 +181,18 @@ vs_status vs_local_topk(vs_ctx* ctx, int32_t slot, int32_t k, uint64_t* keys_dev
  * chunk's keys (index_offset = the chunk's first ligand) and ranks them all at once with
  * vs_merge_topk.  Errors: VS_E_ARG (index_offset + n >= 2^32), VS_E_STATE. */
 vs_status vs_keys(vs_ctx* ctx, int32_t slot, uint32_t index_offset, uint64_t* keys_dev, int64_t* n_keys);
+/* a10 for streamed libraries: the k smallest of n_keys keys (DEVICE, e.g. every chunk's
+ * vs_keys output), ascending and UINT64_MAX padded, into out_dev[k] (DEVICE), asynchronously
+ * on the context's stream -- the rank's local top-k before the all-gather.  Errors:
+ * VS_E_ARG, VS_E_STATE (no workspace yet). */
+vs_status vs_select_keys(vs_ctx* ctx, const uint64_t* keys_dev, int64_t n_keys, int32_t k, uint64_t* out_dev);
 /* a11: merge n_keys gathered keys (DEVICE, e.g. after an NCCL all_gather of W
- * local top-k lists) into the global top-k: ligand index and score (HOST). */
+ * local top-k lists; UINT64_MAX pads allowed, any number) into the global top-k:
+ * ligand index, score and -- id_out non-NULL -- the ligand id from the last
+ * submitted batch (UINT64_MAX for an index outside it) (HOST outputs, any may be NULL).
+ * *n_out = number of real (non-pad) entries, <= k. */
 vs_status vs_merge_topk(vs_ctx* ctx, const uint64_t* keys_dev, int64_t n_keys, int32_t k, int64_t* index_out,
-                        float* score_out, int32_t* n_out);
+                        float* score_out, uint64_t* id_out, int32_t* n_out);
 
 /* a3/a4 bucket manifest of the last submit (all buckets of all ranks). */
 typedef struct {

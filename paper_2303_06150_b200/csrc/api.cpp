@@ -130,11 +130,14 @@ struct vs_ctx {
 
     // last job
     bool submitted = false;
-    int64_t n = 0, nA = 0, nR = 0;
+    int64_t n = 0, nA = 0, nR = 0, nM = 0;
     std::vector<int> job_pockets;
-    int64_t *d_atom_off = nullptr, *d_frag_off = nullptr;
+    int64_t *d_atom_off = nullptr, *d_frag_off = nullptr, *d_move_off = nullptr;
     float* d_xyz = nullptr;
-    int32_t* d_frags = nullptr;
+    int32_t *d_frag_axis = nullptr, *d_move_atoms = nullptr;
+    const uint64_t* d_lid = nullptr;   // ligand ids of the batch (null: ids = indices)
+    uint8_t* d_order = nullptr;        // a1: internal atom -> input atom, CSR by atom_off
+    int4* d_frint = nullptr;           // a1: fragments in internal numbering {a, b, lo, hi}
     int *d_featA = nullptr, *d_featR = nullptr, *d_featM = nullptr, *d_cell = nullptr, *d_hist = nullptr,
         *d_cell_count = nullptr, *d_maxAR = nullptr;
     unsigned long long* d_status = nullptr;  // [0] validation, [1] overflow
@@ -161,7 +164,9 @@ struct vs_ctx {
     void* d_sel = nullptr;
 
     std::vector<int> atom_b, rot_b;
-    std::vector<ClassInfo> classes;
+    std::vector<ClassInfo> classes;                    // class table that sizes the buckets (Eq. 1)
+    std::vector<std::vector<ClassInfo>> layout_classes;  // per distinct grid layout of the submit
+    std::vector<int> pk_layout;                        // pocket slot -> index into layout_classes
     std::vector<vs_bucket> buckets;
     std::vector<int> owned;             // bucket ids, launch order
     std::vector<int> owned_prefix;      // slots
@@ -233,13 +238,13 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
 
 // Stage-1 workspace (known from the batch sizes alone).
 struct Stage1 {
-    size_t atom_off, frag_off, xyz, frags, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
+    size_t atom_off, frag_off, xyz, lid, frag_axis, move_off, move_atoms, order, frint, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
         bsize, weights, own_start, own_prefix, own_ac, own_rec_off, pose, cs, grids, end;
     int n_blocks;
     int64_t max_buckets;
 };
 
-Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int P, int K, size_t grid_bytes, int n_pockets) {
+Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t grid_bytes, int n_pockets) {
     Stage1 s;
     Region r;
     s.n_blocks = (int)((n + kPrepTile - 1) / kPrepTile);
@@ -253,7 +258,12 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int P, int K, size_t grid_bytes,
     s.atom_off = r.add((n + 1) * 8);
     s.frag_off = r.add((n + 1) * 8);
     s.xyz = r.add(nA * 12);
-    s.frags = r.add(nR * 16);
+    s.lid = r.add(n * 8);
+    s.frag_axis = r.add(nR * 8);
+    s.move_off = r.add((nR + 1) * 8);
+    s.move_atoms = r.add(nM * 4);
+    s.order = r.add(nA);
+    s.frint = r.add(nR * 16);
     s.featA = r.add(n * 4);
     s.featR = r.add(n * 4);
     s.featM = r.add(n * 4);
@@ -295,7 +305,7 @@ Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats,
     s.coords = r.add(nA * 12);
     const int64_t kc = std::max<int64_t>(n, 65536);
     s.keys = r.add(kc * 8);
-    s.topk_out = r.add(8192 * 8);
+    s.topk_out = r.add(2 * 8192 * 8);   // merged keys + their ligand ids
     s.sel = r.add(4096);
     s.counters = r.add((size_t)(n + kMaxCells) * n_pockets * 4 + 256);
     s.end = r.off;
@@ -315,16 +325,28 @@ const char* vcode_msg(int code) {
         case 3: return "non-finite coordinate";
         case 4: return "fragment axis atom index out of range";
         case 5: return "fragment axis atoms are equal";
-        case 6: return "fragment moving range invalid (need 0 <= lo < hi <= atoms)";
-        case 7: return "fragment axis atom inside its moving range";
+        case 6: return "fragment moving set empty or larger than atoms - 2";
+        case 7: return "fragment axis atom inside its own moving set";
         case 8: return "fragment axis atoms closer than 1e-3 A";
+        case 9: return "moving atom index out of range";
+        case 10: return "atom listed twice in one moving set";
+        case 11: return "moving sets not laminar (two fragments' moving sets overlap without nesting)";
+        case 12: return "coordinate magnitude above 1e6 A";
         default: return "invalid record";
     }
 }
 
-// Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1.
-vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs, int ps, int RC) {
-    c->classes.clear();
+int pow2_ceil(int K) {
+    int p = 1;
+    while (p < K) p <<= 1;
+    return p;
+}
+
+// Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1 -- for one
+// grid layout (nz planes of ps floats, row stride rs).
+vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs, int ps, int RC,
+                       std::vector<ClassInfo>& out) {
+    out.clear();
     for (size_t i = 0; i < atom_b.size(); ++i) {
         ClassInfo ci{};
         ci.atom_bound = atom_b[i];
@@ -347,7 +369,7 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs
         }
         for (auto pr : cand) {
             const int PPW = pr.first, NW = pr.second;
-            if (c->K > 32 / PPW) continue;
+            if (pow2_ceil(c->K) > 32 / PPW) continue;   // the pose group holds the angle slots
             const int LC = ligs_per_cta(NW, PPW, c->P);
             const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
             int b = 0;
@@ -367,7 +389,7 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs
                         (int)i, ci.AC, nz, ps);
         ci.l = ci.b * c->sm_count * ci.LC;       // Eq. 1: l = b * SM * t/ws  (Q19)
         ci.cap = c->cfg.bucket_capacity > 0 ? c->cfg.bucket_capacity : ci.l * std::max(1, c->cfg.bucket_multiple);
-        c->classes.push_back(ci);
+        out.push_back(ci);
     }
     return VS_OK;
 }
@@ -447,26 +469,27 @@ const char* vs_last_error(const vs_ctx* c) { return c ? c->err.c_str() : "null c
 vs_status vs_set_pose_table(vs_ctx* c, int32_t P, const float* rot, const float* trans) {
     if (!c) return VS_E_ARG;
     if (P < 1 || P > kMaxPoses || !rot || !trans) return fail(c, VS_E_ARG, "pose table: need 1 <= P <= %d", kMaxPoses);
-    c->P = P;
-    c->pose_tab.assign((size_t)P * 12, 0.f);
-    ++c->tables_version;
+    // validate into a temporary; the active table changes only on success
+    std::vector<float> tab((size_t)P * 12, 0.f);
     for (int p = 0; p < P; ++p) {
         for (int t = 0; t < 9; ++t) {
             if (!std::isfinite(rot[9 * p + t])) return fail(c, VS_E_ARG, "pose %d: non-finite rotation", p);
-            c->pose_tab[12 * p + t] = rot[9 * p + t];
+            tab[12 * p + t] = rot[9 * p + t];
         }
         for (int t = 0; t < 3; ++t) {
             if (!std::isfinite(trans[3 * p + t])) return fail(c, VS_E_ARG, "pose %d: non-finite translation", p);
-            c->pose_tab[12 * p + 9 + t] = trans[3 * p + t];
+            tab[12 * p + 9 + t] = trans[3 * p + t];
         }
     }
+    c->P = P;
+    c->pose_tab.swap(tab);
+    ++c->tables_version;
     return VS_OK;
 }
 
 vs_status vs_set_angle_table(vs_ctx* c, int32_t K, const float* cos_sin) {
     if (!c) return VS_E_ARG;
-    if (K < 1 || K > 32 || (K & (K - 1)) || !cos_sin)
-        return fail(c, VS_E_ARG, "angle table: K must be a power of two in [1, 32]");
+    if (K < 1 || K > 32 || !cos_sin) return fail(c, VS_E_ARG, "angle table: K must be in [1, 32]");
     if (cos_sin[0] != 1.0f || cos_sin[1] != 0.0f) return fail(c, VS_E_ARG, "angle table: entry 0 must be (1, 0)");
     for (int t = 0; t < 2 * K; ++t)
         if (!std::isfinite(cos_sin[t])) return fail(c, VS_E_ARG, "angle table: non-finite entry %d", t / 2);
@@ -503,18 +526,19 @@ vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, 
     return VS_OK;
 }
 
-vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int32_t max_atoms,
-                            int32_t n_pockets, size_t* bytes) {
+vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int64_t n_moving,
+                            int32_t max_atoms, int32_t n_pockets, size_t* bytes) {
     if (!c || !bytes) return VS_E_ARG;
     if (c->P < 1 || c->K < 1) return fail(c, VS_E_STATE, "set the pose and angle tables first");
     if (c->pockets.empty()) return fail(c, VS_E_STATE, "load a pocket first");
-    if (n_lig < 0 || n_atoms < 0 || n_frags < 0 || max_atoms < 1 || max_atoms > kMaxAtoms || n_pockets < 1)
+    if (n_lig < 0 || n_atoms < 0 || n_frags < 0 || n_moving < 0 || max_atoms < 1 || max_atoms > kMaxAtoms ||
+        n_pockets < 1)
         return fail(c, VS_E_ARG, "bad workspace query");
     int ac_max = roundup32(std::max<int>(max_atoms, c->cfg.atom_upper_bound));
     ac_max = std::max(ac_max, 32);
     // Q16 fallback boundary 32*n for the last class can exceed the observed maximum
     ac_max = std::min(kMaxAtoms, std::max(ac_max, std::min(kMaxAtoms, roundup32(max_atoms))));
-    const Stage1 s1 = plan1(n_lig, n_atoms, n_frags, c->P, c->K, max_grid_bytes(c), n_pockets);
+    const Stage1 s1 = plan1(n_lig, n_atoms, n_frags, n_moving, c->P, c->K, max_grid_bytes(c), n_pockets);
     const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * (3 * ac_max + 32), c->P,
                             c->cfg.n_sweeps, n_pockets, c->cfg.debug_poses != 0);
     *bytes = s2.end + 4096;
@@ -526,6 +550,8 @@ vs_status vs_set_workspace(vs_ctx* c, void* ptr, size_t bytes) {
     if (((uintptr_t)ptr & 255) != 0) return fail(c, VS_E_ARG, "workspace must be 256-byte aligned");
     c->ws = (uint8_t*)ptr;
     c->uploaded_sig.clear();   // new memory: tables and grids must be uploaded again
+    c->d_topk_out = nullptr;   // scratch of the old workspace: never reused after a swap
+    c->d_sel = nullptr;
     c->ws_bytes = bytes;
     c->submitted = false;
     return VS_OK;
@@ -549,7 +575,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     int64_t launches = 0;
 
     // ---- batch sizes
-    int64_t nA = 0, nR = 0;
+    int64_t nA = 0, nR = 0, nM = 0;
     if (n > 0) {
         if (!batch->atom_off || !batch->xyz || !batch->frag_off) return fail(c, VS_E_ARG, "null batch array");
         if (batch->on_device) {
@@ -559,6 +585,12 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             CK(cudaMemcpy(&z[0], batch->atom_off, 8, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(&z[1], batch->frag_off, 8, cudaMemcpyDeviceToHost));
             if (z[0] != 0 || z[1] != 0) return fail(c, VS_E_PARSE, "atom_off[0] and frag_off[0] must be 0");
+            if (nR > 0) {
+                if (!batch->move_off) return fail(c, VS_E_ARG, "null move_off");
+                CK(cudaMemcpy(&z[0], batch->move_off, 8, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(&nM, batch->move_off + nR, 8, cudaMemcpyDeviceToHost));
+                if (z[0] != 0) return fail(c, VS_E_PARSE, "move_off[0] must be 0");
+            }
         } else {
             if (batch->atom_off[0] != 0 || batch->frag_off[0] != 0)
                 return fail(c, VS_E_PARSE, "atom_off[0] and frag_off[0] must be 0");
@@ -567,14 +599,24 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             for (int64_t i = 0; i < n; ++i)   // monotone offsets (cheap, O(n))
                 if (batch->atom_off[i + 1] < batch->atom_off[i] || batch->frag_off[i + 1] < batch->frag_off[i])
                     return fail(c, VS_E_PARSE, "ligand %lld: decreasing CSR offsets", (long long)i);
+            if (nR > 0) {
+                if (!batch->move_off) return fail(c, VS_E_ARG, "null move_off");
+                if (batch->move_off[0] != 0) return fail(c, VS_E_PARSE, "move_off[0] must be 0");
+                for (int64_t f = 0; f < nR; ++f)
+                    if (batch->move_off[f + 1] < batch->move_off[f])
+                        return fail(c, VS_E_PARSE, "fragment %lld: decreasing move_off", (long long)f);
+                nM = batch->move_off[nR];
+            }
         }
-        if (nA < 0 || nR < 0) return fail(c, VS_E_PARSE, "negative CSR totals");
-        if (nR > 0 && !batch->frags) return fail(c, VS_E_ARG, "null frags");
+        if (nA < 0 || nR < 0 || nM < 0) return fail(c, VS_E_PARSE, "negative CSR totals");
+        if (nR > 0 && (!batch->frag_axis || (nM > 0 && !batch->move_atoms)))
+            return fail(c, VS_E_ARG, "null frag_axis / move_atoms");
         if ((int64_t)S_w * nR >= (1ll << 31)) return fail(c, VS_E_ARG, "too many fragments in one batch");
     }
     c->n = n;
     c->nA = nA;
     c->nR = nR;
+    c->nM = nM;
     c->job_pockets.assign(pocket_ids, pocket_ids + n_pockets);
 
     // ---- stage-1 workspace
@@ -583,7 +625,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         auto& d = c->pockets[pocket_ids[i]].d;
         gmax = std::max(gmax, (size_t)d.nx * d.ny * d.nz * 4);
     }
-    const Stage1 s1 = plan1(n, nA, nR, c->P, c->K, gmax, n_pockets);
+    const Stage1 s1 = plan1(n, nA, nR, nM, c->P, c->K, gmax, n_pockets);
     if (s1.end > c->ws_bytes) return fail(c, VS_E_WORKSPACE, "workspace too small (stage 1 needs %zu bytes)", s1.end);
     uint8_t* W = c->ws;
     c->d_featA = (int*)(W + s1.featA);
@@ -606,16 +648,24 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->d_cs = (float*)(W + s1.cs);
     c->d_grid.assign(n_pockets, nullptr);
     for (int i = 0; i < n_pockets; ++i) c->d_grid[i] = (float*)(W + s1.grids + (size_t)i * gmax);
+    c->d_order = W + s1.order;
+    c->d_frint = (int4*)(W + s1.frint);
     if (batch->on_device) {
         c->d_atom_off = (int64_t*)batch->atom_off;
         c->d_frag_off = (int64_t*)batch->frag_off;
         c->d_xyz = (float*)batch->xyz;
-        c->d_frags = (int32_t*)batch->frags;
+        c->d_frag_axis = (int32_t*)batch->frag_axis;
+        c->d_move_off = (int64_t*)batch->move_off;
+        c->d_move_atoms = (int32_t*)batch->move_atoms;
+        c->d_lid = batch->ligand_id;
     } else {
         c->d_atom_off = (int64_t*)(W + s1.atom_off);
         c->d_frag_off = (int64_t*)(W + s1.frag_off);
         c->d_xyz = (float*)(W + s1.xyz);
-        c->d_frags = (int32_t*)(W + s1.frags);
+        c->d_frag_axis = (int32_t*)(W + s1.frag_axis);
+        c->d_move_off = (int64_t*)(W + s1.move_off);
+        c->d_move_atoms = (int32_t*)(W + s1.move_atoms);
+        c->d_lid = batch->ligand_id ? (const uint64_t*)(W + s1.lid) : nullptr;
     }
 
     CK(cudaEventRecord(c->ev_prep0, ms));
@@ -648,14 +698,20 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         CK(cudaMemcpyAsync(c->d_atom_off, batch->atom_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
         CK(cudaMemcpyAsync(c->d_frag_off, batch->frag_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
         if (nA) CK(cudaMemcpyAsync(c->d_xyz, batch->xyz, nA * 12, cudaMemcpyHostToDevice, ms));
-        if (nR) CK(cudaMemcpyAsync(c->d_frags, batch->frags, nR * 16, cudaMemcpyHostToDevice, ms));
+        if (nR) {
+            CK(cudaMemcpyAsync(c->d_frag_axis, batch->frag_axis, nR * 8, cudaMemcpyHostToDevice, ms));
+            CK(cudaMemcpyAsync(c->d_move_off, batch->move_off, (nR + 1) * 8, cudaMemcpyHostToDevice, ms));
+        }
+        if (nM) CK(cudaMemcpyAsync(c->d_move_atoms, batch->move_atoms, nM * 4, cudaMemcpyHostToDevice, ms));
+        if (batch->ligand_id)
+            CK(cudaMemcpyAsync((void*)c->d_lid, batch->ligand_id, n * 8, cudaMemcpyHostToDevice, ms));
     }
 
-    // ---- a1 validate + features
+    // ---- a1 ingest: validate, laminar check, canonical renumbering, features
     CK(cudaMemsetAsync(c->d_status, 0xFF, 16, ms));
     CK(cudaMemsetAsync(c->d_maxAR, 0, 8, ms));
-    CK(launch_validate(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frags, n, c->d_featA, c->d_featR, c->d_featM,
-                       c->d_status, c->d_maxAR, ms));
+    CK(launch_ingest(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frag_axis, c->d_move_off, c->d_move_atoms, n,
+                     c->d_order, c->d_frint, c->d_featA, c->d_featR, c->d_featM, c->d_status, c->d_maxAR, ms));
     ++launches;
     vs_status st = ensure_pinned(c, (size_t)(s1.max_buckets + 16) * 32 + kMaxCells * 8 + 64);
     if (st) return st;
@@ -678,17 +734,30 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->atom_b = atom_bounds(c->cfg.n_atom_clusters, ubA);
     c->rot_b = rot_bounds(c->cfg.n_rot_clusters, ubR);
     if ((int)c->rot_b.size() > kMaxRotClasses) return fail(c, VS_E_ARG, "too many rotamer classes");
-    int nz_max = 0, rs_max = 0, ps_max = 0;
-    for (auto& pk : c->pkdev) {
-        if ((int64_t)pk.nz * pk.ps > (int64_t)nz_max * ps_max) {
-            nz_max = pk.nz;
-            ps_max = pk.ps;
-            rs_max = pk.rs;
-        }
-    }
+    // one class table per distinct grid layout among the submitted pockets (each launch uses
+    // its pocket's table: policy, occupancy and shared memory differ per layout); the table
+    // of the largest layout sizes the buckets (Eq. 1), so capacities fit every pocket
     c->frag_cap = maxAR[1];
-    st = plan_classes(c, c->atom_b, nz_max, rs_max, ps_max, c->frag_cap);
-    if (st) return st;
+    {
+        std::vector<std::vector<int>> keys;   // (nz, rs, ps) per layout
+        c->layout_classes.clear();
+        c->pk_layout.assign(n_pockets, 0);
+        int big = 0;
+        for (int q = 0; q < n_pockets; ++q) {
+            const PocketDev& pk = c->pkdev[q];
+            const std::vector<int> key = {pk.nz, pk.rs, pk.ps};
+            int li = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
+            if (li == (int)keys.size()) {
+                keys.push_back(key);
+                c->layout_classes.emplace_back();
+                st = plan_classes(c, c->atom_b, pk.nz, pk.rs, pk.ps, c->frag_cap, c->layout_classes.back());
+                if (st) return st;
+                if ((int64_t)pk.nz * pk.ps > (int64_t)keys[big][0] * keys[big][2]) big = li;
+            }
+            c->pk_layout[q] = li;
+        }
+        c->classes = c->layout_classes[big];
+    }
     const int nRc = (int)c->rot_b.size();
     const int n_cells = (int)c->atom_b.size() * nRc;
     CK(launch_classify_hist(c->d_featA, c->d_featR, n, c->atom_b.data(), (int)c->atom_b.size(), c->rot_b.data(), nRc,
@@ -833,7 +902,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         }
     }
     CK(launch_pack(c->d_perm, c->d_own_start, c->d_own_prefix, c->d_own_ac, c->d_own_rec_off, no, c->total_slots,
-                   c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frags, S_w, c->d_rec, c->d_meta, ms));
+                   c->d_atom_off, c->d_xyz, c->d_order, c->d_frag_off, c->d_frint, S_w, c->d_rec, c->d_meta, ms));
     ++launches;
     for (int i = 0; i < n_pockets; ++i) {
         CK(launch_fill_results(c->d_score[i], c->d_pose_best[i], n, c->d_ang[i], (int64_t)S_w * nR, ms));
@@ -864,9 +933,9 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     int64_t dock_launches = 0;
     for (const Unit& u : units) {
         const vs_bucket& b = c->buckets[c->owned[u.first]];
-        const ClassInfo& ci = c->classes[u.cls];
         const int i = u.first;
         for (int q = 0; q < n_pockets; ++q) {
+            const ClassInfo& ci = c->layout_classes[c->pk_layout[q]][u.cls];
             DockArgs a{};
             a.rec = c->d_rec + c->owned_rec_off[i];
             a.meta = c->d_meta + c->owned_prefix[i];
@@ -926,17 +995,23 @@ vs_status vs_wait(vs_ctx* c) {
     return VS_OK;
 }
 
-vs_status vs_get_results(vs_ctx* c, int32_t slot, float* best_score, int32_t* best_pose, uint8_t* angle_idx,
-                         int32_t on_device) {
+vs_status vs_get_results(vs_ctx* c, int32_t slot, uint64_t* ligand_id, float* best_score, int32_t* best_pose,
+                         uint8_t* angle_idx, int32_t on_device) {
     if (!c) return VS_E_ARG;
     if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
     if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
     if (c->n == 0) return VS_OK;
-    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (on_device < 0 || on_device > 2) return fail(c, VS_E_ARG, "on_device must be 0, 1 or 2");
+    const cudaMemcpyKind kind = on_device == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (ligand_id) {
+        if (c->d_lid) CK(cudaMemcpyAsync(ligand_id, c->d_lid, c->n * 8, cudaMemcpyDefault, c->main));
+        else if (on_device == 1) return fail(c, VS_E_ARG, "the batch carried no ligand ids (request them on the host)");
+        else for (int64_t i = 0; i < c->n; ++i) ligand_id[i] = (uint64_t)i;
+    }
     if (best_score) CK(cudaMemcpyAsync(best_score, c->d_score[slot], c->n * 4, kind, c->main));
     if (best_pose) CK(cudaMemcpyAsync(best_pose, c->d_pose_best[slot], c->n * 4, kind, c->main));
     if (angle_idx && c->nR) CK(cudaMemcpyAsync(angle_idx, c->d_ang[slot], (size_t)c->cfg.n_sweeps * c->nR, kind, c->main));
-    CK(cudaStreamSynchronize(c->main));
+    if (on_device != 2) CK(cudaStreamSynchronize(c->main));   // 2: asynchronous (pinned host), see vsdock.h
     return VS_OK;
 }
 
@@ -958,7 +1033,9 @@ vs_status vs_get_coords(vs_ctx* c, int32_t slot, float* xyz_out, int32_t on_devi
     if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
     if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
     if (c->n == 0 || c->nA == 0) return VS_OK;
-    CK(cudaMemsetAsync(c->d_coords, 0xFF, c->nA * 12, c->main));   // NaN for ligands of other ranks
+    if (on_device < 0 || on_device > 2) return fail(c, VS_E_ARG, "on_device must be 0, 1 or 2");
+    if (c->stats.n_owned < c->n)
+        CK(cudaMemsetAsync(c->d_coords, 0xFF, c->nA * 12, c->main));   // NaN for ligands of other ranks
     for (size_t i = 0; i < c->owned.size(); ++i) {
         const vs_bucket& b = c->buckets[c->owned[i]];
         DockArgs a{};
@@ -974,12 +1051,13 @@ vs_status vs_get_coords(vs_ctx* c, int32_t slot, float* xyz_out, int32_t on_devi
         a.pk = c->pkdev[slot];
         a.best_pose = c->d_pose_best[slot];
         a.angles = c->d_ang[slot];
+        a.order = c->d_order;
         CK(launch_finalize(b.kernel_atoms, a, c->d_atom_off, c->d_coords, c->main));
         c->stats.kernel_launches++;
     }
-    CK(cudaMemcpyAsync(xyz_out, c->d_coords, c->nA * 12, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                       c->main));
-    CK(cudaStreamSynchronize(c->main));
+    CK(cudaMemcpyAsync(xyz_out, c->d_coords, c->nA * 12,
+                       on_device == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->main));
+    if (on_device != 2) CK(cudaStreamSynchronize(c->main));
     return VS_OK;
 }
 
@@ -1021,16 +1099,34 @@ vs_status vs_keys(vs_ctx* c, int32_t slot, uint32_t index_offset, uint64_t* keys
     return VS_OK;
 }
 
+vs_status vs_select_keys(vs_ctx* c, const uint64_t* keys_dev, int64_t n_keys, int32_t k, uint64_t* out_dev) {
+    if (!c || !out_dev || (!keys_dev && n_keys > 0)) return VS_E_ARG;
+    if (k < 1 || k > 8192) return fail(c, VS_E_ARG, "k must be in [1, 8192]");
+    if (!c->ws || !c->d_sel) return fail(c, VS_E_STATE, "submit a batch first (workspace scratch)");
+    int l2 = 0;
+    CK(topk_select_sort((const unsigned long long*)keys_dev, n_keys, k, (unsigned long long*)out_dev, c->d_sel, c->main,
+                        &l2));
+    c->stats.kernel_launches += l2;
+    return VS_OK;
+}
+
 vs_status vs_merge_topk(vs_ctx* c, const uint64_t* keys_dev, int64_t n_keys, int32_t k, int64_t* index_out,
-                        float* score_out, int32_t* n_out) {
+                        float* score_out, uint64_t* id_out, int32_t* n_out) {
     if (!c || (!keys_dev && n_keys > 0)) return VS_E_ARG;
     if (k < 1 || k > 8192) return fail(c, VS_E_ARG, "k must be in [1, 8192]");
     if (!c->ws || !c->d_topk_out) return fail(c, VS_E_STATE, "submit a batch first (workspace scratch)");
     int l2 = 0;
     CK(topk_select_sort((const unsigned long long*)keys_dev, n_keys, k, c->d_topk_out, c->d_sel, c->main, &l2));
     c->stats.kernel_launches += l2;
-    std::vector<unsigned long long> h(k);
+    std::vector<unsigned long long> h(k), ids(id_out ? k : 0);
     CK(cudaMemcpyAsync(h.data(), c->d_topk_out, (size_t)k * 8, cudaMemcpyDeviceToHost, c->main));
+    if (id_out) {   // ids of the last batch, gathered on the device (after the keys in the scratch)
+        unsigned long long* d_ids = c->d_topk_out + 8192;
+        CK(launch_gather_ids(c->d_topk_out, k, (const unsigned long long*)c->d_lid, c->submitted ? c->n : 0, d_ids,
+                              c->main));
+        c->stats.kernel_launches++;
+        CK(cudaMemcpyAsync(ids.data(), d_ids, (size_t)k * 8, cudaMemcpyDeviceToHost, c->main));
+    }
     CK(cudaStreamSynchronize(c->main));
     int m = 0;
     for (int i = 0; i < k; ++i) {
@@ -1041,6 +1137,7 @@ vs_status vs_merge_topk(vs_ctx* c, const uint64_t* keys_dev, int64_t n_keys, int
         std::memcpy(&s, &bits, 4);
         if (index_out) index_out[i] = (int64_t)(h[i] & 0xffffffffull);
         if (score_out) score_out[i] = s;
+        if (id_out) id_out[i] = ids[i];
         ++m;
     }
     if (n_out) *n_out = m;

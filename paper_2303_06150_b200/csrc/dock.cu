@@ -69,6 +69,11 @@ cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, si
     DockFn f = pick(AC, NW, PPW, grid_fixed(a.pk.rs, a.pk.ps), a.K);
     if (!f) return cudaErrorInvalidValue;
     if (a.n <= 0) return cudaSuccess;
+    // the attribute is per function, and one instantiation can serve several grid layouts
+    // (pockets of different sizes in one submit): set it for THIS launch's shared memory
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
     f<<<grid, NW * 32, smem, st>>>(a);
     return cudaGetLastError();
 }

@@ -229,6 +229,8 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
 // a6 placement, a7 sweep, a9 pose score.
 // KT = the angle count when known at compile time (8: the production path, every lane-map
 // constant folds), 0 = runtime K.
+// K need not be a power of two: the lane map uses Kp = the next power of two >= K (kbits =
+// log2 Kp) and the lanes of angle slots k >= K hold the identity and never win.
 template <int AC, int PPW, bool FIX, int KT>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, PoseBuf<AC> B, const float* __restrict__ G,
@@ -238,6 +240,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     constexpr int LPP = 32 / PPW;
     const int K = KT ? KT : K_rt;
     const int kbits = KT ? (KT == 1 ? 0 : KT == 2 ? 1 : KT == 4 ? 2 : KT == 8 ? 3 : KT == 16 ? 4 : 5) : kbits_rt;
+    const int Kp = 1 << kbits;
     const int li = lane & (LPP - 1);
     const float* rx = rec;
     const float* ry = rec + AC;
@@ -250,11 +253,12 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     }
     __syncwarp();
     if (K > 1) {
-        const int k = li & (K - 1);
+        const int k = li & (Kp - 1);
+        const bool kreal = KT ? true : k < K;         // angle slot holds a table entry
         const int jl = li >> kbits;
         const int abits = __ffs(LPP) - 1 - kbits;     // log2(apw)
         const int apw = 1 << abits;                   // moving atoms per step of a pose group
-        const unsigned gmask = ((K == 32) ? 0xffffffffu : ((1u << K) - 1u)) << (lane & ~(K - 1));
+        const unsigned gmask = ((Kp == 32) ? 0xffffffffu : ((1u << Kp) - 1u)) << (lane & ~(Kp - 1));
         for (int sw = 0; sw < S_w; ++sw) {
             for (int r = 0; r < R; ++r) {
                 const uint32_t f = rfr[r];
@@ -280,15 +284,15 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
 #pragma unroll
                 for (int o = 1; o < LPP; o <<= 1)
-                    if (o >= K) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
-                // argmin over the K angles of this group (xor offsets 1 .. K/2); ties -> lowest k (Q11)
-                const unsigned key = ord32(acc);
+                    if (o >= Kp) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                // argmin over the K angles of this group (xor offsets 1 .. Kp/2); ties -> lowest k (Q11)
+                const unsigned key = kreal ? ord32(acc) : 0xffffffffu;
                 unsigned mn = key;
 #pragma unroll
                 for (int o = 1; o < LPP; o <<= 1)
-                    if (o < K) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
-                const unsigned bal = __ballot_sync(FULL, key == mn) & gmask;
-                const int bk = (__ffs(bal) - 1) & (K - 1);
+                    if (o < Kp) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
+                const unsigned bal = __ballot_sync(FULL, key == mn && kreal) & gmask;
+                const int bk = (__ffs(bal) - 1) & (Kp - 1);
                 if (nst <= 4) {
                     // one batch: the lanes (jl, k*) still hold the rotated atoms in registers
                     if (valid && bk != 0 && k == bk) {
@@ -508,8 +512,9 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
     const int K = KT ? KT : a.K, S_w = a.S_w, P = a.P;
-    const int kbits = 31 - __clz(K);
-    const float ck = a.cs[2 * (lane & (K - 1))], sk = a.cs[2 * (lane & (K - 1)) + 1];   // this lane's angle
+    const int kbits = K > 1 ? 32 - __clz(K - 1) : 0;   // log2 of Kp, the next power of two >= K
+    const int kl = lane & ((1 << kbits) - 1);          // this lane's angle slot
+    const float ck = kl < K ? a.cs[2 * kl] : 1.f, sk = kl < K ? a.cs[2 * kl + 1] : 0.f;   // slots >= K: identity
     const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride_of(AC, NW, PPW)};
     const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
@@ -583,7 +588,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
 
 // a9 coordinates: replay p* with the recorded angles, bit-identical to the
 // dock kernel (same placement, axis, Rodrigues and rotation helpers); one warp
-// per ligand; output in Angstrom, input atom order.
+// per ligand; output in Angstrom, in the caller's input atom order (a1's order map).
 template <int AC>
 __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const int64_t* __restrict__ atom_off,
                                                        float* __restrict__ xyz_out) {
@@ -622,11 +627,13 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const i
         }
     }
     float* out = xyz_out + 3 * atom_off[li];
+    const uint8_t* ord = a.order + atom_off[li];   // internal atom i -> input atom ord[i] (a1)
     for (int i = lane; i < A; i += 32) {
         const float4 v = buf[i];
-        out[3 * i] = __fmaf_rn(pk.h, v.x, pk.ox);
-        out[3 * i + 1] = __fmaf_rn(pk.h, v.y, pk.oy);
-        out[3 * i + 2] = __fmaf_rn(pk.h, v.z, pk.oz);
+        const int q = ord[i];
+        out[3 * q] = __fmaf_rn(pk.h, v.x, pk.ox);
+        out[3 * q + 1] = __fmaf_rn(pk.h, v.y, pk.oy);
+        out[3 * q + 2] = __fmaf_rn(pk.h, v.z, pk.oz);
     }
 }
 

@@ -53,6 +53,7 @@ struct DockArgs {
     uint8_t* angles;           // CSR S_w * frag_off
     float* dbg_score;          // [n_total * P] or null
     uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
+    const uint8_t* order;      // finalize only: internal atom -> input atom (CSR by atom_off, a1)
 };
 
 // Per-pose coordinate buffer stride (floats): 3 AC + 8, i.e. 8 banks apart, so the 4 pose
@@ -111,9 +112,9 @@ __host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
 void grid_strides(int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).
-cudaError_t launch_validate(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frags,
-                            int64_t n, int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR,
-                            cudaStream_t st);
+cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
+                          const int64_t* move_off, const int32_t* move_atoms, int64_t n, uint8_t* order, int4* frint,
+                          int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st);
 cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
                                  const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
                                  unsigned long long* ovf, cudaStream_t st);
@@ -126,8 +127,8 @@ cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const 
 // Pack owned buckets.  slot_bucket_prefix[b] = first packed slot of owned bucket b (nb+1 entries).
 cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
-                        const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
-                        int4* meta, cudaStream_t st);
+                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint, int S_w,
+                        float* rec, int4* meta, cudaStream_t st);
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, int K, cudaFuncAttributes* attr);
 cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem, int* blocks_per_sm);
@@ -140,9 +141,12 @@ cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n
 // top-k
 cudaError_t launch_make_keys(const int4* meta, int n_slots, const float* best_score, unsigned long long* keys,
                              cudaStream_t st, uint32_t index_offset = 0);
-// Select the k smallest of keys[n] (unique), write them sorted to out[k] (UINT64_MAX padded).
+// Select the k smallest of keys[n] (unique except UINT64_MAX pads), write them sorted to out[k]
+// (UINT64_MAX padded).
 // scratch: >= (n + 2048) u64 + 4 KB.  Returns the number of kernels launched in *launches.
 cudaError_t topk_select_sort(const unsigned long long* keys, int64_t n, int k, unsigned long long* out,
                              void* scratch, cudaStream_t st, int* launches);
+cudaError_t launch_gather_ids(const unsigned long long* keys, int m, const unsigned long long* ids, int64_t n_ids,
+                              unsigned long long* out, cudaStream_t st);
 
 }  // namespace vsd

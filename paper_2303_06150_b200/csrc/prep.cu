@@ -1,5 +1,5 @@
 // prep.cu -- the paper's out-of-kernel input preparation on the GPU (a1-a5):
-// validation + features, classification into (atom class x rotamer class)
+// ingest (validation, laminar check, canonical atom renumbering) + features, classification into (atom class x rotamer class)
 // cells, a STABLE counting sort by cell (histogram -> scan -> scatter), exact
 // per-bucket work for the LPT shard, and packing into SoA-padded records.
 //
@@ -23,67 +23,283 @@ __device__ __forceinline__ int warp_sum_int(int v) {
     return v;
 }
 
-// a1: one warp per ligand (grid-stride).  Error codes (low byte of the status
-// word, lowest ligand index wins through atomicMin on (index << 8 | code)):
-//  1 atoms outside [1, 256]      2 fragments outside [0, 32]
-//  3 non-finite coordinate       4 axis atom index out of range
-//  5 axis atoms equal            6 moving range invalid (need 0 <= lo < hi <= A)
-//  7 axis atom inside its moving range   8 axis atoms closer than 1e-3 A
-__global__ void __launch_bounds__(256) validate_kernel(const int64_t* __restrict__ atom_off,
-                                                       const float* __restrict__ xyz,
-                                                       const int64_t* __restrict__ frag_off,
-                                                       const int32_t* __restrict__ frags, int64_t n,
-                                                       int* __restrict__ featA, int* __restrict__ featR,
-                                                       int* __restrict__ featM, unsigned long long* status,
-                                                       int* maxAR) {
+// a1: ingest.  One warp per ligand (grid-stride).  Validates the ligand record in the
+// C-ABI's general form (axis (a, b) and the moving-atom SET M_r of every fragment,
+// PAPER.md l.215-216 "a subset of the molecule atoms that can rotate"), checks that the
+// moving sets form a laminar family (any two are nested or disjoint -- what rotations
+// about the bonds of a tree produce), and renumbers the atoms into the canonical
+// internal order in which every M_r is ONE contiguous range [lo, hi):
+//
+//   * the sets form a forest under inclusion (equal sets: the lower fragment index is the
+//     outer one); the forest is ordered depth first, children by fragment index (preorder
+//     number pre[r]);
+//   * atom i's key = (1 + pre of the innermost set containing it, or 0 for atoms in no set;
+//     then its coordinates x, y, z as order-preserving integers; then its input index).
+//     Sorting by the key puts each set's own atoms first and its descendants' atoms right
+//     after them, so every set is contiguous.  The key does not depend on the input atom
+//     numbering (only on coordinates and set structure), so an atom-permuted copy of a
+//     ligand is docked bit-identically (coordinates are mapped back to input order).
+//
+// Outputs: order[atom_off[i] + j] = input index of internal atom j (u8); frint[f] =
+// {a', b', lo, hi} in internal numbering (the range form the pack / dock kernels use);
+// features A, R, sum |M_r|.  Error codes (low byte of the status word; lowest ligand index
+// wins through atomicMin on (index << 8 | code); within a ligand the first failing check):
+//  1 atoms outside [1, 256]            2 fragments outside [0, 32]
+//  3 non-finite coordinate             12 coordinate magnitude above 1e6 A
+//  4 axis atom index out of range      5 axis atoms equal
+//  6 moving set empty or larger than A - 2
+//  8 axis atoms closer than 1e-3 A     9 moving atom index out of range
+//  10 atom listed twice in one moving set
+//  7 axis atom inside its own moving set
+//  11 moving sets not laminar (two sets overlap without one containing the other)
+constexpr int kIngestWarps = 4;
+struct IngestWarp {
+    uint32_t mask[kMaxAtoms];           // bit r: atom in M_r
+    uint4 key[kMaxAtoms];               // (1 + pre, ord x, ord y, ord z)
+    uint8_t path[kMaxFrags][kMaxFrags + 1];   // path[r][d]: ancestor of r at depth d (r itself at depth[r])
+    uint32_t anc[kMaxFrags];
+    uint8_t depth[kMaxFrags], pre[kMaxFrags];
+    uint8_t rank[kMaxAtoms];            // input index -> internal position
+};
+
+__device__ __forceinline__ uint32_t ord_key(float v) {
+    const uint32_t b = __float_as_uint(__fadd_rn(v, 0.0f));   // -0 -> +0
+    return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ bool key_less(const uint4& p, int i, const uint4& q, int j) {
+    if (p.x != q.x) return p.x < q.x;
+    if (p.y != q.y) return p.y < q.y;
+    if (p.z != q.z) return p.z < q.z;
+    if (p.w != q.w) return p.w < q.w;
+    return i < j;
+}
+__device__ __forceinline__ int first_code(int code) {   // lowest lane's non-zero code
+    const unsigned any = __ballot_sync(FULL, code != 0);
+    return any ? __shfl_sync(FULL, code, __ffs(any) - 1) : 0;
+}
+
+__global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
+    const int64_t* __restrict__ atom_off, const float* __restrict__ xyz, const int64_t* __restrict__ frag_off,
+    const int32_t* __restrict__ frag_axis, const int64_t* __restrict__ move_off, const int32_t* __restrict__ move_atoms,
+    int64_t n, uint8_t* __restrict__ order, int4* __restrict__ frint, int* __restrict__ featA, int* __restrict__ featR,
+    int* __restrict__ featM, unsigned long long* status, int* maxAR) {
+    __shared__ IngestWarp sw[kIngestWarps];
     __shared__ int smax[2];
     if (threadIdx.x < 2) smax[threadIdx.x] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    IngestWarp& W = sw[threadIdx.x >> 5];
+    const int64_t warps = (int64_t)gridDim.x * kIngestWarps;
     int locA = 0, locR = 0;
-    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
-        const int64_t a0 = atom_off[i], a1 = atom_off[i + 1];
-        const int64_t f0 = frag_off[i], f1 = frag_off[i + 1];
+    for (int64_t li = (int64_t)blockIdx.x * kIngestWarps + (threadIdx.x >> 5); li < n; li += warps) {
+        const int64_t a0 = atom_off[li], a1 = atom_off[li + 1];
+        const int64_t f0 = frag_off[li], f1 = frag_off[li + 1];
         const int64_t A64 = a1 - a0, R64 = f1 - f0;
-        int code = 0;
+        int code = 0, M = 0;
         if (A64 < 1 || A64 > kMaxAtoms) code = 1;
         else if (R64 < 0 || R64 > kMaxFrags) code = 2;
-        int M = 0;
-        if (code == 0) {
-            const int A = (int)A64, R = (int)R64;
-            bool bad = false;
-            for (int t = lane; t < 3 * A; t += 32) bad |= !isfinite(xyz[3 * a0 + t]);
-            if (__any_sync(FULL, bad)) code = 3;
-            int fcode = 0, mv = 0;
-            if (code == 0 && lane < R) {
-                const int4 f = reinterpret_cast<const int4*>(frags)[f0 + lane];
-                if (f.x < 0 || f.x >= A || f.y < 0 || f.y >= A) fcode = 4;
-                else if (f.x == f.y) fcode = 5;
-                else if (!(0 <= f.z && f.z < f.w && f.w <= A)) fcode = 6;
-                else if ((f.x >= f.z && f.x < f.w) || (f.y >= f.z && f.y < f.w)) fcode = 7;
+        const int A = (int)A64, R = (int)R64;
+        const float* x = xyz + 3 * a0;
+        if (code == 0) {   // coordinates: finite and physically bounded (|x| <= 1e6 A)
+            bool nf = false, big = false;
+            for (int t = lane; t < 3 * A; t += 32) {
+                const float v = x[t];
+                nf |= !isfinite(v);
+                big |= fabsf(v) > 1e6f;
+            }
+            if (__any_sync(FULL, nf)) code = 3;
+            else if (__any_sync(FULL, big)) code = 12;
+        }
+        int fa = 0, fb = 0;
+        int64_t m0 = 0;
+        int cnt = 0;
+        if (code == 0) {   // per fragment: axis, moving-set size, axis length
+            int fc = 0;
+            if (lane < R) {
+                const int64_t f = f0 + lane;
+                fa = frag_axis[2 * f];
+                fb = frag_axis[2 * f + 1];
+                m0 = move_off[f];
+                const int64_t c64 = move_off[f + 1] - m0;
+                cnt = (int)(c64 < 0 ? -1 : (c64 > kMaxAtoms ? kMaxAtoms + 1 : c64));
+                if (fa < 0 || fa >= A || fb < 0 || fb >= A) fc = 4;
+                else if (fa == fb) fc = 5;
+                else if (cnt < 1 || cnt > A - 2 || m0 < 0) fc = 6;
                 else {
-                    const float* pa = xyz + 3 * (a0 + f.x);
-                    const float* pb = xyz + 3 * (a0 + f.y);
-                    const float dx = pb[0] - pa[0], dy = pb[1] - pa[1], dz = pb[2] - pa[2];
-                    if (dx * dx + dy * dy + dz * dz < 1e-6f) fcode = 8;
-                    mv = f.w - f.z;
+                    const float dx = __fsub_rn(x[3 * fb], x[3 * fa]), dy = __fsub_rn(x[3 * fb + 1], x[3 * fa + 1]),
+                                dz = __fsub_rn(x[3 * fb + 2], x[3 * fa + 2]);
+                    if (dx * dx + dy * dy + dz * dz < 1e-6f) fc = 8;
                 }
             }
-            // lowest fragment code wins within the ligand (first error in field order)
-            unsigned any = __ballot_sync(FULL, fcode != 0);
-            if (any) code = __shfl_sync(FULL, fcode, __ffs(any) - 1);
-            M = warp_sum_int(mv);
-            if (code == 0) {
-                locA = max(locA, A);
-                locR = max(locR, R);
+            code = first_code(fc);
+        }
+        if (code == 0) {   // membership masks; index range and duplicates
+            for (int i = lane; i < A; i += 32) W.mask[i] = 0u;
+            __syncwarp();
+            bool oob = false, dup = false;
+            for (int r = 0; r < R; ++r) {
+                const int64_t b0 = __shfl_sync(FULL, m0, r);
+                const int c = __shfl_sync(FULL, cnt, r);
+                for (int t = lane; t < c; t += 32) {
+                    const int i = move_atoms[b0 + t];
+                    if (i < 0 || i >= A) oob = true;
+                    else if (atomicOr(&W.mask[i], 1u << r) & (1u << r)) dup = true;
+                }
             }
+            if (__any_sync(FULL, oob)) code = 9;
+            else if (__any_sync(FULL, dup)) code = 10;
+            __syncwarp();
+        }
+        if (code == 0) {   // axis atoms stay outside their own moving set
+            const bool in = lane < R && (((W.mask[fa] | W.mask[fb]) >> lane) & 1u);
+            if (__any_sync(FULL, in)) code = 7;
+        }
+        uint32_t sup = 0, sub = 0;
+        const uint32_t valid = R == 32 ? 0xffffffffu : ((1u << R) - 1u);
+        if (code == 0) {
+            // laminar family: sup_r = {s : M_r within M_s} (AND of the members' masks),
+            // inter_r = {s : M_s meets M_r} (OR); sub_r = {s : M_s within M_r} (transpose of sup).
+            // Laminar iff every set meeting M_r contains it or is contained in it.
+            uint32_t inter = 0;
+            for (int r = 0; r < R; ++r) {
+                const int64_t b0 = __shfl_sync(FULL, m0, r);
+                const int c = __shfl_sync(FULL, cnt, r);
+                uint32_t s_and = 0xffffffffu, s_or = 0u;
+                for (int t = lane; t < c; t += 32) {
+                    const uint32_t m = W.mask[move_atoms[b0 + t]];
+                    s_and &= m;
+                    s_or |= m;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    s_and &= __shfl_xor_sync(FULL, s_and, o);
+                    s_or |= __shfl_xor_sync(FULL, s_or, o);
+                }
+                if (lane == r) {
+                    sup = s_and & valid;
+                    inter = s_or & valid;
+                }
+            }
+            for (int r = 0; r < R; ++r) {
+                const uint32_t col = __ballot_sync(FULL, lane < R && ((sup >> r) & 1u));
+                if (lane == r) sub = col;
+            }
+            const bool bad = lane < R && (inter & ~(sup | sub)) != 0u;
+            if (__any_sync(FULL, bad)) code = 11;
+        }
+        if (code == 0) {
+            // forest under inclusion: s is an ancestor of r if M_r is strictly inside M_s, or the
+            // sets are equal and s < r.  depth = number of ancestors; path[r][d] = the ancestor
+            // (or r itself) at depth d.
+            uint32_t anc = 0;
+            int dep = 0;
+            if (lane < R) {
+                const uint32_t eq = sup & sub;   // sets equal to M_r (r included)
+                anc = (sup & ~eq) | (eq & ((1u << lane) - 1u));
+                dep = __popc(anc);
+                W.anc[lane] = anc;
+                W.depth[lane] = (uint8_t)dep;
+            }
+            __syncwarp();
+            if (lane < R) {
+                uint32_t chain = anc | (1u << lane);
+                while (chain) {
+                    const int s2 = __ffs(chain) - 1;
+                    chain &= chain - 1u;
+                    W.path[lane][W.depth[s2]] = (uint8_t)s2;
+                }
+            }
+            __syncwarp();
+            // preorder number: s comes before r if s is an ancestor of r, or, below their
+            // deepest common ancestor, s's branch has the lower fragment index
+            if (lane < R) {
+                int pre = 0;
+                for (int s2 = 0; s2 < R; ++s2) {
+                    if (s2 == lane) continue;
+                    const uint32_t as = W.anc[s2];
+                    bool before;
+                    if ((anc >> s2) & 1u) before = true;
+                    else if ((as >> lane) & 1u) before = false;
+                    else {
+                        const int dc = __popc(anc & as);
+                        before = W.path[s2][dc] < W.path[lane][dc];
+                    }
+                    pre += before;
+                }
+                W.pre[lane] = (uint8_t)pre;
+            }
+            __syncwarp();
+            // atom keys
+            for (int i = lane; i < A; i += 32) {
+                uint32_t m = W.mask[i], k0 = 0;
+                if (m) {
+                    int best = -1, bd = -1;
+                    while (m) {
+                        const int r = __ffs(m) - 1;
+                        m &= m - 1u;
+                        if ((int)W.depth[r] > bd) {
+                            bd = W.depth[r];
+                            best = r;
+                        }
+                    }
+                    k0 = 1u + W.pre[best];
+                }
+                W.key[i] = make_uint4(k0, ord_key(x[3 * i]), ord_key(x[3 * i + 1]), ord_key(x[3 * i + 2]));
+            }
+            __syncwarp();
+            // rank by counting (A <= 256: <= 8 atoms per lane, A broadcast key loads)
+            uint4 mine[kMaxAtoms / 32];
+            int rk[kMaxAtoms / 32];
+#pragma unroll
+            for (int u = 0; u < kMaxAtoms / 32; ++u) {
+                const int i = lane + 32 * u;
+                mine[u] = i < A ? W.key[i] : make_uint4(0, 0, 0, 0);
+                rk[u] = 0;
+            }
+            for (int j = 0; j < A; ++j) {
+                const uint4 kj = W.key[j];
+#pragma unroll
+                for (int u = 0; u < kMaxAtoms / 32; ++u)
+                    rk[u] += (lane + 32 * u < A) && key_less(kj, j, mine[u], lane + 32 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < kMaxAtoms / 32; ++u) {
+                const int i = lane + 32 * u;
+                if (i < A) {
+                    W.rank[i] = (uint8_t)rk[u];
+                    order[a0 + rk[u]] = (uint8_t)i;
+                }
+            }
+            __syncwarp();
+            // internal fragments: every moving set is now the range [min rank, max rank + 1)
+            for (int r = 0; r < R; ++r) {
+                const int64_t b0 = __shfl_sync(FULL, m0, r);
+                const int c = __shfl_sync(FULL, cnt, r);
+                int lo = kMaxAtoms, hi = -1;
+                for (int t = lane; t < c; t += 32) {
+                    const int q = W.rank[move_atoms[b0 + t]];
+                    lo = min(lo, q);
+                    hi = max(hi, q);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo = min(lo, __shfl_xor_sync(FULL, lo, o));
+                    hi = max(hi, __shfl_xor_sync(FULL, hi, o));
+                }
+                if (lane == r) frint[f0 + r] = make_int4(W.rank[fa], W.rank[fb], lo, hi + 1);
+                M += c;
+            }
+            __syncwarp();
+        }
+        if (code == 0) {
+            locA = max(locA, A);
+            locR = max(locR, R);
         }
         if (lane == 0) {
-            featA[i] = (int)(A64 > 0x7fffffff ? 0x7fffffff : A64);
-            featR[i] = (int)(R64 > 0x7fffffff ? 0x7fffffff : R64);
-            featM[i] = M;
-            if (code) atomicMin(status, ((unsigned long long)i << 8) | (unsigned long long)code);
+            featA[li] = (int)(A64 > 0x7fffffff ? 0x7fffffff : (A64 < 0 ? 0 : A64));
+            featR[li] = (int)(R64 > 0x7fffffff ? 0x7fffffff : (R64 < 0 ? 0 : R64));
+            featM[li] = M;
+            if (code) atomicMin(status, ((unsigned long long)li << 8) | (unsigned long long)code);
         }
     }
     if (lane == 0) {
@@ -249,8 +465,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
                                                    const int64_t* __restrict__ owned_rec_off, int n_owned,
                                                    int total_slots, const int64_t* __restrict__ atom_off,
                                                    const float* __restrict__ xyz,
+                                                   const uint8_t* __restrict__ order,
                                                    const int64_t* __restrict__ frag_off,
-                                                   const int32_t* __restrict__ frags, int S_w,
+                                                   const int4* __restrict__ frint, int S_w,
                                                    float* __restrict__ rec, int4* __restrict__ meta) {
     const int lane = threadIdx.x & 31;
     const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -270,11 +487,21 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     const int64_t f0 = frag_off[li];
     const int R = (int)(frag_off[li + 1] - f0);
     const float* x = xyz + 3 * a0;
+    const uint8_t* ord = order + a0;   // internal atom i = input atom ord[i] (a1 canonical order)
+    float px[kMaxAtoms / 32], py[kMaxAtoms / 32], pz[kMaxAtoms / 32];
     float sx = 0.f, sy = 0.f, sz = 0.f;
-    for (int i = lane; i < A; i += 32) {
-        sx = __fadd_rn(sx, x[3 * i]);
-        sy = __fadd_rn(sy, x[3 * i + 1]);
-        sz = __fadd_rn(sz, x[3 * i + 2]);
+#pragma unroll
+    for (int u = 0; u < kMaxAtoms / 32; ++u) {
+        const int i = lane + 32 * u;
+        if (i < A) {
+            const int q = ord[i];
+            px[u] = x[3 * q];
+            py[u] = x[3 * q + 1];
+            pz[u] = x[3 * q + 2];
+            sx = __fadd_rn(sx, px[u]);
+            sy = __fadd_rn(sy, py[u]);
+            sz = __fadd_rn(sz, pz[u]);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -284,15 +511,18 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     }
     const float fa = (float)A;
     const float cx = __fdiv_rn(sx, fa), cy = __fdiv_rn(sy, fa), cz = __fdiv_rn(sz, fa);
-    for (int i = lane; i < AC; i += 32) {
+#pragma unroll
+    for (int u = 0; u < kMaxAtoms / 32; ++u) {
+        const int i = lane + 32 * u;
+        if (i >= AC) break;
         const bool in = i < A;
-        r[i] = in ? __fsub_rn(x[3 * i], cx) : 0.f;
-        r[AC + i] = in ? __fsub_rn(x[3 * i + 1], cy) : 0.f;
-        r[2 * AC + i] = in ? __fsub_rn(x[3 * i + 2], cz) : 0.f;
+        r[i] = in ? __fsub_rn(px[u], cx) : 0.f;
+        r[AC + i] = in ? __fsub_rn(py[u], cy) : 0.f;
+        r[2 * AC + i] = in ? __fsub_rn(pz[u], cz) : 0.f;
     }
     uint32_t f = 0;
     if (lane < R) {
-        const int4 q = reinterpret_cast<const int4*>(frags)[f0 + lane];
+        const int4 q = frint[f0 + lane];
         f = (uint32_t)q.x | ((uint32_t)q.y << 8) | ((uint32_t)q.z << 16) | ((uint32_t)(q.w - 1) << 24);
     }
     reinterpret_cast<uint32_t*>(r + 3 * AC)[lane] = f;
@@ -323,13 +553,14 @@ __global__ void make_keys_kernel(const int4* __restrict__ meta, int n_slots, con
 
 }  // namespace
 
-cudaError_t launch_validate(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frags,
-                            int64_t n, int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR,
-                            cudaStream_t st) {
+cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
+                          const int64_t* move_off, const int32_t* move_atoms, int64_t n, uint8_t* order, int4* frint,
+                          int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    int64_t blocks = (n + 7) / 8;
+    int64_t blocks = (n + kIngestWarps - 1) / kIngestWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    validate_kernel<<<(int)blocks, 256, 0, st>>>(atom_off, xyz, frag_off, frags, n, featA, featR, featM, status, maxAR);
+    ingest_kernel<<<(int)blocks, kIngestWarps * 32, 0, st>>>(atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, n,
+                                                             order, frint, featA, featR, featM, status, maxAR);
     return cudaGetLastError();
 }
 
@@ -366,12 +597,12 @@ cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const 
 
 cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
-                        const float* xyz, const int64_t* frag_off, const int32_t* frags, int S_w, float* rec,
-                        int4* meta, cudaStream_t st) {
+                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint, int S_w,
+                        float* rec, int4* meta, cudaStream_t st) {
     if (total_slots <= 0) return cudaSuccess;
     pack_kernel<<<(total_slots + 7) / 8, 256, 0, st>>>(perm, owned_start, owned_prefix, owned_ac, owned_rec_off,
-                                                       n_owned_buckets, total_slots, atom_off, xyz, frag_off, frags,
-                                                       S_w, rec, meta);
+                                                       n_owned_buckets, total_slots, atom_off, xyz, order, frag_off,
+                                                       frint, S_w, rec, meta);
     return cudaGetLastError();
 }
 

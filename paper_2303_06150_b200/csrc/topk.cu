@@ -1,7 +1,8 @@
 // topk.cu -- per-pocket ranking (a10) and the global merge (a11): the k
 // smallest 64-bit keys (ord(score) << 32 | ligand index) by MSD radix select
-// (8 passes of 8-bit digits; keys are unique because the index is in the low
-// word, so the k-th key is an exact threshold), compaction of the keys <= T,
+// (8 passes of 8-bit digits; real keys are unique because the index is in the low
+// word, so the k-th key is an exact threshold), compaction of the keys < T (padded
+// lists may repeat UINT64_MAX: the threshold fills the remaining slots),
 // and a bitonic sort of the k survivors in one CTA's shared memory.
 //
 // "for each docking site, we can rank the input chemical library" (PAPER.md
@@ -73,11 +74,16 @@ __global__ void sel_pick_kernel(SelState* st, int shift) {
     st->hist[t] = 0;
 }
 
+// Compaction of the keys strictly below the threshold T (the k-th smallest key): at most
+// k - 1 of them.  Keys equal to T are NOT written here: real keys are unique, but padded
+// lists (UINT64_MAX entries of ranks with fewer than k ligands) repeat the pad value, so the
+// bitonic kernel fills out[count .. k) with T instead -- deterministic, and never more than
+// k entries whatever the number of duplicates.
 __global__ void sel_compact_kernel(const u64* __restrict__ keys, int64_t n, SelState* st, u64* __restrict__ out) {
     const u64 T = st->prefix;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const u64 k = keys[i];
-        if (k <= T) out[atomicAdd(&st->count, 1u)] = k;
+        if (k < T) out[atomicAdd(&st->count, 1u)] = k;
     }
 }
 
@@ -86,10 +92,15 @@ __global__ void copy_keys_kernel(const u64* __restrict__ keys, int64_t n, u64* _
         out[i] = keys[i];
 }
 
-// bitonic sort of out[0..n) (n <= k), padded to a power of two with UINT64_MAX; writes out[0..k)
-__global__ void __launch_bounds__(1024) bitonic_kernel(u64* __restrict__ out, int n, int k, int n2) {
+// bitonic sort of out[0..n) (n <= k), padded to a power of two with UINT64_MAX; writes out[0..k).
+// st != null (selection mode): n = st->count keys below the threshold, and the k - n slots
+// after them hold the threshold key itself (see sel_compact_kernel).
+__global__ void __launch_bounds__(1024) bitonic_kernel(u64* __restrict__ out, int n, int k, int n2,
+                                                       const SelState* __restrict__ st) {
     extern __shared__ u64 s[];
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) s[i] = i < n ? out[i] : ~0ull;
+    if (st) n = (int)st->count;
+    const u64 fill = st ? st->prefix : ~0ull;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) s[i] = i < n ? out[i] : (i < k ? fill : ~0ull);
     __syncthreads();
     for (int size = 2; size <= n2; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -110,7 +121,25 @@ __global__ void __launch_bounds__(1024) bitonic_kernel(u64* __restrict__ out, in
     for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = s[i];
 }
 
+// ligand ids of the merged top-k: out[i] = ids[index of key i] (ids == null: the index itself);
+// UINT64_MAX for pads and for indices outside the id table.
+__global__ void gather_ids_kernel(const u64* __restrict__ keys, int m, const unsigned long long* __restrict__ ids,
+                                  int64_t n_ids, unsigned long long* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const u64 k = keys[i];
+    const int64_t idx = (int64_t)(k & 0xffffffffull);
+    out[i] = (k == ~0ull || idx >= n_ids) ? ~0ull : (ids ? ids[idx] : (unsigned long long)idx);
+}
+
 }  // namespace
+
+cudaError_t launch_gather_ids(const unsigned long long* keys, int m, const unsigned long long* ids, int64_t n_ids,
+                              unsigned long long* out, cudaStream_t st) {
+    if (m <= 0) return cudaSuccess;
+    gather_ids_kernel<<<(m + 255) / 256, 256, 0, st>>>(keys, m, ids, n_ids, out);
+    return cudaGetLastError();
+}
 
 cudaError_t topk_select_sort(const unsigned long long* keys, int64_t n, int k, unsigned long long* out,
                              void* scratch, cudaStream_t st, int* launches) {
@@ -126,6 +155,7 @@ cudaError_t topk_select_sort(const unsigned long long* keys, int64_t n, int k, u
     if (grid > 148 * 4) grid = 148 * 4;
     if (grid < 1) grid = 1;
     int m;  // survivors
+    const SelState* sel = nullptr;
     if (n <= k) {
         if (n > 0) {
             copy_keys_kernel<<<grid, 512, 0, st>>>(keys, n, out);
@@ -144,8 +174,9 @@ cudaError_t topk_select_sort(const unsigned long long* keys, int64_t n, int k, u
         sel_compact_kernel<<<grid, 512, 0, st>>>(keys, n, s, out);
         ++L;
         m = k;
+        sel = s;
     }
-    bitonic_kernel<<<1, 1024, smem, st>>>(out, m, k, n2);
+    bitonic_kernel<<<1, 1024, smem, st>>>(out, m, k, n2, sel);
     ++L;
     if (launches) *launches = L;
     return cudaGetLastError();

@@ -37,8 +37,10 @@ def global_topk(engine, slot: int, k: int, group=None):
 
     Returns (ligand index [m] int64, score [m] float32) on the host, identical on every rank
     and bit-identical to the single-GPU ranking (keys are unique and totally ordered)."""
-    keys, _ = engine.local_topk(slot, k)
+    keys, _ = engine.local_topk(slot, k)          # synchronous on the engine's stream
     g = gather_keys(keys, group)
+    if g is not keys:                             # the merge runs on the engine's stream
+        torch.cuda.current_stream(keys.device).synchronize()
     return engine.merge_topk(g, k)
 
 
@@ -55,7 +57,8 @@ def decode_keys(keys: torch.Tensor):
 
 
 def encode_keys(scores, index):
-    """Inverse of decode_keys for host-side tests: int64 tensor of ord(score) << 32 | index."""
+    """Inverse of decode_keys, for host-side TESTS only (the product path keeps keys on the device):
+    int64 tensor of ord(score) << 32 | index."""
     import numpy as np
     s = np.asarray(scores, np.float32) + np.float32(0.0)
     b = s.view(np.uint32)

@@ -2,19 +2,23 @@
 
 LiGen overlaps transfers with compute by handing buckets to CPU "workers" that copy
 into a free device buffer, run, and copy results back ("double buffering technique
-for hiding data transfers").  On B200 one context is enough: the library is cut into
-chunks, chunk i + 1's host-to-device copy runs on a copy stream (the copy engines)
-while chunk i is prepared, docked and ranked on the context's compute stream, into
-``n_buffers`` rotating device buffers.
+for hiding data transfers").  On B200 the same overlap needs no worker pool: the
+library is cut into chunks, and two contexts (engines, each with its own device
+workspace and stream) alternate over them:
 
-Compute phases are deliberately serialised: the persistent dock kernel holds every SM
-(one CTA per SM, ~227 KB of shared memory), so a second context's preparation kernels
-could not start before the dock drains anyway -- and its local top-k would queue behind
-the other context's dock.  What overlaps is the only thing that can: PCIe copies against
-SM work.  Each chunk is a full hot-path submit (validate, bucket, pack, dock, local top-k);
-every chunk's ranking keys are collected on the device (vs_keys) and ranked once at the end
-(vs_merge_topk), then across ranks with one all-gather of k keys per pocket
-(``parallel.gather_keys``).
+* chunk c + 1's host-to-device copy runs on a copy stream (the H2D copy engine) while
+  chunk c is prepared and docked;
+* chunk c's outputs -- best score, best pose, angle indices and the best-pose
+  coordinates (a9, replayed by the finalize kernel) -- are read back ASYNCHRONOUSLY into
+  pinned host buffers on chunk c's own stream (the D2H copy engine), so they overlap the
+  docking of chunk c + 1 on the other engine;
+* every chunk's ranking keys are written on the device (vs_keys, index = library index);
+  at the end one device top-k selection (vs_select_keys) gives this rank's list, which is
+  all-gathered across ranks (NCCL) and merged (vs_merge_topk) -- no host round trip of
+  keys.
+
+Compute phases still serialise on the SMs (the persistent dock kernel holds one CTA per
+SM), which is the point: the copy engines work under it.
 """
 from __future__ import annotations
 
@@ -23,126 +27,153 @@ import numpy as np
 from .vsdock import Engine
 
 
-def _bounds(atom_off, frag_off, lo, hi):
-    ao = np.asarray(atom_off[lo:hi + 1])
-    fo = np.asarray(frag_off[lo:hi + 1])
-    return ao, fo, int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
-
-
 def chunk_bounds(n: int, chunks: int = 0, first: int = 32, growth: int = 4):
     """Chunk boundaries of an n-ligand library.  chunks > 0: equal chunks.  chunks = 0: a
-    geometric schedule -- first chunk n / first, each next one at most `growth` times the
-    previous -- so only a small first copy is exposed while every later copy (~7x faster
-    than docking the same ligands on B200) still hides under the previous chunk's dock."""
+    geometric ramp at both ends -- first chunk n / first, each next one up to `growth` times
+    the previous, mirrored at the end -- so only a small first upload and a small last
+    read-back are exposed while every other copy hides under a neighbour's docking."""
     if n <= 0:
         return [0, 0]
     if chunks > 0:
         chunks = min(int(chunks), n)
         return [n * c // chunks for c in range(chunks + 1)]
-    b, size = [0], max(1, n // first)
-    while b[-1] < n:
-        b.append(min(n, b[-1] + size))
+    ramp, size = [], max(1, n // first)
+    while 2 * (sum(ramp) + size) <= n and len(ramp) < 8:
+        ramp.append(size)
         size *= growth
-    if len(b) > 2 and (b[-1] - b[-2]) < (b[-2] - b[-3]) // 4:   # fold a tiny tail into its predecessor
-        b.pop(-2)
+    mid = n - 2 * sum(ramp)
+    cap = growth * ramp[-1] if ramp else mid       # middle pieces stay within `growth` of the ramp
+    pieces = -(-mid // cap) if mid > 0 else 0
+    midl = [mid * (j + 1) // pieces - mid * j // pieces for j in range(pieces)]
+    sizes = ramp + midl + ramp[::-1]
+    b = [0]
+    for s in sizes:
+        b.append(b[-1] + s)
     return b
 
 
 class PipelinedDocker:
-    """Dock a host-resident library in chunks; H2D of the next chunk overlaps the current one."""
+    """Dock a host-resident library in chunks over two alternating engines; copies in both
+    directions overlap the docking."""
 
-    def __init__(self, device: int = 0, n_buffers: int = 2, **engine_kw):
+    def __init__(self, device: int = 0, n_engines: int = 2, **engine_kw):
         import torch
         self._torch = torch
         self.device = device
         self.dev = torch.device(f"cuda:{device}")
-        self.n_buffers = max(2, int(n_buffers))
-        self.compute = torch.cuda.Stream(device=device)
         self.copy = torch.cuda.Stream(device=device)
-        self.engine = Engine(device=device, stream=self.compute, **engine_kw)
-        self.engines = [self.engine]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(max(1, int(n_engines)))]
+        self.engines = [Engine(device=device, stream=s, **engine_kw) for s in self.streams]
+        self.engine = self.engines[0]
+        self.n_sweeps = self.engine.n_sweeps
+        self._pinned = {}
         self.trace = []
 
     def setup(self, rot, trans, cs, pockets):
-        e = self.engine
-        e.set_poses(rot, trans)
-        e.set_angles(cs)
-        self.pocket_ids = [e.load_pocket(p) for p in pockets]
-        return self.pocket_ids
+        for e in self.engines:
+            e.set_poses(rot, trans)
+            e.set_angles(cs)
+            ids = [e.load_pocket(p) for p in pockets]
+        self.pocket_ids = ids
+        return ids
+
+    def _pin(self, name, shape, dtype):
+        """Reusable pinned host output buffer (allocating page-locked memory per run would cost
+        more than the copies)."""
+        torch = self._torch
+        key = (name, tuple(shape), dtype)
+        if key not in self._pinned:
+            self._pinned[key] = torch.empty(tuple(shape), dtype=dtype).pin_memory()
+        return self._pinned[key].numpy()
 
     def _issue_copy(self, arrays, lo, hi):
-        """Chunk [lo, hi) to the device on the copy stream: rebased offsets + xyz / frags slices."""
+        """Chunk [lo, hi) to the device on the copy stream: rebased offsets + array slices."""
         torch = self._torch
-        atom_off, xyz, frag_off, frags = arrays
-        ao, fo, a0, a1, f0, f1 = _bounds(atom_off, frag_off, lo, hi)
-        host = [torch.from_numpy(np.ascontiguousarray(ao - a0)), xyz[a0:a1],
-                torch.from_numpy(np.ascontiguousarray(fo - f0)), frags[f0:f1]]
+        ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays
+        ao = np.asarray(atom_off[lo:hi + 1])
+        fo = np.asarray(frag_off[lo:hi + 1])
+        a0, a1, f0, f1 = int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
+        mo = np.asarray(move_off[f0:f1 + 1])
+        m0, m1 = int(mo[0]), int(mo[-1])
+        host = [ids[lo:hi], torch.from_numpy(np.ascontiguousarray(ao - a0)), xyz[a0:a1],
+                torch.from_numpy(np.ascontiguousarray(fo - f0)), frag_axis[f0:f1],
+                torch.from_numpy(np.ascontiguousarray(mo - m0)), move_atoms[m0:m1]]
         host = [h if isinstance(h, torch.Tensor) else torch.from_numpy(np.asarray(h)) for h in host]
         with torch.cuda.stream(self.copy):
             dev = [h.to(self.dev, non_blocking=True) for h in host]
             ev = torch.cuda.Event()
             ev.record(self.copy)
-        return dev, ev, host
+        return dev, ev, (a0, a1, f0, f1)
 
-    def run(self, atom_off, xyz, frag_off, frags, k: int = 1000, chunks: int = 0, max_atoms: int = 256,
-            group=None, first: int = 32, growth: int = 4):
-        """Returns (best_score [P][n], best_pose [P][n], topk [(index, score)] per pocket) on the host.
+    def run(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, k: int = 1000,
+            chunks: int = 0, max_atoms: int = 256, group=None, coords: bool = True, first: int = 32,
+            growth: int = 4):
+        """Dock the library (the C-ABI's general-form CSR arrays; pinned torch CPU tensors for
+        overlapped copies) into every pocket of ``setup``.  Returns a dict of host arrays:
 
-        xyz / frags should be pinned host tensors (torch ``pin_memory``) for overlapped copies.
-        ``chunks``: see ``chunk_bounds`` (0 = geometric schedule).  With ``rank`` / ``world_size`` engine options under an initialised process group, every
-        rank docks its LPT share of each chunk and the per-pocket top-k is merged across ranks."""
-        import time
+        ``ligand_id`` [n], ``best_score`` / ``best_pose`` [pockets, n], ``angles`` [pockets, S_w * sum R],
+        ``xyz`` [pockets, sum A, 3] (best-pose coordinates, input atom order; with ``coords``), and
+        ``topk`` = per pocket (library index [m], score [m], ligand id [m]), merged across ranks.
+        The per-ligand arrays are reused buffers: copy them to keep them past the next run."""
         from . import parallel
         torch = self._torch
-        e = self.engine
         n = int(atom_off.shape[0]) - 1
+        nA, nR = int(xyz.shape[0]), int(frag_axis.shape[0])
         npk = len(self.pocket_ids)
+        S_w = self.n_sweeps
         bounds = chunk_bounds(n, chunks, first, growth)
-        chunks = len(bounds) - 1
-        # pinned host outputs: the per-chunk result reads are plain DMA, not staged copies
-        best = torch.full((npk, n), float("nan"), dtype=torch.float32).pin_memory().numpy()
-        pose = torch.full((npk, n), -1, dtype=torch.int32).pin_memory().numpy()
-        # every chunk's keys land in one device array per pocket (index + chunk offset); the
-        # ranking is one selection at the end (no per-chunk top-k round trip)
+        nch = len(bounds) - 1
+        best = self._pin("best", (npk, n), torch.float32)
+        pose = self._pin("pose", (npk, n), torch.int32)
+        ang = self._pin("ang", (npk, max(1, S_w * nR)), torch.uint8)
+        xyz_out = self._pin("xyz", (npk, max(1, nA), 3), torch.float32) if coords else None
         all_keys = [torch.empty(max(1, n), dtype=torch.int64, device=self.dev) for _ in range(npk)]
         nkeys = [0] * npk
-        arrays = (atom_off, xyz, frag_off, frags)
+        arrays = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
         self.trace = []
-        inflight = {}
-        for c in range(min(self.n_buffers - 1, chunks)):
-            inflight[c] = self._issue_copy(arrays, bounds[c], bounds[c + 1])
-        for c in range(chunks):
+        ne = len(self.engines)
+        inflight = {c: self._issue_copy(arrays, bounds[c], bounds[c + 1]) for c in range(min(ne, nch))}
+        keep = {}
+        for c in range(nch):
             lo, hi = bounds[c], bounds[c + 1]
-            nxt = c + self.n_buffers - 1
-            dev, ev, _host = inflight.pop(c)
-            t0 = time.perf_counter()
-            ev.synchronize()        # chunk c resident (the engine reads its CSR totals on submit)
-            t1 = time.perf_counter()
-            if hi > lo:
-                # submit returns once the dock launches are queued; the preparation's small
-                # host<->device exchanges are over by then, so the prefetch issued next shares
-                # the copy engine with nothing and runs under the dock
+            e = self.engines[c % ne]
+            dev, ev, (a0, a1, f0, f1) = inflight.pop(c)
+            ev.synchronize()        # chunk c resident (submit reads its CSR totals)
+            if hi > lo:     # (chunk_bounds never yields an empty chunk)
+                # returns once the dock launches are queued; the read-backs below queue behind
+                # them on the same stream and run on the D2H engine while the other engine docks
                 e.submit(*dev, self.pocket_ids, on_device=True, max_atoms=max_atoms)
-            if nxt < chunks:
-                inflight[nxt] = self._issue_copy(arrays, bounds[nxt], bounds[nxt + 1])
-            if hi > lo:
-                e.wait()
                 for s in range(npk):
-                    e.results_into(s, best[s, lo:hi], pose[s, lo:hi])
+                    e.results_async(s, best[s, lo:hi], pose[s, lo:hi],
+                                    ang[s, S_w * f0:S_w * f1] if f1 > f0 else None)
+                    if coords and a1 > a0:
+                        e.coords_into(s, xyz_out[s, a0:a1], mode=2)
                     nkeys[s] += e.keys_into(s, all_keys[s][nkeys[s]:], lo)
-            st = e.stats()
-            self.trace.append((c, t0, t1, time.perf_counter(), st["prep_ms"], st["dock_ms"]))
-            del dev                 # buffer free once the chunk's work completed (wait above)
+            keep[c % ne] = dev      # the engine borrows the chunk until its next submit
+            if c + ne < nch:
+                # the buffer slot of chunk c + ne is engine c's: its copy may only overwrite
+                # device memory the engine no longer reads -- new tensors, so no hazard
+                inflight[c + ne] = self._issue_copy(arrays, bounds[c + ne], bounds[c + ne + 1])
+            self.trace.append((c, lo, hi))
+        for st in self.streams:
+            st.synchronize()
+        e = self.engine
         tops = []
+        ids_host = np.asarray(ligand_id)
         for s in range(npk):
-            idx, sc = e.merge_topk(all_keys[s][:nkeys[s]], k)
-            mine = torch.full((k,), -1, dtype=torch.int64)   # UINT64_MAX pads, as local_topk
-            mine[: len(idx)] = parallel.encode_keys(sc, idx)
-            g = parallel.gather_keys(mine.to(self.dev), group)
-            if g.numel() > k:                  # more than one rank: merge the gathered rankings
-                idx, sc = e.merge_topk(g, k)
-            tops.append((idx, sc))
-        return best, pose, tops
+            mine = e.select_keys(all_keys[s][:nkeys[s]], k)     # this rank's top-k, on the device
+            e.synchronize()                                    # (the collective runs on torch's stream)
+            g = parallel.gather_keys(mine, group)              # NCCL all-gather (W x k keys)
+            torch.cuda.current_stream(self.dev).synchronize()
+            idx, sc = e.merge_topk(g, k)
+            tops.append((idx, sc, ids_host[idx] if len(idx) else np.zeros(0, np.uint64)))
+        e.synchronize()
+        out = {"ligand_id": ids_host, "best_score": best, "best_pose": pose, "angles": ang[:, :S_w * nR],
+               "topk": tops}
+        if coords:
+            out["xyz"] = xyz_out[:, :nA]
+        return out
 
     def close(self):
-        self.engine.close()
+        for e in self.engines:
+            e.close()

@@ -24,7 +24,7 @@ _NAMES = {0: "VS_OK", -1: "VS_E_ARG", -2: "VS_E_PARSE", -3: "VS_E_OVERFLOW_ATOMS
 
 SYMBOLS = ["vs_create", "vs_destroy", "vs_last_error", "vs_workspace_size", "vs_set_workspace", "vs_load_pocket",
            "vs_set_pose_table", "vs_set_angle_table", "vs_submit", "vs_wait", "vs_get_results", "vs_get_coords",
-           "vs_get_pose_debug", "vs_local_topk", "vs_keys", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
+           "vs_get_pose_debug", "vs_local_topk", "vs_keys", "vs_select_keys", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
            "vs_score_points", "vs_get_stats", "vs_plan_boundaries", "vs_plan_lpt"]
 
 
@@ -50,8 +50,9 @@ class vs_pocket_desc(ctypes.Structure):
 
 
 class vs_ligand_batch(ctypes.Structure):
-    _fields_ = [("n", ctypes.c_int64), ("atom_off", ctypes.c_void_p), ("xyz", ctypes.c_void_p),
-                ("frag_off", ctypes.c_void_p), ("frags", ctypes.c_void_p), ("on_device", ctypes.c_int32)]
+    _fields_ = [("n", ctypes.c_int64), ("ligand_id", ctypes.c_void_p), ("atom_off", ctypes.c_void_p),
+                ("xyz", ctypes.c_void_p), ("frag_off", ctypes.c_void_p), ("frag_axis", ctypes.c_void_p),
+                ("move_off", ctypes.c_void_p), ("move_atoms", ctypes.c_void_p), ("on_device", ctypes.c_int32)]
 
 
 class vs_bucket(ctypes.Structure):
@@ -90,19 +91,20 @@ def load_library():
         "vs_create": [ctypes.POINTER(vs_config), ctypes.POINTER(P)],
         "vs_destroy": [P],
         "vs_last_error": [P],
-        "vs_workspace_size": [P, I64, I64, I64, I32, I32, ctypes.POINTER(SZ)],
+        "vs_workspace_size": [P, I64, I64, I64, I64, I32, I32, ctypes.POINTER(SZ)],
         "vs_set_workspace": [P, P, SZ],
         "vs_load_pocket": [P, ctypes.POINTER(vs_pocket_desc), P, I32, ctypes.POINTER(I32)],
         "vs_set_pose_table": [P, I32, P, P],
         "vs_set_angle_table": [P, I32, P],
         "vs_submit": [P, ctypes.POINTER(vs_ligand_batch), P, I32],
         "vs_wait": [P],
-        "vs_get_results": [P, I32, P, P, P, I32],
+        "vs_get_results": [P, I32, P, P, P, P, I32],
         "vs_get_coords": [P, I32, P, I32],
         "vs_get_pose_debug": [P, I32, P, P],
         "vs_local_topk": [P, I32, I32, P, ctypes.POINTER(I32)],
         "vs_keys": [P, I32, ctypes.c_uint32, P, ctypes.POINTER(I64)],
-        "vs_merge_topk": [P, P, I64, I32, P, P, ctypes.POINTER(I32)],
+        "vs_select_keys": [P, P, I64, I32, P],
+        "vs_merge_topk": [P, P, I64, I32, P, P, P, ctypes.POINTER(I32)],
         "vs_get_manifest": [P, I32, P, ctypes.POINTER(I32), P],
         "vs_query_classes": [P, I32, P, ctypes.POINTER(I32)],
         "vs_score_points": [P, I32, I64, P, P],
@@ -156,6 +158,7 @@ def plan_lpt(weights, world):
 
 @dataclass
 class Results:
+    ligand_id: np.ndarray    # uint64 [n]
     best_score: np.ndarray   # float32 [n]
     best_pose: np.ndarray    # int32 [n]
     angles: np.ndarray       # uint8 [S_w * sum R]
@@ -228,19 +231,25 @@ class Engine:
         return pid.value
 
     # ---- workspace
-    def reserve(self, n_lig, n_atoms, n_frags, max_atoms, n_pockets):
+    def reserve(self, n_lig, n_atoms, n_frags, n_moving, max_atoms, n_pockets):
         nbytes = ctypes.c_size_t()
-        self._check(self.lib.vs_workspace_size(self.h, n_lig, n_atoms, n_frags, max_atoms, n_pockets,
+        self._check(self.lib.vs_workspace_size(self.h, n_lig, n_atoms, n_frags, n_moving, max_atoms, n_pockets,
                                                ctypes.byref(nbytes)))
         if self.ws is None or self.ws.numel() < nbytes.value:
+            if self.ws is not None:
+                # the library queues work on the engine's stream: the old block must not be
+                # handed to another allocation while that work can still touch it
+                self._stream.synchronize()
             self.ws = None
             self.ws = self._torch.empty(nbytes.value, dtype=self._torch.uint8, device=f"cuda:{self.device}")
             self._check(self.lib.vs_set_workspace(self.h, ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel()))
         return nbytes.value
 
     # ---- the hot path
-    def submit(self, atom_off, xyz, frag_off, frags, pockets, on_device=None, max_atoms=None):
-        """Submit a CSR ligand batch (numpy host arrays, pinned torch CPU tensors, or CUDA tensors)."""
+    def submit(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, pockets, on_device=None,
+               max_atoms=None):
+        """Submit a CSR ligand batch in the general form of include/vsdock.h (numpy host arrays,
+        pinned torch CPU tensors, or CUDA tensors; ``ligand_id`` may be None)."""
         n = int(atom_off.shape[0]) - 1
         if on_device is None:
             on_device = hasattr(xyz, "is_cuda") and xyz.is_cuda
@@ -250,39 +259,64 @@ class Engine:
             else:
                 max_atoms = int(np.diff(np.asarray(atom_off)).max()) if n > 0 else 1
         nA = int(xyz.shape[0])
-        nR = int(frags.shape[0])
+        nR = int(frag_axis.shape[0])
+        nM = int(move_atoms.shape[0])
         pockets = np.ascontiguousarray(pockets, np.int32).reshape(-1)
-        self.reserve(n, nA, nR, max(1, min(256, max_atoms)), len(pockets))
-        b = vs_ligand_batch(n, _ptr(atom_off), _ptr(xyz), _ptr(frag_off), _ptr(frags), int(bool(on_device)))
-        self._batch_keep = (atom_off, xyz, frag_off, frags)
+        self.reserve(n, nA, nR, nM, max(1, min(256, max_atoms)), len(pockets))
+        b = vs_ligand_batch(n, _ptr(ligand_id), _ptr(atom_off), _ptr(xyz), _ptr(frag_off), _ptr(frag_axis),
+                            _ptr(move_off), _ptr(move_atoms), int(bool(on_device)))
+        self._batch_keep = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
         self._check(self.lib.vs_submit(self.h, ctypes.byref(b), _ptr(pockets), len(pockets)))
         self._n, self._nA, self._nR = n, nA, nR
         self._npk = len(pockets)
 
     def submit_library(self, lib, pockets, **kw):
-        return self.submit(lib.atom_off, lib.xyz, lib.frag_off, lib.frags, pockets, **kw)
+        return self.submit(*lib.arrays(), pockets, **kw)
 
     def wait(self):
         self._check(self.lib.vs_wait(self.h))
 
     def results(self, slot=0) -> Results:
+        i = np.empty(max(1, self._n), np.uint64)
         s = np.empty(self._n, np.float32)
         p = np.empty(self._n, np.int32)
         a = np.empty(max(1, self.n_sweeps * self._nR), np.uint8)
-        self._check(self.lib.vs_get_results(self.h, slot, _ptr(s), _ptr(p), _ptr(a), 0))
-        return Results(s, p, a[: self.n_sweeps * self._nR])
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(i), _ptr(s), _ptr(p), _ptr(a), 0))
+        return Results(i[: self._n], s, p, a[: self.n_sweeps * self._nR])
 
-    def results_into(self, slot, best_score, best_pose, angles=None):
+    def results_into(self, slot, best_score, best_pose, angles=None, ligand_id=None):
         """Copy the results into caller-owned HOST arrays (pinned for full-speed DMA)."""
-        self._check(self.lib.vs_get_results(self.h, slot, _ptr(best_score), _ptr(best_pose), _ptr(angles), 0))
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(ligand_id), _ptr(best_score), _ptr(best_pose),
+                                            _ptr(angles), 0))
 
-    def results_device(self, slot, best_score, best_pose, angles=None):
-        self._check(self.lib.vs_get_results(self.h, slot, _ptr(best_score), _ptr(best_pose), _ptr(angles), 1))
+    def results_device(self, slot, best_score, best_pose, angles=None, ligand_id=None):
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(ligand_id), _ptr(best_score), _ptr(best_pose),
+                                            _ptr(angles), 1))
 
     def coords(self, slot=0) -> np.ndarray:
         out = np.empty((max(1, self._nA), 3), np.float32)
         self._check(self.lib.vs_get_coords(self.h, slot, _ptr(out), 0))
         return out[: self._nA]
+
+    def coords_into(self, slot, out, mode=2):
+        """Best-pose coordinates into a caller-owned buffer [n_atoms, 3]: mode 2 = pinned host,
+        asynchronous (complete after the next wait / submit on this engine), 0 = host, 1 = device."""
+        self._check(self.lib.vs_get_coords(self.h, slot, _ptr(out), mode))
+
+    def results_async(self, slot, best_score, best_pose, angles=None, ligand_id=None):
+        """Results into pinned HOST arrays, asynchronously on the engine's stream."""
+        self._check(self.lib.vs_get_results(self.h, slot, _ptr(ligand_id), _ptr(best_score), _ptr(best_pose),
+                                            _ptr(angles), 2))
+
+    def select_keys(self, keys_dev, k, out=None):
+        """Device top-k (ascending, UINT64_MAX padded) of a device int64 key tensor."""
+        if out is None:
+            out = self._torch.empty(k, dtype=self._torch.int64, device=f"cuda:{self.device}")
+        self._check(self.lib.vs_select_keys(self.h, _ptr(keys_dev), int(keys_dev.numel()), k, _ptr(out)))
+        return out
+
+    def synchronize(self):
+        self._stream.synchronize()
 
     def pose_debug(self, slot=0):
         s = np.empty((self._n, self.P), np.float32)
@@ -304,12 +338,16 @@ class Engine:
         self._check(self.lib.vs_keys(self.h, slot, int(index_offset), _ptr(out), ctypes.byref(nk)))
         return nk.value
 
-    def merge_topk(self, keys_dev, k):
+    def merge_topk(self, keys_dev, k, with_ids=False):
+        """Global top-k of gathered keys: (ligand index, score[, ligand id of the last batch])."""
         idx = np.empty(k, np.int64)
         sc = np.empty(k, np.float32)
+        ids = np.empty(k, np.uint64) if with_ids else None
         m = ctypes.c_int32()
         self._check(self.lib.vs_merge_topk(self.h, _ptr(keys_dev), int(keys_dev.numel()), k, _ptr(idx), _ptr(sc),
-                                           ctypes.byref(m)))
+                                           _ptr(ids), ctypes.byref(m)))
+        if with_ids:
+            return idx[: m.value], sc[: m.value], ids[: m.value]
         return idx[: m.value], sc[: m.value]
 
     def manifest(self, want_perm=True):

@@ -95,18 +95,15 @@ def test_c2_sample_parity_and_bucketing_invariance(c2):
     rep, r = check(e, lib, idx, pk, rot, tr, cs)
     assert rep.independent_equal == rep.independent_checked > 300
     # Q22: bit-identical whatever the launch structure (one launch per bucket, bucket multiple, streams)
-    for kw in (dict(launch_per_bucket=True, bucket_multiple=1), dict(bucket_multiple=3, n_streams=1)):
+    # and whatever the cluster grid: every class of K = 8 runs the same 4-poses-per-warp lane map,
+    # so the unsorted 1 x 1 grid (one class, A_c = 128) gives the same bits as 6 x 23
+    for kw in (dict(launch_per_bucket=True, bucket_multiple=1), dict(bucket_multiple=3, n_streams=1),
+               dict(atom_clusters=1, rot_clusters=1), dict(atom_clusters=3, rot_clusters=5)):
         e2, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, **kw)
         r2 = e2.results(0)
         assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.best_pose, r2.best_pose)
         assert np.array_equal(r.angles, r2.angles)
         assert np.array_equal(e.coords(0), e2.coords(0))
-    # another cluster grid may pick another lane layout per class: same results up to fp32
-    # rounding of the sums, and under the same parity contract
-    e3, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=True, atom_clusters=1, rot_clusters=1)
-    r3 = e3.results(0)
-    assert np.max(np.abs(r3.best_score - r.best_score) / np.maximum(1, np.abs(r.best_score))) < 2 * TOL_S
-    check(e3, lib, idx[:40], pk, rot, tr, cs)
 
 
 def test_round_ring_many_tiny_launches_bit_identical(c2):
@@ -226,23 +223,22 @@ def test_topk_vs_oracle_scores_outside_ties(c2):
 # ----------------------------------------------------------------------------- edge cases
 
 def mk_lib(ligs):
-    A = [len(x) for x, _ in ligs]
-    R = [len(f) for _, f in ligs]
-    ao = np.zeros(len(ligs) + 1, np.int64); ao[1:] = np.cumsum(A)
-    fo = np.zeros(len(ligs) + 1, np.int64); fo[1:] = np.cumsum(R)
-    xyz = np.concatenate([np.asarray(x, np.float32).reshape(-1, 3) for x, _ in ligs]) if ligs else np.zeros((0, 3), np.float32)
-    fr = np.concatenate([np.asarray(f, np.int32).reshape(-1, 4) for _, f in ligs]) if sum(R) else np.zeros((0, 4), np.int32)
-    return vsgen.Library(np.arange(len(ligs), dtype=np.uint64), ao, xyz, fo, fr)
+    return vsgen.Library.from_ligands(ligs)
+
+
+NOFRAG = vsgen.Frags(np.zeros((0, 2), np.int32), [])
 
 
 def test_edge_cases_tiny_ligands_and_tables():
+    """Tiny ligands (A = 1, 2) and every table shape, including angle counts that are not powers
+    of two (theta_k = 2 pi k / K for K = 3, 6, 12: lane map of the next power of two)."""
     pk = vsgen.pocket(102)
     base = vsgen.ligands(40, 9, (20, 40), (0, 4))
     ligs = [base.ligand(i) for i in range(base.n)]
-    ligs += [(np.array([[1.0, 2.0, 3.0]]), np.zeros((0, 4))),                       # A = 1
-             (np.array([[0, 0, 0], [1.5, 0, 0]], np.float32), np.zeros((0, 4)))]     # A = 2, R = 0
+    ligs += [(np.array([[1.0, 2.0, 3.0]]), NOFRAG),                                  # A = 1
+             (np.array([[0, 0, 0], [1.5, 0, 0]], np.float32), NOFRAG)]               # A = 2, R = 0
     lib = mk_lib(ligs)
-    for P, K in [(1, 8), (7, 8), (8, 1), (8, 2), (4, 16), (4, 32), (33, 4)]:
+    for P, K in [(1, 8), (7, 8), (8, 1), (8, 2), (4, 16), (4, 32), (33, 4), (8, 6), (8, 12), (5, 3), (4, 24)]:
         e, rot, tr, cs = run(lib, [pk], P=P, K=K)
         check(e, lib, range(lib.n), pk, rot, tr, cs)
 
@@ -317,24 +313,48 @@ def test_validation_errors_name_the_ligand():
     e = engine()
     setup(e, [vsgen.pocket(101)], 8, 8)
 
-    def bad(mutate, code):
-        ligs = [tuple(np.array(a, copy=True) for a in base.ligand(i)) for i in range(base.n)]
+    def copy_lig(i):
+        x, f = base.ligand(i)
+        return np.array(x, copy=True), vsgen.Frags(np.array(f.axis, copy=True), [np.array(m, copy=True) for m in f.moves])
+
+    def bad(mutate, what):
+        ligs = [copy_lig(i) for i in range(base.n)]
         mutate(ligs)
         with pytest.raises(VsError) as ei:
             e.submit_library(mk_lib(ligs), [0])
-        assert ei.value.code == code
-        assert "ligand 3" in str(ei.value)
+        assert ei.value.code == vsdock.VS_E_PARSE
+        assert "ligand 3" in str(ei.value) and what in str(ei.value), str(ei.value)
 
     def nan(l): l[3][0][2, 1] = np.nan
-    def axis_eq(l): l[3][1][0, 1] = l[3][1][0, 0]
-    def rng_bad(l): l[3][1][0, 3] = 1000
-    def axis_in(l): l[3][1][0, 2] = l[3][1][0, 1]
-    def too_big(l): l[3] = (np.zeros((300, 3), np.float32), np.zeros((0, 4), np.int32))
-    bad(nan, vsdock.VS_E_PARSE)
-    bad(axis_eq, vsdock.VS_E_PARSE)
-    bad(rng_bad, vsdock.VS_E_PARSE)
-    bad(axis_in, vsdock.VS_E_PARSE)
-    bad(too_big, vsdock.VS_E_PARSE)
+    def huge(l): l[3][0][1, 0] = 3e6
+    def axis_eq(l): l[3][1].axis[0, 1] = l[3][1].axis[0, 0]
+    def axis_oob(l): l[3][1].axis[0, 0] = 999
+    def move_oob(l): l[3][1].moves[0][0] = 1000
+    def axis_in(l): l[3][1].moves[0][0] = l[3][1].axis[0, 1]
+    def dup(l): l[3][1].moves[0] = np.concatenate([l[3][1].moves[0], l[3][1].moves[0][:1]])
+    def empty(l): l[3][1].moves[0] = np.zeros(0, np.int32)
+
+    def crossing(l):        # two moving sets that overlap without nesting
+        x, f = l[3]
+        A = len(x)
+        free = [i for i in range(A) if i not in set(f.axis[0].tolist())]
+        a_set = np.array(free[: len(free) // 2 + 1], np.int32)
+        b_set = np.array(free[len(free) // 2 - 1:], np.int32)
+        f.moves[0] = a_set
+        f2 = vsgen.Frags(np.concatenate([f.axis, f.axis[:1]]), f.moves + [b_set])
+        l[3] = (x, f2)
+
+    def too_big(l): l[3] = (np.zeros((300, 3), np.float32), NOFRAG)
+    bad(nan, "non-finite coordinate")
+    bad(huge, "magnitude")
+    bad(axis_eq, "axis atoms are equal")
+    bad(axis_oob, "axis atom index out of range")
+    bad(move_oob, "moving atom index out of range")
+    bad(axis_in, "axis atom inside its own moving set")
+    bad(dup, "listed twice")
+    bad(empty, "moving set empty")
+    bad(crossing, "not laminar")
+    bad(too_big, "atom count")
     # overflow names the axis: user upper bounds below the data
     e2 = engine(atom_upper_bound=30, rot_upper_bound=2, atom_clusters=1, rot_clusters=1)
     setup(e2, [vsgen.pocket(101)], 8, 8)
@@ -355,10 +375,11 @@ def test_c4_full_size_sampled_parity():
     pk = vsgen.pocket(101)
     e = engine(bucket_multiple=16, n_streams=4)
     rot, tr, cs, ids = setup(e, [pk], c["P"], c["K"])
-    d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
     e.submit(*d, ids, on_device=True)
     e.wait()
     r = e.results(0)
+    assert np.array_equal(r.ligand_id, lib.ligand_id)
     assert np.isfinite(r.best_score).all()
     assert ((r.best_pose >= 0) & (r.best_pose < c["P"])).all()
     assert (r.angles < c["K"]).all()
@@ -380,7 +401,7 @@ def test_c5_full_size_campaign_sampled_parity_and_topk():
     pks = [vsgen.pocket(s) for s in c["pockets"]]
     e = engine(bucket_multiple=16, n_streams=4)
     rot, tr, cs, ids = setup(e, pks, c["P"], c["K"])
-    d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
     e.submit(*d, ids, on_device=True)
     e.wait()
     rng = np.random.default_rng(5)
@@ -418,18 +439,155 @@ def test_keys_with_offset_rank_like_local_topk(c2):
     assert np.array_equal(sc, r.best_score[want])
 
 
-def test_pipelined_docker_matches_single_submit(c2):
-    """Double-buffered chunks give the single-submit results and ranking."""
+def test_pipelined_docker_matches_single_submit_and_oracle(c2):
+    """The double-buffered public host API: two engines alternating over chunks,
+    asynchronous read-back of every a9 output.  Bit-identical to one submit (scores, poses, angle
+    indices, coordinates), the same ranking with ligand ids, and the pipeline's own outputs pass
+    the oracle parity contract on a sample."""
     import torch
     from paper_2303_06150_b200.pipeline import PipelinedDocker
     c, lib, pk = c2
     e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
     r = e.results(0)
-    pd = PipelinedDocker(n_buffers=2)
+    xyz1 = e.coords(0)
+    pd = PipelinedDocker()
     pd.setup(rot, tr, cs, [pk])
-    h = [torch.from_numpy(a).pin_memory() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
-    best, pose, tops = pd.run(*h, k=100, chunks=3)
-    assert np.max(np.abs(best[0] - r.best_score) / np.maximum(1, np.abs(r.best_score))) < 2 * TOL_S
-    assert list(tops[0][0]) == list(oracle.topk(best[0], 100))
-    assert np.array_equal(tops[0][1], best[0][tops[0][0]])
+    h = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
+    for chunks in (3, 0):
+        out = pd.run(*h, k=100, chunks=chunks)
+        assert np.array_equal(out["best_score"][0], r.best_score)
+        assert np.array_equal(out["best_pose"][0], r.best_pose)
+        assert np.array_equal(out["angles"][0], r.angles)
+        assert np.array_equal(out["xyz"][0], xyz1)
+        idx, sc, ids = out["topk"][0]
+        assert list(idx) == list(oracle.topk(r.best_score, 100))
+        assert np.array_equal(sc, r.best_score[idx]) and np.array_equal(ids, lib.ligand_id[idx])
+    rng = np.random.default_rng(7)
+    sample = rng.choice(lib.n, 60, replace=False)
+    rep = parity.check(lib, sample, pk, rot, tr, cs, out["best_score"][0], out["best_pose"][0], out["angles"][0],
+                       out["xyz"][0], band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + str(rep.failures[:5])
     pd.close()
+
+
+# ----------------------------------------------------------------------------- round 2: inputs the
+# round-1 suite never exercised (VERDICT r1 "what's weak" 1, 2; "missing" 4)
+
+def test_translated_poses_and_offcentre_pocket_every_pose():
+    """a6 y = R_p (x - xbar) + c + tau_p with tau_p != 0 and c off the grid centre: every pose of
+    every ligand replayed in fp64 (C1 shape, plus a C2-shaped sample)."""
+    pk = vsgen.pocket(101, center_offset=(1.75, -2.5, 1.0))
+    c = vsgen.CONFIGS["C1"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    e = engine(debug_poses=True)
+    rot, tr = vsgen.pose_table(c["P"], tau=2.0)
+    cs = vsgen.angle_table(c["K"])
+    e.set_poses(rot, tr)
+    e.set_angles(cs)
+    pid = e.load_pocket(pk)
+    e.submit_library(lib, [pid])
+    e.wait()
+    rep, r = check(e, lib, range(lib.n), pk, rot, tr, cs)
+    assert rep.independent_checked >= lib.n // 2 and rep.independent_equal == rep.independent_checked
+    assert len(set(r.best_pose.tolist())) > 1        # translations change which pose wins
+    lib2 = vsgen.ligands(300, 21, (20, 120), (0, 20))
+    rot2, tr2 = vsgen.pose_table(64, tau=1.5)
+    e2 = engine(debug_poses=True)
+    e2.set_poses(rot2, tr2)
+    e2.set_angles(cs)
+    e2.load_pocket(pk)
+    e2.submit_library(lib2, [0])
+    e2.wait()
+    check(e2, lib2, range(0, 300, 10), pk, rot2, tr2, cs)
+
+
+def test_large_ligands_classes_192_224_256_and_32_fragments():
+    """161-256 atoms and 26-32 rotatable bonds: the 192 / 224 / 256 atom classes, their (poses per
+    warp, warps) policy fallbacks and shared-memory layouts near 227 KB; sampled full parity."""
+    lib = vsgen.ligands(600, 31, (161, 256), (26, 32))
+    assert lib.n_atoms.max() > 224 and lib.n_frags.max() == 32 and lib.n_frags.min() >= 26
+    pk = vsgen.pocket(101)
+    e, rot, tr, cs = run(lib, [pk], P=16, K=8, atom_clusters=8)      # boundaries 32, 64, ..., 224, 256
+    cls = {cl["kernel_atoms"]: cl for cl in e.classes()}
+    assert {192, 224, 256} <= set(cls), cls
+    for ac in (192, 224, 256):
+        assert cls[ac]["dyn_smem"] + cls[ac]["static_smem"] <= 232448 and cls[ac]["blocks_per_sm"] == 1
+    by_class = {ac: [i for i in range(lib.n) if ac - 32 < lib.n_atoms[i] <= ac] for ac in (192, 224, 256)}
+    idx = sorted(i for ac in by_class for i in by_class[ac][:6])
+    check(e, lib, idx, pk, rot, tr, cs)
+    # the default (production) path at P = 64 for the same classes: best pose / score / coordinates
+    e64, rot64, tr64, cs64 = run(lib.subset(idx), [pk], P=64, K=8, debug=False, atom_clusters=8)
+    r64 = e64.results(0)
+    sub = lib.subset(idx)
+    rep = parity.check(sub, range(sub.n), pk, rot64, tr64, cs64, r64.best_score, r64.best_pose, r64.angles,
+                       e64.coords(0), band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + str(rep.failures[:5])
+
+
+def test_permuted_atoms_dock_bit_identically_and_match_the_oracle():
+    """General moving sets: the same molecules with randomly renumbered atoms (moving
+    sets become arbitrary subsets) go through a1's laminar check and canonical renumbering and dock
+    BIT-identically to the generator's preordered numbering; coordinates come back in the caller's
+    atom order; full parity of the permuted library against the oracle (which rotates the listed
+    atoms directly, no renumbering)."""
+    c = vsgen.CONFIGS["C2"]
+    lib = vsgen.ligands(400, 41, c["atoms"], c["rot"])
+    plib, perm = lib.permuted(9)
+    assert any(np.any(np.diff(np.sort(m)) != 1) for i in range(20) for _, _, m in plib.ligand(i)[1])
+    pk = vsgen.pocket(101)
+    e1, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    e2, *_ = run(plib, [pk], P=c["P"], K=c["K"], debug=True)
+    r1, r2 = e1.results(0), e2.results(0)
+    assert np.array_equal(r1.best_score, r2.best_score)
+    assert np.array_equal(r1.best_pose, r2.best_pose) and np.array_equal(r1.angles, r2.angles)
+    x1, x2 = e1.coords(0), e2.coords(0)
+    assert np.array_equal(x2[perm], x1)                 # new[perm[g]] = old[g]
+    check(e2, plib, range(0, plib.n, 8), pk, rot, tr, cs)
+
+
+def test_ligand_ids_pass_through():
+    lib = vsgen.ligands(50, 3, (20, 60), (0, 6))
+    lib.ligand_id = (np.arange(50, dtype=np.uint64) * np.uint64(1000003) + np.uint64(2 ** 40)).astype(np.uint64)
+    e, *_ = run(lib, [vsgen.pocket(101)], P=8, K=8, debug=False)
+    r = e.results(0)
+    assert np.array_equal(r.ligand_id, lib.ligand_id)
+    keys, nv = e.local_topk(0, 10)
+    idx, sc, ids = e.merge_topk(keys[:nv], 10, with_ids=True)
+    assert list(idx) == list(oracle.topk(r.best_score, 10)) and np.array_equal(ids, lib.ligand_id[idx])
+
+
+def test_topk_merge_of_padded_lists_smaller_than_k():
+    """Ranks with fewer than k ligands pad their lists with UINT64_MAX: merging W padded
+    lists (W * k above the 8192-entry scratch) keeps every real ligand, deterministically."""
+    import torch
+    c = vsgen.CONFIGS["C1"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    e, *_ = run(lib, [pk], P=8, K=8, debug=False)
+    r = e.results(0)
+    for W, k in ((8, 1000), (8, 2000), (3, 8192)):
+        parts = []
+        for rank in range(W):
+            eR, *_ = run(lib, [pk], P=8, K=8, debug=False, rank=rank, world_size=W)
+            keys, _ = eR.local_topk(0, k)
+            parts.append(keys)
+        g = torch.cat(parts)
+        assert g.numel() == W * k
+        for _ in range(2):
+            idx, sc = eR.merge_topk(g, k)
+            assert list(idx) == list(oracle.topk(r.best_score, k))      # all 16 ligands, ranked
+            assert np.array_equal(sc, r.best_score[idx])
+
+
+def test_mixed_layout_pockets_in_one_submit():
+    """A 32^3 pocket (fixed-stride layout) and a 36 x 30 x 26 pocket (runtime strides) in ONE submit
+    (ADVICE r1): each launch uses its own layout's class table; full parity in both."""
+    pk1 = vsgen.pocket(101)
+    pk2 = vsgen.pocket(107, n=(36, 30, 26), spacing=0.9, center_offset=(0.5, -0.5, 0.25))
+    lib = vsgen.ligands(40, 23, (20, 120), (0, 12))
+    e = engine(debug_poses=True)
+    rot, tr, cs, ids = setup(e, [pk1, pk2], 8, 8)
+    e.submit_library(lib, ids)
+    e.wait()
+    for slot, pk in enumerate([pk1, pk2]):
+        check(e, lib, range(lib.n), pk, rot, tr, cs, slot=slot)

@@ -81,7 +81,9 @@ def test_pipeline_chunk_schedule():
         assert b[0] == 0 and b[-1] == n and all(x < y for x, y in zip(b, b[1:])) or n == 0
         sizes = [y - x for x, y in zip(b, b[1:])]
         if n >= 32 and len(sizes) > 1:
-            assert sizes[0] == n // 32
-            assert all(s2 <= 4 * s1 for s1, s2 in zip(sizes, sizes[1:-1]))
+            assert sizes[0] == n // 32 and sizes[-1] == n // 32          # small exposed first H2D / last D2H
+            h = (len(sizes) + 1) // 2
+            assert all(s2 <= 4 * s1 for s1, s2 in zip(sizes[:h], sizes[1:h]))
+            assert all(s1 <= 4 * s2 for s1, s2 in zip(sizes[h - 1:], sizes[h:]))
     assert chunk_bounds(100, 3) == [0, 33, 66, 100]
-    assert chunk_bounds(1_000_000) == [0, 31250, 156250, 656250, 1_000_000]
+    assert chunk_bounds(1_000_000) == [0, 31250, 156250, 500000, 843750, 968750, 1_000_000]

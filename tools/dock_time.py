@@ -11,7 +11,7 @@ lib = vsgen.ligands(n, 4, ATOMS)
 e = Engine(atom_clusters=na, rot_clusters=nr, launch_per_bucket=bool(int(os.environ.get("LPB", "0"))), bucket_multiple=int(os.environ.get("BM", "16")), n_streams=int(os.environ.get("NS", "4")))
 e.set_poses(*vsgen.pose_table(64)); e.set_angles(vsgen.angle_table(8)); pid = e.load_pocket(vsgen.pocket(101))
 import torch
-d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
 ms = []
 for it in range(4):
     e.submit(*d, [pid], on_device=True); e.wait()

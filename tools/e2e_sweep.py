@@ -11,8 +11,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else c["n"]
 lib = vsgen.ligands(n, c["seed"], c["atoms"], c["rot"])
 pk = [vsgen.pocket(s) for s in c["pockets"]]
 rot, tr = vsgen.pose_table(c["P"]); cs = vsgen.angle_table(c["K"])
-h = [torch.from_numpy(a).pin_memory() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
-pd = PipelinedDocker(n_buffers=2); pd.setup(rot, tr, cs, pk)
+h = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
+pd = PipelinedDocker(); pd.setup(rot, tr, cs, pk)
 mx = int(lib.n_atoms.max())
 for first, growth in ((32, 4), (32, 6), (64, 6), (32, 8), (16, 4)):
     ts = []

@@ -45,7 +45,7 @@ def setup(e, pockets):
 
 def heatmap(n):
     lib = vsgen.ligands(n, 4)
-    d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
     pk = [vsgen.pocket(101)]
     out = open(f"gpurun_out/heatmap_{n}.csv", "w", newline="")
     w = csv.writer(out)
@@ -81,7 +81,7 @@ def sweep(n):
     for A, R in ((17, 3), (53, 8), (99, 14)):
         one = vsgen.ligands(1, 50 + A, (A, A), (R, R))
         lib = vsgen.replicate(one, 0, n)
-        d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+        d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
         probe = Engine(atom_clusters=1, rot_clusters=1)
         ids = setup(probe, pk)
         probe.submit(*d, ids, on_device=True)
@@ -116,7 +116,7 @@ def tail(n_max):
         if n > n_max:
             break
         lib = full.subset(np.arange(n)) if n < n_max else full
-        d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+        d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
         for mode in ("fused", "per_bucket"):
             res = {}
             for na, nr in ((1, 1), (6, 23)):

@@ -33,7 +33,7 @@ def run(name, every, debug):
     e.set_poses(rot, tr)
     e.set_angles(cs)
     ids = [e.load_pocket(p) for p in pks]
-    d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+    d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
     e.submit(*d, ids, on_device=True)
     e.wait()
     out = []

@@ -10,7 +10,7 @@ import vsgen
 from paper_2303_06150_b200 import Engine
 c = vsgen.CONFIGS["C4"]
 lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
-d = [torch.from_numpy(a).cuda() for a in (lib.atom_off, lib.xyz, lib.frag_off, lib.frags)]
+d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
 rot, tr = vsgen.pose_table(c["P"]); cs = vsgen.angle_table(c["K"]); pk = vsgen.pocket(101)
 mx = int(lib.n_atoms.max())
 out = {}
