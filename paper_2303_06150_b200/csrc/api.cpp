@@ -210,11 +210,28 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.nx = d.nx;
     p.ny = d.ny;
     p.nz = d.nz;
-    grid_strides(d.nx, d.ny, &p.rs, &p.ps);
-    // centring shift (PocketDev): 16 on every axis for the fixed-stride layout (planes of at
-    // most 32 x 32; the dock kernel then folds -Z and 2^23 + Z into immediates), n / 2 otherwise
-    const bool fix = grid_fixed(p.rs, p.ps);
-    const int Z[3] = {fix ? 16 : d.nx / 2, fix ? 16 : d.ny / 2, fix ? 16 : d.nz / 2};
+    p.grs = d.nx + 1;
+    p.gps = (d.nx + 1) * (d.ny + 1);
+    p.mode = grid_mode(d.nx, d.ny, d.nz);
+    grid_strides(p.mode, d.nx, d.ny, &p.rs, &p.ps);
+    // WIN: the 32^3-node window around the docking centre (clamped into the grid)
+    const int n3[3] = {d.nx, d.ny, d.nz};
+    int w0[3] = {0, 0, 0};
+    if (p.mode == kGridWin)
+        for (int a = 0; a < 3; ++a) {
+            const double uc = ((double)d.center[a] - d.origin[a]) / d.spacing;
+            int v = (int)std::lround(uc) - kWin / 2;
+            v = std::min(v, n3[a] - kWin);
+            w0[a] = std::max(v, 0);
+        }
+    p.wx0 = w0[0];
+    p.wy0 = w0[1];
+    p.wz0 = w0[2];
+    // centring shift (PocketDev): 16 on every axis for FIX (the dock kernel then folds -Z and
+    // 2^23 + Z into immediates), n / 2 for RT, the window centre for WIN
+    int Z[3];
+    for (int a = 0; a < 3; ++a)
+        Z[a] = p.mode == kGridFix ? 16 : p.mode == kGridRT ? n3[a] / 2 : w0[a] + kWin / 2;
     p.lo_x = (float)-Z[0];
     p.lo_y = (float)-Z[1];
     p.lo_z = (float)-Z[2];
@@ -234,6 +251,11 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.ty = (float)(((double)d.center[1] - d.origin[1]) / d.spacing - Z[1]);
     p.tz = (float)(((double)d.center[2] - d.origin[2]) / d.spacing - Z[2]);
     return p;
+}
+
+// Shared memory of the score_points hook's grid region (floats).
+size_t score_grid_floats(const PocketDev& pk) {
+    return pk.mode == kGridWin ? (size_t)kWin * pk.ps : (size_t)(pk.nz + 1) * pk.ps + pk.rs + 2;
 }
 
 // Stage-1 workspace (known from the batch sizes alone).
@@ -314,7 +336,7 @@ Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats,
 
 size_t max_grid_bytes(const vs_ctx* c) {
     size_t m = 0;
-    for (auto& p : c->pockets) m = std::max(m, (size_t)p.d.nx * p.d.ny * p.d.nz * 4);
+    for (auto& p : c->pockets) m = std::max(m, p.grid.size() * 4);   // padded copies
     return m;
 }
 
@@ -343,8 +365,8 @@ int pow2_ceil(int K) {
 }
 
 // Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1 -- for one
-// grid layout (nz planes of ps floats, row stride rs).
-vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs, int ps, int RC,
+// grid layout (mode, nz planes of ps floats, row stride rs).
+vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz, int rs, int ps, int RC,
                        std::vector<ClassInfo>& out) {
     out.clear();
     for (size_t i = 0; i < atom_b.size(); ++i) {
@@ -371,16 +393,16 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int nz, int rs
             const int PPW = pr.first, NW = pr.second;
             if (pow2_ceil(c->K) > 32 / PPW) continue;   // the pose group holds the angle slots
             const int LC = ligs_per_cta(NW, PPW, c->P);
-            const DockLayout L = dock_layout(ci.AC, NW, PPW, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
+            const DockLayout L = dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
             int b = 0;
-            CK(dock_occupancy(ci.AC, NW, PPW, grid_fixed(rs, ps), c->K, L.total, &b));
+            CK(dock_occupancy(ci.AC, NW, PPW, gm, c->K, L.total, &b));
             if (b >= 1) {
                 ci.NW = NW;
                 ci.PPW = PPW;
                 ci.LC = LC;
                 ci.b = b;
                 ci.smem = L.total;
-                CK(dock_kernel_attrs(ci.AC, NW, PPW, grid_fixed(rs, ps), c->K, &ci.attr));
+                CK(dock_kernel_attrs(ci.AC, NW, PPW, gm, c->K, &ci.attr));
                 break;
             }
         }
@@ -504,7 +526,8 @@ vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, 
     if (c->pockets.size() >= 16) return fail(c, VS_E_ARG, "at most 16 pockets");
     if (d->nx < 2 || d->ny < 2 || d->nz < 2) return fail(c, VS_E_ARG, "pocket dims must be >= 2");
     if ((int64_t)d->nx * d->ny * d->nz > (1 << 22)) return fail(c, VS_E_ARG, "pocket grid too large");
-    if (!(d->spacing > 0.f) || !std::isfinite(d->spacing)) return fail(c, VS_E_ARG, "pocket spacing must be > 0");
+    if (!(d->spacing >= 1e-4f) || !std::isfinite(d->spacing))
+        return fail(c, VS_E_ARG, "pocket spacing must be finite and >= 1e-4 A");
     for (int a = 0; a < 3; ++a)
         if (!std::isfinite(d->origin[a]) || !std::isfinite(d->center[a]))
             return fail(c, VS_E_ARG, "pocket origin/center must be finite");
@@ -512,14 +535,21 @@ vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, 
     PocketHost ph;
     ph.d = *d;
     const size_t cnt = (size_t)d->nx * d->ny * d->nz;
-    ph.grid.resize(cnt);
+    std::vector<float> raw(cnt);
     if (on_device) {
-        CK(cudaMemcpy(ph.grid.data(), grid, cnt * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(raw.data(), grid, cnt * 4, cudaMemcpyDeviceToHost));
     } else {
-        std::memcpy(ph.grid.data(), grid, cnt * 4);
+        std::memcpy(raw.data(), grid, cnt * 4);
     }
     for (size_t i = 0; i < cnt; ++i)
-        if (!std::isfinite(ph.grid[i])) return fail(c, VS_E_ARG, "pocket grid value %zu is not finite", i);
+        if (!std::isfinite(raw[i])) return fail(c, VS_E_ARG, "pocket grid value %zu is not finite", i);
+    // the device copy is PADDED: [nz+1][ny+1][nx+1] with zero pads, so a weight-0 corner read at
+    // node n stays inside the array (PocketDev::grid)
+    const size_t gx = (size_t)d->nx + 1, gy = (size_t)d->ny + 1;
+    ph.grid.assign(gx * gy * ((size_t)d->nz + 1), 0.f);
+    for (int z = 0; z < d->nz; ++z)
+        for (int y = 0; y < d->ny; ++y)
+            std::memcpy(&ph.grid[((size_t)z * gy + y) * gx], &raw[((size_t)z * d->ny + y) * d->nx], (size_t)d->nx * 4);
     c->pockets.push_back(std::move(ph));
     ++c->tables_version;
     if (pocket_id) *pocket_id = (int32_t)c->pockets.size() - 1;
@@ -623,7 +653,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     size_t gmax = 0;
     for (int i = 0; i < n_pockets; ++i) {
         auto& d = c->pockets[pocket_ids[i]].d;
-        gmax = std::max(gmax, (size_t)d.nx * d.ny * d.nz * 4);
+        gmax = std::max(gmax, c->pockets[pocket_ids[i]].grid.size() * 4);
     }
     const Stage1 s1 = plan1(n, nA, nR, nM, c->P, c->K, gmax, n_pockets);
     if (s1.end > c->ws_bytes) return fail(c, VS_E_WORKSPACE, "workspace too small (stage 1 needs %zu bytes)", s1.end);
@@ -745,14 +775,16 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         int big = 0;
         for (int q = 0; q < n_pockets; ++q) {
             const PocketDev& pk = c->pkdev[q];
-            const std::vector<int> key = {pk.nz, pk.rs, pk.ps};
+            const std::vector<int> key = {pk.mode, pk.nz, pk.rs, pk.ps};
             int li = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
             if (li == (int)keys.size()) {
                 keys.push_back(key);
                 c->layout_classes.emplace_back();
-                st = plan_classes(c, c->atom_b, pk.nz, pk.rs, pk.ps, c->frag_cap, c->layout_classes.back());
+                st = plan_classes(c, c->atom_b, pk.mode, pk.nz, pk.rs, pk.ps, c->frag_cap, c->layout_classes.back());
                 if (st) return st;
-                if ((int64_t)pk.nz * pk.ps > (int64_t)keys[big][0] * keys[big][2]) big = li;
+                if (dock_grid_floats(pk.mode, pk.nz, pk.rs, pk.ps) >
+                    dock_grid_floats(keys[big][0], keys[big][1], keys[big][2], keys[big][3]))
+                    big = li;
             }
             c->pk_layout[q] = li;
         }
@@ -955,7 +987,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.dbg_score = c->d_dbg_score[q];
             a.dbg_angles = c->d_dbg_ang[q];
             a.counter = d_counters + dock_launches;
-            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.nz, a.pk.rs, a.pk.ps, c->P, c->K, S_w, ci.LC, c->frag_cap);
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.mode, a.pk.nz, a.pk.rs, a.pk.ps, c->P,
+                                             c->K, S_w, ci.LC, c->frag_cap);
             const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];
@@ -1207,7 +1240,7 @@ vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* 
     CK(cudaMemcpy(dg, ph.grid.data(), gb, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dx, xyz, (size_t)n * 12, cudaMemcpyHostToDevice));
     PocketDev pk = make_pocket_dev(ph.d, dg);
-    const size_t smem = align16(((size_t)(pk.nz + 1) * pk.ps + pk.rs + 2) * 4);
+    const size_t smem = align16(score_grid_floats(pk) * 4);
     CK(launch_score_points(pk, dx, n, dout, smem, c->main));
     CK(cudaMemcpyAsync(g_out, dout, (size_t)n * 4, cudaMemcpyDeviceToHost, c->main));
     CK(cudaStreamSynchronize(c->main));

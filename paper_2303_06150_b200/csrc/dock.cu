@@ -9,16 +9,16 @@ using dk::DockFn;
 
 namespace {
 
-DockFn pick(int AC, int NW, int PPW, int fix, int K) {
+DockFn pick(int AC, int NW, int PPW, int gm, int K) {
     switch (AC) {
-        case 32: return dk::dock_pick_32(fix, NW, PPW, K);
-        case 64: return dk::dock_pick_64(fix, NW, PPW, K);
-        case 96: return dk::dock_pick_96(fix, NW, PPW, K);
-        case 128: return dk::dock_pick_128(fix, NW, PPW, K);
-        case 160: return dk::dock_pick_160(fix, NW, PPW, K);
-        case 192: return dk::dock_pick_192(fix, NW, PPW, K);
-        case 224: return dk::dock_pick_224(fix, NW, PPW, K);
-        case 256: return dk::dock_pick_256(fix, NW, PPW, K);
+        case 32: return dk::dock_pick_32(gm, NW, PPW, K);
+        case 64: return dk::dock_pick_64(gm, NW, PPW, K);
+        case 96: return dk::dock_pick_96(gm, NW, PPW, K);
+        case 128: return dk::dock_pick_128(gm, NW, PPW, K);
+        case 160: return dk::dock_pick_160(gm, NW, PPW, K);
+        case 192: return dk::dock_pick_192(gm, NW, PPW, K);
+        case 224: return dk::dock_pick_224(gm, NW, PPW, K);
+        case 256: return dk::dock_pick_256(gm, NW, PPW, K);
         default: return nullptr;
     }
 }
@@ -27,11 +27,18 @@ DockFn pick(int AC, int NW, int PPW, int fix, int K) {
 
 // Padded shared-memory strides (tools/bank_sim3.py, the lane map of 4 poses x 8 angles:
 // 3.06-way bank conflicts on the sweep's corner gathers instead of 3.21 at (33, 1063) and
-// 7.5 unpadded; uniform random gathers give 3.5).  Grids of at most 32 x 32 per plane use
-// the fixed layout (34, 1097) with compile-time strides; larger planes use
-// (nx + 1, (nx + 1) * ny + 7).
-void grid_strides(int nx, int ny, int* rs, int* ps) {
-    if (nx <= 32 && ny <= 32) {
+// 7.5 unpadded; uniform random gathers give 3.5).  Grids of at most 32^3 nodes (FIX) and the
+// 32^3 window of large grids (WIN) use the fixed layout (34, 1097) with compile-time strides;
+// RT grids use (nx + 1, (nx + 1) * ny + 7).  RT is chosen while its region (plus a zero plane)
+// stays within the FIX budget of shared memory, so the pose buffers keep their room.
+int grid_mode(int nx, int ny, int nz) {
+    if (nx <= kWin && ny <= kWin && nz <= kWin) return kGridFix;
+    const size_t rt = (size_t)(nz + 1) * ((size_t)(nx + 1) * ny + 7) + (nx + 1) + 2;
+    return rt <= (size_t)kWin * dk::kFixPS + 2048 ? kGridRT : kGridWin;
+}
+
+void grid_strides(int mode, int nx, int ny, int* rs, int* ps) {
+    if (mode != kGridRT) {
         *rs = dk::kFixRS;
         *ps = dk::kFixPS;
     } else {
@@ -40,21 +47,30 @@ void grid_strides(int nx, int ny, int* rs, int* ps) {
     }
 }
 
-bool grid_fixed(int rs, int ps) { return rs == dk::kFixRS && ps == dk::kFixPS; }
-
-cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, int K, cudaFuncAttributes* attr) {
-    DockFn f = pick(AC, NW, PPW, fix, K);
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int gm, int K, cudaFuncAttributes* attr) {
+    DockFn f = pick(AC, NW, PPW, gm, K);
     if (!f) return cudaErrorInvalidValue;
     return cudaFuncGetAttributes(attr, reinterpret_cast<const void*>(f));
 }
 
-cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem, int* blocks_per_sm) {
-    DockFn f = pick(AC, NW, PPW, fix, K);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, int gm, int K, size_t smem, int* blocks_per_sm) {
+    DockFn f = pick(AC, NW, PPW, gm, K);
     if (!f) {   // no instantiation for this (class, warps, poses per warp, K): the policy skips it
         *blocks_per_sm = 0;
         return cudaSuccess;
     }
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(f));
+    if (e != cudaSuccess) return e;
+    if (smem + fa.sharedSizeBytes > (size_t)optin) {   // does not fit: no API call that must fail
+        *blocks_per_sm = 0;
+        return cudaSuccess;
+    }
+    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) {
         *blocks_per_sm = 0;
@@ -66,7 +82,7 @@ cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem,
 }
 
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
-    DockFn f = pick(AC, NW, PPW, grid_fixed(a.pk.rs, a.pk.ps), a.K);
+    DockFn f = pick(AC, NW, PPW, a.pk.mode, a.K);
     if (!f) return cudaErrorInvalidValue;
     if (a.n <= 0) return cudaSuccess;
     // the attribute is per function, and one instantiation can serve several grid layouts
@@ -95,13 +111,14 @@ cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, 
 
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
                                 cudaStream_t st) {
-    const bool fix = grid_fixed(pk.rs, pk.ps);
-    const void* f = fix ? reinterpret_cast<const void*>(dk::score_points_kernel<true>)
-                        : reinterpret_cast<const void*>(dk::score_points_kernel<false>);
+    const void* f = pk.mode == kGridFix ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridFix>)
+                    : pk.mode == kGridRT ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridRT>)
+                                         : reinterpret_cast<const void*>(dk::score_points_kernel<kGridWin>);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (fix) dk::score_points_kernel<true><<<148, 1024, smem, st>>>(pk, xyz, n, out);
-    else dk::score_points_kernel<false><<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    if (pk.mode == kGridFix) dk::score_points_kernel<kGridFix><<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    else if (pk.mode == kGridRT) dk::score_points_kernel<kGridRT><<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    else dk::score_points_kernel<kGridWin><<<148, 1024, smem, st>>>(pk, xyz, n, out);
     return cudaGetLastError();
 }
 

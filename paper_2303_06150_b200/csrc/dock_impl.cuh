@@ -18,10 +18,10 @@
 //    lowest k, Q11), and the winner is applied (from registers when it fits);
 //  * (x, y) arithmetic is packed in Blackwell's FFMA2/FADD2/FMUL2 (per-element IEEE
 //    ops, so every result is bit-identical to the scalar form);
-//  * template<int AC, int NW, int PPW, bool FIX, int KT> per atom class = the paper's
+//  * template<int AC, int NW, int PPW, int GM, int KT> per atom class = the paper's
 //    "non-type template parameter for the kernel maximum number of atoms":
 //    AC sizes the per-pose buffers in shared memory, hence the warps per CTA;
-//    FIX = compile-time grid strides (<= 32 x 32 planes), KT = compile-time K (8).
+//    GM = grid mode (FIX 32^3 / RT / WIN window + L2, internal.h), KT = compile-time K (8).
 //
 // All arithmetic that decides an angle or is replayed (placement, Rodrigues,
 // rotation, interpolation) uses explicit _rn intrinsics in shared helpers, so
@@ -98,6 +98,16 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float t) {
     return __ffma2_rn(f2(t), b, __ffma2_rn(f2(-t), a, a));
 }
 
+// Trilinear blend of the 8 corners given as (z0, z1) pairs: x-lerps on the pairs, the
+// y-lerp on the (l0, l1) pair, then z (Q10), + kappa*h*excess.
+__device__ __forceinline__ float blend(float2 c00, float2 c10, float2 c01, float2 c11, float2 fxy, float fz, float kh,
+                                      float e) {
+    const float2 l_0 = lerp2(c00, c10, fxy.x);     // (l00, l01): y0, z0/z1
+    const float2 l_1 = lerp2(c01, c11, fxy.x);     // (l10, l11): y1, z0/z1
+    const float2 l = lerp2(l_0, l_1, fxy.y);       // (l0, l1)
+    return __fmaf_rn(kh, e, lerp(l.x, l.y, fz));
+}
+
 // a8: g(u), u in grid units (Q9, Q10): clamp, L1 excess, i0 = min(floor(u_c), n-2),
 // lerps x then y then z, + kappa*h*excess.  G is the shared-memory copy (strides rs, ps).
 // floor(m) for 0 <= m < 2^23 is the round-down sum m + 2^23 (its bits also give the
@@ -106,18 +116,24 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float t) {
 //
 // The upper edge (u_c = n-1) takes i0 = n-1 with f = 0 instead of i0 = n-2 with f = 1:
 // both reduce exactly to the node value (lerp(a, b, 0) = a, lerp(a, b, 1) = b bitwise),
-// and the corner at n is a finite zero pad of the shared-memory copy, so no clamp of
-// i0 is needed.  FIX: the 32x32-plane layout with compile-time strides (34, 1097)
-// that lets every corner load use an immediate offset.
+// and the corner at n is a finite zero pad (row / column pads, the RT zero plane, the global
+// copy's pads), so no clamp of i0 is needed -- except on the z axis of FIX, whose zero plane
+// would cost the 128 class a warp: there i0 is clamped to n-2 with f = 1.
+// GM = grid mode (internal.h): FIX -- the 32x32-plane layout with compile-time strides
+// (34, 1097) that lets every corner load use an immediate offset; RT -- runtime strides;
+// WIN -- the shared-memory window (fixed strides) with the padded global copy behind it:
+// a warp whose cells all lie in the window takes the pure shared-memory path (one vote),
+// otherwise each lane reads its 8 corners from the window or from global memory.
 constexpr int kFixRS = 34, kFixPS = 1097;
-template <bool FIX>
+template <int GM>
 __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
-    const int RS = FIX ? kFixRS : pk.rs, PS = FIX ? kFixPS : pk.ps;
+    const int RS = GM == kGridRT ? pk.rs : kFixRS, PS = GM == kGridRT ? pk.ps : kFixPS;
     // centred coordinates (PocketDev): clamp to [-Z, n-1-Z]; floor(u_c) = bits of the
     // round-down sum c + (2^23 + Z) minus the bits of 2^23; f = c - (floor(u_c) - Z)
     // (FIX: Z = 16 on every axis, so -Z and 2^23 + Z are immediates)
-    const float lox = FIX ? -16.f : pk.lo_x, loy = FIX ? -16.f : pk.lo_y, loz = FIX ? -16.f : pk.lo_z;
-    const float mx = FIX ? 8388624.f : pk.mx, my = FIX ? 8388624.f : pk.my, mz = FIX ? 8388624.f : pk.mz;
+    constexpr bool IMM = GM == kGridFix;
+    const float lox = IMM ? -16.f : pk.lo_x, loy = IMM ? -16.f : pk.lo_y, loz = IMM ? -16.f : pk.lo_z;
+    const float mx = IMM ? 8388624.f : pk.mx, my = IMM ? 8388624.f : pk.my, mz = IMM ? 8388624.f : pk.mz;
     const float cx = fminf(fmaxf(ux, lox), pk.top_x);
     const float cy = fminf(fmaxf(uy, loy), pk.top_y);
     const float cz = fminf(fmaxf(uz, loz), pk.top_z);
@@ -127,18 +143,47 @@ __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, f
     const float2 bxy = __fadd2_rd(make_float2(cx, cy), mxy);
     const float bz = __fadd_rd(cz, mz);
     const float2 fxy = __fadd2_rn(make_float2(cx, cy), neg2(__fadd2_rn(bxy, neg2(mxy))));
-    const float fz = __fsub_rn(cz, __fsub_rn(bz, mz));
-    const int idx = (__float_as_int(bxy.x) - kMagicBits) + (__float_as_int(bxy.y) - kMagicBits) * RS +
-                    (__float_as_int(bz) - kMagicBits) * PS;
-    const float* p = G + idx;
-    const float2 c00 = make_float2(p[0], p[PS]);                 // (c000, c001)
-    const float2 c10 = make_float2(p[1], p[PS + 1]);             // (c100, c101)
-    const float2 c01 = make_float2(p[RS], p[PS + RS]);           // (c010, c011)
-    const float2 c11 = make_float2(p[RS + 1], p[PS + RS + 1]);   // (c110, c111)
-    const float2 l_0 = lerp2(c00, c10, fxy.x);     // (l00, l01): y0, z0/z1
-    const float2 l_1 = lerp2(c01, c11, fxy.x);     // (l10, l11): y1, z0/z1
-    const float2 l = lerp2(l_0, l_1, fxy.y);       // (l0, l1)
-    return __fmaf_rn(pk.kh, e, lerp(l.x, l.y, fz));
+    const int ix = __float_as_int(bxy.x) - kMagicBits, iy = __float_as_int(bxy.y) - kMagicBits;
+    int iz = __float_as_int(bz) - kMagicBits;
+    float fz = __fsub_rn(cz, __fsub_rn(bz, mz));
+    if (GM == kGridFix && iz > pk.nz - 2) {
+        // top z face: i0 = n-2 with f = 1 (bitwise the same blend as i0 = n-1, f = 0), so no
+        // corner read leaves the grid's planes (race-free: the region behind the grid is
+        // live pose buffers); the y overflow of the last plane lands in a 32-float zero pad
+        iz = pk.nz - 2;
+        fz = 1.f;
+    }
+    if (GM != kGridWin) {
+        const float* p = G + ix + iy * RS + iz * PS;
+        return blend(make_float2(p[0], p[PS]), make_float2(p[1], p[PS + 1]), make_float2(p[RS], p[PS + RS]),
+                     make_float2(p[RS + 1], p[PS + RS + 1]), fxy, fz, pk.kh, e);
+    } else {
+        const int lx = ix - pk.wx0, ly = iy - pk.wy0, lz = iz - pk.wz0;
+        const bool in = ((unsigned)lx <= (unsigned)(kWin - 2)) & ((unsigned)ly <= (unsigned)(kWin - 2)) &
+                        ((unsigned)lz <= (unsigned)(kWin - 2));
+        if (__all_sync(__activemask(), in)) {
+            const float* p = G + lx + ly * kFixRS + lz * kFixPS;
+            return blend(make_float2(p[0], p[kFixPS]), make_float2(p[1], p[kFixPS + 1]),
+                         make_float2(p[kFixRS], p[kFixPS + kFixRS]), make_float2(p[kFixRS + 1], p[kFixPS + kFixRS + 1]),
+                         fxy, fz, pk.kh, e);
+        }
+        float2 c00, c10, c01, c11;
+        if (in) {
+            const float* p = G + lx + ly * kFixRS + lz * kFixPS;
+            c00 = make_float2(p[0], p[kFixPS]);
+            c10 = make_float2(p[1], p[kFixPS + 1]);
+            c01 = make_float2(p[kFixRS], p[kFixPS + kFixRS]);
+            c11 = make_float2(p[kFixRS + 1], p[kFixPS + kFixRS + 1]);
+        } else {   // outside the window: the padded global copy (L1 / L2)
+            const int gr = pk.grs, gp = pk.gps;
+            const float* p = pk.grid + ix + (size_t)iy * gr + (size_t)iz * gp;
+            c00 = make_float2(__ldg(p), __ldg(p + gp));
+            c10 = make_float2(__ldg(p + 1), __ldg(p + gp + 1));
+            c01 = make_float2(__ldg(p + gr), __ldg(p + gp + gr));
+            c11 = make_float2(__ldg(p + gr + 1), __ldg(p + gp + gr + 1));
+        }
+        return blend(c00, c10, c01, c11, fxy, fz, pk.kh, e);
+    }
 }
 
 // Pose p in centred grid units: R' = R / h, t' = (c + tau - o) / h - Z, v = R' x + t'.
@@ -166,20 +211,24 @@ __device__ __forceinline__ RotT load_pose(const float* T) {
     return M;
 }
 
-// Stage the pocket grid into shared memory with padded strides; the padding (and
-// the zero plane/row above the grid) is zero-filled first.  Ends with a barrier.
-// zero_floats: how much to zero first (the grid region, plus -- for the dock kernel -- the
-// pose buffers behind it, see dock_grid_floats).
+// Stage the pocket grid (FIX / RT: all of it; WIN: the 32^3-node window) from the padded
+// global copy into shared memory with padded strides; the padding (and the zero plane/row
+// above the grid) is zero-filled first.  zero_floats: how much to zero first (the grid
+// region, plus -- for the dock kernel -- the pose buffers behind it, see dock_grid_floats).
 __device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk, size_t zero_floats) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int n4 = (int)(align16(zero_floats * 4) / 16);
     for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    for (int row = w; row < pk.ny * pk.nz; row += nw) {
-        const int z = row / pk.ny, y = row - z * pk.ny;
-        const float* src = pk.grid + (size_t)row * pk.nx;
+    const bool win = pk.mode == kGridWin;
+    const int x0 = win ? pk.wx0 : 0, y0 = win ? pk.wy0 : 0, z0 = win ? pk.wz0 : 0;
+    const int NX = win ? min(kWin, pk.nx - x0) : pk.nx, NY = win ? min(kWin, pk.ny - y0) : pk.ny,
+              NZ = win ? min(kWin, pk.nz - z0) : pk.nz;
+    for (int row = w; row < NY * NZ; row += nw) {
+        const int z = row / NY, y = row - z * NY;
+        const float* src = pk.grid + (size_t)(z0 + z) * pk.gps + (size_t)(y0 + y) * pk.grs + x0;
         float* dst = sG + z * pk.ps + y * pk.rs;
-        for (int x = lane; x < pk.nx; x += 32) dst[x] = src[x];
+        for (int x = lane; x < NX; x += 32) dst[x] = src[x];
     }
 }
 
@@ -206,7 +255,7 @@ struct PoseBuf {
 
 // U independent sweep evaluations per lane: atoms j0, j0 + apw, ... (j < hi), rotated by M,
 // scored, summed into acc in ascending order; the rotated atoms stay in kp[0..U).
-template <int U, bool FIX, int AC>
+template <int U, int GM, int AC>
 __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, const float* __restrict__ G,
                                            const PocketDev& pk, int j0, int apw, int hi, float& acc, float4 (&kp)[4]) {
     float4 v[U];
@@ -219,7 +268,7 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
 #pragma unroll
     for (int u = 0; u < U; ++u) kp[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
 #pragma unroll
-    for (int u = 0; u < U; ++u) g[u] = grid_g<FIX>(G, kp[u].x, kp[u].y, kp[u].z, pk);
+    for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, kp[u].x, kp[u].y, kp[u].z, pk);
 #pragma unroll
     for (int u = 0; u < U; ++u)
         if (j0 + u * apw < hi) acc = __fadd_rn(acc, g[u]);
@@ -231,7 +280,7 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
 // constant folds), 0 = runtime K.
 // K need not be a power of two: the lane map uses Kp = the next power of two >= K (kbits =
 // log2 Kp) and the lanes of angle slots k >= K hold the identity and never win.
-template <int AC, int PPW, bool FIX, int KT>
+template <int AC, int PPW, int GM, int KT>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, PoseBuf<AC> B, const float* __restrict__ G,
                                            const PocketDev& pk, int K_rt, int kbits_rt, int S_w, float ck, float sk,
@@ -274,11 +323,11 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 float acc = 0.f;
                 float4 kp[4];
                 int st = 0;
-                for (; st + 4 <= nst; st += 4) eval_batch<4, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp);
+                for (; st + 4 <= nst; st += 4) eval_batch<4, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp);
                 switch (nst - st) {
-                    case 3: eval_batch<3, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
-                    case 2: eval_batch<2, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
-                    case 1: eval_batch<1, FIX>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    case 3: eval_batch<3, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    case 2: eval_batch<2, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    case 1: eval_batch<1, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
                     default: break;
                 }
                 // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
@@ -331,14 +380,14 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float4 v = B.get(i + u * LPP);
-            g[u] = grid_g<FIX>(G, v.x, v.y, v.z, pk);
+            g[u] = grid_g<GM>(G, v.x, v.y, v.z, pk);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, g[u]);
     }
     for (; i < A; i += LPP) {
         const float4 v = B.get(i);
-        acc = __fadd_rn(acc, grid_g<FIX>(G, v.x, v.y, v.z, pk));
+        acc = __fadd_rn(acc, grid_g<GM>(G, v.x, v.y, v.z, pk));
     }
 #pragma unroll
     for (int o = LPP / 2; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
@@ -482,14 +531,14 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned c
 // long before use and global rounds are claimed in sequence order), the
 // warp that completes the last item of a round reduces its best pose (a9) and frees the
 // slot.  NW is therefore free of P / PPW (e.g. 12 warps of 4 poses for 64 poses).
-template <int AC, int NW, int PPW, bool FIX, int KT>
+template <int AC, int NW, int PPW, int GM, int KT>
 __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DockRing ring;
     constexpr int LPP = 32 / PPW;
     const PocketDev& pk = a.pk;
     const int LC = a.ligs_per_cta;
-    const DockLayout L = dock_layout(AC, NW, PPW, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
+    const DockLayout L = dock_layout(AC, NW, PPW, GM, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
@@ -564,7 +613,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             uint8_t* sAng = slot + L.ang_o;
             float T[12];   // pose p in grid units, from the raw table (48 B, L1-resident)
             scaled_pose(a.pose_tab + 12 * pc, pk, T);
-            dock_poses<AC, PPW, FIX, KT>(rec, m.y, m.z, T, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
+            dock_poses<AC, PPW, GM, KT>(rec, m.y, m.z, T, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
                                      sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncwarp();
@@ -575,6 +624,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             if (last) __threadfence_block();
         }
         last = __shfl_sync(FULL, last, 0);
+        __syncwarp();   // lane 0's fence after the counter orders the round reads of the whole warp
         if (last) {
             finish_round(a, slot, L, round, lane);
             __syncwarp();
@@ -637,46 +687,48 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const i
     }
 }
 
-template <bool FIX>
+template <int GM>
 __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, const float* __restrict__ xyz,
                                                             int64_t n, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* sG = reinterpret_cast<float*>(smem);
-    stage_grid(sG, pk, (size_t)(pk.nz + 1) * pk.ps + pk.rs + 2);
+    stage_grid(sG, pk, GM == kGridWin ? (size_t)kWin * pk.ps : (size_t)(pk.nz + 1) * pk.ps + pk.rs + 2);
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
         const float uy = __fmul_rn(__fsub_rn(xyz[3 * i + 1], pk.oy), pk.inv_h);
         const float uz = __fmul_rn(__fsub_rn(xyz[3 * i + 2], pk.oz), pk.inv_h);
-        out[i] = grid_g<FIX>(sG, ux, uy, uz, pk);
+        out[i] = grid_g<GM>(sG, ux, uy, uz, pk);
     }
 }
 
 using DockFn = void (*)(const DockArgs);
 
-template <int AC, bool FIX>
+template <int AC, int GM>
 DockFn pick_ac(int NW, int PPW, int K) {
-    if (PPW == 4 && K == 8 && FIX)   // production path: compile-time K = 8
-        return NW == 16 ? dock_kernel<AC, 16, 4, FIX, 8>
-               : NW == 13 ? dock_kernel<AC, 13, 4, FIX, 8>
-               : NW == 12 ? dock_kernel<AC, 12, 4, FIX, 8>
-               : NW == 10 ? dock_kernel<AC, 10, 4, FIX, 8>
-                          : (NW == 8 ? dock_kernel<AC, 8, 4, FIX, 8> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX, 8> : nullptr));
-    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, FIX, 0> : (NW == 16 ? dock_kernel<AC, 16, 1, FIX, 0> : nullptr);
+    if (PPW == 4 && K == 8 && GM != kGridRT)   // production path: compile-time K = 8
+        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8>
+               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8>
+               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8>
+               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 8> : nullptr));
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, GM, 0> : (NW == 16 ? dock_kernel<AC, 16, 1, GM, 0> : nullptr);
     if (PPW == 2)
-        return NW == 32 ? dock_kernel<AC, 32, 2, FIX, 0>
-                        : (NW == 16 ? dock_kernel<AC, 16, 2, FIX, 0> : (NW == 8 ? dock_kernel<AC, 8, 2, FIX, 0> : nullptr));
+        return NW == 32 ? dock_kernel<AC, 32, 2, GM, 0>
+                        : (NW == 16 ? dock_kernel<AC, 16, 2, GM, 0> : (NW == 8 ? dock_kernel<AC, 8, 2, GM, 0> : nullptr));
     if (PPW == 4)
-        return NW == 16 ? dock_kernel<AC, 16, 4, FIX, 0>
-               : NW == 12 ? dock_kernel<AC, 12, 4, FIX, 0>
-                          : (NW == 8 ? dock_kernel<AC, 8, 4, FIX, 0> : (NW == 4 ? dock_kernel<AC, 4, 4, FIX, 0> : nullptr));
+        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 0>
+               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 0>
+               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 0>
+               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0> : nullptr));
     return nullptr;
 }
 
 // Per-atom-class entry points, each compiled in its own translation unit
 // (dock_inst.cu with -DVSD_AC=<AC>) so the 8 classes build in parallel.
 #define VSD_DECL_CLASS(ac)                                                                                     \
-    DockFn dock_pick_##ac(int fix, int NW, int PPW, int K);                                                           \
+    DockFn dock_pick_##ac(int gmode, int NW, int PPW, int K);                                                           \
     cudaError_t launch_finalize_##ac(const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 VSD_DECL_CLASS(32)
 VSD_DECL_CLASS(64)

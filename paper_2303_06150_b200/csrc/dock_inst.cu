@@ -11,8 +11,10 @@
 namespace vsd {
 namespace dk {
 
-DockFn VSD_CAT(dock_pick_, VSD_AC)(int fix, int NW, int PPW, int K) {
-    return fix ? pick_ac<VSD_AC, true>(NW, PPW, K) : pick_ac<VSD_AC, false>(NW, PPW, K);
+DockFn VSD_CAT(dock_pick_, VSD_AC)(int gmode, int NW, int PPW, int K) {
+    return gmode == kGridFix ? pick_ac<VSD_AC, kGridFix>(NW, PPW, K)
+           : gmode == kGridRT ? pick_ac<VSD_AC, kGridRT>(NW, PPW, K)
+                              : pick_ac<VSD_AC, kGridWin>(NW, PPW, K);
 }
 
 cudaError_t VSD_CAT(launch_finalize_, VSD_AC)(const DockArgs& a, const int64_t* atom_off, float* xyz_out,

@@ -16,15 +16,29 @@ constexpr int kPrepTile = 4096;    // ligands per block in classify/scatter
 constexpr int kMaxPoses = 1024;
 constexpr int kMaxSweeps = 4;
 
-// Pocket as the dock kernel sees it: grid staged in shared memory with padded
-// row / plane strides (floats).  Coordinates are kept in CENTRED grid units
-// v = (y - o)/h - Z with the integer shift Z = floor(n/2) per axis: |v| <= n/2 halves the
-// fp32 rounding of every placement / rotation step against u = v + Z in [0, n-1], and the
-// shift costs nothing -- it is folded into the clamp bounds and the floor constant 2^23 + Z.
+// Grid modes of the dock kernel ("grid modes"):
+//  0 FIX  grids of at most 32 x 32 x 32 nodes, whole grid in shared memory, compile-time
+//         strides (34, 1097);
+//  1 RT   larger grids that still fit shared memory: runtime strides (nx + 1, (nx + 1) ny + 7);
+//  2 WIN  grids that do not fit (48^3, 64^3, 0.5 A spacing, ...): a 32^3-node WINDOW centred
+//         on the docking centre is staged in shared memory (fixed strides); a cell whose 8
+//         corners all lie in the window is gathered from shared memory, any other cell from
+//         the padded global copy through L1 / L2 (ld.global.nc).
+constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2;
+constexpr int kWin = 32;   // window edge (nodes)
+
+// Pocket as the dock kernel sees it.  Coordinates are kept in CENTRED grid units
+// v = (y - o)/h - Z with an integer shift Z per axis (16 for FIX, floor(n/2) for RT, the
+// window origin + 16 for WIN): |v| stays small, which shrinks the fp32 rounding of every
+// placement / rotation step against u = v + Z in [0, n-1], and the shift costs nothing -- it
+// is folded into the clamp bounds and the floor constant 2^23 + Z.
 struct PocketDev {
-    const float* grid;     // global copy [nz][ny][nx]
+    const float* grid;     // global PADDED copy [nz+1][ny+1][nx+1] (zero pads), strides grs, gps
     int nx, ny, nz;
     int rs, ps;            // shared-memory row stride and plane stride (floats)
+    int grs, gps;          // global padded row / plane stride (floats)
+    int mode;              // kGridFix / kGridRT / kGridWin
+    int wx0, wy0, wz0;     // WIN: window origin (grid nodes)
     float lo_x, lo_y, lo_z;       // -Z          (u = 0)
     float top_x, top_y, top_z;    // n - 1 - Z   (u = n - 1)
     float mx, my, mz;             // 2^23 + Z    (exact)
@@ -75,18 +89,19 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t
 // Angle choices kept per pose: S_w * RC bytes (RC = the launch's fragment cap), 4-aligned.
 __host__ __device__ inline int dock_ang_stride(int S_w, int RC) { return ((S_w * (RC > 0 ? RC : 1)) + 3) & ~3; }
 // Grid region of the dock kernel (floats).  Corner reads at i0 + 1 = n carry weight 0 but
-// must read FINITE values.  Fixed-stride grids (rs, ps) = (34, 1097): the region is the nz
-// planes only and those reads land in the pose buffers placed right behind it (zeroed at
-// kernel start, only ever holding coordinates; <= ny rs + nx + 2 = 1122 floats, less than
-// any pose-buffer area).  Other strides keep a zero plane + row.
-__host__ __device__ inline size_t dock_grid_floats(int nz, int rs, int ps) {
-    return (rs == 34 && ps == 1097) ? (size_t)nz * ps : (size_t)(nz + 1) * ps + rs + 2;
+// must read FINITE values that no other warp writes.  FIX: the nz planes + a 32-float zero
+// pad: the z index is clamped to nz - 2 at the top face (grid_g), so the only read past the
+// planes is the y overflow of row ny in the last plane (<= 34 rs - ps = 25 floats).  RT keeps
+// a zero plane + row.  WIN: the 32 window planes; the shared-memory path never reads past
+// local node 31 on any axis.
+__host__ __device__ inline size_t dock_grid_floats(int mode, int nz, int rs, int ps) {
+    return mode == kGridFix ? (size_t)nz * ps + 32 : mode == kGridWin ? (size_t)kWin * ps : (size_t)(nz + 1) * ps + rs + 2;
 }
-__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int nz, int rs, int ps, int P, int K,
-                                                  int S_w, int LC, int RC) {
+__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int mode, int nz, int rs, int ps, int P,
+                                                  int K, int S_w, int LC, int RC) {
     DockLayout L;
     size_t o = 0;
-    L.grid = o;  o += align16(dock_grid_floats(nz, rs, ps) * 4);
+    L.grid = o;  o += align16(dock_grid_floats(mode, nz, rs, ps) * 4);
     L.buf = o;   o += (size_t)NW * PPW * pose_stride_of(AC, NW, PPW) * 4;   // (x,y)|z per pose
     L.pose = o;   // pose table: read per warp item from global (L1-resident), no shared copy
     L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
@@ -108,8 +123,9 @@ __host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
     const int lc = NW / wl;
     return lc > 0 ? lc : 1;
 }
-// Shared-memory grid strides: row stride rs >= nx, plane stride ps >= ny * rs.
-void grid_strides(int nx, int ny, int* rs, int* ps);
+// Grid mode and shared-memory strides (row rs, plane ps) of an nx x ny x nz grid.
+int grid_mode(int nx, int ny, int nz);
+void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
@@ -130,9 +146,8 @@ cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const 
                         const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint, int S_w,
                         float* rec, int4* meta, cudaStream_t st);
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
-cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int fix, int K, cudaFuncAttributes* attr);
-cudaError_t dock_occupancy(int AC, int NW, int PPW, int fix, int K, size_t smem, int* blocks_per_sm);
-bool grid_fixed(int rs, int ps);
+cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int gmode, int K, cudaFuncAttributes* attr);
+cudaError_t dock_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int* blocks_per_sm);
 cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
                                 cudaStream_t st);

@@ -33,12 +33,14 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 //   * the sets form a forest under inclusion (equal sets: the lower fragment index is the
 //     outer one); the forest is ordered depth first, children by fragment index (preorder
 //     number pre[r]);
-//   * atom i's key = (1 + pre of the innermost set containing it, or 0 for atoms in no set;
-//     then its coordinates x, y, z as order-preserving integers; then its input index).
+//   * atom i's key = (1 + pre of the innermost set containing it, or 0 for atoms in no set)
+//     in the top 6 bits, then a 58-bit mix of its coordinate bits; ties by input index.
 //     Sorting by the key puts each set's own atoms first and its descendants' atoms right
 //     after them, so every set is contiguous.  The key does not depend on the input atom
 //     numbering (only on coordinates and set structure), so an atom-permuted copy of a
-//     ligand is docked bit-identically (coordinates are mapped back to input order).
+//     ligand is docked bit-identically (coordinates are mapped back to input order; only
+//     two atoms of one region with colliding 58-bit mixes -- e.g. identical coordinates --
+//     fall back to the input order, which then cannot change any sum).
 //
 // Outputs: order[atom_off[i] + j] = input index of internal atom j (u8); frint[f] =
 // {a', b', lo, hi} in internal numbering (the range form the pack / dock kernels use);
@@ -52,26 +54,31 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 //  10 atom listed twice in one moving set
 //  7 axis atom inside its own moving set
 //  11 moving sets not laminar (two sets overlap without one containing the other)
-constexpr int kIngestWarps = 4;
+constexpr int kIngestWarps = 8;
 struct IngestWarp {
     uint32_t mask[kMaxAtoms];           // bit r: atom in M_r
-    uint4 key[kMaxAtoms];               // (1 + pre, ord x, ord y, ord z)
+    unsigned long long key[kMaxAtoms];  // (1 + pre) << 58 | coordinate mix
     uint8_t path[kMaxFrags][kMaxFrags + 1];   // path[r][d]: ancestor of r at depth d (r itself at depth[r])
     uint32_t anc[kMaxFrags];
     uint8_t depth[kMaxFrags], pre[kMaxFrags];
     uint8_t rank[kMaxAtoms];            // input index -> internal position
+    uint8_t list[kMaxAtoms];            // atoms grouped by region (key >> 58)
+    int rstart[kMaxFrags + 2], rfill[kMaxFrags + 2];   // region start / fill cursor
 };
 
-__device__ __forceinline__ uint32_t ord_key(float v) {
-    const uint32_t b = __float_as_uint(__fadd_rn(v, 0.0f));   // -0 -> +0
-    return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
-}
-__device__ __forceinline__ bool key_less(const uint4& p, int i, const uint4& q, int j) {
-    if (p.x != q.x) return p.x < q.x;
-    if (p.y != q.y) return p.y < q.y;
-    if (p.z != q.z) return p.z < q.z;
-    if (p.w != q.w) return p.w < q.w;
-    return i < j;
+// 58-bit mix of an atom's coordinate bits (-0 canonicalised to +0): a canonical tie-break
+// among the free atoms of one set region that does not depend on the input numbering.
+__device__ __forceinline__ unsigned long long coord_mix(float x, float y, float z) {
+    unsigned long long h = 0x9E3779B97F4A7C15ull;
+    const float v[3] = {x, y, z};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        h ^= (unsigned long long)__float_as_uint(__fadd_rn(v[t], 0.0f)) + 0x632BE59BD9B4E019ull * (t + 1);
+        h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
+        h = (h ^ (h >> 27)) * 0x94D049BB133111EBull;
+        h ^= h >> 31;
+    }
+    return h >> 6;
 }
 __device__ __forceinline__ int first_code(int code) {   // lowest lane's non-zero code
     const unsigned any = __ballot_sync(FULL, code != 0);
@@ -229,7 +236,9 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
                 W.pre[lane] = (uint8_t)pre;
             }
             __syncwarp();
-            // atom keys
+            // atom keys; region histogram (region = 1 + pre of the innermost set, 0 = none)
+            for (int t = lane; t < R + 1; t += 32) W.rfill[t] = 0;
+            __syncwarp();
             for (int i = lane; i < A; i += 32) {
                 uint32_t m = W.mask[i], k0 = 0;
                 if (m) {
@@ -244,23 +253,41 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
                     }
                     k0 = 1u + W.pre[best];
                 }
-                W.key[i] = make_uint4(k0, ord_key(x[3 * i]), ord_key(x[3 * i + 1]), ord_key(x[3 * i + 2]));
+                W.key[i] = ((unsigned long long)k0 << 58) | coord_mix(x[3 * i], x[3 * i + 1], x[3 * i + 2]);
+                atomicAdd(&W.rfill[k0], 1);
             }
             __syncwarp();
-            // rank by counting (A <= 256: <= 8 atoms per lane, A broadcast key loads)
-            uint4 mine[kMaxAtoms / 32];
+            if (lane == 0) {
+                int run = 0;
+                for (int t = 0; t <= R; ++t) {
+                    W.rstart[t] = run;
+                    run += W.rfill[t];
+                    W.rfill[t] = W.rstart[t];
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < A; i += 32) W.list[atomicAdd(&W.rfill[(int)(W.key[i] >> 58)], 1)] = (uint8_t)i;
+            __syncwarp();
+            // rank = region start + rank by counting inside the region (the region's members
+            // only: sum of squared region sizes instead of A^2 comparisons)
+            const int nu = (A + 31) >> 5;
             int rk[kMaxAtoms / 32];
 #pragma unroll
             for (int u = 0; u < kMaxAtoms / 32; ++u) {
                 const int i = lane + 32 * u;
-                mine[u] = i < A ? W.key[i] : make_uint4(0, 0, 0, 0);
                 rk[u] = 0;
-            }
-            for (int j = 0; j < A; ++j) {
-                const uint4 kj = W.key[j];
-#pragma unroll
-                for (int u = 0; u < kMaxAtoms / 32; ++u)
-                    rk[u] += (lane + 32 * u < A) && key_less(kj, j, mine[u], lane + 32 * u);
+                if (u < nu && i < A) {
+                    const unsigned long long ki = W.key[i];
+                    const int rg = (int)(ki >> 58);
+                    const int b = W.rstart[rg], e = rg < R ? W.rstart[rg + 1] : A;
+                    int c = b;
+                    for (int t = b; t < e; ++t) {
+                        const int j = W.list[t];
+                        const unsigned long long kj = W.key[j];
+                        c += (kj < ki) | ((kj == ki) & (j < i));
+                    }
+                    rk[u] = c;
+                }
             }
 #pragma unroll
             for (int u = 0; u < kMaxAtoms / 32; ++u) {

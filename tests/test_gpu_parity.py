@@ -580,14 +580,45 @@ def test_topk_merge_of_padded_lists_smaller_than_k():
 
 
 def test_mixed_layout_pockets_in_one_submit():
-    """A 32^3 pocket (fixed-stride layout) and a 36 x 30 x 26 pocket (runtime strides) in ONE submit
-    (ADVICE r1): each launch uses its own layout's class table; full parity in both."""
+    """A 32^3 pocket (fixed-stride layout), a 36 x 30 x 26 pocket (runtime strides) and a 56^3 pocket
+    (window + global) in ONE submit: each launch uses its own layout's class table; full
+    parity in all three."""
     pk1 = vsgen.pocket(101)
     pk2 = vsgen.pocket(107, n=(36, 30, 26), spacing=0.9, center_offset=(0.5, -0.5, 0.25))
+    pk3 = vsgen.pocket(109, n=56, spacing=0.75)                       # WIN mode
     lib = vsgen.ligands(40, 23, (20, 120), (0, 12))
     e = engine(debug_poses=True)
-    rot, tr, cs, ids = setup(e, [pk1, pk2], 8, 8)
+    rot, tr, cs, ids = setup(e, [pk1, pk2, pk3], 8, 8)
     e.submit_library(lib, ids)
     e.wait()
-    for slot, pk in enumerate([pk1, pk2]):
+    for slot, pk in enumerate([pk1, pk2, pk3]):
         check(e, lib, range(lib.n), pk, rot, tr, cs, slot=slot)
+
+
+# ----------------------------------------------------------------------------- grids beyond shared
+# memory (VERDICT r1 "missing" 3): the WIN mode -- a 32^3-node window around the docking centre in
+# shared memory, every other cell from the padded global copy through L1 / L2
+
+@pytest.mark.parametrize("n,h,offset", [(64, 1.0, (0.0, 0.0, 0.0)), (48, 0.5, (0.0, 0.0, 0.0)),
+                                        (64, 1.0, (19.0, -21.5, 12.0))])
+def test_large_grids_window_plus_global_path(n, h, offset):
+    """64^3 at 1 A (ligands inside the window: shared-memory path), 48^3 at 0.5 A (the window spans
+    only +-7.75 A: many corners come from global memory), and a 64^3 pocket whose centre sits near
+    a corner (the window clamps to the grid edge).  Score hook against the oracle everywhere
+    (inside / outside the window / outside the grid), then docking parity, every pose replayed."""
+    pk = vsgen.pocket(108, n=n, spacing=h, center_offset=offset)
+    e = engine()
+    pid = e.load_pocket(pk)
+    rng = np.random.default_rng(n)
+    lo = np.array(pk.origin) - 4.0
+    hi = np.array(pk.origin) + h * (n - 1) + 4.0
+    pts = rng.uniform(lo, hi, size=(40000, 3)).astype(np.float32)
+    near = (np.array(pk.center) + rng.normal(0, 6.0, size=(20000, 3))).astype(np.float32)
+    pts = np.concatenate([pts, near])
+    g = e.score_points(pid, pts)
+    ref = oracle.grid_score(pk, pts.astype(np.float64))
+    tol = 2e-6 if h == 1.0 else 2e-5      # 1/h inexact for h != 1 (see the non-cubic test)
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < tol
+    lib = vsgen.ligands(24, 50 + n, (20, 120), (0, 12))
+    e2, rot, tr, cs = run(lib, [pk], P=8, K=8)
+    check(e2, lib, range(lib.n), pk, rot, tr, cs)
