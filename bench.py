@@ -26,14 +26,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FLOPS_PER_EVAL = 43          # rotation 18 + fractions 3 + 7 lerps x 3 + accumulate 1
+BYTES_PER_EVAL = 32          # 8 fp32 corners
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4 (SMs x FP32 lanes x FMA x max clock)
 SMEM_PEAK_TBPS = 148 * 128 * 1.965e9 / 1e12          # 37.2: 128 B / clk / SM shared-memory crossbar (guide)
-# measured ceiling of random 8-corner trilinear gathers from a shared-memory 32^3 grid on this
-# B200 (tools/microbench_gather.cu, profiles/r01_gather_microbench.txt): 337 G evaluations / s
-GATHER_CEILING_EVALS = 337.4e9
-# measured L2 read bandwidth of this B200 (tools/microbench_l2.cu, 48-96 MB L2-resident buffer,
-# ld.global.cg; profiles/r01_l2_microbench.txt): BJ's "FP32/L2" roof = min(FP32, AI x BW_L2)
-L2_READ_TBPS = 16.6
+
+
+def measure_ceilings():
+    """The roofline denominators, measured LIVE on this GPU (tools/ceilings.cu): L2 read bandwidth
+    (48 MB L2-resident buffer) and random 8-corner shared-memory gathers per second."""
+    import ctypes
+    so = os.path.join(ROOT, "tools", "libceilings.so")
+    src = os.path.join(ROOT, "tools", "ceilings.cu")
+    if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
+                               "-shared", "-o", so, src])
+    lib = ctypes.CDLL(so)
+    lib.l2_read_gbps.restype = ctypes.c_double
+    lib.l2_read_gbps.argtypes = [ctypes.c_size_t, ctypes.c_int]
+    lib.smem_gather_gevals.restype = ctypes.c_double
+    lib.smem_gather_gevals.argtypes = [ctypes.c_int, ctypes.c_int]
+    return {"l2_read_TBps": lib.l2_read_gbps(48 << 20, 20) / 1e3,
+            "gather_evals_per_s": lib.smem_gather_gevals(4096, 512) * 1e9}
 
 
 def parse():
@@ -278,6 +291,9 @@ def main():
         achieved = reduce_scalar(achieved, dist.ReduceOp.MIN)
         exec_rate = reduce_scalar(exec_rate, dist.ReduceOp.MIN)
     classes = eng.classes()
+    torch.cuda.synchronize()
+    ceil = measure_ceilings()          # after the timed region: live roofline denominators
+    roof = min(FP32_PEAK_TFLOPS, FLOPS_PER_EVAL / BYTES_PER_EVAL * ceil["l2_read_TBps"])
 
     e2e = None
     if not args.no_e2e:
@@ -348,30 +364,26 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": describe(c, args, world),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                         "kernel": "dock_kernel<AC,NW> (all launches of the dock phase)",
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": roof, "unit": "TFLOP/s",
+                         "frac": achieved / roof, "traffic": traffic,
+                         "kernel": "dock_kernel<AC,NW,PPW,GM,K> (all launches of the dock phase)",
+                         "peak_source": "BASELINE.json's 'FP32/L2 roofline' (SURVEY 8(d)): min(FP32 peak, 43/32 "
+                                        "flop/B x L2 read bandwidth measured live in this run by tools/ceilings.cu); "
+                                        "FP32 peak = 148 SMs x 128 lanes x 2 x 1.965 GHz (guide unit counts)",
                          "dock_ms_per_step": dock_avg, "evals_per_step": evals_step,
-                         "flops_per_eval": FLOPS_PER_EVAL,
-                         "fp32_l2": {"peak": min(FP32_PEAK_TFLOPS, FLOPS_PER_EVAL / 32 * L2_READ_TBPS),
-                                     "unit": "TFLOP/s", "l2_read_TBps": L2_READ_TBPS,
-                                     "ai_flop_per_byte": FLOPS_PER_EVAL / 32,
-                                     "frac": achieved / min(FP32_PEAK_TFLOPS, FLOPS_PER_EVAL / 32 * L2_READ_TBPS),
-                                     "note": "BASELINE.json's 'FP32/L2 roofline' (SURVEY 8(d)): achieved / "
-                                             "min(FP32 peak, algorithmic intensity x measured L2 bandwidth); the "
-                                             "grid itself is served from shared memory"},
+                         "flops_per_eval": FLOPS_PER_EVAL, "l2_read_TBps_measured": ceil["l2_read_TBps"],
+                         "fp32": {"peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS},
                          "smem": {"bound": "smem", "unit": "TB/s",
-                                  "achieved": achieved / FLOPS_PER_EVAL * 32,
+                                  "achieved": achieved / FLOPS_PER_EVAL * BYTES_PER_EVAL,
                                   "peak": SMEM_PEAK_TBPS,
-                                  "frac": achieved / FLOPS_PER_EVAL * 32 / SMEM_PEAK_TBPS,
-                                  "bytes_per_eval": 32,
+                                  "frac": achieved / FLOPS_PER_EVAL * BYTES_PER_EVAL / SMEM_PEAK_TBPS,
+                                  "bytes_per_eval": BYTES_PER_EVAL,
                                   "executed_evals_per_s": exec_rate,
-                                  "random_gather_ceiling_evals_per_s": GATHER_CEILING_EVALS,
-                                  "frac_of_gather_ceiling": exec_rate / GATHER_CEILING_EVALS,
+                                  "random_gather_ceiling_evals_per_s": ceil["gather_evals_per_s"],
+                                  "frac_of_gather_ceiling": exec_rate / ceil["gather_evals_per_s"],
                                   "note": "8 fp32 corner gathers per evaluation from the shared-memory grid; random "
-                                          "4-byte gathers run ~3.1-way bank-conflicted, so the measured ceiling "
-                                          "(microbenchmark) is ~1/3.2 of the crossbar peak"},
-                         "peak_source": "148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (guide unit counts, max clock)"},
+                                          "4-byte gathers run ~3-way bank-conflicted, so the gather ceiling (measured "
+                                          "live, uniformly random points) is ~1/3.5 of the crossbar peak"}},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
             "cpu_baseline": cpu, "unsorted": unsorted,
             "classes": [{k: cl[k] for k in ("kernel_atoms", "warps_per_cta", "regs_per_thread", "dyn_smem", "blocks_per_sm",

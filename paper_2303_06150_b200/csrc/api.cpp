@@ -138,6 +138,8 @@ struct vs_ctx {
     const uint64_t* d_lid = nullptr;   // ligand ids of the batch (null: ids = indices)
     uint8_t* d_order = nullptr;        // a1: internal atom -> input atom, CSR by atom_off
     int4* d_frint = nullptr;           // a1: fragments in internal numbering {a, b, lo, hi}
+    uint8_t* d_fown = nullptr;         // a1: own-region length per fragment
+    int* d_lflag = nullptr;            // a1: n_root | ancestors-first << 16 per ligand
     int *d_featA = nullptr, *d_featR = nullptr, *d_featM = nullptr, *d_cell = nullptr, *d_hist = nullptr,
         *d_cell_count = nullptr, *d_maxAR = nullptr;
     unsigned long long* d_status = nullptr;  // [0] validation, [1] overflow
@@ -260,7 +262,7 @@ size_t score_grid_floats(const PocketDev& pk) {
 
 // Stage-1 workspace (known from the batch sizes alone).
 struct Stage1 {
-    size_t atom_off, frag_off, xyz, lid, frag_axis, move_off, move_atoms, order, frint, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
+    size_t atom_off, frag_off, xyz, lid, frag_axis, move_off, move_atoms, order, frint, fown, lflag, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
         bsize, weights, own_start, own_prefix, own_ac, own_rec_off, pose, cs, grids, end;
     int n_blocks;
     int64_t max_buckets;
@@ -286,6 +288,8 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t
     s.move_atoms = r.add(nM * 4);
     s.order = r.add(nA);
     s.frint = r.add(nR * 16);
+    s.fown = r.add(nR);
+    s.lflag = r.add(n * 4);
     s.featA = r.add(n * 4);
     s.featR = r.add(n * 4);
     s.featM = r.add(n * 4);
@@ -569,7 +573,7 @@ vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n
     // Q16 fallback boundary 32*n for the last class can exceed the observed maximum
     ac_max = std::min(kMaxAtoms, std::max(ac_max, std::min(kMaxAtoms, roundup32(max_atoms))));
     const Stage1 s1 = plan1(n_lig, n_atoms, n_frags, n_moving, c->P, c->K, max_grid_bytes(c), n_pockets);
-    const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * (3 * ac_max + 32), c->P,
+    const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * rec_floats_of(ac_max), c->P,
                             c->cfg.n_sweeps, n_pockets, c->cfg.debug_poses != 0);
     *bytes = s2.end + 4096;
     return VS_OK;
@@ -680,6 +684,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     for (int i = 0; i < n_pockets; ++i) c->d_grid[i] = (float*)(W + s1.grids + (size_t)i * gmax);
     c->d_order = W + s1.order;
     c->d_frint = (int4*)(W + s1.frint);
+    c->d_fown = W + s1.fown;
+    c->d_lflag = (int*)(W + s1.lflag);
     if (batch->on_device) {
         c->d_atom_off = (int64_t*)batch->atom_off;
         c->d_frag_off = (int64_t*)batch->frag_off;
@@ -741,7 +747,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     CK(cudaMemsetAsync(c->d_status, 0xFF, 16, ms));
     CK(cudaMemsetAsync(c->d_maxAR, 0, 8, ms));
     CK(launch_ingest(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frag_axis, c->d_move_off, c->d_move_atoms, n,
-                     c->d_order, c->d_frint, c->d_featA, c->d_featR, c->d_featM, c->d_status, c->d_maxAR, ms));
+                     c->d_order, c->d_frint, c->d_fown, c->d_lflag, c->d_featA, c->d_featR, c->d_featM, c->d_status,
+                     c->d_maxAR, ms));
     ++launches;
     vs_status st = ensure_pinned(c, (size_t)(s1.max_buckets + 16) * 32 + kMaxCells * 8 + 64);
     if (st) return st;
@@ -885,7 +892,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         const vs_bucket& b = c->buckets[c->owned[i]];
         c->owned_prefix[i + 1] = c->owned_prefix[i] + b.size;
         c->owned_rec_off[i] = rec_floats;
-        rec_floats += (int64_t)b.size * (3 * b.kernel_atoms + 32);
+        rec_floats += (int64_t)b.size * rec_floats_of(b.kernel_atoms);
         evals += (double)b.weight;
     }
     c->total_slots = c->owned_prefix[no];
@@ -934,7 +941,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         }
     }
     CK(launch_pack(c->d_perm, c->d_own_start, c->d_own_prefix, c->d_own_ac, c->d_own_rec_off, no, c->total_slots,
-                   c->d_atom_off, c->d_xyz, c->d_order, c->d_frag_off, c->d_frint, S_w, c->d_rec, c->d_meta, ms));
+                   c->d_atom_off, c->d_xyz, c->d_order, c->d_frag_off, c->d_frint, c->d_fown, c->d_lflag, S_w,
+                   c->d_rec, c->d_meta, ms));
     ++launches;
     for (int i = 0; i < n_pockets; ++i) {
         CK(launch_fill_results(c->d_score[i], c->d_pose_best[i], n, c->d_ang[i], (int64_t)S_w * nR, ms));
@@ -972,7 +980,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.rec = c->d_rec + c->owned_rec_off[i];
             a.meta = c->d_meta + c->owned_prefix[i];
             a.n = u.slots;
-            a.rec_floats = 3 * b.kernel_atoms + 32;
+            a.rec_floats = rec_floats_of(b.kernel_atoms);
             a.P = c->P;
             a.K = c->K;
             a.S_w = S_w;
@@ -1075,7 +1083,7 @@ vs_status vs_get_coords(vs_ctx* c, int32_t slot, float* xyz_out, int32_t on_devi
         a.rec = c->d_rec + c->owned_rec_off[i];
         a.meta = c->d_meta + c->owned_prefix[i];
         a.n = b.size;
-        a.rec_floats = 3 * b.kernel_atoms + 32;
+        a.rec_floats = rec_floats_of(b.kernel_atoms);
         a.P = c->P;
         a.K = c->K;
         a.S_w = c->cfg.n_sweeps;

@@ -254,10 +254,12 @@ struct PoseBuf {
 };
 
 // U independent sweep evaluations per lane: atoms j0, j0 + apw, ... (j < hi), rotated by M,
-// scored, summed into acc in ascending order; the rotated atoms stay in kp[0..U).
+// scored, summed into acc in ascending order; the atoms j < own_end (the step's finalised own
+// region) are also summed into own; the rotated atoms stay in kp[0..U).
 template <int U, int GM, int AC>
 __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, const float* __restrict__ G,
-                                           const PocketDev& pk, int j0, int apw, int hi, float& acc, float4 (&kp)[4]) {
+                                           const PocketDev& pk, int j0, int apw, int hi, int own_end, float& acc,
+                                           float& own, float4 (&kp)[4]) {
     float4 v[U];
     float g[U];
 #pragma unroll
@@ -270,8 +272,11 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
 #pragma unroll
     for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, kp[u].x, kp[u].y, kp[u].z, pk);
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-        if (j0 + u * apw < hi) acc = __fadd_rn(acc, g[u]);
+    for (int u = 0; u < U; ++u) {
+        const int j = j0 + u * apw;
+        if (j < hi) acc = __fadd_rn(acc, g[u]);
+        if (j < own_end) own = __fadd_rn(own, g[u]);
+    }
 }
 
 // PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
@@ -295,6 +300,15 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     const float* ry = rec + AC;
     const float* rz = rec + 2 * AC;
     const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
+    const uint8_t* rown = reinterpret_cast<const uint8_t*>(rec + 3 * AC + 32);
+    const uint32_t hdr = reinterpret_cast<const uint32_t*>(rec + 3 * AC + 40)[0];
+    // finalised own regions: with ancestors swept before descendants, the atoms
+    // whose innermost moving set is r (the first rown[r] atoms of r's range) never move after
+    // step r of the last sweep, so the winner's partial sum over them is their final score;
+    // the pose score then needs a final pass over the n_root atoms in no set only
+    const bool fin = K > 1 && ((hdr >> 16) & 1u);
+    const int n_final = fin ? (int)(hdr & 0xffffu) : A;
+    float fsum = 0.f;   // finalised own-region scores, in fragment order
     {
         const RotT Pz = load_pose(T);
         if (valid)
@@ -320,20 +334,26 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 // warp dock the same ligand), so the batch dispatch below never diverges.
                 // Every lane sums its atoms in ascending order (the canonical order).
                 const int nst = (hi - lo + apw - 1) >> abits;
-                float acc = 0.f;
+                const bool last = fin && sw == S_w - 1;
+                const int own_end = last ? lo + rown[r] : lo;
+                float acc = 0.f, own = 0.f;
                 float4 kp[4];
                 int st = 0;
-                for (; st + 4 <= nst; st += 4) eval_batch<4, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp);
+                for (; st + 4 <= nst; st += 4)
+                    eval_batch<4, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp);
                 switch (nst - st) {
-                    case 3: eval_batch<3, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
-                    case 2: eval_batch<2, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
-                    case 1: eval_batch<1, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, acc, kp); break;
+                    case 3: eval_batch<3, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
+                    case 2: eval_batch<2, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
+                    case 1: eval_batch<1, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
                     default: break;
                 }
                 // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
 #pragma unroll
                 for (int o = 1; o < LPP; o <<= 1)
-                    if (o >= Kp) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                    if (o >= Kp) {
+                        acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                        if (last) own = __fadd_rn(own, __shfl_xor_sync(FULL, own, o));
+                    }
                 // argmin over the K angles of this group (xor offsets 1 .. Kp/2); ties -> lowest k (Q11)
                 const unsigned key = kreal ? ord32(acc) : 0xffffffffu;
                 unsigned mn = key;
@@ -342,6 +362,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                     if (o < Kp) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
                 const unsigned bal = __ballot_sync(FULL, key == mn && kreal) & gmask;
                 const int bk = (__ffs(bal) - 1) & (Kp - 1);
+                if (last) fsum = __fadd_rn(fsum, __shfl_sync(FULL, own, (lane & ~(LPP - 1)) | bk));
                 if (nst <= 4) {
                     // one batch: the lanes (jl, k*) still hold the rotated atoms in registers
                     if (valid && bk != 0 && k == bk) {
@@ -371,11 +392,12 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     } else if (valid) {
         for (int t = li; t < S_w * R; t += LPP) angOut[t] = 0;
     }
-    // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree) (Q22)
-    // four independent evaluations in flight, summed in the same ascending order
+    // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree, then the
+    // finalised own regions in fragment order) (Q22); four independent evaluations in flight,
+    // summed in the same ascending order
     float acc = 0.f;
     int i = li;
-    for (; i + 3 * LPP < A; i += 4 * LPP) {
+    for (; i + 3 * LPP < n_final; i += 4 * LPP) {
         float g[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -385,12 +407,13 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, g[u]);
     }
-    for (; i < A; i += LPP) {
+    for (; i < n_final; i += LPP) {
         const float4 v = B.get(i);
         acc = __fadd_rn(acc, grid_g<GM>(G, v.x, v.y, v.z, pk));
     }
 #pragma unroll
     for (int o = LPP / 2; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+    if (fin) acc = __fadd_rn(acc, fsum);
     if (valid && li == 0) *scoreOut = acc;
     __syncwarp();
 }

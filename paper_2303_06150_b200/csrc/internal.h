@@ -70,6 +70,11 @@ struct DockArgs {
     const uint8_t* order;      // finalize only: internal atom -> input atom (CSR by atom_off, a1)
 };
 
+// Packed ligand record of atom class AC (floats): x | y | z (3 AC), fragment table u32[32],
+// own-region lengths u8[32] (8 words), header (n_root | ancestors-first << 16) + 3 pad words;
+// a multiple of 4 floats (16-byte TMA granularity).
+__host__ __device__ constexpr int rec_floats_of(int AC) { return 3 * AC + 44; }
+
 // Per-pose coordinate buffer stride (floats): 3 AC + 8, i.e. 8 banks apart, so the 4 pose
 // groups of a warp write 8-atom blocks of (x, y) pairs in 2 wavefronts and of z in 1 (the
 // sweep's broadcast loads stay conflict-free).
@@ -106,7 +111,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int m
     L.pose = o;   // pose table: read per warp item from global (L1-resident), no shared copy
     L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
     size_t q = 0;
-    L.rec_o = q;   q += align16((size_t)LC * (3 * AC + 32) * 4);
+    L.rec_o = q;   q += align16((size_t)LC * rec_floats_of(AC) * 4);
     L.meta_o = q;  q += (size_t)LC * 16;
     L.score_o = q; q += align16((size_t)LC * P * 4);
     L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC));
@@ -130,7 +135,8 @@ void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
                           const int64_t* move_off, const int32_t* move_atoms, int64_t n, uint8_t* order, int4* frint,
-                          int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st);
+                          uint8_t* fown, int* lflag, int* featA, int* featR, int* featM, unsigned long long* status,
+                          int* maxAR, cudaStream_t st);
 cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
                                  const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
                                  unsigned long long* ovf, cudaStream_t st);
@@ -143,8 +149,8 @@ cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const 
 // Pack owned buckets.  slot_bucket_prefix[b] = first packed slot of owned bucket b (nb+1 entries).
 cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
-                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint, int S_w,
-                        float* rec, int4* meta, cudaStream_t st);
+                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint,
+                        const uint8_t* fown, const int* lflag, int S_w, float* rec, int4* meta, cudaStream_t st);
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int gmode, int K, cudaFuncAttributes* attr);
 cudaError_t dock_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int* blocks_per_sm);

@@ -64,7 +64,21 @@ struct IngestWarp {
     uint8_t rank[kMaxAtoms];            // input index -> internal position
     uint8_t list[kMaxAtoms];            // atoms grouped by region (key >> 58)
     int rstart[kMaxFrags + 2], rfill[kMaxFrags + 2];   // region start / fill cursor
+    int moff[kMaxFrags + 1];            // the ligand's moving-atom entries of fragment r: [moff[r], moff[r+1])
+    uint32_t sup[kMaxFrags], inter[kMaxFrags];
+    int lo[kMaxFrags], hi[kMaxFrags];
 };
+
+// Fragment of moving-atom entry t of the ligand (moff strictly increasing: every set non-empty).
+__device__ __forceinline__ int frag_of(const int* moff, int R, int t) {
+    int lo = 0, hi = R;   // moff[lo] <= t < moff[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (moff[mid] <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
 
 // 58-bit mix of an atom's coordinate bits (-0 canonicalised to +0): a canonical tie-break
 // among the free atoms of one set region that does not depend on the input numbering.
@@ -88,8 +102,9 @@ __device__ __forceinline__ int first_code(int code) {   // lowest lane's non-zer
 __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
     const int64_t* __restrict__ atom_off, const float* __restrict__ xyz, const int64_t* __restrict__ frag_off,
     const int32_t* __restrict__ frag_axis, const int64_t* __restrict__ move_off, const int32_t* __restrict__ move_atoms,
-    int64_t n, uint8_t* __restrict__ order, int4* __restrict__ frint, int* __restrict__ featA, int* __restrict__ featR,
-    int* __restrict__ featM, unsigned long long* status, int* maxAR) {
+    int64_t n, uint8_t* __restrict__ order, int4* __restrict__ frint, uint8_t* __restrict__ fown,
+    int* __restrict__ lflag, int* __restrict__ featA, int* __restrict__ featR, int* __restrict__ featM,
+    unsigned long long* status, int* maxAR) {
     __shared__ IngestWarp sw[kIngestWarps];
     __shared__ int smax[2];
     if (threadIdx.x < 2) smax[threadIdx.x] = 0;
@@ -140,18 +155,24 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
             }
             code = first_code(fc);
         }
+        // the ligand's moving-atom entries are one contiguous range of move_atoms (CSR): the
+        // passes below run flat over it, each entry finding its fragment by binary search
+        const int64_t mbase = R > 0 ? __shfl_sync(FULL, m0, 0) : 0;
+        int total = 0;
         if (code == 0) {   // membership masks; index range and duplicates
             for (int i = lane; i < A; i += 32) W.mask[i] = 0u;
+            if (lane < R) W.moff[lane] = (int)(m0 - mbase);
+            if (lane == 0) W.moff[R] = 0;
             __syncwarp();
+            if (R > 0 && lane == R - 1) W.moff[R] = (int)(m0 - mbase) + cnt;
+            __syncwarp();
+            total = W.moff[R];
             bool oob = false, dup = false;
-            for (int r = 0; r < R; ++r) {
-                const int64_t b0 = __shfl_sync(FULL, m0, r);
-                const int c = __shfl_sync(FULL, cnt, r);
-                for (int t = lane; t < c; t += 32) {
-                    const int i = move_atoms[b0 + t];
-                    if (i < 0 || i >= A) oob = true;
-                    else if (atomicOr(&W.mask[i], 1u << r) & (1u << r)) dup = true;
-                }
+            for (int t = lane; t < total; t += 32) {
+                const int r = frag_of(W.moff, R, t);
+                const int i = move_atoms[mbase + t];
+                if (i < 0 || i >= A) oob = true;
+                else if (atomicOr(&W.mask[i], 1u << r) & (1u << r)) dup = true;
             }
             if (__any_sync(FULL, oob)) code = 9;
             else if (__any_sync(FULL, dup)) code = 10;
@@ -167,25 +188,22 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
             // laminar family: sup_r = {s : M_r within M_s} (AND of the members' masks),
             // inter_r = {s : M_s meets M_r} (OR); sub_r = {s : M_s within M_r} (transpose of sup).
             // Laminar iff every set meeting M_r contains it or is contained in it.
+            if (lane < R) {
+                W.sup[lane] = 0xffffffffu;
+                W.inter[lane] = 0u;
+            }
+            __syncwarp();
+            for (int t = lane; t < total; t += 32) {
+                const int r = frag_of(W.moff, R, t);
+                const uint32_t m = W.mask[move_atoms[mbase + t]];
+                atomicAnd(&W.sup[r], m);
+                atomicOr(&W.inter[r], m);
+            }
+            __syncwarp();
             uint32_t inter = 0;
-            for (int r = 0; r < R; ++r) {
-                const int64_t b0 = __shfl_sync(FULL, m0, r);
-                const int c = __shfl_sync(FULL, cnt, r);
-                uint32_t s_and = 0xffffffffu, s_or = 0u;
-                for (int t = lane; t < c; t += 32) {
-                    const uint32_t m = W.mask[move_atoms[b0 + t]];
-                    s_and &= m;
-                    s_or |= m;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    s_and &= __shfl_xor_sync(FULL, s_and, o);
-                    s_or |= __shfl_xor_sync(FULL, s_or, o);
-                }
-                if (lane == r) {
-                    sup = s_and & valid;
-                    inter = s_or & valid;
-                }
+            if (lane < R) {
+                sup = W.sup[lane] & valid;
+                inter = W.inter[lane] & valid;
             }
             for (int r = 0; r < R; ++r) {
                 const uint32_t col = __ballot_sync(FULL, lane < R && ((sup >> r) & 1u));
@@ -299,28 +317,36 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
             }
             __syncwarp();
             // internal fragments: every moving set is now the range [min rank, max rank + 1)
-            for (int r = 0; r < R; ++r) {
-                const int64_t b0 = __shfl_sync(FULL, m0, r);
-                const int c = __shfl_sync(FULL, cnt, r);
-                int lo = kMaxAtoms, hi = -1;
-                for (int t = lane; t < c; t += 32) {
-                    const int q = W.rank[move_atoms[b0 + t]];
-                    lo = min(lo, q);
-                    hi = max(hi, q);
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    lo = min(lo, __shfl_xor_sync(FULL, lo, o));
-                    hi = max(hi, __shfl_xor_sync(FULL, hi, o));
-                }
-                if (lane == r) frint[f0 + r] = make_int4(W.rank[fa], W.rank[fb], lo, hi + 1);
-                M += c;
+            if (lane < R) {
+                W.lo[lane] = kMaxAtoms;
+                W.hi[lane] = -1;
             }
+            __syncwarp();
+            for (int t = lane; t < total; t += 32) {
+                const int r = frag_of(W.moff, R, t);
+                const int q = W.rank[move_atoms[mbase + t]];
+                atomicMin(&W.lo[r], q);
+                atomicMax(&W.hi[r], q);
+            }
+            __syncwarp();
+            if (lane < R) {
+                frint[f0 + lane] = make_int4(W.rank[fa], W.rank[fb], W.lo[lane], W.hi[lane] + 1);
+                // own region of r: the atoms whose innermost set is r -- the first own atoms of
+                // its range (preorder), final after step r when no ancestor sweeps later
+                const int rg = 1 + W.pre[lane];
+                fown[f0 + lane] = (uint8_t)(W.rfill[rg] - W.rstart[rg]);
+            }
+            // ancestors-first fragment order (every ancestor of r has a lower index): the dock
+            // kernel then finalises each own region in the sweep
+            const bool anc_first = __all_sync(FULL, lane >= R || (W.anc[lane] >> lane) == 0u);
+            if (lane == 0) lflag[li] = (W.rfill[0] - W.rstart[0]) | (anc_first ? (1 << 16) : 0);
+            M = total;
             __syncwarp();
         }
         if (code == 0) {
             locA = max(locA, A);
             locR = max(locR, R);
+            if (R == 0 && lane == 0) lflag[li] = A | (1 << 16);   // no sets: every atom is root
         }
         if (lane == 0) {
             featA[li] = (int)(A64 > 0x7fffffff ? 0x7fffffff : (A64 < 0 ? 0 : A64));
@@ -481,8 +507,9 @@ __global__ void __launch_bounds__(256) bucket_weights_kernel(const uint32_t* __r
     }
 }
 
-// a5: one warp per packed slot.  Record layout (floats): x[AC] | y[AC] | z[AC] |
-// frags u32[32] = a | b << 8 | lo << 16 | (hi - 1) << 24.  Coordinates are
+// a5: one warp per packed slot.  Record layout (floats, rec_floats_of): x[AC] | y[AC] | z[AC] |
+// frags u32[32] = a | b << 8 | lo << 16 | (hi - 1) << 24 | own-region lengths u8[32] |
+// header u32 (n_root | ancestors-first << 16) + 3 pad words.  Coordinates are
 // centred on the ligand centroid (a6, Q8); padding is 0.  The centroid sum is
 // lane-strided then xor-reduced: an order that does not depend on AC (Q22).
 __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ perm,
@@ -494,7 +521,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
                                                    const float* __restrict__ xyz,
                                                    const uint8_t* __restrict__ order,
                                                    const int64_t* __restrict__ frag_off,
-                                                   const int4* __restrict__ frint, int S_w,
+                                                   const int4* __restrict__ frint,
+                                                   const uint8_t* __restrict__ fown,
+                                                   const int* __restrict__ lflag, int S_w,
                                                    float* __restrict__ rec, int4* __restrict__ meta) {
     const int lane = threadIdx.x & 31;
     const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -508,7 +537,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     const int s = slot - owned_prefix[b];
     const uint32_t li = perm[owned_start[b] + s];
     const int AC = owned_ac[b];
-    float* r = rec + owned_rec_off[b] + (int64_t)s * (3 * AC + 32);
+    float* r = rec + owned_rec_off[b] + (int64_t)s * rec_floats_of(AC);
     const int64_t a0 = atom_off[li];
     const int A = (int)(atom_off[li + 1] - a0);
     const int64_t f0 = frag_off[li];
@@ -553,6 +582,11 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
         f = (uint32_t)q.x | ((uint32_t)q.y << 8) | ((uint32_t)q.z << 16) | ((uint32_t)(q.w - 1) << 24);
     }
     reinterpret_cast<uint32_t*>(r + 3 * AC)[lane] = f;
+    // own-region lengths (bytes) and the header: n_root | ancestors-first << 16
+    const uint8_t own = lane < R ? fown[f0 + lane] : (uint8_t)0;
+    uint8_t* ob = reinterpret_cast<uint8_t*>(r + 3 * AC + 32);
+    ob[lane] = own;
+    if (lane < 4) reinterpret_cast<uint32_t*>(r + 3 * AC + 40)[lane] = lane == 0 ? (uint32_t)lflag[li] : 0u;
     if (lane == 0) meta[slot] = make_int4((int)li, A, R, (int)(S_w * f0));
 }
 
@@ -582,12 +616,14 @@ __global__ void make_keys_kernel(const int4* __restrict__ meta, int n_slots, con
 
 cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
                           const int64_t* move_off, const int32_t* move_atoms, int64_t n, uint8_t* order, int4* frint,
-                          int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st) {
+                          uint8_t* fown, int* lflag, int* featA, int* featR, int* featM, unsigned long long* status,
+                          int* maxAR, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     int64_t blocks = (n + kIngestWarps - 1) / kIngestWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
     ingest_kernel<<<(int)blocks, kIngestWarps * 32, 0, st>>>(atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, n,
-                                                             order, frint, featA, featR, featM, status, maxAR);
+                                                             order, frint, fown, lflag, featA, featR, featM, status,
+                                                             maxAR);
     return cudaGetLastError();
 }
 
@@ -624,12 +660,12 @@ cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const 
 
 cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
-                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint, int S_w,
-                        float* rec, int4* meta, cudaStream_t st) {
+                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint,
+                        const uint8_t* fown, const int* lflag, int S_w, float* rec, int4* meta, cudaStream_t st) {
     if (total_slots <= 0) return cudaSuccess;
     pack_kernel<<<(total_slots + 7) / 8, 256, 0, st>>>(perm, owned_start, owned_prefix, owned_ac, owned_rec_off,
                                                        n_owned_buckets, total_slots, atom_off, xyz, order, frag_off,
-                                                       frint, S_w, rec, meta);
+                                                       frint, fown, lflag, S_w, rec, meta);
     return cudaGetLastError();
 }
 
