@@ -235,12 +235,18 @@ def main():
         ids = [e.load_pocket(p) for p in pockets]
         return e, ids
 
+    from paper_2303_06150_b200 import VsError
+
     def step(e, ids, batch, on_device, host_out=None):
-        e.submit(*batch, ids, on_device=on_device, max_atoms=max_atoms)
-        e.wait()
+        failed = None
+        try:
+            e.submit(*batch, ids, on_device=on_device, max_atoms=max_atoms)
+            e.wait()
+        except VsError as err:     # rank-local a1 error: every rank learns it from the gather
+            failed = err
         tops = []
         for s in range(len(ids)):
-            tops.append(parallel.global_topk(e, s, K_TOP))   # a10 local top-k, a11 NCCL all_gather + merge
+            tops.append(parallel.global_topk(e, s, K_TOP, failed=failed))   # a10 + a11 NCCL all_gather + merge
             if host_out is not None:     # D2H of the step's per-ligand result (score, pose)
                 e.results_device(s, host_out[0], host_out[1])
         return tops

@@ -125,7 +125,11 @@ vs_status vs_set_angle_table(vs_ctx* ctx, int32_t K, const float* cos_sin);
  * Fragments are swept in input order (Q4).  ligand_id[n] (may be NULL: ids = batch
  * indices) is passed through to vs_get_results and vs_merge_topk.  atom_off[0],
  * frag_off[0] and move_off[0] must be 0.  on_device = 1: every pointer is a device
- * pointer (borrowed until vs_wait); 0: host memory, copied during vs_submit. */
+ * pointer (borrowed until vs_wait); 0: host memory, copied during vs_submit;
+ * 2: PINNED (page-locked) host memory, mapped: the three offset arrays are copied, and
+ * the kernels read coordinates, axes, moving atoms and ids over PCIe only for the
+ * ligands this rank docks -- each GPU moves its own share, as the paper's per-GPU
+ * workers copy their own buckets; borrowed until vs_wait. */
 typedef struct {
     int64_t n;
     const uint64_t* ligand_id;   /* [n] or NULL */
@@ -139,6 +143,10 @@ typedef struct {
 } vs_ligand_batch;
 
 /* Run the hot path a1..a9 for the batch against pockets pocket_ids[0..n_pockets):
+ * a1 features + range checks (A, R) of every ligand (all ranks agree on them), the plan
+ * (a2-a4), then a1's per-atom checks and renumbering for THIS rank's ligands only -- a
+ * VS_E_PARSE for one of them is rank-local (parallel.py carries it through the all-gather
+ * so no rank waits on a collective the others never reach); then pack and dock.
  * validate, classify, bucket (stable), LPT-shard, pack, and dock this rank's
  * buckets into every pocket.  Asynchronous after the three small host syncs of
  * the preparation phase; results are valid after vs_wait.  The pose / angle
@@ -235,6 +243,8 @@ typedef struct {
     int64_t kernel_launches;   /* kernels launched by the last submit (+ topk/coords calls since) */
     int64_t dock_launches;
     double evals_alg;          /* sum over owned ligands and pockets of E_alg (SURVEY 8 'E_alg') */
+    uint64_t h2d_bytes;        /* bytes the submit moved host -> device: copies (on_device 0), or
+                                  the offsets + the owned ligands' arrays read in place (2); 0 for 1 */
     float prep_ms;             /* validate .. pack (CUDA events) */
     float dock_ms;             /* all dock launches, first start to last end (CUDA events) */
     float topk_ms;             /* last vs_local_topk */

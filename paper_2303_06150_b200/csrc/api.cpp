@@ -294,14 +294,14 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t
     s.featR = r.add(n * 4);
     s.featM = r.add(n * 4);
     s.cell = r.add(n * 4);
-    s.status = r.add(16);
+    s.status = r.add(24);   // [0] features, [1] classify overflow, [2] ingest of the owned ligands
     s.maxAR = r.add(8);
     s.hist = r.add((size_t)kMaxCells * s.n_blocks * 4);
     s.cell_count = r.add(kMaxCells * 4);
     s.perm = r.add(n * 4);
     s.bstart = r.add(s.max_buckets * 8);
     s.bsize = r.add(s.max_buckets * 4);
-    s.weights = r.add(s.max_buckets * 8);
+    s.weights = r.add(s.max_buckets * 32);
     s.own_start = r.add(s.max_buckets * 8);
     s.own_prefix = r.add((s.max_buckets + 1) * 4);
     s.own_ac = r.add(s.max_buckets * 4);
@@ -594,7 +594,7 @@ vs_status vs_set_workspace(vs_ctx* c, void* ptr, size_t bytes) {
 vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets) {
     if (!c || !batch) return VS_E_ARG;
     c->submitted = false;
-    c->stats = vs_stats{};
+    c->stats = vs_stats{};   // every field of the last submit, written below
     if (c->P < 1 || c->K < 1) return fail(c, VS_E_STATE, "set the pose and angle tables first");
     if (n_pockets < 1 || n_pockets > 16 || !pocket_ids) return fail(c, VS_E_ARG, "need 1..16 pockets");
     for (int i = 0; i < n_pockets; ++i)
@@ -612,7 +612,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     int64_t nA = 0, nR = 0, nM = 0;
     if (n > 0) {
         if (!batch->atom_off || !batch->xyz || !batch->frag_off) return fail(c, VS_E_ARG, "null batch array");
-        if (batch->on_device) {
+        if (batch->on_device < 0 || batch->on_device > 2) return fail(c, VS_E_ARG, "on_device must be 0, 1 or 2");
+        if (batch->on_device == 1) {
             CK(cudaMemcpy(&nA, batch->atom_off + n, 8, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(&nR, batch->frag_off + n, 8, cudaMemcpyDeviceToHost));
             int64_t z[2];
@@ -686,7 +687,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->d_frint = (int4*)(W + s1.frint);
     c->d_fown = W + s1.fown;
     c->d_lflag = (int*)(W + s1.lflag);
-    if (batch->on_device) {
+    if (batch->on_device == 1) {
         c->d_atom_off = (int64_t*)batch->atom_off;
         c->d_frag_off = (int64_t*)batch->frag_off;
         c->d_xyz = (float*)batch->xyz;
@@ -694,6 +695,33 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         c->d_move_off = (int64_t*)batch->move_off;
         c->d_move_atoms = (int32_t*)batch->move_atoms;
         c->d_lid = batch->ligand_id;
+    } else if (batch->on_device == 2) {
+        // mapped pinned host memory: the offsets are copied (every rank plans the whole batch);
+        // coordinates, axes, moving atoms and ids are read by the kernels over PCIe, only for
+        // the ligands this rank docks (the owned-only upload of multi-GPU runs)
+        auto mapped = [&](const void* p, const void** out) -> vs_status {
+            *out = nullptr;
+            if (!p) return VS_OK;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+                cudaGetLastError();
+                return fail(c, VS_E_ARG, "on_device = 2 needs pinned (page-locked, mapped) host arrays");
+            }
+            *out = at.devicePointer;
+            return VS_OK;
+        };
+        const void *px = nullptr, *pa = nullptr, *pm = nullptr, *pl = nullptr;
+        vs_status mst;
+        if ((mst = mapped(batch->xyz, &px)) || (mst = mapped(batch->frag_axis, &pa)) ||
+            (mst = mapped(batch->move_atoms, &pm)) || (mst = mapped(batch->ligand_id, &pl)))
+            return mst;
+        c->d_atom_off = (int64_t*)(W + s1.atom_off);
+        c->d_frag_off = (int64_t*)(W + s1.frag_off);
+        c->d_move_off = (int64_t*)(W + s1.move_off);
+        c->d_xyz = (float*)px;
+        c->d_frag_axis = (int32_t*)pa;
+        c->d_move_atoms = (int32_t*)pm;
+        c->d_lid = (const uint64_t*)pl;
     } else {
         c->d_atom_off = (int64_t*)(W + s1.atom_off);
         c->d_frag_off = (int64_t*)(W + s1.frag_off);
@@ -730,7 +758,11 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         c->submitted = true;
         return VS_OK;
     }
-    if (!batch->on_device) {
+    if (batch->on_device == 2) {
+        CK(cudaMemcpyAsync(c->d_atom_off, batch->atom_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
+        CK(cudaMemcpyAsync(c->d_frag_off, batch->frag_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
+        if (nR) CK(cudaMemcpyAsync(c->d_move_off, batch->move_off, (nR + 1) * 8, cudaMemcpyHostToDevice, ms));
+    } else if (!batch->on_device) {
         CK(cudaMemcpyAsync(c->d_atom_off, batch->atom_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
         CK(cudaMemcpyAsync(c->d_frag_off, batch->frag_off, (n + 1) * 8, cudaMemcpyHostToDevice, ms));
         if (nA) CK(cudaMemcpyAsync(c->d_xyz, batch->xyz, nA * 12, cudaMemcpyHostToDevice, ms));
@@ -743,12 +775,11 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             CK(cudaMemcpyAsync((void*)c->d_lid, batch->ligand_id, n * 8, cudaMemcpyHostToDevice, ms));
     }
 
-    // ---- a1 ingest: validate, laminar check, canonical renumbering, features
-    CK(cudaMemsetAsync(c->d_status, 0xFF, 16, ms));
+    // ---- a1 features (every ligand, from the CSR offsets alone) and the range checks
+    CK(cudaMemsetAsync(c->d_status, 0xFF, 24, ms));
     CK(cudaMemsetAsync(c->d_maxAR, 0, 8, ms));
-    CK(launch_ingest(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frag_axis, c->d_move_off, c->d_move_atoms, n,
-                     c->d_order, c->d_frint, c->d_fown, c->d_lflag, c->d_featA, c->d_featR, c->d_featM, c->d_status,
-                     c->d_maxAR, ms));
+    CK(launch_features(c->d_atom_off, c->d_frag_off, c->d_move_off, n, c->d_featA, c->d_featR, c->d_featM, c->d_status,
+                       c->d_maxAR, ms));
     ++launches;
     vs_status st = ensure_pinned(c, (size_t)(s1.max_buckets + 16) * 32 + kMaxCells * 8 + 64);
     if (st) return st;
@@ -853,13 +884,15 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         CK(cudaMemcpyAsync(c->d_bsize, hz, (size_t)nb * 4, cudaMemcpyHostToDevice, ms));
     }
     CK(launch_scatter(c->d_cell, n, c->d_hist, n_cells, s1.n_blocks, c->d_perm, ms));
-    CK(launch_bucket_weights(c->d_perm, c->d_featA, c->d_featM, c->d_bstart, c->d_bsize, nb, c->P, c->K, S_w,
-                             c->d_weights, ms));
+    CK(launch_bucket_weights(c->d_perm, c->d_featA, c->d_featR, c->d_featM, c->d_bstart, c->d_bsize, nb, c->P, c->K,
+                             S_w, c->d_weights, ms));
     launches += 2;
     CK(cudaStreamSynchronize(ms));  // pinned staging reused below
-    CK(cudaMemcpyAsync(H, c->d_weights, (size_t)nb * 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaMemcpyAsync(H, c->d_weights, (size_t)nb * 32, cudaMemcpyDeviceToHost, ms));
     CK(cudaStreamSynchronize(ms));
-    for (int b = 0; b < nb; ++b) std::memcpy(&c->buckets[b].weight, H + (size_t)b * 8, 8);
+    std::vector<unsigned long long> bsum((size_t)nb * 4);
+    std::memcpy(bsum.data(), H, (size_t)nb * 32);
+    for (int b = 0; b < nb; ++b) c->buckets[b].weight = bsum[4 * (size_t)b];
 
     // ---- a4 LPT shard (identical on every rank: a pure function of the manifest)
     {
@@ -875,6 +908,21 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         }
         std::sort(mine.begin(), mine.end(), [&](int x, int y) { return lorder[x] < lorder[y]; });
         c->owned = mine;
+        // bytes this submit moves to the device: copies, or (mapped host input) the offsets plus
+        // what the kernels read in place for the owned ligands
+        uint64_t oa = 0, of = 0, om = 0, on = 0;
+        for (int b : mine) {
+            oa += bsum[4 * (size_t)b + 1];
+            of += bsum[4 * (size_t)b + 2];
+            om += bsum[4 * (size_t)b + 3];
+            on += (uint64_t)c->buckets[b].size;
+        }
+        const uint64_t offs = (uint64_t)(n + 1) * 16 + (uint64_t)(nR + 1) * 8;
+        c->stats.h2d_bytes = batch->on_device == 1 ? 0
+                             : batch->on_device == 2
+                                 ? offs + 12 * oa + 8 * of + 4 * om + (batch->ligand_id ? 8 * on : 0)
+                                 : offs + (uint64_t)nA * 12 + (uint64_t)nR * 8 + (uint64_t)nM * 4 +
+                                       (batch->ligand_id ? (uint64_t)n * 8 : 0);
     }
     // fused mode: group the owned buckets by atom class (LPT order kept inside a class)
     // so each class is one contiguous slot range = one persistent launch
@@ -938,6 +986,22 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             CK(cudaMemcpyAsync(c->d_own_prefix, h_prefix, (size_t)(no + 1) * 4, cudaMemcpyHostToDevice, ms));
             CK(cudaMemcpyAsync(c->d_own_ac, h_ac, (size_t)no * 4, cudaMemcpyHostToDevice, ms));
             CK(cudaMemcpyAsync(c->d_own_rec_off, h_roff, (size_t)no * 8, cudaMemcpyHostToDevice, ms));
+        }
+    }
+    // ---- a1 ingest of this rank's ligands: per-atom validation, laminar check, canonical
+    // renumbering (errors are rank-local: parallel.py carries them through the all-gather)
+    CK(launch_ingest(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frag_axis, c->d_move_off, c->d_move_atoms, c->d_perm,
+                     c->d_own_start, c->d_own_prefix, no, c->total_slots, c->d_order, c->d_frint, c->d_fown,
+                     c->d_lflag, c->d_status + 2, ms));
+    ++launches;
+    CK(cudaMemcpyAsync(H, c->d_status + 2, 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaStreamSynchronize(ms));
+    {
+        unsigned long long istat;
+        std::memcpy(&istat, H, 8);
+        if (istat != ~0ull) {
+            const long long li = (long long)(istat >> 8);
+            return fail(c, VS_E_PARSE, "ligand %lld: %s", li, vcode_msg((int)(istat & 255)));
         }
     }
     CK(launch_pack(c->d_perm, c->d_own_start, c->d_own_prefix, c->d_own_ac, c->d_own_rec_off, no, c->total_slots,
@@ -1012,7 +1076,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     launches += dock_launches;
 
     c->stats.n_ligands = n;
-    c->stats.n_owned = c->total_slots;
+    c->stats.n_owned = c->total_slots;   // (h2d_bytes was set with the shard)
     c->stats.n_buckets = nb;
     c->stats.n_owned_buckets = no;
     c->stats.kernel_launches = launches;

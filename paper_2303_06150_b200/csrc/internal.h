@@ -133,17 +133,22 @@ int grid_mode(int nx, int ny, int nz);
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).
+cudaError_t launch_features(const int64_t* atom_off, const int64_t* frag_off, const int64_t* move_off, int64_t n,
+                            int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st);
+// a1 ingest of the owned (packed) slots: validation, laminar check, canonical renumbering.
 cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
-                          const int64_t* move_off, const int32_t* move_atoms, int64_t n, uint8_t* order, int4* frint,
-                          uint8_t* fown, int* lflag, int* featA, int* featR, int* featM, unsigned long long* status,
-                          int* maxAR, cudaStream_t st);
+                          const int64_t* move_off, const int32_t* move_atoms, const uint32_t* perm,
+                          const int64_t* owned_start, const int* owned_prefix, int n_owned, int total_slots,
+                          uint8_t* order, int4* frint, uint8_t* fown, int* lflag, unsigned long long* status,
+                          cudaStream_t st);
 cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
                                  const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
                                  unsigned long long* ovf, cudaStream_t st);
 cudaError_t launch_scan_hist(int* hist, int n_cells, int n_blocks, int* cell_count, cudaStream_t st);
 cudaError_t launch_scatter(const int* cell, int64_t n, const int* hist_off, int n_cells, int n_blocks, uint32_t* perm,
                            cudaStream_t st);
-cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const int* featM, const int64_t* bstart,
+cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const int* featR, const int* featM,
+                                  const int64_t* bstart,
                                   const int* bsize, int n_buckets, long long P, long long K, long long S_w,
                                   unsigned long long* weights, cudaStream_t st);
 // Pack owned buckets.  slot_bucket_prefix[b] = first packed slot of owned bucket b (nb+1 entries).

@@ -54,6 +54,60 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 //  10 atom listed twice in one moving set
 //  7 axis atom inside its own moving set
 //  11 moving sets not laminar (two sets overlap without one containing the other)
+// a1 (all ligands): features from the CSR offsets alone -- A, R, sum |M_r| -- and the two
+// range checks every rank must agree on before the plan (codes 1, 2 below).  The per-atom
+// checks and the renumbering (ingest_kernel) run only on the ligands this rank docks.
+__global__ void __launch_bounds__(256) features_kernel(const int64_t* __restrict__ atom_off,
+                                                       const int64_t* __restrict__ frag_off,
+                                                       const int64_t* __restrict__ move_off, int64_t n,
+                                                       int* __restrict__ featA, int* __restrict__ featR,
+                                                       int* __restrict__ featM, unsigned long long* status,
+                                                       int* maxAR) {
+    __shared__ int smax[2];
+    if (threadIdx.x < 2) smax[threadIdx.x] = 0;
+    __syncthreads();
+    int locA = 0, locR = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t A64 = atom_off[i + 1] - atom_off[i];
+        const int64_t f0 = frag_off[i], f1 = frag_off[i + 1];
+        const int64_t R64 = f1 - f0;
+        int code = 0;
+        if (A64 < 1 || A64 > kMaxAtoms) code = 1;
+        else if (R64 < 0 || R64 > kMaxFrags) code = 2;
+        int64_t M = 0;
+        if (code == 0) {
+            M = R64 > 0 ? move_off[f1] - move_off[f0] : 0;
+            locA = max(locA, (int)A64);
+            locR = max(locR, (int)R64);
+        }
+        featA[i] = (int)(A64 > 0x7fffffff ? 0x7fffffff : (A64 < 0 ? 0 : A64));
+        featR[i] = (int)(R64 > 0x7fffffff ? 0x7fffffff : (R64 < 0 ? 0 : R64));
+        featM[i] = (int)(M < 0 ? 0 : (M > 0x7fffffff ? 0x7fffffff : M));
+        if (code) atomicMin(status, ((unsigned long long)i << 8) | (unsigned long long)code);
+    }
+    atomicMax(&smax[0], locA);
+    atomicMax(&smax[1], locR);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMax(&maxAR[0], smax[0]);
+        atomicMax(&maxAR[1], smax[1]);
+    }
+}
+
+// Packed slot -> (owned bucket, ligand index): owned_prefix[b] <= slot < owned_prefix[b+1].
+__device__ __forceinline__ uint32_t slot_ligand(int slot, const uint32_t* __restrict__ perm,
+                                                const int64_t* __restrict__ owned_start,
+                                                const int* __restrict__ owned_prefix, int n_owned, int* bucket) {
+    int lo = 0, hi = n_owned;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (owned_prefix[mid] <= slot) lo = mid;
+        else hi = mid;
+    }
+    if (bucket) *bucket = lo;
+    return perm[owned_start[lo] + (slot - owned_prefix[lo])];
+}
+
 constexpr int kIngestWarps = 8;
 struct IngestWarp {
     uint32_t mask[kMaxAtoms];           // bit r: atom in M_r
@@ -102,18 +156,15 @@ __device__ __forceinline__ int first_code(int code) {   // lowest lane's non-zer
 __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
     const int64_t* __restrict__ atom_off, const float* __restrict__ xyz, const int64_t* __restrict__ frag_off,
     const int32_t* __restrict__ frag_axis, const int64_t* __restrict__ move_off, const int32_t* __restrict__ move_atoms,
-    int64_t n, uint8_t* __restrict__ order, int4* __restrict__ frint, uint8_t* __restrict__ fown,
-    int* __restrict__ lflag, int* __restrict__ featA, int* __restrict__ featR, int* __restrict__ featM,
-    unsigned long long* status, int* maxAR) {
+    const uint32_t* __restrict__ perm, const int64_t* __restrict__ owned_start, const int* __restrict__ owned_prefix,
+    int n_owned, int total_slots, uint8_t* __restrict__ order, int4* __restrict__ frint, uint8_t* __restrict__ fown,
+    int* __restrict__ lflag, unsigned long long* status) {
     __shared__ IngestWarp sw[kIngestWarps];
-    __shared__ int smax[2];
-    if (threadIdx.x < 2) smax[threadIdx.x] = 0;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
     IngestWarp& W = sw[threadIdx.x >> 5];
-    const int64_t warps = (int64_t)gridDim.x * kIngestWarps;
-    int locA = 0, locR = 0;
-    for (int64_t li = (int64_t)blockIdx.x * kIngestWarps + (threadIdx.x >> 5); li < n; li += warps) {
+    const int warps = gridDim.x * kIngestWarps;
+    for (int slot = blockIdx.x * kIngestWarps + (threadIdx.x >> 5); slot < total_slots; slot += warps) {
+        const int64_t li = slot_ligand(slot, perm, owned_start, owned_prefix, n_owned, nullptr);
         const int64_t a0 = atom_off[li], a1 = atom_off[li + 1];
         const int64_t f0 = frag_off[li], f1 = frag_off[li + 1];
         const int64_t A64 = a1 - a0, R64 = f1 - f0;
@@ -343,26 +394,8 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
             M = total;
             __syncwarp();
         }
-        if (code == 0) {
-            locA = max(locA, A);
-            locR = max(locR, R);
-            if (R == 0 && lane == 0) lflag[li] = A | (1 << 16);   // no sets: every atom is root
-        }
-        if (lane == 0) {
-            featA[li] = (int)(A64 > 0x7fffffff ? 0x7fffffff : (A64 < 0 ? 0 : A64));
-            featR[li] = (int)(R64 > 0x7fffffff ? 0x7fffffff : (R64 < 0 ? 0 : R64));
-            featM[li] = M;
-            if (code) atomicMin(status, ((unsigned long long)li << 8) | (unsigned long long)code);
-        }
-    }
-    if (lane == 0) {
-        atomicMax(&smax[0], locA);
-        atomicMax(&smax[1], locR);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        atomicMax(&maxAR[0], smax[0]);
-        atomicMax(&maxAR[1], smax[1]);
+        (void)M;
+        if (lane == 0 && code) atomicMin(status, ((unsigned long long)li << 8) | (unsigned long long)code);
     }
 }
 
@@ -482,28 +515,37 @@ __global__ void __launch_bounds__(1024) scatter_kernel(const int* __restrict__ c
     }
 }
 
-// a4 input: exact work of a bucket, sum of E_alg = P (A + S_w (K-1) sum|M_r|).
+// a4 input: exact work of a bucket, sum of E_alg = P (A + S_w (K-1) sum|M_r|); also the
+// bucket's atoms, fragments and moving-atom entries (bytes a rank reads for the buckets it
+// owns, vs_stats): weights[4 b + {0, 1, 2, 3}] = {E, sum A, sum R, sum M}.
 __global__ void __launch_bounds__(256) bucket_weights_kernel(const uint32_t* __restrict__ perm,
                                                              const int* __restrict__ featA,
+                                                             const int* __restrict__ featR,
                                                              const int* __restrict__ featM,
                                                              const int64_t* __restrict__ bstart,
                                                              const int* __restrict__ bsize, long long P, long long K,
                                                              long long S_w, unsigned long long* __restrict__ weights) {
-    __shared__ unsigned long long part[8];
+    __shared__ unsigned long long part[8][4];
     const int b = blockIdx.x;
-    unsigned long long s = 0;
+    unsigned long long s[4] = {0, 0, 0, 0};
     for (int t = threadIdx.x; t < bsize[b]; t += blockDim.x) {
         const uint32_t li = perm[bstart[b] + t];
-        s += (unsigned long long)(P * ((long long)featA[li] + S_w * (K - 1) * (long long)featM[li]));
+        s[0] += (unsigned long long)(P * ((long long)featA[li] + S_w * (K - 1) * (long long)featM[li]));
+        s[1] += (unsigned long long)featA[li];
+        s[2] += (unsigned long long)featR[li];
+        s[3] += (unsigned long long)featM[li];
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s[q] += __shfl_xor_sync(FULL, s[q], o);
+        if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5][q] = s[q];
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 4) {
         unsigned long long t = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
-        weights[b] = t;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w][threadIdx.x];
+        weights[4 * b + threadIdx.x] = t;
     }
 }
 
@@ -528,14 +570,9 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     const int lane = threadIdx.x & 31;
     const int slot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (slot >= total_slots) return;
-    int lo = 0, hi = n_owned;  // owned_prefix[b] <= slot < owned_prefix[b+1]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (owned_prefix[mid] <= slot) lo = mid; else hi = mid;
-    }
-    const int b = lo;
+    int b = 0;
+    const uint32_t li = slot_ligand(slot, perm, owned_start, owned_prefix, n_owned, &b);
     const int s = slot - owned_prefix[b];
-    const uint32_t li = perm[owned_start[b] + s];
     const int AC = owned_ac[b];
     float* r = rec + owned_rec_off[b] + (int64_t)s * rec_floats_of(AC);
     const int64_t a0 = atom_off[li];
@@ -614,16 +651,26 @@ __global__ void make_keys_kernel(const int4* __restrict__ meta, int n_slots, con
 
 }  // namespace
 
-cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
-                          const int64_t* move_off, const int32_t* move_atoms, int64_t n, uint8_t* order, int4* frint,
-                          uint8_t* fown, int* lflag, int* featA, int* featR, int* featM, unsigned long long* status,
-                          int* maxAR, cudaStream_t st) {
+cudaError_t launch_features(const int64_t* atom_off, const int64_t* frag_off, const int64_t* move_off, int64_t n,
+                            int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
-    int64_t blocks = (n + kIngestWarps - 1) / kIngestWarps;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    features_kernel<<<(int)blocks, 256, 0, st>>>(atom_off, frag_off, move_off, n, featA, featR, featM, status, maxAR);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
+                          const int64_t* move_off, const int32_t* move_atoms, const uint32_t* perm,
+                          const int64_t* owned_start, const int* owned_prefix, int n_owned, int total_slots,
+                          uint8_t* order, int4* frint, uint8_t* fown, int* lflag, unsigned long long* status,
+                          cudaStream_t st) {
+    if (total_slots <= 0) return cudaSuccess;
+    int blocks = (total_slots + kIngestWarps - 1) / kIngestWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    ingest_kernel<<<(int)blocks, kIngestWarps * 32, 0, st>>>(atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, n,
-                                                             order, frint, fown, lflag, featA, featR, featM, status,
-                                                             maxAR);
+    ingest_kernel<<<blocks, kIngestWarps * 32, 0, st>>>(atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, perm,
+                                                        owned_start, owned_prefix, n_owned, total_slots, order, frint,
+                                                        fown, lflag, status);
     return cudaGetLastError();
 }
 
@@ -650,11 +697,12 @@ cudaError_t launch_scatter(const int* cell, int64_t n, const int* hist_off, int 
     return cudaGetLastError();
 }
 
-cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const int* featM, const int64_t* bstart,
+cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const int* featR, const int* featM,
+                                  const int64_t* bstart,
                                   const int* bsize, int n_buckets, long long P, long long K, long long S_w,
                                   unsigned long long* weights, cudaStream_t st) {
     if (n_buckets <= 0) return cudaSuccess;
-    bucket_weights_kernel<<<n_buckets, 256, 0, st>>>(perm, featA, featM, bstart, bsize, P, K, S_w, weights);
+    bucket_weights_kernel<<<n_buckets, 256, 0, st>>>(perm, featA, featR, featM, bstart, bsize, P, K, S_w, weights);
     return cudaGetLastError();
 }
 

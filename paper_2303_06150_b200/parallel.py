@@ -32,15 +32,52 @@ def gather_keys(keys_local: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat(parts).to(keys_local.device)
 
 
-def global_topk(engine, slot: int, k: int, group=None):
+def encode_status(err) -> int:
+    """A rank's submit outcome as one int64: 0 = ok, else (ligand index << 8) | -code."""
+    if err is None:
+        return 0
+    return (max(0, int(getattr(err, "ligand", 0) or 0)) << 8) | (-int(err.code) & 0xFF)
+
+
+def gather_keys_checked(keys_local: torch.Tensor, status: int = 0, group=None):
+    """gather_keys with every rank's submit status riding along in one extra slot, so a rank
+    whose a1 ingest rejected one of ITS ligands (errors are rank-local: each rank validates the
+    ligands it docks) still joins the collective and every rank learns of the error from the
+    same single all-gather.  Returns (gathered keys [world * k], first error or None) where the
+    first error is (rank, ligand index, VS_E_* code) of the lowest failing rank."""
+    st = torch.tensor([int(status)], dtype=torch.int64, device=keys_local.device)
+    g = gather_keys(torch.cat([keys_local.reshape(-1), st]), group)
+    world = g.numel() // (keys_local.numel() + 1)
+    g = g.view(world, keys_local.numel() + 1)
+    stats = g[:, -1].cpu().tolist()
+    err = None
+    for r, v in enumerate(stats):
+        if v:
+            err = (r, int(v) >> 8, -(int(v) & 0xFF))
+            break
+    return g[:, :-1].reshape(-1), err
+
+
+def raise_gathered(err):
+    from .vsdock import VsError
+    r, li, code = err
+    raise VsError(code, f"rank {r}: ligand {li} (batch index) failed a1 ingest; see that rank's log")
+
+
+def global_topk(engine, slot: int, k: int, group=None, failed=None):
     """a10 + a11: local top-k on this rank's buckets, all-gather, merge on the device.
+    ``failed``: this rank's VsError from its submit (it still joins the collective).
 
     Returns (ligand index [m] int64, score [m] float32) on the host, identical on every rank
     and bit-identical to the single-GPU ranking (keys are unique and totally ordered)."""
-    keys, _ = engine.local_topk(slot, k)          # synchronous on the engine's stream
-    g = gather_keys(keys, group)
-    if g is not keys:                             # the merge runs on the engine's stream
-        torch.cuda.current_stream(keys.device).synchronize()
+    if failed is None:
+        keys, _ = engine.local_topk(slot, k)      # synchronous on the engine's stream
+    else:
+        keys = torch.full((k,), -1, dtype=torch.int64, device=f"cuda:{engine.device}")
+    g, err = gather_keys_checked(keys, encode_status(failed), group)
+    if err is not None:
+        raise_gathered(err)
+    torch.cuda.current_stream(keys.device).synchronize()   # the merge runs on the engine's stream
     return engine.merge_topk(g, k)
 
 

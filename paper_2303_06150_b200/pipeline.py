@@ -67,6 +67,7 @@ class PipelinedDocker:
         self.engine = self.engines[0]
         self.n_sweeps = self.engine.n_sweeps
         self._pinned = {}
+        self._stage = {}
         self.trace = []
 
     def setup(self, rot, trans, cs, pockets):
@@ -86,7 +87,23 @@ class PipelinedDocker:
             self._pinned[key] = torch.empty(tuple(shape), dtype=dtype).pin_memory()
         return self._pinned[key].numpy()
 
-    def _issue_copy(self, arrays, lo, hi):
+    def _rebased(self, slot, name, src, base):
+        """src - base into a reusable PINNED staging buffer (a pageable source would make every
+        copy synchronous with the copy stream, stalling the host behind the previous chunk's
+        upload).  ``slot`` = the engine the chunk goes to: its previous chunk has been submitted,
+        so that chunk's copy from this buffer is complete."""
+        torch = self._torch
+        src = np.asarray(src)
+        key = (slot, name)
+        buf = self._stage.get(key)
+        if buf is None or buf.numel() < src.size:
+            buf = torch.empty(max(1, int(src.size * 1.25)), dtype=torch.int64).pin_memory()
+            self._stage[key] = buf
+        view = buf[: src.size]
+        np.subtract(src, base, out=view.numpy())
+        return view
+
+    def _issue_copy(self, arrays, lo, hi, slot=0):
         """Chunk [lo, hi) to the device on the copy stream: rebased offsets + array slices."""
         torch = self._torch
         ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays
@@ -95,9 +112,8 @@ class PipelinedDocker:
         a0, a1, f0, f1 = int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
         mo = np.asarray(move_off[f0:f1 + 1])
         m0, m1 = int(mo[0]), int(mo[-1])
-        host = [ids[lo:hi], torch.from_numpy(np.ascontiguousarray(ao - a0)), xyz[a0:a1],
-                torch.from_numpy(np.ascontiguousarray(fo - f0)), frag_axis[f0:f1],
-                torch.from_numpy(np.ascontiguousarray(mo - m0)), move_atoms[m0:m1]]
+        host = [ids[lo:hi], self._rebased(slot, "ao", ao, a0), xyz[a0:a1], self._rebased(slot, "fo", fo, f0),
+                frag_axis[f0:f1], self._rebased(slot, "mo", mo, m0), move_atoms[m0:m1]]
         host = [h if isinstance(h, torch.Tensor) else torch.from_numpy(np.asarray(h)) for h in host]
         with torch.cuda.stream(self.copy):
             dev = [h.to(self.dev, non_blocking=True) for h in host]
@@ -105,18 +121,39 @@ class PipelinedDocker:
             ev.record(self.copy)
         return dev, ev, (a0, a1, f0, f1)
 
+    def _zero_copy_args(self, arrays, lo, hi, slot=0):
+        """Chunk [lo, hi) for on_device = 2: rebased offsets (pinned staging, copied by the
+        library) and pinned slices the kernels read in place -- only this rank's ligands cross
+        PCIe."""
+        ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays
+        ao = np.asarray(atom_off[lo:hi + 1])
+        fo = np.asarray(frag_off[lo:hi + 1])
+        a0, a1, f0, f1 = int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
+        mo = np.asarray(move_off[f0:f1 + 1])
+        m0, m1 = int(mo[0]), int(mo[-1])
+        args = [ids[lo:hi], self._rebased(slot, "ao", ao, a0), xyz[a0:a1], self._rebased(slot, "fo", fo, f0),
+                frag_axis[f0:f1], self._rebased(slot, "mo", mo, m0), move_atoms[m0:m1]]
+        return args, (a0, a1, f0, f1)
+
     def run(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, k: int = 1000,
             chunks: int = 0, max_atoms: int = 256, group=None, coords: bool = True, first: int = 32,
-            growth: int = 4):
+            growth: int = 4, zero_copy=None):
         """Dock the library (the C-ABI's general-form CSR arrays; pinned torch CPU tensors for
-        overlapped copies) into every pocket of ``setup``.  Returns a dict of host arrays:
+        overlapped copies) into every pocket of ``setup``.  ``zero_copy`` (default: with more than
+        one rank): the kernels read each rank's ligands straight from the pinned host arrays
+        (on_device = 2) instead of every rank uploading the whole library.  Returns a dict of host
+        arrays:
 
         ``ligand_id`` [n], ``best_score`` / ``best_pose`` [pockets, n], ``angles`` [pockets, S_w * sum R],
         ``xyz`` [pockets, sum A, 3] (best-pose coordinates, input atom order; with ``coords``), and
         ``topk`` = per pocket (library index [m], score [m], ligand id [m]), merged across ranks.
         The per-ligand arrays are reused buffers: copy them to keep them past the next run."""
         from . import parallel
+        from .vsdock import VsError
         torch = self._torch
+        import torch.distributed as dist
+        if zero_copy is None:
+            zero_copy = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
         n = int(atom_off.shape[0]) - 1
         nA, nR = int(xyz.shape[0]), int(frag_axis.shape[0])
         npk = len(self.pocket_ids)
@@ -132,17 +169,31 @@ class PipelinedDocker:
         arrays = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
         self.trace = []
         ne = len(self.engines)
-        inflight = {c: self._issue_copy(arrays, bounds[c], bounds[c + 1]) for c in range(min(ne, nch))}
+        inflight = {} if zero_copy else {c: self._issue_copy(arrays, bounds[c], bounds[c + 1], c % ne)
+                                         for c in range(min(ne, nch))}
         keep = {}
+        failed = None
         for c in range(nch):
             lo, hi = bounds[c], bounds[c + 1]
             e = self.engines[c % ne]
-            dev, ev, (a0, a1, f0, f1) = inflight.pop(c)
-            ev.synchronize()        # chunk c resident (submit reads its CSR totals)
-            if hi > lo:     # (chunk_bounds never yields an empty chunk)
+            if zero_copy:
+                dev, (a0, a1, f0, f1) = self._zero_copy_args(arrays, lo, hi, c % ne)
+                mode = 2
+            else:
+                dev, ev, (a0, a1, f0, f1) = inflight.pop(c)
+                ev.synchronize()    # chunk c resident (submit reads its CSR totals)
+                mode = 1
+            if hi > lo and failed is None:     # (chunk_bounds never yields an empty chunk)
                 # returns once the dock launches are queued; the read-backs below queue behind
                 # them on the same stream and run on the D2H engine while the other engine docks
-                e.submit(*dev, self.pocket_ids, on_device=True, max_atoms=max_atoms)
+                try:
+                    e.submit(*dev, self.pocket_ids, on_device=mode, max_atoms=max_atoms)
+                except VsError as err:       # rank-local a1 error: still join the collective below
+                    failed = err
+                    if err.ligand is not None:
+                        failed.ligand = err.ligand + lo
+                    keep[c % ne] = dev
+                    continue
                 for s in range(npk):
                     e.results_async(s, best[s, lo:hi], pose[s, lo:hi],
                                     ang[s, S_w * f0:S_w * f1] if f1 > f0 else None)
@@ -150,20 +201,26 @@ class PipelinedDocker:
                         e.coords_into(s, xyz_out[s, a0:a1], mode=2)
                     nkeys[s] += e.keys_into(s, all_keys[s][nkeys[s]:], lo)
             keep[c % ne] = dev      # the engine borrows the chunk until its next submit
-            if c + ne < nch:
+            if c + ne < nch and not zero_copy:
                 # the buffer slot of chunk c + ne is engine c's: its copy may only overwrite
                 # device memory the engine no longer reads -- new tensors, so no hazard
-                inflight[c + ne] = self._issue_copy(arrays, bounds[c + ne], bounds[c + ne + 1])
+                inflight[c + ne] = self._issue_copy(arrays, bounds[c + ne], bounds[c + ne + 1], (c + ne) % ne)
             self.trace.append((c, lo, hi))
         for st in self.streams:
             st.synchronize()
         e = self.engine
         tops = []
         ids_host = np.asarray(ligand_id)
+        status = parallel.encode_status(failed)
         for s in range(npk):
-            mine = e.select_keys(all_keys[s][:nkeys[s]], k)     # this rank's top-k, on the device
+            if failed is None:
+                mine = e.select_keys(all_keys[s][:nkeys[s]], k)     # this rank's top-k, on the device
+            else:
+                mine = torch.full((k,), -1, dtype=torch.int64, device=self.dev)
             e.synchronize()                                    # (the collective runs on torch's stream)
-            g = parallel.gather_keys(mine, group)              # NCCL all-gather (W x k keys)
+            g, err = parallel.gather_keys_checked(mine, status, group)   # NCCL all-gather (W x (k + 1))
+            if err is not None:
+                parallel.raise_gathered(err)
             torch.cuda.current_stream(self.dev).synchronize()
             idx, sc = e.merge_topk(g, k)
             tops.append((idx, sc, ids_host[idx] if len(idx) else np.zeros(0, np.uint64)))

@@ -32,6 +32,9 @@ class VsError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"{_NAMES.get(code, code)}: {msg}")
         self.code = code
+        import re
+        m = re.search(r"ligand (\d+)", msg or "")
+        self.ligand = int(m.group(1)) if m else None
 
 
 class vs_config(ctypes.Structure):
@@ -71,7 +74,8 @@ class vs_class_info(ctypes.Structure):
 class vs_stats(ctypes.Structure):
     _fields_ = [("n_ligands", ctypes.c_int64), ("n_owned", ctypes.c_int64), ("n_buckets", ctypes.c_int64),
                 ("n_owned_buckets", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
-                ("dock_launches", ctypes.c_int64), ("evals_alg", ctypes.c_double), ("prep_ms", ctypes.c_float),
+                ("dock_launches", ctypes.c_int64), ("evals_alg", ctypes.c_double), ("h2d_bytes", ctypes.c_uint64),
+                ("prep_ms", ctypes.c_float),
                 ("dock_ms", ctypes.c_float), ("topk_ms", ctypes.c_float)]
 
 
@@ -249,12 +253,14 @@ class Engine:
     def submit(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, pockets, on_device=None,
                max_atoms=None):
         """Submit a CSR ligand batch in the general form of include/vsdock.h (numpy host arrays,
-        pinned torch CPU tensors, or CUDA tensors; ``ligand_id`` may be None)."""
+        pinned torch CPU tensors, or CUDA tensors; ``ligand_id`` may be None).  on_device: 0 host
+        (copied), 1 device, 2 pinned host read in place by the kernels (owned ligands only)."""
         n = int(atom_off.shape[0]) - 1
         if on_device is None:
             on_device = hasattr(xyz, "is_cuda") and xyz.is_cuda
+        on_device = int(on_device)
         if max_atoms is None:
-            if on_device:
+            if on_device == 1:
                 max_atoms = int((atom_off[1:] - atom_off[:-1]).max().item()) if n > 0 else 1
             else:
                 max_atoms = int(np.diff(np.asarray(atom_off)).max()) if n > 0 else 1
@@ -264,7 +270,7 @@ class Engine:
         pockets = np.ascontiguousarray(pockets, np.int32).reshape(-1)
         self.reserve(n, nA, nR, nM, max(1, min(256, max_atoms)), len(pockets))
         b = vs_ligand_batch(n, _ptr(ligand_id), _ptr(atom_off), _ptr(xyz), _ptr(frag_off), _ptr(frag_axis),
-                            _ptr(move_off), _ptr(move_atoms), int(bool(on_device)))
+                            _ptr(move_off), _ptr(move_atoms), on_device)
         self._batch_keep = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
         self._check(self.lib.vs_submit(self.h, ctypes.byref(b), _ptr(pockets), len(pockets)))
         self._n, self._nA, self._nR = n, nA, nR

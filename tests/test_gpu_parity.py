@@ -622,3 +622,88 @@ def test_large_grids_window_plus_global_path(n, h, offset):
     lib = vsgen.ligands(24, 50 + n, (20, 120), (0, 12))
     e2, rot, tr, cs = run(lib, [pk], P=8, K=8)
     check(e2, lib, range(lib.n), pk, rot, tr, cs)
+
+
+# ----------------------------------------------------------------------------- owned-only input
+# (VERDICT r1 "missing" 5): mapped pinned host arrays read in place, per-rank a1 ingest
+
+def test_mapped_host_input_matches_device_input_and_counts_owned_bytes():
+    """on_device = 2: the offsets are copied and the kernels read coordinates / axes / moving atoms /
+    ids from pinned host memory.  Bit-identical to device input; with W virtual ranks each rank moves
+    only the offsets plus its own ligands' arrays (vs_stats.h2d_bytes)."""
+    import torch
+    c = vsgen.CONFIGS["C2"]
+    lib = vsgen.ligands(3000, 61, c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    e, rot, tr, cs = run(lib, [pk], P=16, K=8, debug=False)
+    r = e.results(0)
+    pinned = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
+    e2 = engine()
+    setup(e2, [pk], 16, 8)
+    e2.submit(*pinned, [0], on_device=2)
+    e2.wait()
+    r2 = e2.results(0)
+    assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.angles, r2.angles)
+    assert np.array_equal(r2.ligand_id, lib.ligand_id) and np.array_equal(e.coords(0), e2.coords(0))
+    full = sum(a.nbytes for a in lib.arrays())
+    assert e2.stats()["h2d_bytes"] == full
+    offs = lib.atom_off.nbytes + lib.frag_off.nbytes + lib.move_off.nbytes
+    tot = 0
+    for rank in range(4):
+        eR = engine(rank=rank, world_size=4)
+        setup(eR, [pk], 16, 8)
+        eR.submit(*pinned, [0], on_device=2)
+        eR.wait()
+        rr = eR.results(0)
+        own = ~np.isnan(rr.best_score)
+        assert np.array_equal(rr.best_score[own], r.best_score[own])
+        b = eR.stats()["h2d_bytes"] - offs
+        assert 0 < b < 0.4 * (full - offs)
+        tot += b
+    assert tot == full - offs                       # the shards move every ligand's arrays exactly once
+
+
+def test_rank_local_ingest_errors():
+    """a1's per-atom checks run on each rank's own ligands: with 2 virtual ranks, an invalid ligand
+    makes only its owner's submit fail (the other rank docks its share), naming the ligand."""
+    from paper_2303_06150_b200 import VsError
+    base = vsgen.ligands(400, 5, (20, 60), (1, 6))
+    ligs = []
+    for i in range(base.n):
+        x, f = base.ligand(i)
+        ligs.append((np.array(x, copy=True), vsgen.Frags(np.array(f.axis, copy=True), [np.array(m) for m in f.moves])))
+    bad = 137
+    ligs[bad][1].moves[0] = np.concatenate([ligs[bad][1].moves[0], ligs[bad][1].moves[0][:1]])   # duplicate entry
+    lib = mk_lib(ligs)
+    pk = vsgen.pocket(101)
+    outcomes = {}
+    for rank in range(2):
+        e = engine(rank=rank, world_size=2)
+        setup(e, [pk], 8, 8)
+        try:
+            e.submit_library(lib, [0])
+            e.wait()
+            outcomes[rank] = e.results(0)
+        except VsError as err:
+            outcomes[rank] = err
+    errs = [o for o in outcomes.values() if isinstance(o, VsError)]
+    assert len(errs) == 1 and errs[0].ligand == bad and "listed twice" in str(errs[0])
+    ok = [o for o in outcomes.values() if not isinstance(o, VsError)][0]
+    assert np.isnan(ok.best_score[bad]) and np.isfinite(ok.best_score).sum() > 100
+
+
+def test_pipelined_zero_copy_matches():
+    """PipelinedDocker with zero_copy (the multi-GPU default): identical outputs on one GPU."""
+    import torch
+    from paper_2303_06150_b200.pipeline import PipelinedDocker
+    lib = vsgen.ligands(2000, 62, (20, 120), (0, 20))
+    pk = vsgen.pocket(101)
+    e, rot, tr, cs = run(lib, [pk], P=16, K=8, debug=False)
+    r = e.results(0)
+    pd = PipelinedDocker()
+    pd.setup(rot, tr, cs, [pk])
+    h = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
+    out = pd.run(*h, k=50, chunks=0, zero_copy=True)
+    assert np.array_equal(out["best_score"][0], r.best_score) and np.array_equal(out["xyz"][0], e.coords(0))
+    assert list(out["topk"][0][0]) == list(oracle.topk(r.best_score, 50))
+    pd.close()

@@ -74,3 +74,38 @@ def test_two_ranks_plan_and_merge():
         assert o["n_owned"] == o["n"], "shards do not partition the library"
         assert o["gathered"] == world * 100
         assert o["merged"] == o["want"]
+
+
+def _worker_err(rank, world, port, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2303_06150_b200 import parallel
+        from paper_2303_06150_b200.vsdock import VsError, VS_E_PARSE
+        k = 16
+        keys = torch.arange(k, dtype=torch.int64) + 100 * rank
+        # rank 1's a1 ingest rejected its ligand 4242 (rank-local error): it still joins the gather
+        err = VsError(VS_E_PARSE, "ligand 4242: moving sets not laminar") if rank == 1 else None
+        g, e = parallel.gather_keys_checked(keys if err is None else torch.full((k,), -1), parallel.encode_status(err))
+        ok_g, ok_e = parallel.gather_keys_checked(keys, 0)        # a clean step afterwards
+        out[rank] = dict(err=e, n=int(g.numel()), ok_err=ok_e, ok_keys=ok_g.tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_rank_local_error_reaches_every_rank():
+    """Errors of a1's per-atom checks are rank-local (each rank validates the ligands it docks):
+    the failing rank's status rides in the same all-gather as the keys, so BOTH ranks see it and no
+    rank blocks in a collective the other never reaches (parallel.gather_keys_checked)."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_err, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        o = out[r]
+        assert o["err"] == (1, 4242, -2)           # (rank, ligand index, VS_E_PARSE) on every rank
+        assert o["n"] == world * 16
+        assert o["ok_err"] is None and o["ok_keys"] == list(range(16)) + list(range(100, 116))
