@@ -123,8 +123,10 @@ vs_status vs_set_angle_table(vs_ctx* ctx, int32_t K, const float* cos_sin);
  * checks it and renumbers the atoms on the device so that every set is one contiguous
  * range ("a1 ingest"); results come back in the caller's atom order.
  * Fragments are swept in input order (Q4).  ligand_id[n] (may be NULL: ids = batch
- * indices) is passed through to vs_get_results and vs_merge_topk.  atom_off[0],
- * frag_off[0] and move_off[0] must be 0.  on_device = 1: every pointer is a device
+ * indices) is passed through to vs_get_results and vs_merge_topk.  The offsets may
+ * start at any value b (a slice of a larger library): offset o addresses element o - b
+ * of its data array, so xyz, frag_axis and move_atoms point at the slice's first
+ * element.  Offsets must not decrease.  on_device = 1: every pointer is a device
  * pointer (borrowed until vs_wait); 0: host memory, copied during vs_submit;
  * 2: PINNED (page-locked) host memory, mapped: the three offset arrays are copied, and
  * the kernels read coordinates, axes, moving atoms and ids over PCIe only for the
@@ -169,9 +171,10 @@ vs_status vs_wait(vs_ctx* ctx);
  * the double-buffered result read-back of P:200-203. */
 vs_status vs_get_results(vs_ctx* ctx, int32_t slot, uint64_t* ligand_id, float* best_score, int32_t* best_pose,
                          uint8_t* angle_idx, int32_t on_device);
-/* a9 best-pose coordinates (Angstrom, the caller's input atom order, [3*n_atoms]);
- * replays p* on the GPU bit-identically to the dock kernel.  on_device as for
- * vs_get_results (2: asynchronous into pinned host memory). */
+/* a9 best-pose coordinates (Angstrom, the caller's input atom order, [3*n_atoms]) of
+ * pocket slot s, computed by the dock kernel itself (the warp that picks p* replays it
+ * bit-identically to the docked trajectory); ligands of other ranks: NaN.  on_device as
+ * for vs_get_results (2: asynchronous into pinned host memory). */
 vs_status vs_get_coords(vs_ctx* ctx, int32_t slot, float* xyz_out, int32_t on_device);
 /* Parity hook (requires debug_poses): every pose's final score [n*P] and angle
  * sequence [P*S_w*frag_off ...] (pose p of ligand i at P*S_w*frag_off[i] + p*S_w*R_i). */

@@ -159,7 +159,7 @@ struct vs_ctx {
     std::vector<uint8_t*> d_ang;
     std::vector<float*> d_dbg_score;
     std::vector<uint8_t*> d_dbg_ang;
-    float* d_coords = nullptr;
+    std::vector<float*> d_coords;      // a9 best-pose coordinates per pocket slot (written by the dock kernel)
     unsigned long long* d_keys = nullptr;
     int64_t keys_cap = 0;
     unsigned long long* d_topk_out = nullptr;
@@ -195,6 +195,19 @@ vs_status fail(vs_ctx* c, vs_status code, const char* fmt, ...) {
         cudaError_t e_ = (call);                                                                   \
         if (e_ != cudaSuccess) return fail(c, VS_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
+
+// Large asynchronous read-backs go out in pieces: one copy engine serves the D2H copies of
+// every stream, one request at a time, so a single 300 MB copy would hold up the small
+// status reads of another context's preparation for its whole duration (two engines
+// alternating over chunks, pipeline.py).  4 MB pieces bound that wait to ~80 us.
+cudaError_t copy_pieces(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    constexpr size_t kPiece = 4u << 20;
+    for (size_t o = 0; o < bytes; o += kPiece) {
+        const cudaError_t e = cudaMemcpyAsync((char*)dst + o, (const char*)src + o, std::min(kPiece, bytes - o), kind, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
 
 vs_status ensure_pinned(vs_ctx* c, size_t bytes) {
     if (c->hpin_bytes >= bytes) return VS_OK;
@@ -328,7 +341,7 @@ Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats,
     s.ang = r.add((size_t)S_w * nR * n_pockets + 256 * n_pockets);
     s.dbg_score = r.add(debug ? (size_t)n * P * 4 * n_pockets + 256 * n_pockets : 0);
     s.dbg_ang = r.add(debug ? (size_t)P * S_w * nR * n_pockets + 256 * n_pockets : 0);
-    s.coords = r.add(nA * 12);
+    s.coords = r.add((nA * 12 + 256) * n_pockets);
     const int64_t kc = std::max<int64_t>(n, 65536);
     s.keys = r.add(kc * 8);
     s.topk_out = r.add(2 * 8192 * 8);   // merged keys + their ligand ids
@@ -609,38 +622,51 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     int64_t launches = 0;
 
     // ---- batch sizes
-    int64_t nA = 0, nR = 0, nM = 0;
+    // Offsets may start at any value b (a slice of a larger library): entry i addresses the data
+    // arrays at offset - b.  The library works on rebased copies when b != 0.
+    int64_t nA = 0, nR = 0, nM = 0, base_a = 0, base_f = 0, base_m = 0;
     if (n > 0) {
         if (!batch->atom_off || !batch->xyz || !batch->frag_off) return fail(c, VS_E_ARG, "null batch array");
         if (batch->on_device < 0 || batch->on_device > 2) return fail(c, VS_E_ARG, "on_device must be 0, 1 or 2");
         if (batch->on_device == 1) {
-            CK(cudaMemcpy(&nA, batch->atom_off + n, 8, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(&nR, batch->frag_off + n, 8, cudaMemcpyDeviceToHost));
-            int64_t z[2];
-            CK(cudaMemcpy(&z[0], batch->atom_off, 8, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(&z[1], batch->frag_off, 8, cudaMemcpyDeviceToHost));
-            if (z[0] != 0 || z[1] != 0) return fail(c, VS_E_PARSE, "atom_off[0] and frag_off[0] must be 0");
+            // CSR totals of a device batch: async reads on the context's stream into pinned
+            // staging (a plain cudaMemcpy would run on the legacy default stream and wait for
+            // every blocking stream of the device -- another engine's docking and read-backs)
+            vs_status pst = ensure_pinned(c, 4096);
+            if (pst) return pst;
+            int64_t* hz = (int64_t*)c->hpin;
+            CK(cudaMemcpyAsync(&hz[0], batch->atom_off + n, 8, cudaMemcpyDeviceToHost, ms));
+            CK(cudaMemcpyAsync(&hz[1], batch->frag_off + n, 8, cudaMemcpyDeviceToHost, ms));
+            CK(cudaMemcpyAsync(&hz[2], batch->atom_off, 8, cudaMemcpyDeviceToHost, ms));
+            CK(cudaMemcpyAsync(&hz[3], batch->frag_off, 8, cudaMemcpyDeviceToHost, ms));
+            CK(cudaStreamSynchronize(ms));
+            base_a = hz[2];
+            base_f = hz[3];
+            nA = hz[0] - base_a;
+            nR = hz[1] - base_f;
             if (nR > 0) {
                 if (!batch->move_off) return fail(c, VS_E_ARG, "null move_off");
-                CK(cudaMemcpy(&z[0], batch->move_off, 8, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(&nM, batch->move_off + nR, 8, cudaMemcpyDeviceToHost));
-                if (z[0] != 0) return fail(c, VS_E_PARSE, "move_off[0] must be 0");
+                CK(cudaMemcpyAsync(&hz[0], batch->move_off, 8, cudaMemcpyDeviceToHost, ms));
+                CK(cudaMemcpyAsync(&hz[1], batch->move_off + nR, 8, cudaMemcpyDeviceToHost, ms));
+                CK(cudaStreamSynchronize(ms));
+                base_m = hz[0];
+                nM = hz[1] - base_m;
             }
         } else {
-            if (batch->atom_off[0] != 0 || batch->frag_off[0] != 0)
-                return fail(c, VS_E_PARSE, "atom_off[0] and frag_off[0] must be 0");
-            nA = batch->atom_off[n];
-            nR = batch->frag_off[n];
+            base_a = batch->atom_off[0];
+            base_f = batch->frag_off[0];
+            nA = batch->atom_off[n] - base_a;
+            nR = batch->frag_off[n] - base_f;
             for (int64_t i = 0; i < n; ++i)   // monotone offsets (cheap, O(n))
                 if (batch->atom_off[i + 1] < batch->atom_off[i] || batch->frag_off[i + 1] < batch->frag_off[i])
                     return fail(c, VS_E_PARSE, "ligand %lld: decreasing CSR offsets", (long long)i);
             if (nR > 0) {
                 if (!batch->move_off) return fail(c, VS_E_ARG, "null move_off");
-                if (batch->move_off[0] != 0) return fail(c, VS_E_PARSE, "move_off[0] must be 0");
                 for (int64_t f = 0; f < nR; ++f)
                     if (batch->move_off[f + 1] < batch->move_off[f])
                         return fail(c, VS_E_PARSE, "fragment %lld: decreasing move_off", (long long)f);
-                nM = batch->move_off[nR];
+                base_m = batch->move_off[0];
+                nM = batch->move_off[nR] - base_m;
             }
         }
         if (nA < 0 || nR < 0 || nM < 0) return fail(c, VS_E_PARSE, "negative CSR totals");
@@ -687,12 +713,14 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->d_frint = (int4*)(W + s1.frint);
     c->d_fown = W + s1.fown;
     c->d_lflag = (int*)(W + s1.lflag);
+    const bool rebase = base_a != 0 || base_f != 0 || base_m != 0;
     if (batch->on_device == 1) {
-        c->d_atom_off = (int64_t*)batch->atom_off;
-        c->d_frag_off = (int64_t*)batch->frag_off;
+        // borrowed; offsets that do not start at 0 are rebased into workspace copies below
+        c->d_atom_off = rebase ? (int64_t*)(W + s1.atom_off) : (int64_t*)batch->atom_off;
+        c->d_frag_off = rebase ? (int64_t*)(W + s1.frag_off) : (int64_t*)batch->frag_off;
         c->d_xyz = (float*)batch->xyz;
         c->d_frag_axis = (int32_t*)batch->frag_axis;
-        c->d_move_off = (int64_t*)batch->move_off;
+        c->d_move_off = rebase ? (int64_t*)(W + s1.move_off) : (int64_t*)batch->move_off;
         c->d_move_atoms = (int32_t*)batch->move_atoms;
         c->d_lid = batch->ligand_id;
     } else if (batch->on_device == 2) {
@@ -773,6 +801,14 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         if (nM) CK(cudaMemcpyAsync(c->d_move_atoms, batch->move_atoms, nM * 4, cudaMemcpyHostToDevice, ms));
         if (batch->ligand_id)
             CK(cudaMemcpyAsync((void*)c->d_lid, batch->ligand_id, n * 8, cudaMemcpyHostToDevice, ms));
+    }
+
+    if (rebase) {   // offsets relative to their first entry (slices of a larger library)
+        const bool dev = batch->on_device == 1;
+        CK(launch_rebase(dev ? batch->atom_off : c->d_atom_off, c->d_atom_off, n + 1, base_a, ms));
+        CK(launch_rebase(dev ? batch->frag_off : c->d_frag_off, c->d_frag_off, n + 1, base_f, ms));
+        if (nR) CK(launch_rebase(dev ? batch->move_off : c->d_move_off, c->d_move_off, nR + 1, base_m, ms));
+        launches += nR ? 3 : 2;
     }
 
     // ---- a1 features (every ligand, from the CSR offsets alone) and the range checks
@@ -963,7 +999,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             c->d_dbg_ang[i] = W + s2.dbg_ang + i * al((size_t)c->P * S_w * nR);
         }
     }
-    c->d_coords = (float*)(W + s2.coords);
+    c->d_coords.assign(n_pockets, nullptr);
+    for (int i = 0; i < n_pockets; ++i) c->d_coords[i] = (float*)(W + s2.coords + i * al((size_t)nA * 12));
     c->d_keys = (unsigned long long*)(W + s2.keys);
     c->keys_cap = std::max<int64_t>(n, 65536);
     c->d_topk_out = (unsigned long long*)(W + s2.topk_out);
@@ -1011,6 +1048,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     for (int i = 0; i < n_pockets; ++i) {
         CK(launch_fill_results(c->d_score[i], c->d_pose_best[i], n, c->d_ang[i], (int64_t)S_w * nR, ms));
         ++launches;
+        if (c->total_slots < n && nA)   // NaN coordinates for the ligands of other ranks
+            CK(cudaMemsetAsync(c->d_coords[i], 0xFF, (size_t)nA * 12, ms));
     }
     CK(cudaEventRecord(c->ev_prep1, ms));
 
@@ -1058,6 +1097,9 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             a.angles = c->d_ang[q];
             a.dbg_score = c->d_dbg_score[q];
             a.dbg_angles = c->d_dbg_ang[q];
+            a.order = c->d_order;
+            a.atom_off = c->d_atom_off;
+            a.xyz_out = c->d_coords[q];
             a.counter = d_counters + dock_launches;
             const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.mode, a.pk.nz, a.pk.rs, a.pk.ps, c->P,
                                              c->K, S_w, ci.LC, c->frag_cap);
@@ -1113,9 +1155,9 @@ vs_status vs_get_results(vs_ctx* c, int32_t slot, uint64_t* ligand_id, float* be
         else if (on_device == 1) return fail(c, VS_E_ARG, "the batch carried no ligand ids (request them on the host)");
         else for (int64_t i = 0; i < c->n; ++i) ligand_id[i] = (uint64_t)i;
     }
-    if (best_score) CK(cudaMemcpyAsync(best_score, c->d_score[slot], c->n * 4, kind, c->main));
-    if (best_pose) CK(cudaMemcpyAsync(best_pose, c->d_pose_best[slot], c->n * 4, kind, c->main));
-    if (angle_idx && c->nR) CK(cudaMemcpyAsync(angle_idx, c->d_ang[slot], (size_t)c->cfg.n_sweeps * c->nR, kind, c->main));
+    if (best_score) CK(copy_pieces(best_score, c->d_score[slot], c->n * 4, kind, c->main));
+    if (best_pose) CK(copy_pieces(best_pose, c->d_pose_best[slot], c->n * 4, kind, c->main));
+    if (angle_idx && c->nR) CK(copy_pieces(angle_idx, c->d_ang[slot], (size_t)c->cfg.n_sweeps * c->nR, kind, c->main));
     if (on_device != 2) CK(cudaStreamSynchronize(c->main));   // 2: asynchronous (pinned host), see vsdock.h
     return VS_OK;
 }
@@ -1139,29 +1181,8 @@ vs_status vs_get_coords(vs_ctx* c, int32_t slot, float* xyz_out, int32_t on_devi
     if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
     if (c->n == 0 || c->nA == 0) return VS_OK;
     if (on_device < 0 || on_device > 2) return fail(c, VS_E_ARG, "on_device must be 0, 1 or 2");
-    if (c->stats.n_owned < c->n)
-        CK(cudaMemsetAsync(c->d_coords, 0xFF, c->nA * 12, c->main));   // NaN for ligands of other ranks
-    for (size_t i = 0; i < c->owned.size(); ++i) {
-        const vs_bucket& b = c->buckets[c->owned[i]];
-        DockArgs a{};
-        a.rec = c->d_rec + c->owned_rec_off[i];
-        a.meta = c->d_meta + c->owned_prefix[i];
-        a.n = b.size;
-        a.rec_floats = rec_floats_of(b.kernel_atoms);
-        a.P = c->P;
-        a.K = c->K;
-        a.S_w = c->cfg.n_sweeps;
-        a.pose_tab = c->d_pose;
-        a.cs = c->d_cs;
-        a.pk = c->pkdev[slot];
-        a.best_pose = c->d_pose_best[slot];
-        a.angles = c->d_ang[slot];
-        a.order = c->d_order;
-        CK(launch_finalize(b.kernel_atoms, a, c->d_atom_off, c->d_coords, c->main));
-        c->stats.kernel_launches++;
-    }
-    CK(cudaMemcpyAsync(xyz_out, c->d_coords, c->nA * 12,
-                       on_device == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->main));
+    CK(copy_pieces(xyz_out, c->d_coords[slot], c->nA * 12,
+                   on_device == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->main));
     if (on_device != 2) CK(cudaStreamSynchronize(c->main));
     return VS_OK;
 }

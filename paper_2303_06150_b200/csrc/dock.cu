@@ -1,4 +1,4 @@
-// dock.cu -- host-side dispatch of the dock / finalize kernels per atom class,
+// dock.cu -- host-side dispatch of the dock kernels per atom class,
 // shared-memory grid strides, occupancy queries, the score_points test hook.
 // The kernels themselves are in dock_impl.cuh.
 #include "dock_impl.cuh"
@@ -92,21 +92,6 @@ cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, si
     if (e != cudaSuccess) return e;
     f<<<grid, NW * 32, smem, st>>>(a);
     return cudaGetLastError();
-}
-
-cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st) {
-    if (a.n <= 0) return cudaSuccess;
-    switch (AC) {
-        case 32: return dk::launch_finalize_32(a, atom_off, xyz_out, st);
-        case 64: return dk::launch_finalize_64(a, atom_off, xyz_out, st);
-        case 96: return dk::launch_finalize_96(a, atom_off, xyz_out, st);
-        case 128: return dk::launch_finalize_128(a, atom_off, xyz_out, st);
-        case 160: return dk::launch_finalize_160(a, atom_off, xyz_out, st);
-        case 192: return dk::launch_finalize_192(a, atom_off, xyz_out, st);
-        case 224: return dk::launch_finalize_224(a, atom_off, xyz_out, st);
-        case 256: return dk::launch_finalize_256(a, atom_off, xyz_out, st);
-        default: return cudaErrorInvalidValue;
-    }
 }
 
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,

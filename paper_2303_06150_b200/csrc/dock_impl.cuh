@@ -25,7 +25,7 @@
 //
 // All arithmetic that decides an angle or is replayed (placement, Rodrigues,
 // rotation, interpolation) uses explicit _rn intrinsics in shared helpers, so
-// the finalize kernel reproduces the trajectory bit for bit.
+// the best-pose replay (replay_coords) reproduces the trajectory bit for bit.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -508,14 +508,62 @@ __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, un
     __syncwarp();
 }
 
-// a9 best pose of one round (run by the warp that completes the round's last item).
+// a9 best-pose coordinates of one ligand: replay pose p with the recorded angle choices, bit-
+// identical to the dock trajectory (same placement, axis, Rodrigues and rotation helpers, same
+// table entries) on one warp's pose buffer (all 32 lanes), written in Angstrom in the caller's
+// input atom order (a1's order map).
+template <int AC>
+__device__ __forceinline__ void replay_coords(const DockArgs& a, const float* __restrict__ rec, int li, int A, int R,
+                                              int p, const uint8_t* __restrict__ ang, PoseBuf<AC> buf, int lane) {
+    const PocketDev& pk = a.pk;
+    const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
+    float T[12];
+    scaled_pose(a.pose_tab + 12 * p, pk, T);
+    const RotT Pz = load_pose(T);
+    for (int i = lane; i < A; i += 32) buf.set(i, apply_rot(Pz, rec[i], rec[AC + i], rec[2 * AC + i]));
+    __syncwarp();
+    for (int sw = 0; sw < a.S_w; ++sw) {
+        for (int r = 0; r < R; ++r) {
+            const int bk = ang[sw * R + r];
+            if (bk != 0) {
+                const uint32_t f = rfr[r];
+                const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
+                const float4 ya = buf.get(fa), yb = buf.get(fb);
+                float ux, uy, uz;
+                axis_of(ya, yb, ux, uy, uz);
+                const RotT Ms = rodrigues_t(ux, uy, uz, a.cs[2 * bk], a.cs[2 * bk + 1], yb.x, yb.y, yb.z);
+                for (int j = lo + lane; j < hi; j += 32) {
+                    const float4 v = buf.get(j);
+                    buf.set(j, apply_rot(Ms, v.x, v.y, v.z));
+                }
+            }
+            __syncwarp();
+        }
+    }
+    const int64_t a0 = a.atom_off[li];
+    float* out = a.xyz_out + 3 * a0;
+    const uint8_t* ord = a.order + a0;
+    for (int i = lane; i < A; i += 32) {
+        const float4 v = buf.get(i);
+        const int q = ord[i];
+        out[3 * q] = __fmaf_rn(pk.h, v.x, pk.ox);
+        out[3 * q + 1] = __fmaf_rn(pk.h, v.y, pk.oy);
+        out[3 * q + 2] = __fmaf_rn(pk.h, v.z, pk.oz);
+    }
+    __syncwarp();
+}
+
+// a9 best pose of one round (run by the warp that completes the round's last item), and its
+// coordinates (replayed on the warp's first pose buffer, free once its item completed).
+template <int AC>
 __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned char* slot, const DockLayout& L, int round,
-                                             int lane) {
+                                             PoseBuf<AC> buf, int lane) {
     const int LC = a.ligs_per_cta, P = a.P, S_w = a.S_w;
     const int nl = min(LC, a.n - round * LC);
     const int4* sMeta = reinterpret_cast<const int4*>(slot + L.meta_o);
     const float* sScore = reinterpret_cast<const float*>(slot + L.score_o);
     const uint8_t* sAng = slot + L.ang_o;
+    const float* sRec = reinterpret_cast<const float*>(slot + L.rec_o);
     const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
     for (int l = 0; l < nl; ++l) {   // lowest score, ties -> lowest pose index (Q11)
         const int4 m = sMeta[l];
@@ -544,6 +592,7 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned c
                 const int p = t / nang, q = t - p * nang;
                 a.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
             }
+        if (a.xyz_out) replay_coords<AC>(a, sRec + (size_t)l * a.rec_floats, li, m.y, R, bp, sa, buf, lane);
     }
 }
 
@@ -649,64 +698,13 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         last = __shfl_sync(FULL, last, 0);
         __syncwarp();   // lane 0's fence after the counter orders the round reads of the whole warp
         if (last) {
-            finish_round(a, slot, L, round, lane);
+            finish_round<AC>(a, slot, L, round, PoseBuf<AC>{sBuf + (warp * PPW) * pose_stride_of(AC, NW, PPW)}, lane);
             __syncwarp();
             if (lane == 0) {
                 ring.done[seq % kDockSlots] = 0;
                 st_release_cta(&ring.free_seq[seq % kDockSlots], seq + kDockSlots);
             }
         }
-    }
-}
-
-// a9 coordinates: replay p* with the recorded angles, bit-identical to the
-// dock kernel (same placement, axis, Rodrigues and rotation helpers); one warp
-// per ligand; output in Angstrom, in the caller's input atom order (a1's order map).
-template <int AC>
-__global__ void __launch_bounds__(256) finalize_kernel(const DockArgs a, const int64_t* __restrict__ atom_off,
-                                                       float* __restrict__ xyz_out) {
-    __shared__ __align__(16) float4 sb[8][AC];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int s = blockIdx.x * 8 + w;
-    if (s >= a.n) return;
-    const PocketDev& pk = a.pk;
-    const int4 m = a.meta[s];
-    const int li = m.x, A = m.y, R = m.z;
-    const int p = a.best_pose[li];
-    const float* rec = a.rec + (size_t)s * a.rec_floats;
-    const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
-    float T[12];
-    scaled_pose(a.pose_tab + 12 * p, pk, T);
-    const RotT Pz = load_pose(T);
-    float4* buf = sb[w];
-    for (int i = lane; i < A; i += 32) buf[i] = apply_rot(Pz, rec[i], rec[AC + i], rec[2 * AC + i]);
-    __syncwarp();
-    for (int sw = 0; sw < a.S_w; ++sw) {
-        for (int r = 0; r < R; ++r) {
-            const int bk = a.angles[m.w + sw * R + r];
-            if (bk != 0) {
-                const uint32_t f = rfr[r];
-                const int fa = f & 255, fb = (f >> 8) & 255, lo = (f >> 16) & 255, hi = (int)(f >> 24) + 1;
-                const float4 ya = buf[fa], yb = buf[fb];
-                float ux, uy, uz;
-                axis_of(ya, yb, ux, uy, uz);
-                const RotT Ms = rodrigues_t(ux, uy, uz, a.cs[2 * bk], a.cs[2 * bk + 1], yb.x, yb.y, yb.z);
-                for (int j = lo + lane; j < hi; j += 32) {
-                    const float4 v = buf[j];
-                    buf[j] = apply_rot(Ms, v.x, v.y, v.z);
-                }
-            }
-            __syncwarp();
-        }
-    }
-    float* out = xyz_out + 3 * atom_off[li];
-    const uint8_t* ord = a.order + atom_off[li];   // internal atom i -> input atom ord[i] (a1)
-    for (int i = lane; i < A; i += 32) {
-        const float4 v = buf[i];
-        const int q = ord[i];
-        out[3 * q] = __fmaf_rn(pk.h, v.x, pk.ox);
-        out[3 * q + 1] = __fmaf_rn(pk.h, v.y, pk.oy);
-        out[3 * q + 2] = __fmaf_rn(pk.h, v.z, pk.oz);
     }
 }
 
@@ -752,7 +750,7 @@ DockFn pick_ac(int NW, int PPW, int K) {
 // (dock_inst.cu with -DVSD_AC=<AC>) so the 8 classes build in parallel.
 #define VSD_DECL_CLASS(ac)                                                                                     \
     DockFn dock_pick_##ac(int gmode, int NW, int PPW, int K);                                                           \
-    cudaError_t launch_finalize_##ac(const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
+
 VSD_DECL_CLASS(32)
 VSD_DECL_CLASS(64)
 VSD_DECL_CLASS(96)

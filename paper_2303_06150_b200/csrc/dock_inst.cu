@@ -1,4 +1,4 @@
-// dock_inst.cu -- instantiates the dock and finalize kernels of ONE atom class
+// dock_inst.cu -- instantiates the dock kernels of ONE atom class
 // (compiled once per class with -DVSD_AC=<AC>; see build.py).
 #include "dock_impl.cuh"
 
@@ -15,12 +15,6 @@ DockFn VSD_CAT(dock_pick_, VSD_AC)(int gmode, int NW, int PPW, int K) {
     return gmode == kGridFix ? pick_ac<VSD_AC, kGridFix>(NW, PPW, K)
            : gmode == kGridRT ? pick_ac<VSD_AC, kGridRT>(NW, PPW, K)
                               : pick_ac<VSD_AC, kGridWin>(NW, PPW, K);
-}
-
-cudaError_t VSD_CAT(launch_finalize_, VSD_AC)(const DockArgs& a, const int64_t* atom_off, float* xyz_out,
-                                              cudaStream_t st) {
-    finalize_kernel<VSD_AC><<<(a.n + 7) / 8, 256, 0, st>>>(a, atom_off, xyz_out);
-    return cudaGetLastError();
 }
 
 }  // namespace dk

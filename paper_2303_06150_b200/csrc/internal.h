@@ -67,7 +67,9 @@ struct DockArgs {
     uint8_t* angles;           // CSR S_w * frag_off
     float* dbg_score;          // [n_total * P] or null
     uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
-    const uint8_t* order;      // finalize only: internal atom -> input atom (CSR by atom_off, a1)
+    const uint8_t* order;      // internal atom -> input atom (CSR by atom_off, a1)
+    const int64_t* atom_off;   // [n_total + 1]
+    float* xyz_out;            // a9 best-pose coordinates [3 * n_atoms] (input atom order) or null
 };
 
 // Packed ligand record of atom class AC (floats): x | y | z (3 AC), fragment table u32[32],
@@ -133,6 +135,7 @@ int grid_mode(int nx, int ny, int nz);
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).
+cudaError_t launch_rebase(const int64_t* src, int64_t* dst, int64_t count, int64_t base, cudaStream_t st);
 cudaError_t launch_features(const int64_t* atom_off, const int64_t* frag_off, const int64_t* move_off, int64_t n,
                             int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st);
 // a1 ingest of the owned (packed) slots: validation, laminar check, canonical renumbering.
@@ -159,7 +162,6 @@ cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const 
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int gmode, int K, cudaFuncAttributes* attr);
 cudaError_t dock_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int* blocks_per_sm);
-cudaError_t launch_finalize(int AC, const DockArgs& a, const int64_t* atom_off, float* xyz_out, cudaStream_t st);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
                                 cudaStream_t st);
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,

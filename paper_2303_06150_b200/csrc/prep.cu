@@ -651,6 +651,19 @@ __global__ void make_keys_kernel(const int4* __restrict__ meta, int n_slots, con
 
 }  // namespace
 
+__global__ void rebase_kernel(const int64_t* __restrict__ src, int64_t* __restrict__ dst, int64_t count, int64_t base) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] - base;
+}
+
+cudaError_t launch_rebase(const int64_t* src, int64_t* dst, int64_t count, int64_t base, cudaStream_t st) {
+    if (count <= 0) return cudaSuccess;
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    rebase_kernel<<<(int)blocks, 256, 0, st>>>(src, dst, count, base);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_features(const int64_t* atom_off, const int64_t* frag_off, const int64_t* move_off, int64_t n,
                             int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;

@@ -67,7 +67,6 @@ class PipelinedDocker:
         self.engine = self.engines[0]
         self.n_sweeps = self.engine.n_sweeps
         self._pinned = {}
-        self._stage = {}
         self.trace = []
 
     def setup(self, rot, trans, cs, pockets):
@@ -87,53 +86,38 @@ class PipelinedDocker:
             self._pinned[key] = torch.empty(tuple(shape), dtype=dtype).pin_memory()
         return self._pinned[key].numpy()
 
-    def _rebased(self, slot, name, src, base):
-        """src - base into a reusable PINNED staging buffer (a pageable source would make every
-        copy synchronous with the copy stream, stalling the host behind the previous chunk's
-        upload).  ``slot`` = the engine the chunk goes to: its previous chunk has been submitted,
-        so that chunk's copy from this buffer is complete."""
-        torch = self._torch
-        src = np.asarray(src)
-        key = (slot, name)
-        buf = self._stage.get(key)
-        if buf is None or buf.numel() < src.size:
-            buf = torch.empty(max(1, int(src.size * 1.25)), dtype=torch.int64).pin_memory()
-            self._stage[key] = buf
-        view = buf[: src.size]
-        np.subtract(src, base, out=view.numpy())
-        return view
-
-    def _issue_copy(self, arrays, lo, hi, slot=0):
-        """Chunk [lo, hi) to the device on the copy stream: rebased offsets + array slices."""
-        torch = self._torch
+    @staticmethod
+    def _slices(arrays, lo, hi):
+        """Chunk [lo, hi) as views of the caller's arrays: offsets keep their library values (the
+        library rebases them on the device, vs_ligand_batch), data arrays start at the chunk's
+        first element -- no host-side arithmetic on the critical path."""
         ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays
-        ao = np.asarray(atom_off[lo:hi + 1])
-        fo = np.asarray(frag_off[lo:hi + 1])
-        a0, a1, f0, f1 = int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
-        mo = np.asarray(move_off[f0:f1 + 1])
-        m0, m1 = int(mo[0]), int(mo[-1])
-        host = [ids[lo:hi], self._rebased(slot, "ao", ao, a0), xyz[a0:a1], self._rebased(slot, "fo", fo, f0),
-                frag_axis[f0:f1], self._rebased(slot, "mo", mo, m0), move_atoms[m0:m1]]
+        a0, a1 = int(atom_off[lo]), int(atom_off[hi])
+        f0, f1 = int(frag_off[lo]), int(frag_off[hi])
+        m0, m1 = int(move_off[f0]), int(move_off[f1])
+        return ([ids[lo:hi], atom_off[lo:hi + 1], xyz[a0:a1], frag_off[lo:hi + 1], frag_axis[f0:f1],
+                 move_off[f0:f1 + 1], move_atoms[m0:m1]], (a0, a1, f0, f1))
+
+    def _issue_copy(self, arrays, lo, hi):
+        """Chunk [lo, hi) to the device on the copy stream (pinned sources: asynchronous)."""
+        torch = self._torch
+        host, box = self._slices(arrays, lo, hi)
         host = [h if isinstance(h, torch.Tensor) else torch.from_numpy(np.asarray(h)) for h in host]
         with torch.cuda.stream(self.copy):
-            dev = [h.to(self.dev, non_blocking=True) for h in host]
+            dev = []
+            for h in host:
+                # 8 MB pieces: one copy engine serves every stream's H2D one request at a time,
+                # and the other engine's small preparation copies must not wait behind a whole
+                # chunk upload
+                d = torch.empty(h.shape, dtype=h.dtype, device=self.dev)
+                fd, fh = d.reshape(-1), h.reshape(-1)
+                step = max(1, (8 << 20) // max(1, h.element_size()))
+                for i in range(0, fh.numel(), step):
+                    fd[i:i + step].copy_(fh[i:i + step], non_blocking=True)
+                dev.append(d)
             ev = torch.cuda.Event()
             ev.record(self.copy)
-        return dev, ev, (a0, a1, f0, f1)
-
-    def _zero_copy_args(self, arrays, lo, hi, slot=0):
-        """Chunk [lo, hi) for on_device = 2: rebased offsets (pinned staging, copied by the
-        library) and pinned slices the kernels read in place -- only this rank's ligands cross
-        PCIe."""
-        ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays
-        ao = np.asarray(atom_off[lo:hi + 1])
-        fo = np.asarray(frag_off[lo:hi + 1])
-        a0, a1, f0, f1 = int(ao[0]), int(ao[-1]), int(fo[0]), int(fo[-1])
-        mo = np.asarray(move_off[f0:f1 + 1])
-        m0, m1 = int(mo[0]), int(mo[-1])
-        args = [ids[lo:hi], self._rebased(slot, "ao", ao, a0), xyz[a0:a1], self._rebased(slot, "fo", fo, f0),
-                frag_axis[f0:f1], self._rebased(slot, "mo", mo, m0), move_atoms[m0:m1]]
-        return args, (a0, a1, f0, f1)
+        return dev, ev, box
 
     def run(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, k: int = 1000,
             chunks: int = 0, max_atoms: int = 256, group=None, coords: bool = True, first: int = 32,
@@ -169,20 +153,34 @@ class PipelinedDocker:
         arrays = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
         self.trace = []
         ne = len(self.engines)
-        inflight = {} if zero_copy else {c: self._issue_copy(arrays, bounds[c], bounds[c + 1], c % ne)
+        inflight = {} if zero_copy else {c: self._issue_copy(arrays, bounds[c], bounds[c + 1])
                                          for c in range(min(ne, nch))}
         keep = {}
         failed = None
+        pending = None
+
+        def readback(e, lo, hi, a0, a1, f0, f1):
+            """Asynchronous a9 read-back of one chunk into the pinned outputs (engine e's stream:
+            after its docking)."""
+            for s in range(npk):
+                e.results_async(s, best[s, lo:hi], pose[s, lo:hi], ang[s, S_w * f0:S_w * f1] if f1 > f0 else None)
+                if coords and a1 > a0:
+                    e.coords_into(s, xyz_out[s, a0:a1], mode=2)
+
+        import time
         for c in range(nch):
             lo, hi = bounds[c], bounds[c + 1]
             e = self.engines[c % ne]
+            t0 = time.perf_counter()
             if zero_copy:
-                dev, (a0, a1, f0, f1) = self._zero_copy_args(arrays, lo, hi, c % ne)
+                dev, (a0, a1, f0, f1) = self._slices(arrays, lo, hi)   # read in place (on_device = 2)
                 mode = 2
             else:
                 dev, ev, (a0, a1, f0, f1) = inflight.pop(c)
                 ev.synchronize()    # chunk c resident (submit reads its CSR totals)
                 mode = 1
+            t1 = time.perf_counter()
+            t2 = t1
             if hi > lo and failed is None:     # (chunk_bounds never yields an empty chunk)
                 # returns once the dock launches are queued; the read-backs below queue behind
                 # them on the same stream and run on the D2H engine while the other engine docks
@@ -194,18 +192,23 @@ class PipelinedDocker:
                         failed.ligand = err.ligand + lo
                     keep[c % ne] = dev
                     continue
+                t2 = time.perf_counter()
                 for s in range(npk):
-                    e.results_async(s, best[s, lo:hi], pose[s, lo:hi],
-                                    ang[s, S_w * f0:S_w * f1] if f1 > f0 else None)
-                    if coords and a1 > a0:
-                        e.coords_into(s, xyz_out[s, a0:a1], mode=2)
                     nkeys[s] += e.keys_into(s, all_keys[s][nkeys[s]:], lo)
+                # the read-backs of the PREVIOUS chunk are queued only now, after this chunk's
+                # preparation: the copy engine serves D2H requests in submission order, so a
+                # read-back queued earlier would hold up this preparation's small status reads
+                if pending is not None:
+                    readback(*pending)
+                pending = (e, lo, hi, a0, a1, f0, f1)
             keep[c % ne] = dev      # the engine borrows the chunk until its next submit
             if c + ne < nch and not zero_copy:
                 # the buffer slot of chunk c + ne is engine c's: its copy may only overwrite
                 # device memory the engine no longer reads -- new tensors, so no hazard
-                inflight[c + ne] = self._issue_copy(arrays, bounds[c + ne], bounds[c + ne + 1], (c + ne) % ne)
-            self.trace.append((c, lo, hi))
+                inflight[c + ne] = self._issue_copy(arrays, bounds[c + ne], bounds[c + ne + 1])
+            self.trace.append((c, lo, hi, t0, t1, t2, time.perf_counter()))   # host timeline (diagnostics)
+        if pending is not None:
+            readback(*pending)
         for st in self.streams:
             st.synchronize()
         e = self.engine

@@ -707,3 +707,30 @@ def test_pipelined_zero_copy_matches():
     assert np.array_equal(out["best_score"][0], r.best_score) and np.array_equal(out["xyz"][0], e.coords(0))
     assert list(out["topk"][0][0]) == list(oracle.topk(r.best_score, 50))
     pd.close()
+
+
+def test_offsets_relative_to_their_first_entry():
+    """A slice of a larger library (offsets starting at b != 0, data arrays starting at the slice) is
+    docked exactly like the same ligands as a stand-alone batch, for host, device and mapped input."""
+    import torch
+    lib = vsgen.ligands(600, 63, (20, 120), (0, 20))
+    lo, hi = 217, 431
+    sub = lib.subset(np.arange(lo, hi))
+    pk = vsgen.pocket(101)
+    e, *_ = run(sub, [pk], P=8, K=8, debug=False)
+    want, want_xyz = e.results(0), e.coords(0)
+    a0, a1 = int(lib.atom_off[lo]), int(lib.atom_off[hi])
+    f0, f1 = int(lib.frag_off[lo]), int(lib.frag_off[hi])
+    m0, m1 = int(lib.move_off[f0]), int(lib.move_off[f1])
+    sl = [lib.ligand_id[lo:hi], lib.atom_off[lo:hi + 1], lib.xyz[a0:a1], lib.frag_off[lo:hi + 1],
+          lib.frag_axis[f0:f1], lib.move_off[f0:f1 + 1], lib.move_atoms[m0:m1]]
+    variants = {0: [np.ascontiguousarray(a) for a in sl], 1: [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in sl],
+                2: [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in sl]}
+    for mode, arrs in variants.items():
+        e2 = engine()
+        setup(e2, [pk], 8, 8)
+        e2.submit(*arrs, [0], on_device=mode, max_atoms=120)
+        e2.wait()
+        r = e2.results(0)
+        assert np.array_equal(r.best_score, want.best_score) and np.array_equal(r.angles, want.angles), mode
+        assert np.array_equal(r.ligand_id, lib.ligand_id[lo:hi]) and np.array_equal(e2.coords(0), want_xyz), mode

@@ -1,10 +1,11 @@
-"""e2e pipeline experiment (not a bench value): PipelinedDocker wall time vs chunk schedule on C4."""
+"""e2e pipeline diagnostics (not a bench value): PipelinedDocker wall time vs chunk schedule on C4,
+with the host timeline of every chunk (wait for its upload, submit = prep incl. host syncs,
+read-back queueing).  python tools/e2e_sweep.py [n]"""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import vsgen
-from paper_2303_06150_b200 import Engine
 from paper_2303_06150_b200.pipeline import PipelinedDocker, chunk_bounds
 c = vsgen.CONFIGS["C4"]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else c["n"]
@@ -14,14 +15,18 @@ rot, tr = vsgen.pose_table(c["P"]); cs = vsgen.angle_table(c["K"])
 h = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
 pd = PipelinedDocker(); pd.setup(rot, tr, cs, pk)
 mx = int(lib.n_atoms.max())
-for first, growth in ((32, 4), (32, 6), (64, 6), (32, 8), (16, 4)):
+for chunks, coords, zc in ((0, True, False), (1, True, False), (2, True, False), (4, True, False), (8, True, False),
+                           (0, False, False), (0, True, True), (4, True, True)):
     ts = []
     for _ in range(4):
         torch.cuda.synchronize(); t = time.perf_counter()
-        pd.run(*h, k=1000, chunks=0, max_atoms=mx, first=first, growth=growth)
+        pd.run(*h, k=1000, chunks=chunks, max_atoms=mx, coords=coords, zero_copy=zc)
         ts.append(time.perf_counter() - t)
     dt = float(np.median(ts[1:]))
-    print(f"first=n/{first} growth={growth} {chunk_bounds(n, 0, first, growth)[1:]}: {dt*1e3:.1f} ms  {n/dt:.3e} lig/s", flush=True)
+    print(f"chunks={chunks} coords={coords} zero_copy={zc} {chunk_bounds(n, chunks)[1:]}: {dt*1e3:.1f} ms "
+          f"{n/dt:.3e} lig/s", flush=True)
+    T0 = pd.trace[0][3]
     for r in pd.trace:
-        print(f"   chunk {r[0]} wait-copy {1e3*(r[2]-r[1]):.2f} ms  compute {1e3*(r[3]-r[2]):.2f} ms  prep {r[4]:.2f} dock {r[5]:.2f}")
+        print(f"   chunk {r[0]} [{r[1]},{r[2]}) start {1e3*(r[3]-T0):7.2f}  upload-wait {1e3*(r[4]-r[3]):6.2f}  "
+              f"submit {1e3*(r[5]-r[4]):6.2f}  queue-readback {1e3*(r[6]-r[5]):6.2f} ms")
 pd.close()
