@@ -21,10 +21,15 @@ for (i, name), m in per.items():
     a[0] += 1
     a[1] += m.get("gpu__time_duration.sum", 0.0)
     a[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-tot = sum(a[1] for a in agg.values())
+# bench.py's live roofline denominators (tools/ceilings.cu: k_l2, k_gather) and torch's own
+# kernels run outside the timed step: listed, not counted in the step's shares
+EXTERNAL = ("k_l2", "k_gather", "at::")
+tot = sum(a[1] for k, a in agg.items() if not k.lstrip("<").startswith(EXTERNAL))
 print(f"{'launches':>8} {'time_ms':>10} {'share':>7} {'dram_MB':>10}  kernel   (2 steps: warmup + timed; ncu serialised, cold cache)")
 for k, a in sorted(agg.items(), key=lambda x: -x[1][1]):
-    print(f"{a[0]:8d} {a[1]/1e6:10.3f} {100*a[1]/tot:6.1f}% {a[2]/1e6:10.1f}  {k}")
+    ext = k.lstrip("<").startswith(EXTERNAL)
+    share = "   ext" if ext else f"{100*a[1]/tot:5.1f}%"
+    print(f"{a[0]:8d} {a[1]/1e6:10.3f} {share:>7} {a[2]/1e6:10.1f}  {k}")
 dock = [v for k, v in agg.items() if k.startswith("dock_kernel")]
 steps = 2
 if out_json:
