@@ -342,9 +342,29 @@ def main():
                       f"best scores, poses, angle indices, best-pose coordinates (input atom order) + top-{K_TOP} "
                       f"per pocket; {n_chunks} chunk(s) {chunk_bounds(n, chunks)[1:]} over 2 engines: H2D of chunk "
                       f"i+1 and the D2H of chunk i-1's outputs under the docking of chunk i"}
+    multisite = None
+    if len(pockets) > 1 and not args.no_unsorted:
+        # the same step with the fused multi-site cluster launches (records
+        # staged once per cluster) instead of one launch per pocket
+        if args.no_e2e:
+            eng.close()
+        pe = Engine(device=local, atom_clusters=6, rot_clusters=23, bucket_multiple=args.bucket_multiple,
+                    n_streams=args.streams, rank=rank, world_size=world, fused_sites=True)
+        pe.set_poses(rot, tr)
+        pe.set_angles(cs)
+        pids = [pe.load_pocket(p) for p in pockets]
+        t_p, dock_p, _, _ = timed(pe, pids, d_lib, True)
+        pv = n * len(pockets) / (t_p / args.steps / 1e3)
+        multisite = {"fused_value": pv, "per_pocket_value": value, "unit": "ligand-pockets/s",
+                     "fused_over_per_pocket": pv / value, "fused_dock_ms_per_step": float(np.mean(dock_p)),
+                     "per_pocket_dock_ms_per_step": dock_avg,
+                     "note": "fused = thread-block clusters of one CTA per pocket, each ligand round staged once per "
+                             "cluster by multicast TMA (cluster size chosen by cudaOccupancyMaxActiveClusters); the "
+                             "default (value) is one persistent launch per (class, pocket)"}
+        pe.close()
     unsorted = None
     if not args.no_unsorted:
-        if args.no_e2e:
+        if args.no_e2e and multisite is None:
             eng.close()
         ue, uids = make_engine(1, 1)
         t_u, dock_u, _, _ = timed(ue, uids, d_lib, True)
@@ -391,7 +411,7 @@ def main():
                                           "4-byte gathers run ~3-way bank-conflicted, so the gather ceiling (measured "
                                           "live, uniformly random points) is ~1/3.5 of the crossbar peak"}},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": launches,
-            "cpu_baseline": cpu, "unsorted": unsorted,
+            "cpu_baseline": cpu, "unsorted": unsorted, "multisite": multisite,
             "classes": [{k: cl[k] for k in ("kernel_atoms", "warps_per_cta", "regs_per_thread", "dyn_smem", "blocks_per_sm",
                                             "ligands_per_cta", "l", "capacity")} for cl in classes],
         }

@@ -65,6 +65,10 @@ typedef struct {
                                   persistent launch with dynamic ligand scheduling */
     int32_t bucket_capacity;   /* > 0: every bucket holds this many ligands instead of m * l_c
                                   (the bucket-size sweep of P:283-333); 0 = Eq. 1 */
+    int32_t fused_sites;       /* 1: a submit with 2..8 pockets of one 32^3-class grid layout docks
+                                  them in ONE launch per atom class: thread-block clusters of one
+                                  CTA per pocket, each ligand round staged once per cluster
+                                  (multicast TMA).  0: one launch per pocket */
     void* stream;             /* cudaStream_t the library orders its work on (e.g. torch's); NULL = own */
 } vs_config;
 
@@ -245,6 +249,7 @@ typedef struct {
     int64_t n_buckets, n_owned_buckets;
     int64_t kernel_launches;   /* kernels launched by the last submit (+ topk/coords calls since) */
     int64_t dock_launches;
+    int64_t fused_launches;    /* dock launches that were fused multi-site cluster launches */
     double evals_alg;          /* sum over owned ligands and pockets of E_alg (SURVEY 8 'E_alg') */
     uint64_t h2d_bytes;        /* bytes the submit moved host -> device: copies (on_device 0), or
                                   the offsets + the owned ligands' arrays read in place (2); 0 for 1 */

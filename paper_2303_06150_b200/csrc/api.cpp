@@ -1074,35 +1074,84 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     const int NS = (int)c->workers.size();
     for (int s = 0; s < NS; ++s) CK(cudaStreamWaitEvent(c->workers[s], c->ev_prep1, 0));
     int64_t dock_launches = 0;
+    // fused multi-site: all pockets share one grid layout (FIX) -> one cluster
+    // launch per unit docks every pocket, the records staged once per cluster (multicast)
+    bool fuse = c->cfg.fused_sites && n_pockets >= 2 && n_pockets <= kMaxSites;
+    for (int q = 1; fuse && q < n_pockets; ++q) fuse = c->pk_layout[q] == c->pk_layout[0];
+    fuse = fuse && c->pkdev[0].mode == kGridFix;
+    auto base_args = [&](const Unit& u, const ClassInfo& ci) {
+        const vs_bucket& b = c->buckets[c->owned[u.first]];
+        DockArgs a{};
+        a.rec = c->d_rec + c->owned_rec_off[u.first];
+        a.meta = c->d_meta + c->owned_prefix[u.first];
+        a.n = u.slots;
+        a.rec_floats = rec_floats_of(b.kernel_atoms);
+        a.P = c->P;
+        a.K = c->K;
+        a.S_w = S_w;
+        a.ligs_per_cta = ci.LC;
+        a.frag_cap = c->frag_cap;
+        a.n_sites = 1;
+        a.pose_tab = c->d_pose;
+        a.cs = c->d_cs;
+        a.order = c->d_order;
+        a.atom_off = c->d_atom_off;
+        return a;
+    };
+    auto site = [&](DockArgs& a, int s, int q) {
+        a.pk[s] = c->pkdev[q];
+        a.out[s] = SiteOut{c->d_score[q], c->d_pose_best[q], c->d_ang[q], c->d_dbg_score[q], c->d_dbg_ang[q],
+                           c->d_coords[q]};
+    };
+    c->stats.fused_launches = 0;
     for (const Unit& u : units) {
         const vs_bucket& b = c->buckets[c->owned[u.first]];
-        const int i = u.first;
+        if (fuse) {
+            const ClassInfo& ci = c->layout_classes[c->pk_layout[0]][u.cls];
+            const PocketDev& p0 = c->pkdev[0];
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, p0.mode, p0.nz, p0.rs, p0.ps, c->P, c->K, S_w,
+                                             ci.LC, c->frag_cap);
+            // cluster size g: the one that keeps the most SMs busy (clusters are placed whole
+            // inside a GPC, so large clusters of 227 KB CTAs leave SMs idle); ties -> larger g
+            int best_g = 1, best_sms = ci.b * c->sm_count, best_cl = 0;
+            for (int g = std::min(n_pockets, kMaxSites); g >= 2; --g) {
+                int cl = 0;
+                CK(dock_cluster_occupancy(b.kernel_atoms, ci.NW, ci.PPW, p0.mode, c->K, L.total, g, &cl));
+                if (cl > 0 && (cl * g > best_sms || (best_g == 1 && cl * g * 100 >= best_sms * 97))) {
+                    best_g = g;
+                    best_sms = cl * g;
+                    best_cl = cl;
+                }
+            }
+            if (best_g > 1) {
+                const int rounds = (u.slots + ci.LC - 1) / ci.LC;
+                for (int q0 = 0; q0 < n_pockets; q0 += best_g) {
+                    const int g = std::min(best_g, n_pockets - q0);
+                    DockArgs a = base_args(u, ci);
+                    a.counter = d_counters + dock_launches;
+                    if (g == 1) {
+                        site(a, 0, q0);
+                        CK(launch_dock(b.kernel_atoms, ci.NW, ci.PPW, a, std::min(rounds, ci.b * c->sm_count), L.total,
+                                       c->workers[dock_launches % NS]));
+                    } else {
+                        a.n_sites = g;
+                        for (int s2 = 0; s2 < g; ++s2) site(a, s2, q0 + s2);
+                        const int grid = std::min(rounds, best_cl * best_g / g) * g;
+                        CK(launch_dock(b.kernel_atoms, ci.NW, ci.PPW, a, grid, L.total, c->workers[dock_launches % NS]));
+                        ++c->stats.fused_launches;
+                    }
+                    ++dock_launches;
+                }
+                continue;
+            }
+        }
         for (int q = 0; q < n_pockets; ++q) {
             const ClassInfo& ci = c->layout_classes[c->pk_layout[q]][u.cls];
-            DockArgs a{};
-            a.rec = c->d_rec + c->owned_rec_off[i];
-            a.meta = c->d_meta + c->owned_prefix[i];
-            a.n = u.slots;
-            a.rec_floats = rec_floats_of(b.kernel_atoms);
-            a.P = c->P;
-            a.K = c->K;
-            a.S_w = S_w;
-            a.ligs_per_cta = ci.LC;
-            a.frag_cap = c->frag_cap;
-            a.pose_tab = c->d_pose;
-            a.cs = c->d_cs;
-            a.pk = c->pkdev[q];
-            a.best_score = c->d_score[q];
-            a.best_pose = c->d_pose_best[q];
-            a.angles = c->d_ang[q];
-            a.dbg_score = c->d_dbg_score[q];
-            a.dbg_angles = c->d_dbg_ang[q];
-            a.order = c->d_order;
-            a.atom_off = c->d_atom_off;
-            a.xyz_out = c->d_coords[q];
+            DockArgs a = base_args(u, ci);
+            site(a, 0, q);
             a.counter = d_counters + dock_launches;
-            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk.mode, a.pk.nz, a.pk.rs, a.pk.ps, c->P,
-                                             c->K, S_w, ci.LC, c->frag_cap);
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk[0].mode, a.pk[0].nz, a.pk[0].rs,
+                                             a.pk[0].ps, c->P, c->K, S_w, ci.LC, c->frag_cap);
             const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];

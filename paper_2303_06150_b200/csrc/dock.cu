@@ -9,16 +9,16 @@ using dk::DockFn;
 
 namespace {
 
-DockFn pick(int AC, int NW, int PPW, int gm, int K) {
+DockFn pick(int AC, int NW, int PPW, int gm, int K, bool ms = false) {
     switch (AC) {
-        case 32: return dk::dock_pick_32(gm, NW, PPW, K);
-        case 64: return dk::dock_pick_64(gm, NW, PPW, K);
-        case 96: return dk::dock_pick_96(gm, NW, PPW, K);
-        case 128: return dk::dock_pick_128(gm, NW, PPW, K);
-        case 160: return dk::dock_pick_160(gm, NW, PPW, K);
-        case 192: return dk::dock_pick_192(gm, NW, PPW, K);
-        case 224: return dk::dock_pick_224(gm, NW, PPW, K);
-        case 256: return dk::dock_pick_256(gm, NW, PPW, K);
+        case 32: return dk::dock_pick_32(gm, NW, PPW, K, ms);
+        case 64: return dk::dock_pick_64(gm, NW, PPW, K, ms);
+        case 96: return dk::dock_pick_96(gm, NW, PPW, K, ms);
+        case 128: return dk::dock_pick_128(gm, NW, PPW, K, ms);
+        case 160: return dk::dock_pick_160(gm, NW, PPW, K, ms);
+        case 192: return dk::dock_pick_192(gm, NW, PPW, K, ms);
+        case 224: return dk::dock_pick_224(gm, NW, PPW, K, ms);
+        case 256: return dk::dock_pick_256(gm, NW, PPW, K, ms);
         default: return nullptr;
     }
 }
@@ -82,7 +82,8 @@ cudaError_t dock_occupancy(int AC, int NW, int PPW, int gm, int K, size_t smem, 
 }
 
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st) {
-    DockFn f = pick(AC, NW, PPW, a.pk.mode, a.K);
+    const bool ms = a.n_sites > 1;
+    DockFn f = pick(AC, NW, PPW, a.pk[0].mode, a.K, ms);
     if (!f) return cudaErrorInvalidValue;
     if (a.n <= 0) return cudaSuccess;
     // the attribute is per function, and one instantiation can serve several grid layouts
@@ -90,8 +91,55 @@ cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, si
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    f<<<grid, NW * 32, smem, st>>>(a);
-    return cudaGetLastError();
+    if (!ms) {
+        f<<<grid, NW * 32, smem, st>>>(a);
+        return cudaGetLastError();
+    }
+    // fused multi-site: clusters of n_sites CTAs (grid = n_sites x clusters)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
+    cfg.blockDim = dim3((unsigned)(NW * 32), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)a.n_sites;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, f, a);
+}
+
+// Clusters of `sites` CTAs of the fused multi-site kernel that fit on the device at once
+// (0: not available for this class / layout).
+cudaError_t dock_cluster_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int sites, int* clusters) {
+    *clusters = 0;
+    DockFn f = pick(AC, NW, PPW, gmode, K, true);
+    if (!f || sites < 2 || sites > kMaxSites) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cudaSuccess;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)sites, 1, 1);
+    cfg.blockDim = dim3((unsigned)(NW * 32), 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)sites;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaOccupancyMaxActiveClusters(clusters, reinterpret_cast<const void*>(f), &cfg);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *clusters = 0;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,

@@ -463,6 +463,62 @@ __device__ __forceinline__ void ring_backoff(unsigned& spins) {
     if (++spins > (1u << 26)) __trap();
 }
 
+// ---- thread-block cluster primitives (fused multi-site launches, MS)
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+// shared::cluster address of a local shared variable's copy in CTA `rank` of the cluster
+__device__ __forceinline__ unsigned mapa(const void* p, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(unsigned addr, int v) {
+    asm volatile("st.shared::cluster.b32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_cluster(unsigned addr, int v) {
+    asm volatile("st.release.cluster.shared::cluster.b32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_min_cluster(unsigned addr, int v) {
+    asm volatile("red.shared::cluster.min.s32 [%0], %1;\n" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cluster(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cluster.shared::cta.b32 %0, [%1];\n" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_remote(unsigned addr, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(addr), "r"(tx)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, unsigned parity) {
+    unsigned done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+// TMA bulk copy global -> the same shared-memory offset of every CTA in cta_mask, signalling
+// each destination CTA's mbarrier at the same offset (one L2 read feeds the whole cluster)
+__device__ __forceinline__ void bulk_g2s_multicast(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                                   unsigned short cta_mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 // Ring control in static shared memory (one entry per slot).
 struct DockRing {
     int ready[kDockSlots];   // round sequence number whose record this slot holds
@@ -473,6 +529,7 @@ struct DockRing {
     int item;                // CTA-local item counter
     int end_seq;             // first sequence number that found the launch exhausted (INT_MAX: none yet)
     uint64_t bar[kDockSlots];// record arrival (TMA complete_tx), phase (s / kDockSlots) & 1 for sequence s
+    uint64_t free_bar[kDockSlots];   // MS, rank 0: every CTA of the cluster released the slot
 };
 
 // Stage sequence `seq` into `slot` and publish it: lane 0 issues TMA bulk copies of the
@@ -480,10 +537,46 @@ struct DockRing {
 // round index.  The round was claimed one sequence earlier; the claim for seq + 1 (the
 // launch's global counter: dynamic scheduling across CTAs) is issued here, claims stay in
 // sequence order.
-template <int AC>
+//
+// MS (fused multi-site, run by CTA rank 0 only): the slot is free once EVERY CTA of the cluster
+// released it (free_bar, one phase per use); the round index and the ready flag are written into
+// every CTA's ring (DSMEM stores, release at cluster scope), every CTA's mbarrier is armed remotely
+// with the byte count, and ONE multicast TMA copy stages the records + meta into all of them.
+template <int AC, bool MS>
 __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, unsigned char* slot, const DockLayout& L,
                                            int seq, int n_rounds, int lane) {
     const int sl = seq % kDockSlots;
+    if (MS) {
+        if (lane == 0) {
+            unsigned spins = 0;
+            if (seq >= kDockSlots)
+                while (!mbar_try_wait_cluster(&ring.free_bar[sl], (unsigned)(seq / kDockSlots - 1) & 1u))
+                    ring_backoff(spins);
+            const int round = ring.claim[sl];
+            const int next = atomicAdd(a.counter, 1);
+            ring.claim[(seq + 1) % kDockSlots] = next;
+            const int S = a.n_sites;
+            const bool have = round < n_rounds;
+            const int LC = a.ligs_per_cta;
+            const int slot0 = have ? round * LC : 0;
+            const int nl = have ? min(LC, a.n - slot0) : 0;
+            const unsigned rb = (unsigned)(nl * a.rec_floats * 4), mb = (unsigned)(nl * 16);
+            for (int r = 0; r < S; ++r) {
+                st_cluster(mapa(&ring.round[sl], r), have ? round : -1);
+                if (!have) red_min_cluster(mapa(&ring.end_seq, r), seq);
+                if (have) mbar_arrive_expect_tx_remote(mapa(&ring.bar[sl], r), rb + mb);
+                else mbar_arrive_remote(mapa(&ring.bar[sl], r));
+                st_release_cluster(mapa(&ring.ready[sl], r), seq);
+            }
+            if (have) {
+                const unsigned short mask = (unsigned short)((1u << S) - 1u);
+                bulk_g2s_multicast(slot + L.rec_o, a.rec + (size_t)slot0 * a.rec_floats, rb, &ring.bar[sl], mask);
+                bulk_g2s_multicast(slot + L.meta_o, a.meta + slot0, mb, &ring.bar[sl], mask);
+            }
+        }
+        __syncwarp();
+        return;
+    }
     if (lane == 0) {
         unsigned spins = 0;
         while (ld_acquire_cta(&ring.free_seq[sl]) != seq) ring_backoff(spins);
@@ -513,9 +606,9 @@ __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, un
 // table entries) on one warp's pose buffer (all 32 lanes), written in Angstrom in the caller's
 // input atom order (a1's order map).
 template <int AC>
-__device__ __forceinline__ void replay_coords(const DockArgs& a, const float* __restrict__ rec, int li, int A, int R,
-                                              int p, const uint8_t* __restrict__ ang, PoseBuf<AC> buf, int lane) {
-    const PocketDev& pk = a.pk;
+__device__ __forceinline__ void replay_coords(const DockArgs& a, const PocketDev& pk, float* __restrict__ xyz_out,
+                                              const float* __restrict__ rec, int li, int A, int R, int p,
+                                              const uint8_t* __restrict__ ang, PoseBuf<AC> buf, int lane) {
     const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
     float T[12];
     scaled_pose(a.pose_tab + 12 * p, pk, T);
@@ -541,7 +634,7 @@ __device__ __forceinline__ void replay_coords(const DockArgs& a, const float* __
         }
     }
     const int64_t a0 = a.atom_off[li];
-    float* out = a.xyz_out + 3 * a0;
+    float* out = xyz_out + 3 * a0;
     const uint8_t* ord = a.order + a0;
     for (int i = lane; i < A; i += 32) {
         const float4 v = buf.get(i);
@@ -556,8 +649,9 @@ __device__ __forceinline__ void replay_coords(const DockArgs& a, const float* __
 // a9 best pose of one round (run by the warp that completes the round's last item), and its
 // coordinates (replayed on the warp's first pose buffer, free once its item completed).
 template <int AC>
-__device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned char* slot, const DockLayout& L, int round,
-                                             PoseBuf<AC> buf, int lane) {
+__device__ __forceinline__ void finish_round(const DockArgs& a, const PocketDev& pk, const SiteOut& so,
+                                             const unsigned char* slot, const DockLayout& L, int round, PoseBuf<AC> buf,
+                                             int lane) {
     const int LC = a.ligs_per_cta, P = a.P, S_w = a.S_w;
     const int nl = min(LC, a.n - round * LC);
     const int4* sMeta = reinterpret_cast<const int4*>(slot + L.meta_o);
@@ -580,19 +674,19 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned c
         const int bp = (int)(best & 0xffffffffu);
         const int li = m.x, R = m.z, nang = S_w * R;
         if (lane == 0) {
-            a.best_score[li] = sScore[l * P + bp];
-            a.best_pose[li] = bp;
+            so.best_score[li] = sScore[l * P + bp];
+            so.best_pose[li] = bp;
         }
         const uint8_t* sa = sAng + (size_t)(l * P + bp) * ang_stride;
-        for (int t = lane; t < nang; t += 32) a.angles[m.w + t] = sa[t];
-        if (a.dbg_score)
-            for (int p = lane; p < P; p += 32) a.dbg_score[(size_t)li * P + p] = sScore[l * P + p];
-        if (a.dbg_angles)
+        for (int t = lane; t < nang; t += 32) so.angles[m.w + t] = sa[t];
+        if (so.dbg_score)
+            for (int p = lane; p < P; p += 32) so.dbg_score[(size_t)li * P + p] = sScore[l * P + p];
+        if (so.dbg_angles)
             for (int t = lane; t < P * nang; t += 32) {
                 const int p = t / nang, q = t - p * nang;
-                a.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
+                so.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
             }
-        if (a.xyz_out) replay_coords<AC>(a, sRec + (size_t)l * a.rec_floats, li, m.y, R, bp, sa, buf, lane);
+        if (so.xyz_out) replay_coords<AC>(a, pk, so.xyz_out, sRec + (size_t)l * a.rec_floats, li, m.y, R, bp, sa, buf, lane);
     }
 }
 
@@ -603,12 +697,19 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const unsigned c
 // long before use and global rounds are claimed in sequence order), the
 // warp that completes the last item of a round reduces its best pose (a9) and frees the
 // slot.  NW is therefore free of P / PPW (e.g. 12 warps of 4 poses for 64 poses).
-template <int AC, int NW, int PPW, int GM, int KT>
+// MS = fused multi-site launch: the kernel runs as thread-block clusters of
+// a.n_sites CTAs, CTA rank s docking into pocket s with that pocket's grid in ITS shared memory.
+// Rank 0 claims the rounds and stages each round's records ONCE for the whole cluster (multicast
+// TMA into the same slot of every CTA); a slot is reused only after every CTA released it.
+template <int AC, int NW, int PPW, int GM, int KT, bool MS>
 __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DockRing ring;
     constexpr int LPP = 32 / PPW;
-    const PocketDev& pk = a.pk;
+    const int site = MS ? (int)cluster_rank() : 0;
+    const bool leader = !MS || site == 0;   // the CTA that claims and stages rounds
+    const PocketDev& pk = a.pk[site];
+    const SiteOut& so = a.out[site];
     const int LC = a.ligs_per_cta;
     const DockLayout L = dock_layout(AC, NW, PPW, GM, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
@@ -622,15 +723,22 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         ring.done[tid] = 0;
         ring.free_seq[tid] = tid;
         mbar_init(&ring.bar[tid], 1);
+        if (MS) mbar_init(&ring.free_bar[tid], a.n_sites);
     }
     if (tid == 0) {
         ring.item = 0;
         ring.end_seq = 0x7fffffff;
-        ring.claim[0] = atomicAdd(a.counter, 1);
+        if (leader) ring.claim[0] = atomicAdd(a.counter, 1);
     }
     stage_grid(sG, pk, (L.buf - L.grid) / 4 + (size_t)NW * PPW * pose_stride_of(AC, NW, PPW));   // grid + pose buffers
-    __syncthreads();
-    if (warp == 0) load_round<AC>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
+    if (MS) {
+        // every CTA's ring (mbarriers included) exists before rank 0 writes into it
+        if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        cluster_sync_all();
+    } else {
+        __syncthreads();
+    }
+    if (warp == 0 && leader) load_round<AC, MS>(a, ring, slot_ptr(0), L, 0, n_rounds, lane);
 
     const int K = KT ? KT : a.K, S_w = a.S_w, P = a.P;
     const int kbits = K > 1 ? 32 - __clz(K - 1) : 0;   // log2 of Kp, the next power of two >= K
@@ -653,7 +761,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             const int sl = seq % kDockSlots;
             unsigned spins = 0;
             while (true) {
-                if (ld_acquire_cta(&ring.ready[sl]) == seq) {
+                if ((MS ? ld_acquire_cluster(&ring.ready[sl]) : ld_acquire_cta(&ring.ready[sl])) == seq) {
                     ok = ring.round[sl] >= 0;
                     break;
                 }
@@ -666,11 +774,13 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         if (!ok) break;
         {   // the record itself: TMA arrival on the slot's mbarrier (every lane acquires)
             unsigned spins = 0;
-            while (!mbar_try_wait(&ring.bar[seq % kDockSlots], (unsigned)(seq / kDockSlots) & 1u)) ring_backoff(spins);
+            const unsigned par = (unsigned)(seq / kDockSlots) & 1u;
+            while (!(MS ? mbar_try_wait_cluster(&ring.bar[seq % kDockSlots], par) : mbar_try_wait(&ring.bar[seq % kDockSlots], par)))
+                ring_backoff(spins);
         }
         // round s + 1 is claimed only once round s is (claims follow the sequence order, so
         // the first exhausted sequence bounds all later ones: end_seq is exact)
-        if (it == loader_item) load_round<AC>(a, ring, slot_ptr(seq + 1), L, seq + 1, n_rounds, lane);
+        if (it == loader_item && leader) load_round<AC, MS>(a, ring, slot_ptr(seq + 1), L, seq + 1, n_rounds, lane);
         unsigned char* slot = slot_ptr(seq);
         const int round = ring.round[seq % kDockSlots];
         const int nl = min(LC, a.n - round * LC);
@@ -686,7 +796,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             float T[12];   // pose p in grid units, from the raw table (48 B, L1-resident)
             scaled_pose(a.pose_tab + 12 * pc, pk, T);
             dock_poses<AC, PPW, GM, KT>(rec, m.y, m.z, T, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
-                                     sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
+                                        sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncwarp();
         int last = 0;
@@ -698,14 +808,19 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         last = __shfl_sync(FULL, last, 0);
         __syncwarp();   // lane 0's fence after the counter orders the round reads of the whole warp
         if (last) {
-            finish_round<AC>(a, slot, L, round, PoseBuf<AC>{sBuf + (warp * PPW) * pose_stride_of(AC, NW, PPW)}, lane);
+            finish_round<AC>(a, pk, so, slot, L, round, PoseBuf<AC>{sBuf + (warp * PPW) * pose_stride_of(AC, NW, PPW)},
+                             lane);
             __syncwarp();
             if (lane == 0) {
                 ring.done[seq % kDockSlots] = 0;
-                st_release_cta(&ring.free_seq[seq % kDockSlots], seq + kDockSlots);
+                if (MS) mbar_arrive_remote(mapa(&ring.free_bar[seq % kDockSlots], 0));   // released by this CTA
+                else st_release_cta(&ring.free_seq[seq % kDockSlots], seq + kDockSlots);
             }
         }
     }
+    // MS: rank 0 keeps writing into the other CTAs' rings (and they arrive on its free barriers)
+    // until the launch is exhausted -- nobody leaves before everybody is done
+    if (MS) cluster_sync_all();
 }
 
 template <int GM>
@@ -726,30 +841,38 @@ __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, 
 using DockFn = void (*)(const DockArgs);
 
 template <int AC, int GM>
-DockFn pick_ac(int NW, int PPW, int K) {
+DockFn pick_ac(int NW, int PPW, int K, bool ms) {
+    if (ms) {   // fused multi-site launches: the production lane map only (FIX grids, PPW 4, K 8)
+        if (GM != kGridFix || PPW != 4 || K != 8) return nullptr;
+        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, true>
+               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, true>
+               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, true>
+               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8, true>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8, true> : nullptr);
+    }
     if (PPW == 4 && K == 8 && GM != kGridRT)   // production path: compile-time K = 8
-        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8>
-               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8>
-               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8>
-               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8>
-                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 8> : nullptr));
-    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, GM, 0> : (NW == 16 ? dock_kernel<AC, 16, 1, GM, 0> : nullptr);
+        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, false>
+               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, false>
+               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, false>
+               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8, false>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 8, false> : nullptr));
+    if (PPW == 1) return NW == 32 ? dock_kernel<AC, 32, 1, GM, 0, false> : (NW == 16 ? dock_kernel<AC, 16, 1, GM, 0, false> : nullptr);
     if (PPW == 2)
-        return NW == 32 ? dock_kernel<AC, 32, 2, GM, 0>
-                        : (NW == 16 ? dock_kernel<AC, 16, 2, GM, 0> : (NW == 8 ? dock_kernel<AC, 8, 2, GM, 0> : nullptr));
+        return NW == 32 ? dock_kernel<AC, 32, 2, GM, 0, false>
+                        : (NW == 16 ? dock_kernel<AC, 16, 2, GM, 0, false> : (NW == 8 ? dock_kernel<AC, 8, 2, GM, 0, false> : nullptr));
     if (PPW == 4)
-        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 0>
-               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 0>
-               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 0>
-               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0>
-                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0> : nullptr));
+        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 0, false>
+               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 0, false>
+               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 0, false>
+               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0, false>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0, false> : nullptr));
     return nullptr;
 }
 
 // Per-atom-class entry points, each compiled in its own translation unit
 // (dock_inst.cu with -DVSD_AC=<AC>) so the 8 classes build in parallel.
 #define VSD_DECL_CLASS(ac)                                                                                     \
-    DockFn dock_pick_##ac(int gmode, int NW, int PPW, int K);                                                           \
+    DockFn dock_pick_##ac(int gmode, int NW, int PPW, int K, bool ms);                                                           \
 
 VSD_DECL_CLASS(32)
 VSD_DECL_CLASS(64)

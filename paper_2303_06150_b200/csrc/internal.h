@@ -49,27 +49,37 @@ struct PocketDev {
     float inv_h;
 };
 
-// One bucket launch (a6-a9).
-struct DockArgs {
-    const float* rec;          // packed records of this bucket (slot s at rec + s * rec_floats)
-    const int4* meta;          // [slots] {ligand index, A, R, S_w * frag_off}
-    int n;                     // ligands in the bucket
-    int rec_floats;            // 3 * AC + 32
-    int P, K, S_w;
-    int ligs_per_cta;          // LC
-    int frag_cap;              // RC: no ligand of the launch has more fragments
-    int* counter;              // dynamic round counter of this launch (zeroed before launch)
-    const float* pose_tab;     // [P][12] raw: R (9, row-major) then tau (3)
-    const float* cs;           // [K][2]
-    PocketDev pk;
+// Outputs of one docking site (pocket) of a launch.
+struct SiteOut {
     float* best_score;         // [n_total]
     int* best_pose;            // [n_total]
     uint8_t* angles;           // CSR S_w * frag_off
     float* dbg_score;          // [n_total * P] or null
     uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
+    float* xyz_out;            // a9 best-pose coordinates [3 * n_atoms] (input atom order) or null
+};
+
+// Fused multi-site launches: a thread-block cluster of n_sites CTAs docks
+// the same staged ligands into n_sites pockets, CTA rank s into pocket s.
+constexpr int kMaxSites = 8;
+
+// One dock launch (a6-a9).  Single-site launches use pk[0] / out[0].
+struct DockArgs {
+    const float* rec;          // packed records of this bucket (slot s at rec + s * rec_floats)
+    const int4* meta;          // [slots] {ligand index, A, R, S_w * frag_off}
+    int n;                     // ligands in the bucket
+    int rec_floats;            // rec_floats_of(AC)
+    int P, K, S_w;
+    int ligs_per_cta;          // LC
+    int frag_cap;              // RC: no ligand of the launch has more fragments
+    int n_sites;               // 1, or the cluster size of a fused multi-site launch
+    int* counter;              // dynamic round counter of this launch (zeroed before launch)
+    const float* pose_tab;     // [P][12] raw: R (9, row-major) then tau (3)
+    const float* cs;           // [K][2]
     const uint8_t* order;      // internal atom -> input atom (CSR by atom_off, a1)
     const int64_t* atom_off;   // [n_total + 1]
-    float* xyz_out;            // a9 best-pose coordinates [3 * n_atoms] (input atom order) or null
+    PocketDev pk[kMaxSites];
+    SiteOut out[kMaxSites];
 };
 
 // Packed ligand record of atom class AC (floats): x | y | z (3 AC), fragment table u32[32],
@@ -162,6 +172,7 @@ cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const 
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int gmode, int K, cudaFuncAttributes* attr);
 cudaError_t dock_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int* blocks_per_sm);
+cudaError_t dock_cluster_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int sites, int* clusters);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
                                 cudaStream_t st);
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,

@@ -734,3 +734,32 @@ def test_offsets_relative_to_their_first_entry():
         r = e2.results(0)
         assert np.array_equal(r.best_score, want.best_score) and np.array_equal(r.angles, want.angles), mode
         assert np.array_equal(r.ligand_id, lib.ligand_id[lo:hi]) and np.array_equal(e2.coords(0), want_xyz), mode
+
+
+# ----------------------------------------------------------------------------- fused multi-site
+# docking: one cluster launch per class docks every pocket
+
+@pytest.mark.parametrize("S", [2, 3, 4, 8])
+def test_fused_multisite_bit_identical_to_per_pocket_launches(S):
+    """Thread-block clusters of S CTAs (one per pocket, records multicast once per cluster) give the
+    same bits as one launch per pocket, for every pocket; one pocket's outputs pass the oracle."""
+    lib = vsgen.ligands(1500 if S < 8 else 600, 70 + S, (20, 120), (0, 20))
+    pks = [vsgen.pocket(101 + q, center_offset=(0.5 * q, -0.25 * q, 0.0)) for q in range(S)]
+    outs = {}
+    for fused in (True, False):
+        e = engine(fused_sites=fused)
+        rot, tr, cs, ids = setup(e, pks, 16, 8)
+        e.submit_library(lib, ids)
+        e.wait()
+        st = e.stats()
+        assert (st["fused_launches"] > 0) == fused
+        outs[fused] = [(e.results(q), e.coords(q)) for q in range(S)]
+    for q in range(S):
+        (a, xa), (b, xb) = outs[True][q], outs[False][q]
+        assert np.array_equal(a.best_score, b.best_score) and np.array_equal(a.best_pose, b.best_pose), q
+        assert np.array_equal(a.angles, b.angles) and np.array_equal(xa, xb), q
+    assert not np.array_equal(outs[True][0][0].best_score, outs[True][S - 1][0].best_score)
+    r, x = outs[True][S - 1]
+    rep = parity.check(lib, range(0, lib.n, 50), pks[S - 1], rot, tr, cs, r.best_score, r.best_pose, r.angles, x,
+                       band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + str(rep.failures[:5])
