@@ -65,6 +65,10 @@ typedef struct {
                                   persistent launch with dynamic ligand scheduling */
     int32_t bucket_capacity;   /* > 0: every bucket holds this many ligands instead of m * l_c
                                   (the bucket-size sweep of P:283-333); 0 = Eq. 1 */
+    int32_t n_move_clusters;   /* classes of an optional THIRD bucketing key, the moving-atom count
+                                  sum_r |M_r|; 1 (or 0) = off, <= 8; boundaries
+                                  by the rotamer rule over [0, move_upper_bound] */
+    int32_t move_upper_bound;  /* 0 = observed maximum */
     int32_t fused_sites;       /* 1: a submit with 2..8 pockets of one 32^3-class grid layout docks
                                   them in ONE launch per atom class: thread-block clusters of one
                                   CTA per pocket, each ligand round staged once per cluster
@@ -218,7 +222,7 @@ typedef struct {
     int32_t size;              /* ligands (<= capacity; the last of a cell may be partial) */
     int32_t owner;             /* rank docking it (LPT) */
     int32_t launch_order;      /* position in the owner's launch sequence */
-    int32_t pad;
+    int32_t move_class;        /* class of the optional third key (0 when off) */
     int64_t start;             /* first position in perm */
     uint64_t weight;           /* sum of E_alg over the bucket's ligands */
 } vs_bucket;

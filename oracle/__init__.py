@@ -280,14 +280,20 @@ class StreamingBucketizer:
         return out
 
 
-def bucketize(n_atoms, n_rot, atom_b, rot_b, capacity_per_atom_class) -> List[Bucket]:
+def bucketize(n_atoms, n_rot, atom_b, rot_b, capacity_per_atom_class, n_move=None, move_b=None) -> List[Bucket]:
     """Canonical manifest (Q18): cell-major (atom class, then rotamer class); within a cell,
     input order; each cell cut into consecutive buckets of its atom class's capacity
-    (the last may be partial -- the tail)."""
+    (the last may be partial -- the tail).  With ``move_b`` the cell gets a third
+    key, the moving-atom count class, assigned by the same rule."""
     cells = {}
     for i, (a, r) in enumerate(zip(n_atoms, n_rot)):
         try:
             cell = assign(atom_b, rot_b, int(a), int(r))
+            if move_b is not None:
+                mi = next((j for j, b in enumerate(move_b) if int(n_move[i]) <= b), None)
+                if mi is None:
+                    raise BucketingError(f"moving atoms {n_move[i]} > {move_b[-1]}", axis="moving atoms")
+                cell = cell + (mi,)
         except BucketingError as e:
             e.index = i
             raise

@@ -165,7 +165,7 @@ struct vs_ctx {
     unsigned long long* d_topk_out = nullptr;
     void* d_sel = nullptr;
 
-    std::vector<int> atom_b, rot_b;
+    std::vector<int> atom_b, rot_b, move_b;
     std::vector<ClassInfo> classes;                    // class table that sizes the buckets (Eq. 1)
     std::vector<std::vector<ClassInfo>> layout_classes;  // per distinct grid layout of the submit
     std::vector<int> pk_layout;                        // pocket slot -> index into layout_classes
@@ -308,7 +308,7 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t
     s.featM = r.add(n * 4);
     s.cell = r.add(n * 4);
     s.status = r.add(24);   // [0] features, [1] classify overflow, [2] ingest of the owned ligands
-    s.maxAR = r.add(8);
+    s.maxAR = r.add(16);   // observed max A, R, sum |M_r|
     s.hist = r.add((size_t)kMaxCells * s.n_blocks * 4);
     s.cell_count = r.add(kMaxCells * 4);
     s.perm = r.add(n * 4);
@@ -450,6 +450,8 @@ vs_status vs_create(const vs_config* cfg, vs_ctx** out) {
     if (c->cfg.n_sweeps < 1 || c->cfg.n_sweeps > kMaxSweeps) st = bad("n_sweeps must be in [1, 4]");
     else if (c->cfg.n_atom_clusters < 1 || c->cfg.n_atom_clusters > kMaxAtomClasses) st = bad("n_atom_clusters must be in [1, 8]");
     else if (c->cfg.n_rot_clusters < 1 || c->cfg.n_rot_clusters > kMaxRotClasses) st = bad("n_rot_clusters must be in [1, 33]");
+    else if (c->cfg.n_move_clusters < 0 || c->cfg.n_move_clusters > kMaxMoveClasses) st = bad("n_move_clusters must be in [0, 8]");
+    else if (c->cfg.move_upper_bound < 0) st = bad("move_upper_bound must be >= 0");
     else if (c->cfg.atom_upper_bound < 0 || c->cfg.atom_upper_bound > kMaxAtoms) st = bad("atom_upper_bound must be in [0, 256]");
     else if (c->cfg.rot_upper_bound < 0 || c->cfg.rot_upper_bound > kMaxFrags) st = bad("rot_upper_bound must be in [0, 32]");
     else if (c->cfg.world_size < 1 || c->cfg.rank < 0 || c->cfg.rank >= c->cfg.world_size) st = bad("bad rank / world_size");
@@ -813,7 +815,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
 
     // ---- a1 features (every ligand, from the CSR offsets alone) and the range checks
     CK(cudaMemsetAsync(c->d_status, 0xFF, 24, ms));
-    CK(cudaMemsetAsync(c->d_maxAR, 0, 8, ms));
+    CK(cudaMemsetAsync(c->d_maxAR, 0, 16, ms));
     CK(launch_features(c->d_atom_off, c->d_frag_off, c->d_move_off, n, c->d_featA, c->d_featR, c->d_featM, c->d_status,
                        c->d_maxAR, ms));
     ++launches;
@@ -821,12 +823,12 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     if (st) return st;
     uint8_t* H = (uint8_t*)c->hpin;
     CK(cudaMemcpyAsync(H, c->d_status, 8, cudaMemcpyDeviceToHost, ms));
-    CK(cudaMemcpyAsync(H + 8, c->d_maxAR, 8, cudaMemcpyDeviceToHost, ms));
+    CK(cudaMemcpyAsync(H + 8, c->d_maxAR, 12, cudaMemcpyDeviceToHost, ms));
     CK(cudaStreamSynchronize(ms));
     unsigned long long vstat;
-    int maxAR[2];
+    int maxAR[3];
     std::memcpy(&vstat, H, 8);
-    std::memcpy(maxAR, H + 8, 8);
+    std::memcpy(maxAR, H + 8, 12);
     if (vstat != ~0ull) {
         const long long li = (long long)(vstat >> 8);
         return fail(c, VS_E_PARSE, "ligand %lld: %s", li, vcode_msg((int)(vstat & 255)));
@@ -838,6 +840,15 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->atom_b = atom_bounds(c->cfg.n_atom_clusters, ubA);
     c->rot_b = rot_bounds(c->cfg.n_rot_clusters, ubR);
     if ((int)c->rot_b.size() > kMaxRotClasses) return fail(c, VS_E_ARG, "too many rotamer classes");
+    // optional third key sum_r |M_r|: boundaries by the rotamer rule
+    // over [0, max]; one class = off
+    {
+        const int ubM = c->cfg.move_upper_bound > 0 ? c->cfg.move_upper_bound : maxAR[2];
+        c->move_b = c->cfg.n_move_clusters > 1 ? rot_bounds(c->cfg.n_move_clusters, ubM) : std::vector<int>{ubM};
+        if ((int)c->move_b.size() > kMaxMoveClasses) return fail(c, VS_E_ARG, "too many moving-atom classes");
+        if (c->atom_b.size() * c->rot_b.size() * c->move_b.size() > (size_t)kMaxCells)
+            return fail(c, VS_E_ARG, "more than %d atom x rotamer x moving-atom cells", kMaxCells);
+    }
     // one class table per distinct grid layout among the submitted pockets (each launch uses
     // its pocket's table: policy, occupancy and shared memory differ per layout); the table
     // of the largest layout sizes the buckets (Eq. 1), so capacities fit every pocket
@@ -864,9 +875,10 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         }
         c->classes = c->layout_classes[big];
     }
-    const int nRc = (int)c->rot_b.size();
-    const int n_cells = (int)c->atom_b.size() * nRc;
-    CK(launch_classify_hist(c->d_featA, c->d_featR, n, c->atom_b.data(), (int)c->atom_b.size(), c->rot_b.data(), nRc,
+    const int nRc = (int)c->rot_b.size(), nMc = (int)c->move_b.size();
+    const int n_cells = (int)c->atom_b.size() * nRc * nMc;
+    CK(launch_classify_hist(c->d_featA, c->d_featR, c->d_featM, n, c->atom_b.data(), (int)c->atom_b.size(),
+                            c->rot_b.data(), nRc, c->move_b.data(), nMc,
                             c->d_cell, c->d_hist, s1.n_blocks, c->d_status + 1, ms));
     CK(launch_scan_hist(c->d_hist, n_cells, s1.n_blocks, c->d_cell_count, ms));
     launches += 2;
@@ -880,6 +892,10 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         if ((ovf & 255) == 1)
             return fail(c, VS_E_OVERFLOW_ATOMS, "ligand %lld: atoms above the last atom boundary %d (axis: atoms)", li,
                         c->atom_b.back());
+        if ((ovf & 255) == 3)
+            return fail(c, VS_E_OVERFLOW_ROTAMERS,
+                        "ligand %lld: moving atoms above the last moving-atom boundary %d (axis: moving atoms)", li,
+                        c->move_b.back());
         return fail(c, VS_E_OVERFLOW_ROTAMERS, "ligand %lld: rotamers above the last rotamer boundary %d (axis: rotamers)",
                     li, c->rot_b.back());
     }
@@ -890,13 +906,14 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->buckets.clear();
     int64_t run = 0;
     for (int cell = 0; cell < n_cells; ++cell) {
-        const int ai = cell / nRc, ri = cell % nRc;
+        const int ai = cell / (nRc * nMc), ri = (cell / nMc) % nRc, mi = cell % nMc;
         const ClassInfo& ci = c->classes[ai];
         for (int64_t s = 0; s < cc[cell]; s += ci.cap) {
             vs_bucket b{};
             b.cell = cell;
             b.atom_class = ai;
             b.rot_class = ri;
+            b.move_class = mi;
             b.atom_bound = ci.atom_bound;
             b.kernel_atoms = ci.AC;
             b.capacity = ci.cap;

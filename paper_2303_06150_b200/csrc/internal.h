@@ -11,7 +11,8 @@ constexpr int kMaxAtoms = 256;     // D1 bound per ligand ("up to a few hu
 constexpr int kMaxFrags = 32;      // rotatable bonds per ligand
 constexpr int kMaxAtomClasses = 8; // atom classes (warp multiples up to 256)
 constexpr int kMaxRotClasses = 33; // rotamer classes (0..32)
-constexpr int kMaxCells = kMaxAtomClasses * kMaxRotClasses;
+constexpr int kMaxMoveClasses = 8; // classes of the optional third key, sum_r |M_r|
+constexpr int kMaxCells = 1024;    // atom x rotamer x moving-atom cells of one submit
 constexpr int kPrepTile = 4096;    // ligands per block in classify/scatter
 constexpr int kMaxPoses = 1024;
 constexpr int kMaxSweeps = 4;
@@ -154,8 +155,9 @@ cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64
                           const int64_t* owned_start, const int* owned_prefix, int n_owned, int total_slots,
                           uint8_t* order, int4* frint, uint8_t* fown, int* lflag, unsigned long long* status,
                           cudaStream_t st);
-cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
-                                 const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
+cudaError_t launch_classify_hist(const int* featA, const int* featR, const int* featM, int64_t n, const int* atom_b,
+                                 int n_atom_b, const int* rot_b, int n_rot_b, const int* move_b, int n_move_b, int* cell,
+                                 int* hist, int n_blocks,
                                  unsigned long long* ovf, cudaStream_t st);
 cudaError_t launch_scan_hist(int* hist, int n_cells, int n_blocks, int* cell_count, cudaStream_t st);
 cudaError_t launch_scatter(const int* cell, int64_t n, const int* hist_off, int n_cells, int n_blocks, uint32_t* perm,

@@ -63,10 +63,10 @@ __global__ void __launch_bounds__(256) features_kernel(const int64_t* __restrict
                                                        int* __restrict__ featA, int* __restrict__ featR,
                                                        int* __restrict__ featM, unsigned long long* status,
                                                        int* maxAR) {
-    __shared__ int smax[2];
-    if (threadIdx.x < 2) smax[threadIdx.x] = 0;
+    __shared__ int smax[3];
+    if (threadIdx.x < 3) smax[threadIdx.x] = 0;
     __syncthreads();
-    int locA = 0, locR = 0;
+    int locA = 0, locR = 0, locM = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t A64 = atom_off[i + 1] - atom_off[i];
         const int64_t f0 = frag_off[i], f1 = frag_off[i + 1];
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(256) features_kernel(const int64_t* __restrict
             M = R64 > 0 ? move_off[f1] - move_off[f0] : 0;
             locA = max(locA, (int)A64);
             locR = max(locR, (int)R64);
+            locM = max(locM, (int)(M > 0x7fffffff ? 0x7fffffff : M));
         }
         featA[i] = (int)(A64 > 0x7fffffff ? 0x7fffffff : (A64 < 0 ? 0 : A64));
         featR[i] = (int)(R64 > 0x7fffffff ? 0x7fffffff : (R64 < 0 ? 0 : R64));
@@ -87,10 +88,12 @@ __global__ void __launch_bounds__(256) features_kernel(const int64_t* __restrict
     }
     atomicMax(&smax[0], locA);
     atomicMax(&smax[1], locR);
+    atomicMax(&smax[2], locM);
     __syncthreads();
     if (threadIdx.x == 0) {
         atomicMax(&maxAR[0], smax[0]);
         atomicMax(&maxAR[1], smax[1]);
+        atomicMax(&maxAR[2], smax[2]);
     }
 }
 
@@ -402,32 +405,37 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
 struct Bounds {
     int atom_b[kMaxAtomClasses];
     int rot_b[kMaxRotClasses];
-    int n_atom_b, n_rot_b;
+    int move_b[kMaxMoveClasses];
+    int n_atom_b, n_rot_b, n_move_b;
 };
 
-// a2: cell = atom_class * n_rot + rot_class; each class index is the smallest
-// i with value <= boundary[i].  Block-local histogram -> hist[cell][block].
+// a2: cell = (atom_class * n_rot + rot_class) * n_move + move_class; each class index is the
+// smallest i with value <= boundary[i]; the third key (sum_r |M_r|) is
+// off with one move class.  Block-local histogram -> hist[cell][block].
 __global__ void __launch_bounds__(1024) classify_hist_kernel(const int* __restrict__ featA,
-                                                             const int* __restrict__ featR, int64_t n, Bounds bd,
+                                                             const int* __restrict__ featR,
+                                                             const int* __restrict__ featM, int64_t n, Bounds bd,
                                                              int* __restrict__ cell, int* __restrict__ hist,
                                                              int n_blocks, unsigned long long* ovf) {
     __shared__ int h[kMaxCells];
-    const int n_cells = bd.n_atom_b * bd.n_rot_b;
+    const int n_cells = bd.n_atom_b * bd.n_rot_b * bd.n_move_b;
     for (int c = threadIdx.x; c < n_cells; c += blockDim.x) h[c] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * kPrepTile;
     for (int t = threadIdx.x; t < kPrepTile; t += blockDim.x) {
         const int64_t i = base + t;
         if (i >= n) break;
-        const int A = featA[i], R = featR[i];
-        int ai = 0, ri = 0;
+        const int A = featA[i], R = featR[i], M = featM[i];
+        int ai = 0, ri = 0, mi = 0;
         while (ai < bd.n_atom_b && A > bd.atom_b[ai]) ++ai;
         while (ri < bd.n_rot_b && R > bd.rot_b[ri]) ++ri;
+        while (mi < bd.n_move_b && M > bd.move_b[mi]) ++mi;
         int c = -1;
         if (ai == bd.n_atom_b) atomicMin(ovf, ((unsigned long long)i << 8) | 1ull);
         else if (ri == bd.n_rot_b) atomicMin(ovf, ((unsigned long long)i << 8) | 2ull);
+        else if (mi == bd.n_move_b) atomicMin(ovf, ((unsigned long long)i << 8) | 3ull);
         else {
-            c = ai * bd.n_rot_b + ri;
+            c = (ai * bd.n_rot_b + ri) * bd.n_move_b + mi;
             atomicAdd(&h[c], 1);
         }
         cell[i] = c;
@@ -486,31 +494,32 @@ __global__ void __launch_bounds__(1024) scan_hist_kernel(int* __restrict__ hist,
 __global__ void __launch_bounds__(1024) scatter_kernel(const int* __restrict__ cell, int64_t n,
                                                        const int* __restrict__ hist_off, int n_cells, int n_blocks,
                                                        uint32_t* __restrict__ perm) {
-    __shared__ int wcnt[32][kMaxCells];
-    __shared__ int running[kMaxCells];
+    extern __shared__ int scat_smem[];   // per-warp counts [32][n_cells] + running [n_cells]
+    int* running = scat_smem + 32 * n_cells;
+    auto wcnt = [&](int w, int c) -> int& { return scat_smem[w * n_cells + c]; };
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int c = threadIdx.x; c < n_cells; c += blockDim.x) running[c] = 0;
     const int64_t base = (int64_t)blockIdx.x * kPrepTile;
     for (int chunk = 0; chunk < kPrepTile; chunk += 1024) {
-        for (int e = threadIdx.x; e < 32 * n_cells; e += blockDim.x) wcnt[e / n_cells][e % n_cells] = 0;
+        for (int e = threadIdx.x; e < 32 * n_cells; e += blockDim.x) scat_smem[e] = 0;
         __syncthreads();
         const int64_t i = base + chunk + threadIdx.x;
         const int c = (i < n) ? cell[i] : -1;
         const unsigned peers = __match_any_sync(FULL, c);
         const int rank = __popc(peers & ((1u << lane) - 1u));
-        if (c >= 0 && lane == __ffs(peers) - 1) wcnt[w][c] = __popc(peers);
+        if (c >= 0 && lane == __ffs(peers) - 1) wcnt(w, c) = __popc(peers);
         __syncthreads();
         for (int cc = threadIdx.x; cc < n_cells; cc += blockDim.x) {
             int run = running[cc];
             for (int ww = 0; ww < 32; ++ww) {
-                const int t = wcnt[ww][cc];
-                wcnt[ww][cc] = run;
+                const int t = wcnt(ww, cc);
+                wcnt(ww, cc) = run;
                 run += t;
             }
             running[cc] = run;
         }
         __syncthreads();
-        if (c >= 0) perm[hist_off[(int64_t)c * n_blocks + blockIdx.x] + wcnt[w][c] + rank] = (uint32_t)i;
+        if (c >= 0) perm[hist_off[(int64_t)c * n_blocks + blockIdx.x] + wcnt(w, c) + rank] = (uint32_t)i;
         __syncthreads();
     }
 }
@@ -687,15 +696,17 @@ cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64
     return cudaGetLastError();
 }
 
-cudaError_t launch_classify_hist(const int* featA, const int* featR, int64_t n, const int* atom_b, int n_atom_b,
-                                 const int* rot_b, int n_rot_b, int* cell, int* hist, int n_blocks,
-                                 unsigned long long* ovf, cudaStream_t st) {
+cudaError_t launch_classify_hist(const int* featA, const int* featR, const int* featM, int64_t n, const int* atom_b,
+                                 int n_atom_b, const int* rot_b, int n_rot_b, const int* move_b, int n_move_b, int* cell,
+                                 int* hist, int n_blocks, unsigned long long* ovf, cudaStream_t st) {
     Bounds bd;
     bd.n_atom_b = n_atom_b;
     bd.n_rot_b = n_rot_b;
+    bd.n_move_b = n_move_b;
     for (int i = 0; i < n_atom_b; ++i) bd.atom_b[i] = atom_b[i];
     for (int i = 0; i < n_rot_b; ++i) bd.rot_b[i] = rot_b[i];
-    classify_hist_kernel<<<n_blocks, 1024, 0, st>>>(featA, featR, n, bd, cell, hist, n_blocks, ovf);
+    for (int i = 0; i < n_move_b; ++i) bd.move_b[i] = move_b[i];
+    classify_hist_kernel<<<n_blocks, 1024, 0, st>>>(featA, featR, featM, n, bd, cell, hist, n_blocks, ovf);
     return cudaGetLastError();
 }
 
@@ -706,7 +717,13 @@ cudaError_t launch_scan_hist(int* hist, int n_cells, int n_blocks, int* cell_cou
 
 cudaError_t launch_scatter(const int* cell, int64_t n, const int* hist_off, int n_cells, int n_blocks, uint32_t* perm,
                            cudaStream_t st) {
-    scatter_kernel<<<n_blocks, 1024, 0, st>>>(cell, n, hist_off, n_cells, n_blocks, perm);
+    const size_t smem = (size_t)33 * n_cells * 4;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(scatter_kernel),
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    scatter_kernel<<<n_blocks, 1024, smem, st>>>(cell, n, hist_off, n_cells, n_blocks, perm);
     return cudaGetLastError();
 }
 

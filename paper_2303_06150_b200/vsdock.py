@@ -43,7 +43,8 @@ class vs_config(ctypes.Structure):
                 ("rot_upper_bound", ctypes.c_int32), ("bucket_multiple", ctypes.c_int32),
                 ("n_streams", ctypes.c_int32), ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32),
                 ("debug_poses", ctypes.c_int32), ("launch_per_bucket", ctypes.c_int32),
-                ("bucket_capacity", ctypes.c_int32), ("fused_sites", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+                ("bucket_capacity", ctypes.c_int32), ("n_move_clusters", ctypes.c_int32),
+                ("move_upper_bound", ctypes.c_int32), ("fused_sites", ctypes.c_int32), ("stream", ctypes.c_void_p)]
 
 
 class vs_pocket_desc(ctypes.Structure):
@@ -62,7 +63,7 @@ class vs_bucket(ctypes.Structure):
     _fields_ = [("cell", ctypes.c_int32), ("atom_class", ctypes.c_int32), ("rot_class", ctypes.c_int32),
                 ("atom_bound", ctypes.c_int32), ("kernel_atoms", ctypes.c_int32), ("capacity", ctypes.c_int32),
                 ("size", ctypes.c_int32), ("owner", ctypes.c_int32), ("launch_order", ctypes.c_int32),
-                ("pad", ctypes.c_int32), ("start", ctypes.c_int64), ("weight", ctypes.c_uint64)]
+                ("move_class", ctypes.c_int32), ("start", ctypes.c_int64), ("weight", ctypes.c_uint64)]
 
 
 class vs_class_info(ctypes.Structure):
@@ -175,7 +176,8 @@ class Engine:
     def __init__(self, device: int = 0, n_sweeps: int = 1, atom_clusters: int = 6, rot_clusters: int = 23,
                  atom_upper_bound: int = 0, rot_upper_bound: int = 0, bucket_multiple: int = 16, n_streams: int = 4,
                  rank: int = 0, world_size: int = 1, debug_poses: bool = False, launch_per_bucket: bool = False,
-                 bucket_capacity: int = 0, fused_sites: bool = False, stream=None):
+                 bucket_capacity: int = 0, move_clusters: int = 1, move_upper_bound: int = 0,
+                 fused_sites: bool = False, stream=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("vsdock needs a CUDA device (B200, sm_100a); there is no CPU fallback")
@@ -188,7 +190,8 @@ class Engine:
         self._stream = st
         cfg = vs_config(device, n_sweeps, atom_clusters, rot_clusters, atom_upper_bound, rot_upper_bound,
                         bucket_multiple, n_streams, rank, world_size, int(debug_poses), int(launch_per_bucket),
-                        int(bucket_capacity), int(bool(fused_sites)), ctypes.c_void_p(st.cuda_stream))
+                        int(bucket_capacity), int(move_clusters), int(move_upper_bound), int(bool(fused_sites)),
+                        ctypes.c_void_p(st.cuda_stream))
         h = ctypes.c_void_p()
         self._check(self.lib.vs_create(ctypes.byref(cfg), ctypes.byref(h)), None)
         self.h = h

@@ -763,3 +763,31 @@ def test_fused_multisite_bit_identical_to_per_pocket_launches(S):
     rep = parity.check(lib, range(0, lib.n, 50), pks[S - 1], rot, tr, cs, r.best_score, r.best_pose, r.angles, x,
                        band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
     assert rep.ok, rep.summary() + str(rep.failures[:5])
+
+
+# ----------------------------------------------------------------------------- third bucketing key
+# (SURVEY 8(f) 4(d)): the moving-atom count sum_r |M_r|
+
+@pytest.mark.parametrize("grid", [(6, 23, 4), (4, 5, 8), (1, 1, 3)])
+def test_third_bucketing_key_manifest_bit_exact_and_results_unchanged(c2, grid):
+    """Cells (atom class, rotamer class, moving-atom class): the GPU manifest equals the oracle's
+    stable sort by the three keys chunked at capacity, and docking results are bit-identical to the
+    two-key grid (the kernel's lane map does not depend on the cell)."""
+    c, lib, pk = c2
+    na, nr, nm = grid
+    e, *_ = run(lib, [pk], P=16, K=8, debug=False, atom_clusters=na, rot_clusters=nr, move_clusters=nm,
+                bucket_multiple=1)
+    buckets, perm = e.manifest()
+    cls = e.classes()
+    M = lib.moving_per_ligand
+    ab = oracle.atom_boundaries(na, 32, int(lib.n_atoms.max()))
+    rb = oracle.rotamer_boundaries(nr, int(lib.n_frags.max()))
+    mb = oracle.rotamer_boundaries(nm, int(M.max()))
+    ref = oracle.bucketize(lib.n_atoms, lib.n_frags, ab, rb, [cl["capacity"] for cl in cls], n_move=M, move_b=mb)
+    assert len(ref) == len(buckets) and len({b["move_class"] for b in buckets}) == len(mb)
+    assert np.array_equal(perm, np.concatenate([b.ligands for b in ref]).astype(np.uint32))
+    for b, rbk in zip(buckets, ref):
+        assert (b["atom_class"], b["rot_class"], b["move_class"]) == rbk.cell and b["size"] == len(rbk.ligands)
+    e2, *_ = run(lib, [pk], P=16, K=8, debug=False, atom_clusters=na, rot_clusters=nr)
+    r, r2 = e.results(0), e2.results(0)
+    assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.angles, r2.angles)
