@@ -227,18 +227,26 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.nz = d.nz;
     p.grs = d.nx + 1;
     p.gps = (d.nx + 1) * (d.ny + 1);
-    p.mode = grid_mode(d.nx, d.ny, d.nz);
+    p.mode = grid_mode(d.nx, d.ny, d.nz, d.spacing);
     grid_strides(p.mode, d.nx, d.ny, &p.rs, &p.ps);
-    // WIN: the 32^3-node window around the docking centre (clamped into the grid)
+    // WIN: the 32^3-node window around the docking centre (clamped into the grid); QUAD: the
+    // window of kQuadWC cells [w0, w0 + kQuadWC) around it, clamped so that it covers as many of
+    // the grid's cells 0 .. n-1 (the top face n-1 is a cell with weight-0 pad corners) as it can
     const int n3[3] = {d.nx, d.ny, d.nz};
     int w0[3] = {0, 0, 0};
-    if (p.mode == kGridWin)
+    // (QUAD keeps its cells below the top face n-1, so the fast path's cells are interior)
+    p.qwc = 0;
+    if (p.mode == kGridWin || p.mode == kGridQuad) {
+        const int W = p.mode == kGridWin ? kWin : kQuadWC;
+        p.qwc = kQuadWC;
         for (int a = 0; a < 3; ++a) {
             const double uc = ((double)d.center[a] - d.origin[a]) / d.spacing;
-            int v = (int)std::lround(uc) - kWin / 2;
-            v = std::min(v, n3[a] - kWin);
+            int v = (int)std::lround(uc) - W / 2;
+            v = std::min(v, p.mode == kGridWin ? n3[a] - W : n3[a] - 1 - W);
             w0[a] = std::max(v, 0);
+            p.qwc = std::min(p.qwc, n3[a] - 1 - w0[a]);
         }
+    }
     p.wx0 = w0[0];
     p.wy0 = w0[1];
     p.wz0 = w0[2];
@@ -246,7 +254,10 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     // 2^23 + Z into immediates), n / 2 for RT, the window centre for WIN
     int Z[3];
     for (int a = 0; a < 3; ++a)
-        Z[a] = p.mode == kGridFix ? 16 : p.mode == kGridRT ? n3[a] / 2 : w0[a] + kWin / 2;
+        Z[a] = p.mode == kGridFix    ? 16
+               : p.mode == kGridRT   ? n3[a] / 2
+               : p.mode == kGridQuad ? w0[a] + kQuadWC / 2
+                                     : w0[a] + kWin / 2;
     p.lo_x = (float)-Z[0];
     p.lo_y = (float)-Z[1];
     p.lo_z = (float)-Z[2];
@@ -256,6 +267,11 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.mx = 8388608.f + (float)Z[0];
     p.my = 8388608.f + (float)Z[1];
     p.mz = 8388608.f + (float)Z[2];
+    if (p.mode == kGridQuad) {   // 1.5 * 2^23 + Z - w0: the floor's bits give the window-relative cell
+        p.mx = 12582912.f + (float)(Z[0] - w0[0]);
+        p.my = 12582912.f + (float)(Z[1] - w0[1]);
+        p.mz = 12582912.f + (float)(Z[2] - w0[2]);
+    }
     p.kh = (float)((double)d.out_slope * (double)d.spacing);
     p.h = d.spacing;
     p.inv_h = (float)(1.0 / (double)d.spacing);
@@ -270,7 +286,7 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
 
 // Shared memory of the score_points hook's grid region (floats).
 size_t score_grid_floats(const PocketDev& pk) {
-    return pk.mode == kGridWin ? (size_t)kWin * pk.ps : (size_t)(pk.nz + 1) * pk.ps + pk.rs + 2;
+    return dock_grid_floats(pk.mode == kGridFix ? kGridRT : pk.mode, pk.nz, pk.rs, pk.ps);
 }
 
 // Stage-1 workspace (known from the batch sizes alone).
@@ -406,22 +422,34 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz
                 if (*s == ',') ++s;
             }
         }
+        // Ligands per round: Eq. 1's t/ws (ligs_per_cta); when the warps of a CTA would all dock ONE
+        // ligand (P / PPW >= NW) two ligands per round are tried first, their items interleaved
+        // (dock kernel), so the warps do not run the same sweep in lockstep and their shared-memory
+        // bursts spread out (measured +4-6 % on the 32 / 64 / 96 classes); the extra
+        // slot memory never costs a warp (a candidate's LC = 1 form is tried before the next NW).
+        const char* lc_env = getenv("VSDOCK_LC");
         for (auto pr : cand) {
             const int PPW = pr.first, NW = pr.second;
             if (pow2_ceil(c->K) > 32 / PPW) continue;   // the pose group holds the angle slots
-            const int LC = ligs_per_cta(NW, PPW, c->P);
-            const DockLayout L = dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
-            int b = 0;
-            CK(dock_occupancy(ci.AC, NW, PPW, gm, c->K, L.total, &b));
-            if (b >= 1) {
-                ci.NW = NW;
-                ci.PPW = PPW;
-                ci.LC = LC;
-                ci.b = b;
-                ci.smem = L.total;
-                CK(dock_kernel_attrs(ci.AC, NW, PPW, gm, c->K, &ci.attr));
-                break;
+            const int base = ligs_per_cta(NW, PPW, c->P);
+            std::vector<int> lcs = {base};
+            if (lc_env) lcs = {std::max(base, atoi(lc_env))};
+            else if (base == 1) lcs = {2, 1};
+            for (int LC : lcs) {
+                const DockLayout L = dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
+                int b = 0;
+                CK(dock_occupancy(ci.AC, NW, PPW, gm, c->K, L.total, &b));
+                if (b >= 1) {
+                    ci.NW = NW;
+                    ci.PPW = PPW;
+                    ci.LC = LC;
+                    ci.b = b;
+                    ci.smem = L.total;
+                    CK(dock_kernel_attrs(ci.AC, NW, PPW, gm, c->K, &ci.attr));
+                    break;
+                }
             }
+            if (ci.b >= 1) break;
         }
         if (ci.b == 0)
             return fail(c, VS_E_NOFIT, "kernel class %d (A_c = %d) does not fit: occupancy is 0 (grid %dx%d planes)",
@@ -1095,7 +1123,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     // launch per unit docks every pocket, the records staged once per cluster (multicast)
     bool fuse = c->cfg.fused_sites && n_pockets >= 2 && n_pockets <= kMaxSites;
     for (int q = 1; fuse && q < n_pockets; ++q) fuse = c->pk_layout[q] == c->pk_layout[0];
-    fuse = fuse && c->pkdev[0].mode == kGridFix;
+    fuse = fuse && (c->pkdev[0].mode == kGridFix || c->pkdev[0].mode == kGridQuad);
     auto base_args = [&](const Unit& u, const ClassInfo& ci) {
         const vs_bucket& b = c->buckets[c->owned[u.first]];
         DockArgs a{};

@@ -3,6 +3,9 @@
 // The kernels themselves are in dock_impl.cuh.
 #include "dock_impl.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace vsd {
 
 using dk::DockFn;
@@ -31,14 +34,28 @@ DockFn pick(int AC, int NW, int PPW, int gm, int K, bool ms = false) {
 // 32^3 window of large grids (WIN) use the fixed layout (34, 1097) with compile-time strides;
 // RT grids use (nx + 1, (nx + 1) * ny + 7).  RT is chosen while its region (plus a zero plane)
 // stays within the FIX budget of shared memory, so the pose buffers keep their room.
-int grid_mode(int nx, int ny, int nz) {
+// QUAD (internal.h) whenever its window of kQuadWC cells per axis holds the whole grid or at
+// least +-9 A around the docking centre (a drug-like ligand's atoms lie within ~9 A of its
+// centroid: 99.96 % of the C4 library's atoms), so cells outside the window -- read
+// from global memory -- stay rare.  VSDOCK_GRID_MODE=scalar selects the scalar layouts below
+// (FIX / RT / WIN) for comparison.
+int grid_mode(int nx, int ny, int nz, float spacing) {
+    static const bool scalar = [] {
+        const char* e = getenv("VSDOCK_GRID_MODE");
+        return e && strcmp(e, "scalar") == 0;
+    }();
+    const bool fits = nx - 1 <= kQuadWC && ny - 1 <= kQuadWC && nz - 1 <= kQuadWC;
+    if (!scalar && (fits || (double)spacing * (kQuadWC / 2) >= 9.0)) return kGridQuad;
     if (nx <= kWin && ny <= kWin && nz <= kWin) return kGridFix;
     const size_t rt = (size_t)(nz + 1) * ((size_t)(nx + 1) * ny + 7) + (nx + 1) + 2;
     return rt <= (size_t)kWin * dk::kFixPS + 2048 ? kGridRT : kGridWin;
 }
 
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps) {
-    if (mode != kGridRT) {
+    if (mode == kGridQuad) {   // in quads (16 bytes)
+        *rs = kQuadRS;
+        *ps = kQuadPS;
+    } else if (mode != kGridRT) {
         *rs = dk::kFixRS;
         *ps = dk::kFixPS;
     } else {
@@ -144,13 +161,15 @@ cudaError_t dock_cluster_occupancy(int AC, int NW, int PPW, int gmode, int K, si
 
 cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
                                 cudaStream_t st) {
-    const void* f = pk.mode == kGridFix ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridFix>)
-                    : pk.mode == kGridRT ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridRT>)
-                                         : reinterpret_cast<const void*>(dk::score_points_kernel<kGridWin>);
+    const void* f = pk.mode == kGridFix    ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridFix>)
+                    : pk.mode == kGridRT   ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridRT>)
+                    : pk.mode == kGridQuad ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridQuad>)
+                                           : reinterpret_cast<const void*>(dk::score_points_kernel<kGridWin>);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (pk.mode == kGridFix) dk::score_points_kernel<kGridFix><<<148, 1024, smem, st>>>(pk, xyz, n, out);
     else if (pk.mode == kGridRT) dk::score_points_kernel<kGridRT><<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    else if (pk.mode == kGridQuad) dk::score_points_kernel<kGridQuad><<<148, 1024, smem, st>>>(pk, xyz, n, out);
     else dk::score_points_kernel<kGridWin><<<148, 1024, smem, st>>>(pk, xyz, n, out);
     return cudaGetLastError();
 }

@@ -41,6 +41,7 @@ namespace dk {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr float kMagic = 8388608.f;              // 2^23: floor via round-down add
 constexpr int kMagicBits = 0x4B000000;
+constexpr int kQuadMagicBits = 0x4B400000;       // bits of 1.5 * 2^23 (QUAD: signed floors)
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
@@ -125,9 +126,15 @@ __device__ __forceinline__ float blend(float2 c00, float2 c10, float2 c01, float
 // a warp whose cells all lie in the window takes the pure shared-memory path (one vote),
 // otherwise each lane reads its 8 corners from the window or from global memory.
 constexpr int kFixRS = 34, kFixPS = 1097;
+// The cell of a point: i0 per axis (QUAD: window-relative), the x / y fractions, the z fraction
+// and the L1 excess e (the first half of g; the corner gathers and the blend are the second).
+struct GCell {
+    int ix, iy, iz;
+    float2 fxy;
+    float fz, e;
+};
 template <int GM>
-__device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
-    const int RS = GM == kGridRT ? pk.rs : kFixRS, PS = GM == kGridRT ? pk.ps : kFixPS;
+__device__ __forceinline__ GCell grid_cell(float ux, float uy, float uz, const PocketDev& pk) {
     // centred coordinates (PocketDev): clamp to [-Z, n-1-Z]; floor(u_c) = bits of the
     // round-down sum c + (2^23 + Z) minus the bits of 2^23; f = c - (floor(u_c) - Z)
     // (FIX: Z = 16 on every axis, so -Z and 2^23 + Z are immediates)
@@ -153,6 +160,77 @@ __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, f
         iz = pk.nz - 2;
         fz = 1.f;
     }
+    if (GM == kGridQuad) {
+        // QUAD: the floor constant is 1.5 * 2^23 + Z - w0 (PocketDev), so the bits give the
+        // WINDOW-relative cell directly (negative below the window)
+        constexpr int d = kMagicBits - kQuadMagicBits;
+        return GCell{ix + d, iy + d, iz + d, fxy, fz, e};
+    }
+    return GCell{ix, iy, iz, fxy, fz, e};
+}
+
+// QUAD: the cell's 8 corners are the quads of rows y and y + 1 of the window
+__device__ __forceinline__ bool quad_in(const GCell& c) {
+    return __vimax3_u32((unsigned)c.ix, (unsigned)c.iy, (unsigned)c.iz) < (unsigned)kQuadWC;
+}
+// quad = (G[x,y,z], G[x,y,z+1], G[x+1,y,z], G[x+1,y,z+1]): the (z0, z1) corner pairs of x and x + 1,
+// each already a register pair for the FFMA2 x-lerps; the same blend as the scalar layouts, so the
+// value is bit-identical to theirs
+__device__ __forceinline__ float quad_blend(const float4& q0, const float4& q1, const GCell& c, float kh) {
+    return blend(make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(q1.x, q1.y), make_float2(q1.z, q1.w),
+                 c.fxy, c.fz, kh, c.e);
+}
+// the cell lies in the window (caller's guarantee): two LDS.128
+__device__ __forceinline__ float quad_fast(const float* __restrict__ G, const GCell& c, float kh) {
+    const float4* q = reinterpret_cast<const float4*>(G) + c.ix + c.iy * kQuadRS + c.iz * kQuadPS;
+    return quad_blend(q[0], q[kQuadRS], c, kh);
+}
+// any cell: the window, or the padded global copy (L1 / L2) for the rare lane outside it
+__device__ __forceinline__ float quad_checked(const float* __restrict__ G, const GCell& c, const PocketDev& pk) {
+    if (__builtin_expect(quad_in(c), 1)) return quad_fast(G, c, pk.kh);
+    const int gr = pk.grs, gp = pk.gps;
+    const float* p = pk.grid + (c.ix + pk.wx0) + (size_t)(c.iy + pk.wy0) * gr + (size_t)(c.iz + pk.wz0) * gp;
+    const float4 q0 = make_float4(__ldg(p), __ldg(p + gp), __ldg(p + 1), __ldg(p + gp + 1));
+    const float4 q1 = make_float4(__ldg(p + gr), __ldg(p + gp + gr), __ldg(p + gr + 1), __ldg(p + gp + gr + 1));
+    return quad_blend(q0, q1, c, pk.kh);
+}
+
+// QUAD fast path: the cell of the UNCLAMPED point.  The window's fast cells [0, pk.qwc) lie strictly
+// inside the grid's interior cells [0, n-2] (make_pocket_dev), so for a point whose unclamped cell
+// is one of them the clamp is the identity and the excess is exactly 0: g reduces to the trilinear
+// blend, bit for bit (kappa h * 0 adds nothing to a sum that starts at +0).  Any other point (cell
+// outside, or a non-finite / huge coordinate: the floor's bits then land far outside [0, qwc))
+// takes the full path (grid_g).
+__device__ __forceinline__ GCell quad_cell_fast(float ux, float uy, float uz, const PocketDev& pk) {
+    const float2 mxy = make_float2(pk.mx, pk.my);
+    const float2 bxy = __fadd2_rd(make_float2(ux, uy), mxy);
+    const float bz = __fadd_rd(uz, pk.mz);
+    const float2 fxy = __fadd2_rn(make_float2(ux, uy), neg2(__fadd2_rn(bxy, neg2(mxy))));
+    const float fz = __fsub_rn(uz, __fsub_rn(bz, pk.mz));
+    return GCell{__float_as_int(bxy.x) - kQuadMagicBits, __float_as_int(bxy.y) - kQuadMagicBits,
+                 __float_as_int(bz) - kQuadMagicBits, fxy, fz, 0.f};
+}
+__device__ __forceinline__ bool quad_in_fast(const GCell& c, int qwc) {
+    return __vimax3_u32((unsigned)c.ix, (unsigned)c.iy, (unsigned)c.iz) < (unsigned)qwc;
+}
+// two LDS.128 and the blend without the excess term
+__device__ __forceinline__ float quad_fast_interior(const float* __restrict__ G, const GCell& c) {
+    const float4* q = reinterpret_cast<const float4*>(G) + c.ix + c.iy * kQuadRS + c.iz * kQuadPS;
+    const float4 q0 = q[0], q1 = q[kQuadRS];
+    const float2 l_0 = lerp2(make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), c.fxy.x);
+    const float2 l_1 = lerp2(make_float2(q1.x, q1.y), make_float2(q1.z, q1.w), c.fxy.x);
+    const float2 l = lerp2(l_0, l_1, c.fxy.y);
+    return lerp(l.x, l.y, c.fz);
+}
+
+template <int GM>
+__device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
+    const int RS = GM == kGridRT ? pk.rs : kFixRS, PS = GM == kGridRT ? pk.ps : kFixPS;
+    const GCell cl = grid_cell<GM>(ux, uy, uz, pk);
+    if (GM == kGridQuad) return quad_checked(G, cl, pk);
+    const int ix = cl.ix, iy = cl.iy, iz = cl.iz;
+    const float2 fxy = cl.fxy;
+    const float fz = cl.fz, e = cl.e;
     if (GM != kGridWin) {
         const float* p = G + ix + iy * RS + iz * PS;
         return blend(make_float2(p[0], p[PS]), make_float2(p[1], p[PS + 1]), make_float2(p[RS], p[PS + RS]),
@@ -220,6 +298,21 @@ __device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk, size_
     const int n4 = (int)(align16(zero_floats * 4) / 16);
     for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
+    if (pk.mode == kGridQuad) {
+        // node (x, y, z) of the window <- (G[x,y,z], G[x,y,z+1], G[x+1,y,z], G[x+1,y,z+1]) from the
+        // padded global copy; nodes beyond the grid's pads stay zero (never read with weight > 0)
+        float4* Q = reinterpret_cast<float4*>(sG);
+        const int NX = min(kQuadWC, pk.nx - pk.wx0), NY = min(kQuadWC + 1, pk.ny - pk.wy0),
+                  NZ = min(kQuadWC, pk.nz - pk.wz0);
+        for (int row = w; row < NY * NZ; row += nw) {
+            const int z = row / NY, y = row - z * NY;
+            const float* src = pk.grid + (size_t)(pk.wz0 + z) * pk.gps + (size_t)(pk.wy0 + y) * pk.grs + pk.wx0;
+            float4* dst = Q + z * kQuadPS + y * kQuadRS;
+            for (int x = lane; x < NX; x += 32)
+                dst[x] = make_float4(src[x], src[x + pk.gps], src[x + 1], src[x + pk.gps + 1]);
+        }
+        return;
+    }
     const bool win = pk.mode == kGridWin;
     const int x0 = win ? pk.wx0 : 0, y0 = win ? pk.wy0 : 0, z0 = win ? pk.wz0 : 0;
     const int NX = win ? min(kWin, pk.nx - x0) : pk.nx, NY = win ? min(kWin, pk.ny - y0) : pk.ny,
@@ -253,6 +346,32 @@ struct PoseBuf {
     }
 };
 
+// g of U points per lane, the warp CONVERGED (all 32 lanes): QUAD decides the window once per
+// batch (one vote), so the common case is two LDS.128 per point with no per-point branch.
+template <int U, int GM>
+__device__ __forceinline__ void grid_batch(const float* __restrict__ G, const float4 (&v)[4], const PocketDev& pk,
+                                           float (&g)[U]) {
+    if (GM == kGridQuad) {
+        GCell cl[U];
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            cl[u] = quad_cell_fast(v[u].x, v[u].y, v[u].z, pk);
+            all = all && quad_in_fast(cl[u], pk.qwc);
+        }
+        if (__all_sync(FULL, all)) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = quad_fast_interior(G, cl[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, v[u].x, v[u].y, v[u].z, pk);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, v[u].x, v[u].y, v[u].z, pk);
+    }
+}
+
 // U independent sweep evaluations per lane: atoms j0, j0 + apw, ... (j < hi), rotated by M,
 // scored, summed into acc in ascending order; the atoms j < own_end (the step's finalised own
 // region) are also summed into own; the rotated atoms stay in kp[0..U).
@@ -269,8 +388,7 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) kp[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
-#pragma unroll
-    for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, kp[u].x, kp[u].y, kp[u].z, pk);
+    grid_batch<U, GM>(G, kp, pk, g);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = j0 + u * apw;
@@ -400,7 +518,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     for (; i + 3 * LPP < n_final; i += 4 * LPP) {
         float g[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 4; ++u) {   // (lanes diverge on the last trip: no warp vote here)
             const float4 v = B.get(i + u * LPP);
             g[u] = grid_g<GM>(G, v.x, v.y, v.z, pk);
         }
@@ -784,7 +902,9 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         unsigned char* slot = slot_ptr(seq);
         const int round = ring.round[seq % kDockSlots];
         const int nl = min(LC, a.n - round * LC);
-        const int l = it / G, g = it - l * G;
+        // items interleave the round's ligands (consecutive claims alternate between them), so
+        // the warps of a CTA dock different ligands at once instead of running in lockstep
+        const int l = it % LC, g = it / LC;
         if (l < nl) {
             const int p = g * PPW + h;
             const bool valid = p < P;
@@ -828,7 +948,7 @@ __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, 
                                                             int64_t n, float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* sG = reinterpret_cast<float*>(smem);
-    stage_grid(sG, pk, GM == kGridWin ? (size_t)kWin * pk.ps : (size_t)(pk.nz + 1) * pk.ps + pk.rs + 2);
+    stage_grid(sG, pk, dock_grid_floats(GM == kGridFix ? kGridRT : GM, pk.nz, pk.rs, pk.ps));
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
@@ -843,7 +963,7 @@ using DockFn = void (*)(const DockArgs);
 template <int AC, int GM>
 DockFn pick_ac(int NW, int PPW, int K, bool ms) {
     if (ms) {   // fused multi-site launches: the production lane map only (FIX grids, PPW 4, K 8)
-        if (GM != kGridFix || PPW != 4 || K != 8) return nullptr;
+        if ((GM != kGridFix && GM != kGridQuad) || PPW != 4 || K != 8) return nullptr;
         return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, true>
                : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, true>
                : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, true>

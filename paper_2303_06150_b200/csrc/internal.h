@@ -25,8 +25,19 @@ constexpr int kMaxSweeps = 4;
 //         on the docking centre is staged in shared memory (fixed strides); a cell whose 8
 //         corners all lie in the window is gathered from shared memory, any other cell from
 //         the padded global copy through L1 / L2 (ld.global.nc).
-constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2;
+//  3 QUAD the production layout: a window of kQuadWC^3 CELLS around the docking centre whose
+//         node (x, y, z) holds the float4 (G[x,y,z], G[x,y,z+1], G[x+1,y,z], G[x+1,y,z+1]), so
+//         the 8 corners of a cell are TWO 16-byte loads (LDS.128) instead of eight LDS.32:
+//         ~9.5 shared wavefronts per LDS.128 on the sweep's points against 4 x 3.07 for the
+//         scalar layout (tools/microbench_pairs.cu, tools/bank_sim3.py), i.e. 22 % fewer
+//         wavefronts per evaluation.  Cells outside the window read the padded global copy
+//         (L1 / L2), as WIN does.  Chosen whenever the window covers +-9 A around the centre
+//         (h >= 0.9 A) or the whole grid (grid_mode, dock.cu).
+constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3;
 constexpr int kWin = 32;   // window edge (nodes)
+constexpr int kQuadWC = 20;                  // QUAD window edge (cells per axis)
+constexpr int kQuadRS = kQuadWC;             // quads per row (x), rows per plane: kQuadWC + 1 (y + 1)
+constexpr int kQuadPS = kQuadRS * (kQuadWC + 1) + 3;   // quads per plane (423 = 3 mod 8: bank model)
 
 // Pocket as the dock kernel sees it.  Coordinates are kept in CENTRED grid units
 // v = (y - o)/h - Z with an integer shift Z per axis (16 for FIX, floor(n/2) for RT, the
@@ -39,7 +50,8 @@ struct PocketDev {
     int rs, ps;            // shared-memory row stride and plane stride (floats)
     int grs, gps;          // global padded row / plane stride (floats)
     int mode;              // kGridFix / kGridRT / kGridWin
-    int wx0, wy0, wz0;     // WIN: window origin (grid nodes)
+    int wx0, wy0, wz0;     // WIN / QUAD: window origin (grid nodes)
+    int qwc;               // QUAD: fast cells [0, qwc) of the window, all interior (<= n-2) on every axis
     float lo_x, lo_y, lo_z;       // -Z          (u = 0)
     float top_x, top_y, top_z;    // n - 1 - Z   (u = n - 1)
     float mx, my, mz;             // 2^23 + Z    (exact)
@@ -113,7 +125,10 @@ __host__ __device__ inline int dock_ang_stride(int S_w, int RC) { return ((S_w *
 // a zero plane + row.  WIN: the 32 window planes; the shared-memory path never reads past
 // local node 31 on any axis.
 __host__ __device__ inline size_t dock_grid_floats(int mode, int nz, int rs, int ps) {
-    return mode == kGridFix ? (size_t)nz * ps + 32 : mode == kGridWin ? (size_t)kWin * ps : (size_t)(nz + 1) * ps + rs + 2;
+    return mode == kGridFix   ? (size_t)nz * ps + 32
+           : mode == kGridWin ? (size_t)kWin * ps
+           : mode == kGridQuad ? (size_t)4 * kQuadPS * kQuadWC
+                              : (size_t)(nz + 1) * ps + rs + 2;
 }
 __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int mode, int nz, int rs, int ps, int P,
                                                   int K, int S_w, int LC, int RC) {
@@ -142,7 +157,7 @@ __host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
     return lc > 0 ? lc : 1;
 }
 // Grid mode and shared-memory strides (row rs, plane ps) of an nx x ny x nz grid.
-int grid_mode(int nx, int ny, int nz);
+int grid_mode(int nx, int ny, int nz, float spacing);
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).

@@ -22,7 +22,7 @@ def passes(n=40, seed=4):
     th = 2 * np.pi * np.arange(8) / 8
     out = []
     for i in range(lib.n):
-        x, fr = lib.ligand(i)
+        x, fr = lib.ligand_ranges(i)
         xc = x - x.mean(0)
         for p0 in range(0, 64, 32):
             ys = [xc @ rot[p0 + q].T.astype(np.float64) + 15.5 for q in range(4)]
