@@ -52,9 +52,9 @@ def _load():
         lib = ctypes.CDLL(_SO)
         p, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
         lib.oracle_dock_batch.argtypes = [i64, p, p, p, p, p, p, p, p, p, i32, p, p, i32, p, i32, p, p, p, p, p, p, p, p,
-                                          i32]
+                                          i32, i32, p, p, p, p, i32]
         lib.oracle_dock_batch.restype = i32
-        lib.oracle_replay_pose.argtypes = [p, p, p, i32, p, i32, p, p, p, p, p, i32, p, i32, p, p, p]
+        lib.oracle_replay_pose.argtypes = [p, p, p, i32, p, i32, p, p, p, p, p, i32, p, i32, p, p, p, i32, i32, p, p, p, p]
         lib.oracle_replay_pose.restype = f64
         lib.oracle_grid_score_points.argtypes = [p, p, p, i64, p, p]
         lib.oracle_grid_score_points.restype = i32
@@ -62,6 +62,8 @@ def _load():
         lib.oracle_place.restype = i32
         lib.oracle_rotate.argtypes = [i32, p, i32, i32, p, i32, f64, f64]
         lib.oracle_rotate.restype = i32
+        lib.oracle_rigid_move.argtypes = [p, i32, p, p]
+        lib.oracle_rigid_move.restype = None
         _lib = lib
     return _lib
 
@@ -93,10 +95,25 @@ class DockResult:
     pose_angles: np.ndarray | None  # uint8 [P * S_w * sum R]
     step_margin: np.ndarray | None  # float64 [n, P]
     pose_margin: np.ndarray | None  # float64 [n]
+    refine: np.ndarray | None = None       # uint8 [n, n_ref] refinement moves of the best pose (Q23)
+    pose_refine: np.ndarray | None = None  # uint8 [n, P, n_ref]
 
 
-def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_debug=True, nthreads=None) -> DockResult:
-    """Dock every ligand of ``lib`` (a vsgen.Library-like CSR batch) into ``pocket``; fp64."""
+def _refine_args(refine):
+    """(n_ref, J, rotations [J,9] f32, translations [J,3] f32) of ``refine`` = (n_ref, rot, trans) or None."""
+    if refine is None or int(refine[0]) == 0:
+        return 0, 1, np.eye(3, dtype=np.float32).reshape(1, 9), np.zeros((1, 3), np.float32)
+    n_ref, q, d = refine
+    q = _c(np.asarray(q, np.float32).reshape(-1, 9), np.float32)
+    d = _c(np.asarray(d, np.float32).reshape(-1, 3), np.float32)
+    return int(n_ref), int(q.shape[0]), q, d
+
+
+def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_debug=True, nthreads=None,
+               refine=None) -> DockResult:
+    """Dock every ligand of ``lib`` (a vsgen.Library-like CSR batch) into ``pocket``; fp64.
+    ``refine`` = (n_ref, move rotations [J,3,3], move translations [J,3] in Angstrom): rigid
+    refinement rounds after the sweeps (Q23)."""
     L = _load()
     n = lib.n
     P, K = int(rot.shape[0]), int(cs.shape[0])
@@ -116,12 +133,18 @@ def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_de
     sm = np.zeros((n, P), np.float64) if want_debug else None
     pm = np.zeros(n, np.float64) if want_debug else None
     nthreads = nthreads or (os.cpu_count() or 1)
+    n_ref, J, q, d = _refine_args(refine)
+    rf = np.zeros((max(1, n), max(1, n_ref)), np.uint8)
+    prf = np.zeros((max(1, n), P, max(1, n_ref)), np.uint8) if want_debug else None
     rc = L.oracle_dock_batch(n, _p(ao), _p(xyz), _p(fo), _p(fax), _p(mo), _p(ma), _p(dims), _p(prm), _p(G), P, _p(rot), _p(trans),
-                             K, _p(cs), S_w, _p(bs), _p(bp), _p(ang), _p(xo), _p(ps), _p(pa), _p(sm), _p(pm), nthreads)
+                             K, _p(cs), S_w, _p(bs), _p(bp), _p(ang), _p(xo), _p(ps), _p(pa), _p(sm), _p(pm),
+                             n_ref, J, _p(q), _p(d), _p(rf) if n_ref else None, _p(prf) if (n_ref and prf is not None) else None,
+                             nthreads)
     if rc != 0:
         raise ValueError("oracle_dock_batch: invalid arguments")
     return DockResult(bs, bp, ang[:S_w * nR], None if xo is None else xo[:nA], ps,
-                      None if pa is None else pa[:P * S_w * nR], sm, pm)
+                      None if pa is None else pa[:P * S_w * nR], sm, pm,
+                      rf[:n, :n_ref], None if prf is None else prf[:n, :, :n_ref])
 
 
 def _frags_csr(frags):
@@ -138,11 +161,12 @@ def _frags_csr(frags):
     return ax, mo, (ma if ma.size else np.zeros(1, np.int32)).astype(np.int32)
 
 
-def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1):
-    """Replay a given angle sequence from pose (rot9, tr3).  ``frags``: general form (vsgen.Frags)
-    or range form [R,4].
+def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1, refine=None, mseq=None, want_refine=False):
+    """Replay a given angle sequence from pose (rot9, tr3), then (``refine``, Q23) the given
+    refinement moves ``mseq``.  ``frags``: general form (vsgen.Frags) or range form [R,4].
 
-    Returns (final_score, final_xyz [A,3] fp64, step_scores [S_w*R, K] fp64)."""
+    Returns (final_score, final_xyz [A,3] fp64, step_scores [S_w*R, K] fp64), plus the refinement
+    round scores [n_ref, J] when ``want_refine``."""
     L = _load()
     dims, prm, G = _pocket_args(pocket)
     xyz = _c(xyz, np.float32)
@@ -151,10 +175,24 @@ def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1):
     kseq = _c(kseq, np.uint8)
     steps = np.zeros((max(1, S_w * R), K), np.float64)
     y = np.zeros((max(1, A), 3), np.float64)
+    n_ref, J, q, d = _refine_args(refine)
+    ms = _c(mseq if n_ref else np.zeros(1), np.uint8)
+    rs = np.zeros((max(1, n_ref), J), np.float64)
     s = L.oracle_replay_pose(_p(dims), _p(prm), _p(G), A, _p(xyz), R, _p(ax), _p(mo), _p(ma),
                              _p(_c(rot9, np.float32)), _p(_c(tr3, np.float32)), K, _p(_c(cs, np.float32)), S_w,
-                             _p(kseq), _p(steps), _p(y))
+                             _p(kseq), _p(steps), _p(y), n_ref, J, _p(q), _p(d), _p(ms), _p(rs))
+    if want_refine:
+        return float(s), y[:A], steps[:S_w * R], rs[:n_ref]
     return float(s), y[:A], steps[:S_w * R]
+
+
+def rigid_move(y, q9, d3) -> np.ndarray:
+    """One rigid refinement move about the centroid (Q23), fp64; returns a copy."""
+    L = _load()
+    y = np.array(y, dtype=np.float64, order="C").reshape(-1, 3)
+    L.oracle_rigid_move(_p(y), y.shape[0], _p(_c(np.asarray(q9).reshape(9), np.float32)),
+                        _p(_c(np.asarray(d3).reshape(3), np.float32)))
+    return y
 
 
 def grid_score(pocket, pts) -> np.ndarray:

@@ -27,6 +27,9 @@
  * of the molecule atoms that can rotate"); the oracle rotates exactly the listed atoms
  * and never renumbers them (the CUDA path's DFS renumbering is checked against it).
  *
+ * Rigid refinement after the sweeps (Q23): n_ref rounds over a
+ * caller-given table of J rigid moves about the pose's centroid, same greedy rule.
+ *
  * Pins: tests/test_oracle_pins.py (closed forms, invariants, brute force,
  * library routines scipy.ndimage.map_coordinates / scipy Rotation, renumbering
  * invariance, pose translations tau_p != 0 and a docking centre off the grid centre).
@@ -146,11 +149,58 @@ static void rotate_frag_csr(double* y, const int32_t* frag_axis, const int64_t* 
                            (int)(move_off[f + 1] - move_off[f]), ck, sk);
 }
 
+/*
+ * SURVEY 8(f) 4(b), reading Q23: rigid refinement move m of the move table (rotation Q_m,
+ * row-major, and translation d_m in Angstrom) applied about the CURRENT centroid of the
+ * pose, ybar = (1/A) sum_i y_i (Q8):  y_i <- Q_m (y_i - ybar) + ybar + d_m  for every atom.
+ */
+void oracle_rigid_move(double* y, int A, const float* q9, const float* d3) {
+    double yb[3] = {0, 0, 0};
+    for (int i = 0; i < A; ++i)
+        for (int a = 0; a < 3; ++a) yb[a] += y[3 * i + a];
+    for (int a = 0; a < 3; ++a) yb[a] /= (double)A;
+    for (int i = 0; i < A; ++i) {
+        double v[3];
+        for (int a = 0; a < 3; ++a) v[a] = y[3 * i + a] - yb[a];
+        for (int r = 0; r < 3; ++r) {
+            double s = 0.0;
+            for (int a = 0; a < 3; ++a) s += (double)q9[3 * r + a] * v[a];
+            y[3 * i + r] = s + yb[r] + (double)d3[r];
+        }
+    }
+}
+
+/*
+ * One refinement round (Q23): score every move m of the table (full sum over all atoms, as
+ * for the angle steps), keep the lowest m attaining the minimum (Q11), apply it.  scores[m]
+ * (optional) receives S_m; *margin (optional) the relative gap of the runner-up.
+ */
+static int refine_round(const opocket* pk, double* y, double* ytmp, int A, int J, const float* qrot, const float* dtr,
+                        double* scores, double* margin) {
+    double smin = INFINITY, s2 = INFINITY;
+    int mmin = 0;
+    for (int m = 0; m < J; ++m) {
+        memcpy(ytmp, y, sizeof(double) * 3 * (size_t)A);
+        oracle_rigid_move(ytmp, A, qrot + 9 * m, dtr + 3 * m);
+        double sc = score(pk, ytmp, A);
+        if (scores) scores[m] = sc;
+        if (sc < smin) { s2 = smin; smin = sc; mmin = m; }
+        else if (sc < s2) { s2 = sc; }
+    }
+    if (margin) *margin = J > 1 ? (s2 - smin) / fmax(1.0, fabs(smin)) : INFINITY;
+    oracle_rigid_move(y, A, qrot + 9 * mmin, dtr + 3 * mmin);
+    return mmin;
+}
+
 typedef struct {
     /* problem */
     const opocket* pk;
     int P, K, S_w;
     const float *rot, *tr, *cs;
+    int n_ref, J;                 /* refinement rounds and moves (Q23); n_ref = 0: none */
+    const float *qrot, *dtr;      /* move table: J x 9 rotations, J x 3 translations (Angstrom) */
+    uint8_t* refine;              /* [n * n_ref] chosen moves of the best pose */
+    uint8_t* pose_refine;         /* [n * P * n_ref] chosen moves of every pose */
     /* library (CSR) */
     const int64_t *atom_off, *frag_off, *move_off;
     const float* xyz;
@@ -173,7 +223,8 @@ typedef struct {
  * (full sum), keep the smallest k attaining the minimum (Q11), apply it.  The
  * pose score is S(final y).  Best pose p* = smallest p attaining min S_p (Q11).
  */
-static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, double* ybest, uint8_t* kseq, uint8_t* kbest) {
+static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, double* ybest, uint8_t* kseq, uint8_t* kbest,
+                     uint8_t* mseq, uint8_t* mbest) {
     const opocket* pk = B->pk;
     int A = (int)(B->atom_off[li + 1] - B->atom_off[li]);
     int R = (int)(B->frag_off[li + 1] - B->frag_off[li]);
@@ -205,6 +256,12 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
                 kseq[sw * R + r] = (uint8_t)kmin;
             }
         }
+        for (int t = 0; t < B->n_ref; ++t) {   /* rigid refinement after the sweeps (Q23) */
+            double m;
+            mseq[t] = (uint8_t)refine_round(pk, y, ytmp, A, B->J, B->qrot, B->dtr, NULL, &m);
+            if (m < margin) margin = m;
+        }
+        if (B->pose_refine) memcpy(B->pose_refine + ((size_t)li * B->P + p) * B->n_ref, mseq, (size_t)B->n_ref);
         double sp = score(pk, y, A);
         if (B->pose_score) B->pose_score[li * B->P + p] = sp;
         if (B->step_margin) B->step_margin[li * B->P + p] = margin;
@@ -214,6 +271,7 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
             second = best; best = sp; bestp = p;
             memcpy(ybest, y, sizeof(double) * 3 * (size_t)A);
             memcpy(kbest, kseq, (size_t)B->S_w * R);
+            memcpy(mbest, mseq, (size_t)B->n_ref);
         } else if (sp < second) {
             second = sp;
         }
@@ -222,6 +280,7 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
     B->best_pose[li] = bestp;
     if (B->pose_margin) B->pose_margin[li] = (second - best) / fmax(1.0, fabs(best));
     if (B->angles) memcpy(B->angles + (size_t)B->S_w * B->frag_off[li], kbest, (size_t)B->S_w * R);
+    if (B->refine) memcpy(B->refine + (size_t)li * B->n_ref, mbest, (size_t)B->n_ref);
     if (B->xyz_out) memcpy(B->xyz_out + 3 * B->atom_off[li], ybest, sizeof(double) * 3 * (size_t)A);
 }
 
@@ -239,8 +298,10 @@ static void* batch_worker(void* arg) {
     double* yb = (double*)malloc(sizeof(double) * 3 * (size_t)maxA);
     uint8_t* ks = (uint8_t*)malloc((size_t)B->S_w * maxR + 1);
     uint8_t* kb = (uint8_t*)malloc((size_t)B->S_w * maxR + 1);
-    for (int64_t i = B->lo; i < B->hi; ++i) dock_one(B, i, y, yt, yb, ks, kb);
-    free(y); free(yt); free(yb); free(ks); free(kb);
+    uint8_t* ms = (uint8_t*)malloc((size_t)B->n_ref + 1);
+    uint8_t* mb = (uint8_t*)malloc((size_t)B->n_ref + 1);
+    for (int64_t i = B->lo; i < B->hi; ++i) dock_one(B, i, y, yt, yb, ks, kb, ms, mb);
+    free(y); free(yt); free(yb); free(ks); free(kb); free(ms); free(mb);
     return NULL;
 }
 
@@ -262,8 +323,10 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
                       const int32_t* dims, const double* prm, const float* grid,
                       int P, const float* rot, const float* trans, int K, const float* cs, int S_w,
                       double* best_score, int32_t* best_pose, uint8_t* angles, double* xyz_out,
-                      double* pose_score, uint8_t* pose_angles, double* step_margin, double* pose_margin, int nthreads) {
-    if (n < 0 || P < 1 || K < 1 || S_w < 0) return -1;
+                      double* pose_score, uint8_t* pose_angles, double* step_margin, double* pose_margin,
+                      int n_ref, int J, const float* qrot, const float* dtr, uint8_t* refine, uint8_t* pose_refine,
+                      int nthreads) {
+    if (n < 0 || P < 1 || K < 1 || S_w < 0 || n_ref < 0 || (n_ref > 0 && (J < 1 || !qrot || !dtr))) return -1;
     if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2 || !(prm[3] > 0.0)) return -1;
     opocket pk;
     make_pocket(&pk, dims, prm, grid);
@@ -280,6 +343,7 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
         B->frag_axis = frag_axis; B->move_off = move_off; B->move_atoms = move_atoms;
         B->best_score = best_score; B->best_pose = best_pose; B->angles = angles; B->xyz_out = xyz_out;
         B->pose_score = pose_score; B->pose_angles = pose_angles; B->step_margin = step_margin; B->pose_margin = pose_margin;
+        B->n_ref = n_ref; B->J = J; B->qrot = qrot; B->dtr = dtr; B->refine = refine; B->pose_refine = pose_refine;
         B->lo = n * t / nthreads; B->hi = n * (t + 1) / nthreads;
     }
     for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, batch_worker, &jobs[t]);
@@ -299,7 +363,9 @@ double oracle_replay_pose(const int32_t* dims, const double* prm, const float* g
                           int A, const float* xyz, int R, const int32_t* frag_axis, const int64_t* move_off,
                           const int32_t* move_atoms,
                           const float* rot9, const float* tr3, int K, const float* cs, int S_w,
-                          const uint8_t* kseq, double* step_scores, double* y_out) {
+                          const uint8_t* kseq, double* step_scores, double* y_out,
+                          int n_ref, int J, const float* qrot, const float* dtr, const uint8_t* mseq,
+                          double* ref_scores) {
     opocket pk;
     make_pocket(&pk, dims, prm, grid);
     double* yt = (double*)malloc(sizeof(double) * 3 * (size_t)(A > 0 ? A : 1));
@@ -316,6 +382,15 @@ double oracle_replay_pose(const int32_t* dims, const double* prm, const float* g
             int k = kseq[sw * R + r];
             rotate_frag_csr(y_out, frag_axis, move_off, move_atoms, r, (double)cs[2 * k], (double)cs[2 * k + 1]);
         }
+    }
+    for (int t = 0; t < n_ref; ++t) {   /* the GIVEN refinement moves (Q23), every move scored first */
+        if (ref_scores)
+            for (int m = 0; m < J; ++m) {
+                memcpy(yt, y_out, sizeof(double) * 3 * (size_t)A);
+                oracle_rigid_move(yt, A, qrot + 9 * m, dtr + 3 * m);
+                ref_scores[t * J + m] = score(&pk, yt, A);
+            }
+        oracle_rigid_move(y_out, A, qrot + 9 * mseq[t], dtr + 3 * mseq[t]);
     }
     double s = score(&pk, y_out, A);
     free(yt);

@@ -389,3 +389,93 @@ def test_second_sweep_extends_the_first_and_never_raises_the_score(c1):
     flat = mkpocket(np.full((32, 32, 32), 0.25, np.float32), kappa=0.0)
     r3 = oracle.dock_batch(L, flat, rot, tr, cs, S_w=3)
     assert not r3.angles.any() and not r3.best_pose.any()
+
+
+# ----------------------------------------------------------------------------- rigid refinement (Q23)
+
+def test_rigid_move_matches_scipy_about_the_centroid(c1):
+    """Move m about the current centroid: y' = Q (y - ybar) + ybar + d, checked against scipy's
+    rotation applied to centred coordinates (Q23)."""
+    L, pk, (rot, tr), cs = c1
+    q, d = vsgen.refine_table(0.3, 12.0)
+    x, _ = L.ligand(3)
+    y = oracle.place(pk, x, rot[2], tr[2])
+    yb = y.mean(0)
+    for m in range(q.shape[0]):
+        got = oracle.rigid_move(y, q[m], d[m])
+        R = Rotation.from_matrix(q[m].astype(np.float64))
+        want = R.apply(y - yb) + yb + d[m].astype(np.float64)
+        assert np.max(np.abs(got - want)) < 1e-5   # fp32 table entries vs scipy's orthonormalised matrix
+        # rigid: pairwise distances preserved; centroid moves by exactly d
+        D0 = np.linalg.norm(y[:, None] - y[None], axis=-1)
+        D1 = np.linalg.norm(got[:, None] - got[None], axis=-1)
+        assert np.max(np.abs(D0 - D1)) < 1e-5
+        assert np.max(np.abs(got.mean(0) - (yb + d[m]))) < 1e-9
+    assert np.array_equal(oracle.rigid_move(y, q[0], d[0]), y)   # move 0 is the identity, bit for bit
+
+
+def test_refinement_identity_table_changes_nothing(c1):
+    """A one-move table (the identity) leaves every pose, score and angle exactly as without refinement."""
+    L, pk, (rot, tr), cs = c1
+    base = oracle.dock_batch(L, pk, rot, tr, cs)
+    q, d = vsgen.refine_table()
+    r = oracle.dock_batch(L, pk, rot, tr, cs, refine=(3, q[:1], d[:1]))
+    assert np.array_equal(r.best_score, base.best_score)
+    assert np.array_equal(r.best_pose, base.best_pose)
+    assert np.array_equal(r.angles, base.angles)
+    assert np.array_equal(r.xyz, base.xyz)
+    assert not r.refine.any()
+
+
+def test_refinement_linear_grid_closed_form():
+    """G = w.u + g0 with every atom inside the box: a rotation about the centroid leaves S unchanged
+    (sum of w.Q(y_i - ybar) = 0) and a translation d changes it by A w.d / h, so each greedy round
+    takes the translation with the most negative w.d (ties -> lowest move index, the identity first)
+    and the score falls by exactly A |w.d| / h per round."""
+    n, h = 32, 1.0
+    w = np.array([0.7, -1.3, 0.4])
+    Z, Y, X = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    G = (w[0] * X + w[1] * Y + w[2] * Z + 5.0).astype(np.float32)
+    pk = mkpocket(G, h=h, center=(15.5, 15.5, 15.5))
+    L = vsgen.ligands(6, 11, (20, 40), (0, 3))
+    rot, tr = vsgen.pose_table(3)
+    cs = vsgen.angle_table(4)
+    q, d = vsgen.refine_table(0.5, 15.0)
+    vals = [float(w @ d[m]) for m in range(q.shape[0])]
+    m_best = int(np.argmin(vals))                    # -0.5 along y (w_y = -1.3 < 0): move 3
+    assert m_best == 3
+    base = oracle.dock_batch(L, pk, rot, tr, cs)
+    n_ref = 3
+    r = oracle.dock_batch(L, pk, rot, tr, cs, refine=(n_ref, q, d))
+    A = np.diff(L.atom_off)
+    assert np.array_equal(r.refine, np.full((L.n, n_ref), m_best, np.uint8))
+    want = base.best_score + n_ref * A * vals[m_best] / h
+    # exact up to the fp32 storage of the linear grid's node values (~1e-7 relative)
+    assert np.max(np.abs(r.best_score - want) / np.maximum(1, np.abs(want))) < 1e-6
+    # translations only: the best pose's coordinates are the unrefined ones shifted n_ref times
+    assert np.array_equal(r.best_pose, base.best_pose)
+    assert np.max(np.abs(r.xyz - (base.xyz + n_ref * d[m_best]))) < 1e-5
+
+
+def test_refinement_replay_scores_every_move_and_never_raises_the_score(c1):
+    """Replaying the chosen moves reproduces the docked score; every chosen move is the minimum of
+    its round's move scores (the identity is a candidate, so no round raises the score)."""
+    L, pk, (rot, tr), cs = c1
+    q, d = vsgen.refine_table()
+    n_ref = 2
+    r = oracle.dock_batch(L, pk, rot, tr, cs, refine=(n_ref, q, d))
+    base = oracle.dock_batch(L, pk, rot, tr, cs)
+    for i in range(L.n):
+        x, fr = L.ligand(i)
+        p = int(r.best_pose[i])
+        kseq = r.angles[r_off(L, i): r_off(L, i) + len(fr)]
+        s, y, steps, rs = oracle.replay_pose(pk, x, fr, rot[p], tr[p], cs, kseq, refine=(n_ref, q, d),
+                                             mseq=r.refine[i], want_refine=True)
+        assert abs(s - r.best_score[i]) < 1e-12 * max(1.0, abs(s))
+        prev = rs[0][0]
+        for t in range(n_ref):
+            assert rs[t][r.refine[i][t]] == rs[t].min()
+            assert rs[t][0] == prev if t == 0 else True
+            prev = rs[t].min()
+        assert rs[-1].min() == s or abs(rs[-1].min() - s) < 1e-12 * max(1.0, abs(s))
+        assert r.best_score[i] <= base.pose_score[i, p] + 1e-12 * max(1.0, abs(base.pose_score[i, p]))

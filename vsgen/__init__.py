@@ -346,6 +346,33 @@ def pose_table(P: int, seed: int = 7, tau: float = 0.0):
     return rot.astype(np.float32), trans.astype(np.float32)
 
 
+def refine_table(delta: float = 0.25, degrees: float = 10.0):
+    """Rigid refinement move table (Q23): (rot [J,3,3] float32, trans
+    [J,3] float32, Angstrom).  Move 0 is the identity (exactly); then +-delta translations along
+    x, y, z and +-degrees rotations about x, y, z (about the pose centroid): J = 13."""
+    rots = [np.eye(3)]
+    trs = [np.zeros(3)]
+    for a in range(3):
+        for sg in (1.0, -1.0):
+            t = np.zeros(3)
+            t[a] = sg * delta
+            rots.append(np.eye(3))
+            trs.append(t)
+    th = math.radians(degrees)
+    for a in range(3):
+        for sg in (1.0, -1.0):
+            c, s_ = math.cos(sg * th), math.sin(sg * th)
+            b, d = (a + 1) % 3, (a + 2) % 3
+            m = np.eye(3)
+            m[b, b] = c
+            m[b, d] = -s_
+            m[d, b] = s_
+            m[d, d] = c
+            rots.append(m)
+            trs.append(np.zeros(3))
+    return np.array(rots, np.float32), np.array(trs, np.float32)
+
+
 def angle_table(K: int) -> np.ndarray:
     """[K,2] float32 (cos, sin) of theta_k = 2 pi k / K; entry 0 is exactly (1, 0)."""
     t = np.array([[math.cos(2 * math.pi * k / K), math.sin(2 * math.pi * k / K)] for k in range(K)])
