@@ -119,6 +119,17 @@ vs_status vs_set_pose_table(vs_ctx* ctx, int32_t P, const float* rot, const floa
  * the lane map of the next power of two, the extra lanes idle -- DESIGN.md 6). */
 vs_status vs_set_angle_table(vs_ctx* ctx, int32_t K, const float* cos_sin);
 
+/* Method variant (reading Q23): rigid refinement after the
+ * sweeps.  n_rounds greedy rounds; each scores the n_moves rigid moves of the table about
+ * the pose's current centroid ybar -- y' = Q_m (y - ybar) + ybar + d_m for every atom --
+ * and applies the lowest move index attaining the minimum (Q11).  rot[n_moves*9] (Q_m,
+ * row-major), trans[n_moves*3] (d_m, Angstrom), host memory, fp32, finite; move 0 must be
+ * exactly the identity (Q = I, d = 0), so no round raises the score.  0 <= n_rounds <= 8,
+ * 1 <= n_moves <= 32; n_rounds = 0 turns the variant off (the default).  Applies to the
+ * following submits; the chosen moves come back through vs_get_refine, and vs_get_coords
+ * returns the refined best pose. */
+vs_status vs_set_refine_table(vs_ctx* ctx, int32_t n_rounds, int32_t n_moves, const float* rot, const float* trans);
+
 /* D1: a ligand batch in CSR form.  Ligand i has atoms atom_off[i] ..
  * atom_off[i+1] (1 <= A <= 256) with coordinates xyz[3*atom] in Angstrom (finite,
  * |x| <= 1e6), and fragments f = frag_off[i] .. frag_off[i+1] (0 <= R <= 32).
@@ -184,6 +195,12 @@ vs_status vs_get_results(vs_ctx* ctx, int32_t slot, uint64_t* ligand_id, float* 
  * bit-identically to the docked trajectory); ligands of other ranks: NaN.  on_device as
  * for vs_get_results (2: asynchronous into pinned host memory). */
 vs_status vs_get_coords(vs_ctx* ctx, int32_t slot, float* xyz_out, int32_t on_device);
+/* Q23: the refinement moves of p* for pocket slot s, [n * n_rounds] (ligand i's rounds at
+ * i*n_rounds); ligands of other ranks: 0xFF.  Nothing is written when refinement is off.
+ * on_device as for vs_get_results. */
+vs_status vs_get_refine(vs_ctx* ctx, int32_t slot, uint8_t* moves, int32_t on_device);
+/* Parity hook (requires debug_poses): every pose's refinement moves [n * P * n_rounds]. */
+vs_status vs_get_pose_refine_debug(vs_ctx* ctx, int32_t slot, uint8_t* pose_moves);
 /* Parity hook (requires debug_poses): every pose's final score [n*P] and angle
  * sequence [P*S_w*frag_off ...] (pose p of ligand i at P*S_w*frag_off[i] + p*S_w*R_i). */
 vs_status vs_get_pose_debug(vs_ctx* ctx, int32_t slot, float* pose_score, uint8_t* pose_angles);

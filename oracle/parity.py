@@ -51,13 +51,17 @@ def _rel(a, b):
 
 def check(lib, idx, pocket, rot, trans, cs, gpu_score, gpu_pose, gpu_angles, gpu_xyz=None,
           gpu_pose_score=None, gpu_pose_angles=None, S_w=1, band=1e-5, tol_score=1e-4, tol_xyz=1e-3,
-          nthreads=None) -> ParityReport:
-    """Check ligands ``idx`` of ``lib`` (GPU arrays indexed like the full library)."""
+          nthreads=None, refine=None, gpu_refine=None, gpu_pose_refine=None) -> ParityReport:
+    """Check ligands ``idx`` of ``lib`` (GPU arrays indexed like the full library).  ``refine`` =
+    (n_ref, rot, trans) when the rigid refinement ran (Q23): its moves (``gpu_refine`` [n, n_ref],
+    ``gpu_pose_refine`` [n, P, n_ref]) are replayed and banded like the angle steps."""
     rep = ParityReport()
     idx = [int(i) for i in idx]
     P = rot.shape[0]
+    n_ref = int(refine[0]) if refine is not None else 0
     sub = lib.subset(idx)
-    ref = oracle.dock_batch(sub, pocket, rot, trans, cs, S_w, want_xyz=False, want_debug=True, nthreads=nthreads)
+    ref = oracle.dock_batch(sub, pocket, rot, trans, cs, S_w, want_xyz=False, want_debug=True, nthreads=nthreads,
+                            refine=refine if n_ref else None)
     for j, i in enumerate(idx):
         rep.n_ligands += 1
         x, fr = lib.ligand(i)
@@ -75,7 +79,21 @@ def check(lib, idx, pocket, rot, trans, cs, gpu_score, gpu_pose, gpu_angles, gpu
                 kseq = gpu_pose_angles[P * S_w * f0 + q * S_w * R: P * S_w * f0 + (q + 1) * S_w * R]
             else:
                 kseq = gpu_angles[S_w * f0: S_w * f0 + S_w * R]
-            s, y, steps = oracle.replay_pose(pocket, x, fr, rot[q], trans[q], cs, kseq, S_w)
+            if n_ref:
+                mseq = gpu_pose_refine[i, q] if gpu_pose_refine is not None else gpu_refine[i]
+                s, y, steps, rsc = oracle.replay_pose(pocket, x, fr, rot[q], trans[q], cs, kseq, S_w, refine=refine,
+                                                      mseq=mseq, want_refine=True)
+                for st, m in zip(rsc, mseq):
+                    rep.n_steps += 1
+                    mn = float(st.min())
+                    gap = (float(st[int(m)]) - mn) / max(1.0, abs(mn))
+                    rep.max_step_gap = max(rep.max_step_gap, gap)
+                    if gap > band:
+                        rep.failures.append((i, f"pose {q}: refinement move {int(m)} {gap:.3g} above the fp64 min"))
+                    elif int(m) != int(np.argmin(st)):
+                        rep.near_ties += 1
+            else:
+                s, y, steps = oracle.replay_pose(pocket, x, fr, rot[q], trans[q], cs, kseq, S_w)
             rep_scores[q] = s
             for st, k in zip(steps, kseq):
                 rep.n_steps += 1
@@ -114,6 +132,8 @@ def check(lib, idx, pocket, rot, trans, cs, gpu_score, gpu_pose, gpu_angles, gpu
             ra = ref.angles[S_w * int(sub.frag_off[j]): S_w * int(sub.frag_off[j]) + S_w * R]
             ga = gpu_angles[S_w * f0: S_w * f0 + S_w * R]
             ok = ok and np.array_equal(np.asarray(ra), np.asarray(ga))
+            if n_ref:
+                ok = ok and np.array_equal(np.asarray(ref.refine[j]), np.asarray(gpu_refine[i]))
             e = _rel(float(gpu_score[i]), float(ref.best_score[j]))
             ok = ok and e <= tol_score
             if ok:

@@ -121,6 +121,8 @@ struct vs_ctx {
     std::vector<long long> uploaded_sig;   // (workspace, tables_version, grid size, pocket ids) on the device
     std::vector<float> pose_tab;  // P * 12
     std::vector<float> cs;        // K * 2
+    int n_ref = 0, n_moves = 1;   // rigid refinement rounds / moves (Q23); n_ref = 0: off
+    std::vector<float> ref_tab;   // n_moves * 12: Q (row-major) then d (Angstrom)
     std::vector<PocketHost> pockets;
 
     uint8_t* ws = nullptr;
@@ -153,12 +155,15 @@ struct vs_ctx {
     int4* d_meta = nullptr;
     float* d_pose = nullptr;
     float* d_cs = nullptr;
+    float* d_reftab = nullptr;
     std::vector<float*> d_grid;
     std::vector<float*> d_score;
     std::vector<int*> d_pose_best;
     std::vector<uint8_t*> d_ang;
     std::vector<float*> d_dbg_score;
     std::vector<uint8_t*> d_dbg_ang;
+    std::vector<uint8_t*> d_ref;       // refinement moves of p* per pocket slot [n * n_ref]
+    std::vector<uint8_t*> d_dbg_ref;   // [n * P * n_ref] (debug_poses)
     std::vector<float*> d_coords;      // a9 best-pose coordinates per pocket slot (written by the dock kernel)
     unsigned long long* d_keys = nullptr;
     int64_t keys_cap = 0;
@@ -292,7 +297,7 @@ size_t score_grid_floats(const PocketDev& pk) {
 // Stage-1 workspace (known from the batch sizes alone).
 struct Stage1 {
     size_t atom_off, frag_off, xyz, lid, frag_axis, move_off, move_atoms, order, frint, fown, lflag, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
-        bsize, weights, own_start, own_prefix, own_ac, own_rec_off, pose, cs, grids, end;
+        bsize, weights, own_start, own_prefix, own_ac, own_rec_off, pose, cs, reftab, grids, end;
     int n_blocks;
     int64_t max_buckets;
 };
@@ -307,6 +312,7 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t
     // an unchanged set stays resident across submits and is not re-uploaded
     s.pose = r.add((size_t)P * 12 * 4);
     s.cs = r.add((size_t)K * 2 * 4 + 16);
+    s.reftab = r.add((size_t)kMaxRefineMoves * 12 * 4);
     s.grids = r.add(grid_bytes * n_pockets);
     s.atom_off = r.add((n + 1) * 8);
     s.frag_off = r.add((n + 1) * 8);
@@ -341,12 +347,12 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t
 
 // Stage-2 workspace (records + results), placed after stage 1.
 struct Stage2 {
-    size_t rec, meta, score, pose_best, ang, dbg_score, dbg_ang, coords, keys, topk_out, sel, counters, end;
+    size_t rec, meta, score, pose_best, ang, dbg_score, dbg_ang, ref, dbg_ref, coords, keys, topk_out, sel, counters, end;
     size_t per_slot;  // bytes of results per pocket slot
 };
 
 Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats, int P, int S_w, int n_pockets,
-             bool debug) {
+             bool debug, int n_ref) {
     Stage2 s;
     Region r;
     r.off = base;
@@ -357,6 +363,8 @@ Stage2 plan2(size_t base, int64_t n, int64_t nA, int64_t nR, int64_t rec_floats,
     s.ang = r.add((size_t)S_w * nR * n_pockets + 256 * n_pockets);
     s.dbg_score = r.add(debug ? (size_t)n * P * 4 * n_pockets + 256 * n_pockets : 0);
     s.dbg_ang = r.add(debug ? (size_t)P * S_w * nR * n_pockets + 256 * n_pockets : 0);
+    s.ref = r.add(n_ref ? (size_t)n * n_ref * n_pockets + 256 * n_pockets : 0);
+    s.dbg_ref = r.add(debug && n_ref ? (size_t)n * P * n_ref * n_pockets + 256 * n_pockets : 0);
     s.coords = r.add((nA * 12 + 256) * n_pockets);
     const int64_t kc = std::max<int64_t>(n, 65536);
     s.keys = r.add(kc * 8);
@@ -436,7 +444,8 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz
             if (lc_env) lcs = {std::max(base, atoi(lc_env))};
             else if (base == 1) lcs = {2, 1};
             for (int LC : lcs) {
-                const DockLayout L = dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC);
+                const DockLayout L =
+                    dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC, c->n_ref);
                 int b = 0;
                 CK(dock_occupancy(ci.AC, NW, PPW, gm, c->K, L.total, &b));
                 if (b >= 1) {
@@ -556,6 +565,40 @@ vs_status vs_set_pose_table(vs_ctx* c, int32_t P, const float* rot, const float*
     return VS_OK;
 }
 
+vs_status vs_set_refine_table(vs_ctx* c, int32_t n_rounds, int32_t n_moves, const float* rot, const float* trans) {
+    if (!c) return VS_E_ARG;
+    if (n_rounds < 0 || n_rounds > kMaxRefineRounds)
+        return fail(c, VS_E_ARG, "refinement: n_rounds must be in [0, %d]", kMaxRefineRounds);
+    if (n_rounds == 0) {
+        c->n_ref = 0;
+        c->n_moves = 1;
+        c->ref_tab.clear();
+        ++c->tables_version;
+        return VS_OK;
+    }
+    if (n_moves < 1 || n_moves > kMaxRefineMoves || !rot || !trans)
+        return fail(c, VS_E_ARG, "refinement: n_moves must be in [1, %d]", kMaxRefineMoves);
+    std::vector<float> tab((size_t)n_moves * 12, 0.f);
+    for (int m = 0; m < n_moves; ++m) {
+        for (int t = 0; t < 9; ++t) {
+            if (!std::isfinite(rot[9 * m + t])) return fail(c, VS_E_ARG, "refinement move %d: non-finite rotation", m);
+            tab[12 * m + t] = rot[9 * m + t];
+        }
+        for (int t = 0; t < 3; ++t) {
+            if (!std::isfinite(trans[3 * m + t])) return fail(c, VS_E_ARG, "refinement move %d: non-finite translation", m);
+            tab[12 * m + 9 + t] = trans[3 * m + t];
+        }
+    }
+    static const float ident[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+    if (memcmp(tab.data(), ident, sizeof ident) != 0)
+        return fail(c, VS_E_ARG, "refinement: move 0 must be exactly the identity (Q = I, d = 0)");
+    c->n_ref = n_rounds;
+    c->n_moves = n_moves;
+    c->ref_tab.swap(tab);
+    ++c->tables_version;
+    return VS_OK;
+}
+
 vs_status vs_set_angle_table(vs_ctx* c, int32_t K, const float* cos_sin) {
     if (!c) return VS_E_ARG;
     if (K < 1 || K > 32 || !cos_sin) return fail(c, VS_E_ARG, "angle table: K must be in [1, 32]");
@@ -617,7 +660,7 @@ vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n
     ac_max = std::min(kMaxAtoms, std::max(ac_max, std::min(kMaxAtoms, roundup32(max_atoms))));
     const Stage1 s1 = plan1(n_lig, n_atoms, n_frags, n_moving, c->P, c->K, max_grid_bytes(c), n_pockets);
     const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * rec_floats_of(ac_max), c->P,
-                            c->cfg.n_sweeps, n_pockets, c->cfg.debug_poses != 0);
+                            c->cfg.n_sweeps, n_pockets, c->cfg.debug_poses != 0, c->n_ref);
     *bytes = s2.end + 4096;
     return VS_OK;
 }
@@ -737,6 +780,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->d_own_rec_off = (int64_t*)(W + s1.own_rec_off);
     c->d_pose = (float*)(W + s1.pose);
     c->d_cs = (float*)(W + s1.cs);
+    c->d_reftab = (float*)(W + s1.reftab);
     c->d_grid.assign(n_pockets, nullptr);
     for (int i = 0; i < n_pockets; ++i) c->d_grid[i] = (float*)(W + s1.grids + (size_t)i * gmax);
     c->d_order = W + s1.order;
@@ -800,6 +844,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         if (sig != c->uploaded_sig) {
             CK(cudaMemcpyAsync(c->d_pose, c->pose_tab.data(), c->pose_tab.size() * 4, cudaMemcpyHostToDevice, ms));
             CK(cudaMemcpyAsync(c->d_cs, c->cs.data(), c->cs.size() * 4, cudaMemcpyHostToDevice, ms));
+            if (c->n_ref)
+                CK(cudaMemcpyAsync(c->d_reftab, c->ref_tab.data(), c->ref_tab.size() * 4, cudaMemcpyHostToDevice, ms));
             for (int i = 0; i < n_pockets; ++i) {
                 auto& ph = c->pockets[pocket_ids[i]];
                 CK(cudaMemcpyAsync(c->d_grid[i], ph.grid.data(), ph.grid.size() * 4, cudaMemcpyHostToDevice, ms));
@@ -1025,7 +1071,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         evals += (double)b.weight;
     }
     c->total_slots = c->owned_prefix[no];
-    const Stage2 s2 = plan2(s1.end, n, nA, nR, rec_floats, c->P, S_w, n_pockets, c->cfg.debug_poses != 0);
+    const Stage2 s2 = plan2(s1.end, n, nA, nR, rec_floats, c->P, S_w, n_pockets, c->cfg.debug_poses != 0, c->n_ref);
     if (s2.end > c->ws_bytes) return fail(c, VS_E_WORKSPACE, "workspace too small (needs %zu bytes)", s2.end);
     c->d_rec = (float*)(W + s2.rec);
     c->d_meta = (int4*)(W + s2.meta);
@@ -1034,6 +1080,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->d_ang.assign(n_pockets, nullptr);
     c->d_dbg_score.assign(n_pockets, nullptr);
     c->d_dbg_ang.assign(n_pockets, nullptr);
+    c->d_ref.assign(n_pockets, nullptr);
+    c->d_dbg_ref.assign(n_pockets, nullptr);
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     for (int i = 0; i < n_pockets; ++i) {
         c->d_score[i] = (float*)(W + s2.score + i * al(n * 4));
@@ -1042,7 +1090,9 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         if (c->cfg.debug_poses) {
             c->d_dbg_score[i] = (float*)(W + s2.dbg_score + i * al((size_t)n * c->P * 4));
             c->d_dbg_ang[i] = W + s2.dbg_ang + i * al((size_t)c->P * S_w * nR);
+            if (c->n_ref) c->d_dbg_ref[i] = W + s2.dbg_ref + i * al((size_t)n * c->P * c->n_ref);
         }
+        if (c->n_ref) c->d_ref[i] = W + s2.ref + i * al((size_t)n * c->n_ref);
     }
     c->d_coords.assign(n_pockets, nullptr);
     for (int i = 0; i < n_pockets; ++i) c->d_coords[i] = (float*)(W + s2.coords + i * al((size_t)nA * 12));
@@ -1095,6 +1145,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         ++launches;
         if (c->total_slots < n && nA)   // NaN coordinates for the ligands of other ranks
             CK(cudaMemsetAsync(c->d_coords[i], 0xFF, (size_t)nA * 12, ms));
+        if (c->n_ref && c->total_slots < n)   // refinement moves of other ranks' ligands: 0xFF
+            CK(cudaMemsetAsync(c->d_ref[i], 0xFF, (size_t)n * c->n_ref, ms));
     }
     CK(cudaEventRecord(c->ev_prep1, ms));
 
@@ -1139,6 +1191,9 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         a.n_sites = 1;
         a.pose_tab = c->d_pose;
         a.cs = c->d_cs;
+        a.n_ref = c->n_ref;
+        a.n_moves = c->n_moves;
+        a.ref_tab = c->d_reftab;
         a.order = c->d_order;
         a.atom_off = c->d_atom_off;
         return a;
@@ -1146,7 +1201,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     auto site = [&](DockArgs& a, int s, int q) {
         a.pk[s] = c->pkdev[q];
         a.out[s] = SiteOut{c->d_score[q], c->d_pose_best[q], c->d_ang[q], c->d_dbg_score[q], c->d_dbg_ang[q],
-                           c->d_coords[q]};
+                           c->d_coords[q], c->d_ref[q], c->d_dbg_ref[q]};
     };
     c->stats.fused_launches = 0;
     for (const Unit& u : units) {
@@ -1155,7 +1210,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             const ClassInfo& ci = c->layout_classes[c->pk_layout[0]][u.cls];
             const PocketDev& p0 = c->pkdev[0];
             const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, p0.mode, p0.nz, p0.rs, p0.ps, c->P, c->K, S_w,
-                                             ci.LC, c->frag_cap);
+                                             ci.LC, c->frag_cap, c->n_ref);
             // cluster size g: the one that keeps the most SMs busy (clusters are placed whole
             // inside a GPC, so large clusters of 227 KB CTAs leave SMs idle); ties -> larger g
             int best_g = 1, best_sms = ci.b * c->sm_count, best_cl = 0;
@@ -1196,7 +1251,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             site(a, 0, q);
             a.counter = d_counters + dock_launches;
             const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk[0].mode, a.pk[0].nz, a.pk[0].rs,
-                                             a.pk[0].ps, c->P, c->K, S_w, ci.LC, c->frag_cap);
+                                             a.pk[0].ps, c->P, c->K, S_w, ci.LC, c->frag_cap, c->n_ref);
             const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];
@@ -1265,6 +1320,29 @@ vs_status vs_get_pose_debug(vs_ctx* c, int32_t slot, float* pose_score, uint8_t*
     if (pose_score) CK(cudaMemcpyAsync(pose_score, c->d_dbg_score[slot], (size_t)c->n * c->P * 4, cudaMemcpyDeviceToHost, c->main));
     if (pose_angles && c->nR)
         CK(cudaMemcpyAsync(pose_angles, c->d_dbg_ang[slot], (size_t)c->P * c->cfg.n_sweeps * c->nR, cudaMemcpyDeviceToHost, c->main));
+    CK(cudaStreamSynchronize(c->main));
+    return VS_OK;
+}
+
+vs_status vs_get_refine(vs_ctx* c, int32_t slot, uint8_t* moves, int32_t on_device) {
+    if (!c || !moves) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (on_device < 0 || on_device > 2) return fail(c, VS_E_ARG, "on_device must be 0, 1 or 2");
+    if (c->n == 0 || c->n_ref == 0) return VS_OK;
+    const cudaMemcpyKind kind = on_device == 1 ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(copy_pieces(moves, c->d_ref[slot], (size_t)c->n * c->n_ref, kind, c->main));
+    if (on_device != 2) CK(cudaStreamSynchronize(c->main));
+    return VS_OK;
+}
+
+vs_status vs_get_pose_refine_debug(vs_ctx* c, int32_t slot, uint8_t* pose_moves) {
+    if (!c || !pose_moves) return VS_E_ARG;
+    if (!c->submitted) return fail(c, VS_E_STATE, "nothing submitted");
+    if (!c->cfg.debug_poses) return fail(c, VS_E_STATE, "debug_poses is off");
+    if (slot < 0 || slot >= (int)c->job_pockets.size()) return fail(c, VS_E_ARG, "bad pocket slot");
+    if (c->n == 0 || c->n_ref == 0) return VS_OK;
+    CK(cudaMemcpyAsync(pose_moves, c->d_dbg_ref[slot], (size_t)c->n * c->P * c->n_ref, cudaMemcpyDeviceToHost, c->main));
     CK(cudaStreamSynchronize(c->main));
     return VS_OK;
 }

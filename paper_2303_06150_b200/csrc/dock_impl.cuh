@@ -397,6 +397,48 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
     }
 }
 
+// Centroid of a pose (grid units) for the rigid refinement (Q23), in ONE fixed order shared by
+// the dock sweep and the best-pose replay: lane li of a group of LPP lanes sums atoms li,
+// li + LPP, ... ascending, then an xor butterfly over the group (every lane ends with the
+// same sum), divided by A.  The whole warp must be converged.
+template <int AC, int LPP>
+__device__ __forceinline__ void pose_centroid(const PoseBuf<AC>& B, int A, int li, float& cx, float& cy, float& cz) {
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    for (int i = li; i < A; i += LPP) {
+        const float4 v = B.get(i);
+        sx = __fadd_rn(sx, v.x);
+        sy = __fadd_rn(sy, v.y);
+        sz = __fadd_rn(sz, v.z);
+    }
+#pragma unroll
+    for (int o = 1; o < LPP; o <<= 1) {
+        sx = __fadd_rn(sx, __shfl_xor_sync(FULL, sx, o));
+        sy = __fadd_rn(sy, __shfl_xor_sync(FULL, sy, o));
+        sz = __fadd_rn(sz, __shfl_xor_sync(FULL, sz, o));
+    }
+    const float a = (float)A;
+    cx = __fdiv_rn(sx, a);
+    cy = __fdiv_rn(sy, a);
+    cz = __fdiv_rn(sz, a);
+}
+
+// Rigid refinement move (Q23) in "M v + t" form about the centroid c (grid units):
+// v' = Q (v - c) + c + d / h, i.e. M = Q, t = (c + d / h) - Q c.  tab = the move's 12 floats.
+__device__ __forceinline__ RotT rigid_t(const float* __restrict__ tab, float cx, float cy, float cz, float inv_h) {
+    RotT M;
+    M.c0 = make_float2(tab[0], tab[3]);
+    M.c1 = make_float2(tab[1], tab[4]);
+    M.c2 = make_float2(tab[2], tab[5]);
+    M.m20 = tab[6];
+    M.m21 = tab[7];
+    M.m22 = tab[8];
+    const float2 base = make_float2(__fmaf_rn(tab[9], inv_h, cx), __fmaf_rn(tab[10], inv_h, cy));
+    const float bz = __fmaf_rn(tab[11], inv_h, cz);
+    M.txy = __ffma2_rn(neg2(M.c0), f2(cx), __ffma2_rn(neg2(M.c1), f2(cy), __ffma2_rn(neg2(M.c2), f2(cz), base)));
+    M.tz = __fmaf_rn(-M.m20, cx, __fmaf_rn(-M.m21, cy, __fmaf_rn(-M.m22, cz, bz)));
+    return M;
+}
+
 // PPW poses of one ligand on one warp: lanes [h*LPP, (h+1)*LPP) serve pose h.
 // a6 placement, a7 sweep, a9 pose score.
 // KT = the angle count when known at compile time (8: the production path, every lane-map
@@ -407,6 +449,7 @@ template <int AC, int PPW, int GM, int KT>
 __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A, int R, const float* __restrict__ T,
                                            bool valid, PoseBuf<AC> B, const float* __restrict__ G,
                                            const PocketDev& pk, int K_rt, int kbits_rt, int S_w, float ck, float sk,
+                                           int n_ref, int n_moves, const float* __restrict__ ref_tab,
                                            uint8_t* __restrict__ angOut,
                                            float* __restrict__ scoreOut, int lane) {
     constexpr int LPP = 32 / PPW;
@@ -424,7 +467,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     // whose innermost moving set is r (the first rown[r] atoms of r's range) never move after
     // step r of the last sweep, so the winner's partial sum over them is their final score;
     // the pose score then needs a final pass over the n_root atoms in no set only
-    const bool fin = K > 1 && ((hdr >> 16) & 1u);
+    const bool fin = K > 1 && n_ref == 0 && ((hdr >> 16) & 1u);   // refinement moves every atom again
     const int n_final = fin ? (int)(hdr & 0xffffu) : A;
     float fsum = 0.f;   // finalised own-region scores, in fragment order
     {
@@ -509,6 +552,63 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
         }
     } else if (valid) {
         for (int t = li; t < S_w * R; t += LPP) angOut[t] = 0;
+    }
+    if (n_ref > 0) {
+        // rigid refinement: every round scores the n_moves moves of the
+        // table about the pose's centroid, in groups of Kp on the sweep's lane map (lane slot k
+        // of group g0 = move g0 + k; every atom is a moving atom), and applies the lowest move
+        // index attaining the minimum (Q11: a group replaces the running best only when strictly
+        // lower; slots past the table hold the identity and never win)
+        const int k = li & (Kp - 1);
+        const int jl = li >> kbits;
+        const int abits = __ffs(LPP) - 1 - kbits;
+        const int apw = 1 << abits;
+        const unsigned gmask = ((Kp == 32) ? 0xffffffffu : ((1u << Kp) - 1u)) << (lane & ~(Kp - 1));
+        const int nst = (A + apw - 1) >> abits;
+        for (int t = 0; t < n_ref; ++t) {
+            float cx, cy, cz;
+            pose_centroid<AC, LPP>(B, A, li, cx, cy, cz);
+            unsigned bkey = 0xffffffffu;
+            int bm = 0;
+            for (int g0 = 0; g0 < n_moves; g0 += Kp) {
+                const int m = g0 + k;
+                const bool mreal = m < n_moves;
+                const RotT M = rigid_t(ref_tab + 12 * (mreal ? m : 0), cx, cy, cz, pk.inv_h);
+                float acc = 0.f, own = 0.f;
+                float4 kp[4];
+                int st = 0;
+                for (; st + 4 <= nst; st += 4) eval_batch<4, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp);
+                switch (nst - st) {
+                    case 3: eval_batch<3, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp); break;
+                    case 2: eval_batch<2, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp); break;
+                    case 1: eval_batch<1, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp); break;
+                    default: break;
+                }
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+                    if (o >= Kp) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+                const unsigned key = mreal ? ord32(acc) : 0xffffffffu;
+                unsigned mn = key;
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1)
+                    if (o < Kp) mn = min(mn, __shfl_xor_sync(FULL, mn, o));
+                const unsigned bal = __ballot_sync(FULL, key == mn && mreal) & gmask;
+                const int bk = (__ffs(bal) - 1) & (Kp - 1);
+                if (mn < bkey) {
+                    bkey = mn;
+                    bm = g0 + bk;
+                }
+            }
+            if (valid && bm != 0) {
+                const RotT Ms = rigid_t(ref_tab + 12 * bm, cx, cy, cz, pk.inv_h);
+                for (int j = li; j < A; j += LPP) {
+                    const float4 v = B.get(j);
+                    B.set(j, apply_rot(Ms, v.x, v.y, v.z));
+                }
+            }
+            __syncwarp();
+            if (valid && li == 0) angOut[S_w * R + t] = (uint8_t)bm;
+        }
     }
     // a9: pose score, canonical order (atom i -> lane i mod LPP, ascending, xor tree, then the
     // finalised own regions in fragment order) (Q22); four independent evaluations in flight,
@@ -723,7 +823,7 @@ __device__ __forceinline__ void load_round(const DockArgs& a, DockRing& ring, un
 // identical to the dock trajectory (same placement, axis, Rodrigues and rotation helpers, same
 // table entries) on one warp's pose buffer (all 32 lanes), written in Angstrom in the caller's
 // input atom order (a1's order map).
-template <int AC>
+template <int AC, int LPP>
 __device__ __forceinline__ void replay_coords(const DockArgs& a, const PocketDev& pk, float* __restrict__ xyz_out,
                                               const float* __restrict__ rec, int li, int A, int R, int p,
                                               const uint8_t* __restrict__ ang, PoseBuf<AC> buf, int lane) {
@@ -751,6 +851,19 @@ __device__ __forceinline__ void replay_coords(const DockArgs& a, const PocketDev
             __syncwarp();
         }
     }
+    for (int t = 0; t < a.n_ref; ++t) {   // the recorded refinement moves (Q23), same centroid order
+        float cx, cy, cz;
+        pose_centroid<AC, LPP>(buf, A, lane & (LPP - 1), cx, cy, cz);
+        const int bm = ang[a.S_w * R + t];
+        if (bm != 0) {
+            const RotT Ms = rigid_t(a.ref_tab + 12 * bm, cx, cy, cz, pk.inv_h);
+            for (int j = lane; j < A; j += 32) {
+                const float4 v = buf.get(j);
+                buf.set(j, apply_rot(Ms, v.x, v.y, v.z));
+            }
+        }
+        __syncwarp();
+    }
     const int64_t a0 = a.atom_off[li];
     float* out = xyz_out + 3 * a0;
     const uint8_t* ord = a.order + a0;
@@ -766,7 +879,7 @@ __device__ __forceinline__ void replay_coords(const DockArgs& a, const PocketDev
 
 // a9 best pose of one round (run by the warp that completes the round's last item), and its
 // coordinates (replayed on the warp's first pose buffer, free once its item completed).
-template <int AC>
+template <int AC, int LPP>
 __device__ __forceinline__ void finish_round(const DockArgs& a, const PocketDev& pk, const SiteOut& so,
                                              const unsigned char* slot, const DockLayout& L, int round, PoseBuf<AC> buf,
                                              int lane) {
@@ -776,7 +889,7 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const PocketDev&
     const float* sScore = reinterpret_cast<const float*>(slot + L.score_o);
     const uint8_t* sAng = slot + L.ang_o;
     const float* sRec = reinterpret_cast<const float*>(slot + L.rec_o);
-    const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
+    const int ang_stride = dock_ang_stride(S_w, a.frag_cap, a.n_ref);
     for (int l = 0; l < nl; ++l) {   // lowest score, ties -> lowest pose index (Q11)
         const int4 m = sMeta[l];
         unsigned long long best = ~0ull;
@@ -804,7 +917,15 @@ __device__ __forceinline__ void finish_round(const DockArgs& a, const PocketDev&
                 const int p = t / nang, q = t - p * nang;
                 so.dbg_angles[(size_t)P * m.w + t] = sAng[(size_t)(l * P + p) * ang_stride + q];
             }
-        if (so.xyz_out) replay_coords<AC>(a, pk, so.xyz_out, sRec + (size_t)l * a.rec_floats, li, m.y, R, bp, sa, buf, lane);
+        if (so.refine)
+            for (int t = lane; t < a.n_ref; t += 32) so.refine[(size_t)li * a.n_ref + t] = sa[nang + t];
+        if (so.dbg_refine)
+            for (int t = lane; t < P * a.n_ref; t += 32) {
+                const int p = t / a.n_ref, q = t - p * a.n_ref;
+                so.dbg_refine[(size_t)li * P * a.n_ref + t] = sAng[(size_t)(l * P + p) * ang_stride + nang + q];
+            }
+        if (so.xyz_out)
+            replay_coords<AC, LPP>(a, pk, so.xyz_out, sRec + (size_t)l * a.rec_floats, li, m.y, R, bp, sa, buf, lane);
     }
 }
 
@@ -829,7 +950,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const PocketDev& pk = a.pk[site];
     const SiteOut& so = a.out[site];
     const int LC = a.ligs_per_cta;
-    const DockLayout L = dock_layout(AC, NW, PPW, GM, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap);
+    const DockLayout L = dock_layout(AC, NW, PPW, GM, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap, a.n_ref);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
@@ -863,7 +984,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const int kl = lane & ((1 << kbits) - 1);          // this lane's angle slot
     const float ck = kl < K ? a.cs[2 * kl] : 1.f, sk = kl < K ? a.cs[2 * kl + 1] : 0.f;   // slots >= K: identity
     const PoseBuf<AC> buf{sBuf + (warp * PPW + h) * pose_stride_of(AC, NW, PPW)};
-    const int ang_stride = dock_ang_stride(S_w, a.frag_cap);
+    const int ang_stride = dock_ang_stride(S_w, a.frag_cap, a.n_ref);
     const int G = (P + PPW - 1) / PPW;   // warp items per ligand
     const int IG = LC * G;               // warp items per round
     const int loader_item = IG / 2;
@@ -915,7 +1036,8 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
             uint8_t* sAng = slot + L.ang_o;
             float T[12];   // pose p in grid units, from the raw table (48 B, L1-resident)
             scaled_pose(a.pose_tab + 12 * pc, pk, T);
-            dock_poses<AC, PPW, GM, KT>(rec, m.y, m.z, T, valid, buf, sG, pk, K, kbits, S_w, ck, sk,
+            dock_poses<AC, PPW, GM, KT>(rec, m.y, m.z, T, valid, buf, sG, pk, K, kbits, S_w, ck, sk, a.n_ref, a.n_moves,
+                                        a.ref_tab,
                                         sAng + (size_t)(l * P + pc) * ang_stride, sScore + l * P + pc, lane);
         }
         __syncwarp();
@@ -928,7 +1050,7 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
         last = __shfl_sync(FULL, last, 0);
         __syncwarp();   // lane 0's fence after the counter orders the round reads of the whole warp
         if (last) {
-            finish_round<AC>(a, pk, so, slot, L, round, PoseBuf<AC>{sBuf + (warp * PPW) * pose_stride_of(AC, NW, PPW)},
+            finish_round<AC, LPP>(a, pk, so, slot, L, round, PoseBuf<AC>{sBuf + (warp * PPW) * pose_stride_of(AC, NW, PPW)},
                              lane);
             __syncwarp();
             if (lane == 0) {

@@ -70,6 +70,8 @@ struct SiteOut {
     float* dbg_score;          // [n_total * P] or null
     uint8_t* dbg_angles;       // [P * S_w * frag_off] or null
     float* xyz_out;            // a9 best-pose coordinates [3 * n_atoms] (input atom order) or null
+    uint8_t* refine;           // rigid refinement moves of p* [n_total * n_ref] (Q23) or null
+    uint8_t* dbg_refine;       // [n_total * P * n_ref] or null
 };
 
 // Fused multi-site launches: a thread-block cluster of n_sites CTAs docks
@@ -89,6 +91,8 @@ struct DockArgs {
     int* counter;              // dynamic round counter of this launch (zeroed before launch)
     const float* pose_tab;     // [P][12] raw: R (9, row-major) then tau (3)
     const float* cs;           // [K][2]
+    int n_ref, n_moves;        // rigid refinement rounds after the sweeps and moves per round (Q23)
+    const float* ref_tab;      // [n_moves][12]: Q (9, row-major) then d (3, Angstrom)
     const uint8_t* order;      // internal atom -> input atom (CSR by atom_off, a1)
     const int64_t* atom_off;   // [n_total + 1]
     PocketDev pk[kMaxSites];
@@ -116,8 +120,13 @@ struct DockLayout {
     size_t rec_o, meta_o, score_o, ang_o, slot_b;   // offsets inside one slot, slot size
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
-// Angle choices kept per pose: S_w * RC bytes (RC = the launch's fragment cap), 4-aligned.
-__host__ __device__ inline int dock_ang_stride(int S_w, int RC) { return ((S_w * (RC > 0 ? RC : 1)) + 3) & ~3; }
+// Choices kept per pose: S_w * RC angle indices (RC = the launch's fragment cap), then n_ref
+// refinement moves (Q23), 4-aligned.
+__host__ __device__ inline int dock_ang_stride(int S_w, int RC, int n_ref) {
+    return ((S_w * (RC > 0 ? RC : 1)) + n_ref + 3) & ~3;
+}
+constexpr int kMaxRefineMoves = 32;   // moves per refinement round (u8 indices, Kp-wide lane groups)
+constexpr int kMaxRefineRounds = 8;
 // Grid region of the dock kernel (floats).  Corner reads at i0 + 1 = n carry weight 0 but
 // must read FINITE values that no other warp writes.  FIX: the nz planes + a 32-float zero
 // pad: the z index is clamped to nz - 2 at the top face (grid_g), so the only read past the
@@ -131,7 +140,7 @@ __host__ __device__ inline size_t dock_grid_floats(int mode, int nz, int rs, int
                               : (size_t)(nz + 1) * ps + rs + 2;
 }
 __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int mode, int nz, int rs, int ps, int P,
-                                                  int K, int S_w, int LC, int RC) {
+                                                  int K, int S_w, int LC, int RC, int n_ref) {
     DockLayout L;
     size_t o = 0;
     L.grid = o;  o += align16(dock_grid_floats(mode, nz, rs, ps) * 4);
@@ -142,7 +151,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int m
     L.rec_o = q;   q += align16((size_t)LC * rec_floats_of(AC) * 4);
     L.meta_o = q;  q += (size_t)LC * 16;
     L.score_o = q; q += align16((size_t)LC * P * 4);
-    L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC));
+    L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC, n_ref));
     L.slot_b = q;
     L.slots = o; o += kDockSlots * q;
     L.total = o;

@@ -25,7 +25,8 @@ _NAMES = {0: "VS_OK", -1: "VS_E_ARG", -2: "VS_E_PARSE", -3: "VS_E_OVERFLOW_ATOMS
 SYMBOLS = ["vs_create", "vs_destroy", "vs_last_error", "vs_workspace_size", "vs_set_workspace", "vs_load_pocket",
            "vs_set_pose_table", "vs_set_angle_table", "vs_submit", "vs_wait", "vs_get_results", "vs_get_coords",
            "vs_get_pose_debug", "vs_local_topk", "vs_keys", "vs_select_keys", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
-           "vs_score_points", "vs_get_stats", "vs_plan_boundaries", "vs_plan_lpt"]
+           "vs_score_points", "vs_get_stats", "vs_plan_boundaries", "vs_plan_lpt", "vs_set_refine_table", "vs_get_refine",
+           "vs_get_pose_refine_debug"]
 
 
 class VsError(RuntimeError):
@@ -107,6 +108,9 @@ def load_library():
         "vs_get_results": [P, I32, P, P, P, P, I32],
         "vs_get_coords": [P, I32, P, I32],
         "vs_get_pose_debug": [P, I32, P, P],
+        "vs_set_refine_table": [P, I32, I32, P, P],
+        "vs_get_refine": [P, I32, P, I32],
+        "vs_get_pose_refine_debug": [P, I32, P],
         "vs_local_topk": [P, I32, I32, P, ctypes.POINTER(I32)],
         "vs_keys": [P, I32, ctypes.c_uint32, P, ctypes.POINTER(I64)],
         "vs_select_keys": [P, P, I64, I32, P],
@@ -197,6 +201,7 @@ class Engine:
         self.h = h
         self.ws = None
         self.P = self.K = None
+        self.n_ref = 0
         self._n = 0
         self._batch_keep = None
 
@@ -228,6 +233,32 @@ class Engine:
         cs = np.ascontiguousarray(cs, np.float32).reshape(-1, 2)
         self._check(self.lib.vs_set_angle_table(self.h, cs.shape[0], _ptr(cs)))
         self.K = cs.shape[0]
+
+    def set_refine(self, n_rounds, rot=None, trans=None):
+        """Rigid refinement after the sweeps (Q23): ``n_rounds`` greedy
+        rounds over the move table (rot [J,3,3], trans [J,3] Angstrom; move 0 = identity).  0 = off."""
+        if not n_rounds:
+            self._check(self.lib.vs_set_refine_table(self.h, 0, 0, None, None))
+            self.n_ref = 0
+            return
+        rot = np.ascontiguousarray(rot, np.float32).reshape(-1, 9)
+        trans = np.ascontiguousarray(trans, np.float32).reshape(-1, 3)
+        self._check(self.lib.vs_set_refine_table(self.h, int(n_rounds), rot.shape[0], _ptr(rot), _ptr(trans)))
+        self.n_ref = int(n_rounds)
+
+    def refine(self, slot=0) -> np.ndarray:
+        """Refinement moves of every ligand's best pose, uint8 [n, n_rounds] (0xFF: another rank's)."""
+        out = np.zeros((max(1, self._n), max(1, self.n_ref)), np.uint8)
+        if self.n_ref:
+            self._check(self.lib.vs_get_refine(self.h, slot, _ptr(out), 0))
+        return out[: self._n, : self.n_ref]
+
+    def pose_refine_debug(self, slot=0) -> np.ndarray:
+        """Every pose's refinement moves, uint8 [n, P, n_rounds] (requires debug_poses)."""
+        out = np.zeros((max(1, self._n), self.P, max(1, self.n_ref)), np.uint8)
+        if self.n_ref:
+            self._check(self.lib.vs_get_pose_refine_debug(self.h, slot, _ptr(out)))
+        return out[: self._n, :, : self.n_ref]
 
     def load_pocket(self, pocket) -> int:
         g = np.ascontiguousarray(pocket.grid, np.float32)

@@ -791,3 +791,90 @@ def test_third_bucketing_key_manifest_bit_exact_and_results_unchanged(c2, grid):
     e2, *_ = run(lib, [pk], P=16, K=8, debug=False, atom_clusters=na, rot_clusters=nr)
     r, r2 = e.results(0), e2.results(0)
     assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.angles, r2.angles)
+
+
+# ----------------------------------------------------------------------------- rigid refinement (Q23)
+
+def run_refine(lib, pk, P, K, n_ref, table, debug=True, **kw):
+    e = engine(debug_poses=debug, **kw)
+    rot, tr, cs, ids = setup(e, [pk], P, K)
+    e.set_refine(n_ref, *table)
+    e.submit_library(lib, ids)
+    e.wait()
+    return e, rot, tr, cs
+
+
+def check_refine(e, lib, idx, pk, rot, tr, cs, n_ref, table, debug=True):
+    r = e.results(0)
+    xyz = e.coords(0)
+    ps, pa = e.pose_debug(0) if debug else (None, None)
+    prf = e.pose_refine_debug(0) if debug else None
+    rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, xyz, ps, pa, band=BAND,
+                       tol_score=TOL_S, tol_xyz=TOL_X, refine=(n_ref,) + tuple(table), gpu_refine=e.refine(0),
+                       gpu_pose_refine=prf)
+    assert rep.ok, rep.summary() + "\n" + "\n".join(map(str, rep.failures[:10]))
+    return rep, r
+
+
+def test_refine_c1_full_parity_every_pose():
+    """sweeps, then 2 rounds of 13 rigid moves (two lane groups of 8); every pose's
+    angle AND refinement choices replayed in fp64, best-pose coordinates include the moves."""
+    c = vsgen.CONFIGS["C1"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    table = vsgen.refine_table()
+    e, rot, tr, cs = run_refine(lib, pk, c["P"], c["K"], 2, table)
+    rep, r = check_refine(e, lib, range(lib.n), pk, rot, tr, cs, 2, table)
+    assert rep.independent_checked >= lib.n // 2 and rep.independent_equal == rep.independent_checked
+    mv = e.refine(0)
+    assert mv.shape == (lib.n, 2) and mv.max() < table[0].shape[0] and (mv != 0).any()
+    # refinement never raises a pose's score: compare with the unrefined run
+    e0, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    assert np.all(r.best_score <= e0.results(0).best_score + 1e-5 * np.maximum(1, np.abs(r.best_score)))
+
+
+def test_refine_c2_sample_parity_and_layout_invariance(c2):
+    c, lib, pk = c2
+    table = vsgen.refine_table(0.3, 8.0)
+    e, rot, tr, cs = run_refine(lib, pk, c["P"], c["K"], 1, table)
+    rng = np.random.default_rng(5)
+    idx = rng.choice(lib.n, 300, replace=False)
+    rep, r = check_refine(e, lib, idx, pk, rot, tr, cs, 1, table)
+    assert rep.independent_equal == rep.independent_checked > 100
+    # bit-identical under another cluster grid / launch structure (same lane map)
+    e2, *_ = run_refine(lib, pk, c["P"], c["K"], 1, table, debug=False, atom_clusters=1, rot_clusters=1,
+                        bucket_multiple=3)
+    r2 = e2.results(0)
+    assert np.array_equal(r2.best_score, r.best_score) and np.array_equal(r2.best_pose, r.best_pose)
+    assert np.array_equal(e2.refine(0), e.refine(0))
+
+
+def test_refine_identity_table_keeps_the_sweep_result():
+    """A one-move (identity) table changes no pose, angle or coordinate; scores agree to fp32 rounding
+    (the refined mode re-scores every atom at the end instead of finalising own regions)."""
+    c = vsgen.CONFIGS["C1"]
+    lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
+    pk = vsgen.pocket(101)
+    q, d = vsgen.refine_table()
+    e, *_ = run_refine(lib, pk, c["P"], c["K"], 3, (q[:1], d[:1]), debug=False)
+    e0, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    r, r0 = e.results(0), e0.results(0)
+    assert np.array_equal(r.best_pose, r0.best_pose) and np.array_equal(r.angles, r0.angles)
+    assert np.max(np.abs(r.best_score - r0.best_score) / np.maximum(1, np.abs(r0.best_score))) < 1e-6
+    assert np.array_equal(e.coords(0), e0.coords(0))
+    assert not e.refine(0).any()
+
+
+def test_refine_table_validation():
+    e = engine()
+    q, d = vsgen.refine_table()
+    from paper_2303_06150_b200.vsdock import VsError
+    with pytest.raises(VsError, match="identity"):
+        e.set_refine(1, q[1:], d[1:])
+    with pytest.raises(VsError):
+        e.set_refine(9, q, d)
+    bad = d.copy()
+    bad[3, 1] = np.nan
+    with pytest.raises(VsError, match="non-finite"):
+        e.set_refine(1, q, bad)
+    e.set_refine(0)
