@@ -51,12 +51,13 @@ def _load():
         build()
         lib = ctypes.CDLL(_SO)
         p, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
-        lib.oracle_dock_batch.argtypes = [i64, p, p, p, p, p, p, p, p, p, i32, p, p, i32, p, i32, p, p, p, p, p, p, p, p,
-                                          i32, i32, p, p, p, p, i32]
+        lib.oracle_dock_batch.argtypes = [i64, p, p, p, p, p, p, p, p, p, p, i32, p, p, i32, p, i32, p, p, p, p, p, p, p,
+                                          p, i32, i32, p, p, p, p, i32]
         lib.oracle_dock_batch.restype = i32
-        lib.oracle_replay_pose.argtypes = [p, p, p, i32, p, i32, p, p, p, p, p, i32, p, i32, p, p, p, i32, i32, p, p, p, p]
+        lib.oracle_replay_pose.argtypes = [p, p, p, i32, p, p, i32, p, p, p, p, p, i32, p, i32, p, p, p, i32, i32, p, p, p,
+                                           p]
         lib.oracle_replay_pose.restype = f64
-        lib.oracle_grid_score_points.argtypes = [p, p, p, i64, p, p]
+        lib.oracle_grid_score_points.argtypes = [p, p, p, i64, p, p, p]
         lib.oracle_grid_score_points.restype = i32
         lib.oracle_place.argtypes = [p, p, i32, p, p, p, p]
         lib.oracle_place.restype = i32
@@ -77,8 +78,11 @@ def _c(a, dt):
 
 
 def _pocket_args(pocket):
+    """(dims {nx, ny, nz, T}, prm, grid [T*nz*ny*nx]) -- a pocket with a 4-D grid [T, nz, ny, nx] is
+    typed (Q24)."""
     nx, ny, nz = pocket.dims
-    dims = np.array([nx, ny, nz], np.int32)
+    T = 1 if pocket.grid.ndim == 3 else int(pocket.grid.shape[0])
+    dims = np.array([nx, ny, nz, T], np.int32)
     prm = np.array(list(pocket.origin) + [pocket.spacing] + list(pocket.center) + [pocket.out_slope], np.float64)
     return dims, prm, _c(pocket.grid, np.float32)
 
@@ -109,11 +113,16 @@ def _refine_args(refine):
     return int(n_ref), int(q.shape[0]), q, d
 
 
+def _types(t):
+    return None if t is None else _c(t, np.uint8).reshape(-1)
+
+
 def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_debug=True, nthreads=None,
-               refine=None) -> DockResult:
+               refine=None, atom_type=None) -> DockResult:
     """Dock every ligand of ``lib`` (a vsgen.Library-like CSR batch) into ``pocket``; fp64.
     ``refine`` = (n_ref, move rotations [J,3,3], move translations [J,3] in Angstrom): rigid
-    refinement rounds after the sweeps (Q23)."""
+    refinement rounds after the sweeps (Q23).  ``atom_type`` (uint8
+    per atom, default ``lib.atom_type``) selects each atom's grid channel of a typed pocket (Q24)."""
     L = _load()
     n = lib.n
     P, K = int(rot.shape[0]), int(cs.shape[0])
@@ -125,6 +134,9 @@ def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_de
         ma = np.zeros(1, np.int32)
     rot, trans, cs = _c(rot, np.float32), _c(trans, np.float32), _c(cs, np.float32)
     nA, nR = int(ao[-1]), int(fo[-1])
+    ty = _types(atom_type if atom_type is not None else getattr(lib, "atom_type", None))
+    if ty is not None and ty.size == 0:
+        ty = np.zeros(1, np.uint8)
     bs = np.zeros(n, np.float64); bp = np.zeros(n, np.int32)
     ang = np.zeros(max(1, S_w * nR), np.uint8)
     xo = np.zeros((max(1, nA), 3), np.float64) if want_xyz else None
@@ -136,7 +148,7 @@ def dock_batch(lib, pocket, rot, trans, cs, S_w: int = 1, want_xyz=True, want_de
     n_ref, J, q, d = _refine_args(refine)
     rf = np.zeros((max(1, n), max(1, n_ref)), np.uint8)
     prf = np.zeros((max(1, n), P, max(1, n_ref)), np.uint8) if want_debug else None
-    rc = L.oracle_dock_batch(n, _p(ao), _p(xyz), _p(fo), _p(fax), _p(mo), _p(ma), _p(dims), _p(prm), _p(G), P, _p(rot), _p(trans),
+    rc = L.oracle_dock_batch(n, _p(ao), _p(xyz), _p(ty), _p(fo), _p(fax), _p(mo), _p(ma), _p(dims), _p(prm), _p(G), P, _p(rot), _p(trans),
                              K, _p(cs), S_w, _p(bs), _p(bp), _p(ang), _p(xo), _p(ps), _p(pa), _p(sm), _p(pm),
                              n_ref, J, _p(q), _p(d), _p(rf) if n_ref else None, _p(prf) if (n_ref and prf is not None) else None,
                              nthreads)
@@ -161,9 +173,11 @@ def _frags_csr(frags):
     return ax, mo, (ma if ma.size else np.zeros(1, np.int32)).astype(np.int32)
 
 
-def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1, refine=None, mseq=None, want_refine=False):
+def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1, refine=None, mseq=None, want_refine=False,
+                types=None):
     """Replay a given angle sequence from pose (rot9, tr3), then (``refine``, Q23) the given
-    refinement moves ``mseq``.  ``frags``: general form (vsgen.Frags) or range form [R,4].
+    refinement moves ``mseq``.  ``frags``: general form (vsgen.Frags) or range form [R,4];
+    ``types``: the ligand's atom types (grid channels, Q24) or None.
 
     Returns (final_score, final_xyz [A,3] fp64, step_scores [S_w*R, K] fp64), plus the refinement
     round scores [n_ref, J] when ``want_refine``."""
@@ -178,7 +192,7 @@ def replay_pose(pocket, xyz, frags, rot9, tr3, cs, kseq, S_w: int = 1, refine=No
     n_ref, J, q, d = _refine_args(refine)
     ms = _c(mseq if n_ref else np.zeros(1), np.uint8)
     rs = np.zeros((max(1, n_ref), J), np.float64)
-    s = L.oracle_replay_pose(_p(dims), _p(prm), _p(G), A, _p(xyz), R, _p(ax), _p(mo), _p(ma),
+    s = L.oracle_replay_pose(_p(dims), _p(prm), _p(G), A, _p(xyz), _p(_types(types)), R, _p(ax), _p(mo), _p(ma),
                              _p(_c(rot9, np.float32)), _p(_c(tr3, np.float32)), K, _p(_c(cs, np.float32)), S_w,
                              _p(kseq), _p(steps), _p(y), n_ref, J, _p(q), _p(d), _p(ms), _p(rs))
     if want_refine:
@@ -195,13 +209,17 @@ def rigid_move(y, q9, d3) -> np.ndarray:
     return y
 
 
-def grid_score(pocket, pts) -> np.ndarray:
-    """g(y) at arbitrary points [n,3] (Angstrom), fp64 (a8)."""
+def grid_score(pocket, pts, types=None) -> np.ndarray:
+    """g(y) at arbitrary points [n,3] (Angstrom), fp64 (a8); ``types`` = the channel of every point
+    (typed pocket, Q24), None = channel 0."""
     L = _load()
     dims, prm, G = _pocket_args(pocket)
     pts = _c(pts, np.float64).reshape(-1, 3)
     out = np.zeros(pts.shape[0], np.float64)
-    L.oracle_grid_score_points(_p(dims), _p(prm), _p(G), pts.shape[0], _p(pts), _p(out))
+    ty = _types(types)
+    if ty is not None and (ty.shape[0] != pts.shape[0] or (ty.size and int(ty.max()) >= dims[3])):
+        raise ValueError("grid_score: one type per point, each < the pocket's channels")
+    L.oracle_grid_score_points(_p(dims), _p(prm), _p(G), pts.shape[0], _p(pts), _p(ty), _p(out))
     return out
 
 

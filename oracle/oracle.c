@@ -30,6 +30,9 @@
  * Rigid refinement after the sweeps (Q23): n_ref rounds over a
  * caller-given table of J rigid moves about the pose's centroid, same greedy rule.
  *
+ * Per-atom-type grid channels (Q24): the pocket holds T grids of one
+ * geometry, G_0 .. G_{T-1}; atom i of type t_i is scored on G_{t_i}.  No types = every atom type 0.
+ *
  * Pins: tests/test_oracle_pins.py (closed forms, invariants, brute force,
  * library routines scipy.ndimage.map_coordinates / scipy Rotation, renumbering
  * invariance, pose translations tau_p != 0 and a docking centre off the grid centre).
@@ -46,11 +49,13 @@ typedef struct {
     double h;            /* spacing, Angstrom */
     double c[3];         /* pocket centre */
     double kappa;        /* out-of-box slope, energy per Angstrom (Q9) */
-    const float* G;      /* values [nz][ny][nx], x fastest */
+    int T;               /* grid channels (Q24); 1 = the untyped method */
+    const float* G;      /* values [T][nz][ny][nx], x fastest */
 } opocket;
 
-static double node(const opocket* pk, int i, int j, int k) {
-    return (double)pk->G[((size_t)k * pk->n[1] + j) * pk->n[0] + i];
+/* node (i, j, k) of channel t */
+static double node(const opocket* pk, int t, int i, int j, int k) {
+    return (double)pk->G[(((size_t)t * pk->n[2] + k) * pk->n[1] + j) * pk->n[0] + i];
 }
 
 static double lerp(double a, double b, double f) { return (1.0 - f) * a + f * b; }  /* Q10 */
@@ -59,9 +64,10 @@ static double lerp(double a, double b, double f) { return (1.0 - f) * a + f * b;
  * a8: pocket-grid score g(y) by trilinear interpolation (BJ "pocket-grid score
  * by trilinear interpolation").  Per axis (Q9): u = (y - o)/h, u_c = clamp(u,
  * 0, n-1), excess e += |u - u_c|, i0 = min(floor(u_c), n-2), f = u_c - i0.
- * Interpolate x, then y, then z (Q10).  g = interp + kappa*h*e.
+ * Interpolate x, then y, then z (Q10).  g = interp + kappa*h*e.  Channel t (Q24) selects the
+ * grid G_t; the geometry and the out-of-box term are the same for every channel.
  */
-double oracle_grid_score(const opocket* pk, const double y[3]) {
+double oracle_grid_score(const opocket* pk, int t, const double y[3]) {
     int i0[3];
     double f[3], e = 0.0;
     for (int a = 0; a < 3; ++a) {
@@ -75,20 +81,21 @@ double oracle_grid_score(const opocket* pk, const double y[3]) {
         f[a] = uc - (double)i;
     }
     int i = i0[0], j = i0[1], k = i0[2];
-    double l00 = lerp(node(pk, i, j, k), node(pk, i + 1, j, k), f[0]);
-    double l10 = lerp(node(pk, i, j + 1, k), node(pk, i + 1, j + 1, k), f[0]);
-    double l01 = lerp(node(pk, i, j, k + 1), node(pk, i + 1, j, k + 1), f[0]);
-    double l11 = lerp(node(pk, i, j + 1, k + 1), node(pk, i + 1, j + 1, k + 1), f[0]);
+    double l00 = lerp(node(pk, t, i, j, k), node(pk, t, i + 1, j, k), f[0]);
+    double l10 = lerp(node(pk, t, i, j + 1, k), node(pk, t, i + 1, j + 1, k), f[0]);
+    double l01 = lerp(node(pk, t, i, j, k + 1), node(pk, t, i + 1, j, k + 1), f[0]);
+    double l11 = lerp(node(pk, t, i, j + 1, k + 1), node(pk, t, i + 1, j + 1, k + 1), f[0]);
     double l0 = lerp(l00, l10, f[1]);
     double l1 = lerp(l01, l11, f[1]);
     double v = lerp(l0, l1, f[2]);
     return v + pk->kappa * pk->h * e;
 }
 
-/* S(y) = sum_i g(y_i): the interaction score of a pose (lower is better, Q2). */
-static double score(const opocket* pk, const double* y, int A) {
+/* S(y) = sum_i g_{t_i}(y_i): the interaction score of a pose (lower is better, Q2);
+ * ty = the ligand's atom types (Q24), NULL = all type 0. */
+static double score(const opocket* pk, const double* y, int A, const uint8_t* ty) {
     double s = 0.0;
-    for (int i = 0; i < A; ++i) s += oracle_grid_score(pk, y + 3 * i);
+    for (int i = 0; i < A; ++i) s += oracle_grid_score(pk, ty ? ty[i] : 0, y + 3 * i);
     return s;
 }
 
@@ -175,14 +182,14 @@ void oracle_rigid_move(double* y, int A, const float* q9, const float* d3) {
  * for the angle steps), keep the lowest m attaining the minimum (Q11), apply it.  scores[m]
  * (optional) receives S_m; *margin (optional) the relative gap of the runner-up.
  */
-static int refine_round(const opocket* pk, double* y, double* ytmp, int A, int J, const float* qrot, const float* dtr,
-                        double* scores, double* margin) {
+static int refine_round(const opocket* pk, double* y, double* ytmp, int A, const uint8_t* ty, int J, const float* qrot,
+                        const float* dtr, double* scores, double* margin) {
     double smin = INFINITY, s2 = INFINITY;
     int mmin = 0;
     for (int m = 0; m < J; ++m) {
         memcpy(ytmp, y, sizeof(double) * 3 * (size_t)A);
         oracle_rigid_move(ytmp, A, qrot + 9 * m, dtr + 3 * m);
-        double sc = score(pk, ytmp, A);
+        double sc = score(pk, ytmp, A, ty);
         if (scores) scores[m] = sc;
         if (sc < smin) { s2 = smin; smin = sc; mmin = m; }
         else if (sc < s2) { s2 = sc; }
@@ -205,6 +212,7 @@ typedef struct {
     const int64_t *atom_off, *frag_off, *move_off;
     const float* xyz;
     const int32_t *frag_axis, *move_atoms;
+    const uint8_t* atom_type;   /* [atom_off[n]] (Q24) or NULL */
     /* outputs (any may be NULL except best_score/best_pose) */
     double* best_score;
     int32_t* best_pose;
@@ -229,6 +237,7 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
     int A = (int)(B->atom_off[li + 1] - B->atom_off[li]);
     int R = (int)(B->frag_off[li + 1] - B->frag_off[li]);
     const float* x = B->xyz + 3 * B->atom_off[li];
+    const uint8_t* ty = B->atom_type ? B->atom_type + B->atom_off[li] : NULL;
     const int64_t f0 = B->frag_off[li];
     double best = INFINITY, second = INFINITY;
     int bestp = -1;
@@ -243,7 +252,7 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
                     memcpy(ytmp, y, sizeof(double) * 3 * (size_t)A);
                     rotate_frag_csr(ytmp, B->frag_axis, B->move_off, B->move_atoms, f0 + r, (double)B->cs[2 * k],
                                     (double)B->cs[2 * k + 1]);
-                    double s = score(pk, ytmp, A);
+                    double s = score(pk, ytmp, A, ty);
                     if (s < smin) { s2 = smin; smin = s; kmin = k; }
                     else if (s < s2) { s2 = s; }
                 }
@@ -258,11 +267,11 @@ static void dock_one(const batch_t* B, int64_t li, double* y, double* ytmp, doub
         }
         for (int t = 0; t < B->n_ref; ++t) {   /* rigid refinement after the sweeps (Q23) */
             double m;
-            mseq[t] = (uint8_t)refine_round(pk, y, ytmp, A, B->J, B->qrot, B->dtr, NULL, &m);
+            mseq[t] = (uint8_t)refine_round(pk, y, ytmp, A, ty, B->J, B->qrot, B->dtr, NULL, &m);
             if (m < margin) margin = m;
         }
         if (B->pose_refine) memcpy(B->pose_refine + ((size_t)li * B->P + p) * B->n_ref, mseq, (size_t)B->n_ref);
-        double sp = score(pk, y, A);
+        double sp = score(pk, y, A, ty);
         if (B->pose_score) B->pose_score[li * B->P + p] = sp;
         if (B->step_margin) B->step_margin[li * B->P + p] = margin;
         if (B->pose_angles)
@@ -307,6 +316,7 @@ static void* batch_worker(void* arg) {
 
 static void make_pocket(opocket* pk, const int32_t* dims, const double* prm, const float* G) {
     for (int a = 0; a < 3; ++a) pk->n[a] = dims[a];
+    pk->T = dims[3];
     for (int a = 0; a < 3; ++a) pk->o[a] = prm[a];
     pk->h = prm[3];
     for (int a = 0; a < 3; ++a) pk->c[a] = prm[4 + a];
@@ -315,11 +325,12 @@ static void make_pocket(opocket* pk, const int32_t* dims, const double* prm, con
 }
 
 /*
- * Dock a batch.  dims = {nx, ny, nz}; prm = {ox, oy, oz, h, cx, cy, cz, kappa}.
+ * Dock a batch.  dims = {nx, ny, nz, T}; prm = {ox, oy, oz, h, cx, cy, cz, kappa}; grid =
+ * [T][nz][ny][nx]; atom_type[atom_off[n]] (NULL = all 0), every type < T.
  * Returns 0, or -1 on invalid arguments.
  */
-int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, const int64_t* frag_off,
-                      const int32_t* frag_axis, const int64_t* move_off, const int32_t* move_atoms,
+int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, const uint8_t* atom_type,
+                      const int64_t* frag_off, const int32_t* frag_axis, const int64_t* move_off, const int32_t* move_atoms,
                       const int32_t* dims, const double* prm, const float* grid,
                       int P, const float* rot, const float* trans, int K, const float* cs, int S_w,
                       double* best_score, int32_t* best_pose, uint8_t* angles, double* xyz_out,
@@ -327,7 +338,10 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
                       int n_ref, int J, const float* qrot, const float* dtr, uint8_t* refine, uint8_t* pose_refine,
                       int nthreads) {
     if (n < 0 || P < 1 || K < 1 || S_w < 0 || n_ref < 0 || (n_ref > 0 && (J < 1 || !qrot || !dtr))) return -1;
-    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2 || !(prm[3] > 0.0)) return -1;
+    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 2 || dims[3] < 1 || !(prm[3] > 0.0)) return -1;
+    if (atom_type)
+        for (int64_t i = 0; i < (n > 0 ? atom_off[n] : 0); ++i)
+            if (atom_type[i] >= dims[3]) return -1;
     opocket pk;
     make_pocket(&pk, dims, prm, grid);
     if (nthreads < 1) nthreads = 1;
@@ -339,7 +353,7 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
         batch_t* B = &jobs[t];
         memset(B, 0, sizeof *B);
         B->pk = &pk; B->P = P; B->K = K; B->S_w = S_w; B->rot = rot; B->tr = trans; B->cs = cs;
-        B->atom_off = atom_off; B->frag_off = frag_off; B->xyz = xyz;
+        B->atom_off = atom_off; B->frag_off = frag_off; B->xyz = xyz; B->atom_type = atom_type;
         B->frag_axis = frag_axis; B->move_off = move_off; B->move_atoms = move_atoms;
         B->best_score = best_score; B->best_pose = best_pose; B->angles = angles; B->xyz_out = xyz_out;
         B->pose_score = pose_score; B->pose_angles = pose_angles; B->step_margin = step_margin; B->pose_margin = pose_margin;
@@ -360,7 +374,7 @@ int oracle_dock_batch(int64_t n, const int64_t* atom_off, const float* xyz, cons
  * the fp64 minimum.  Final coordinates -> y_out[3A], final score returned.
  */
 double oracle_replay_pose(const int32_t* dims, const double* prm, const float* grid,
-                          int A, const float* xyz, int R, const int32_t* frag_axis, const int64_t* move_off,
+                          int A, const float* xyz, const uint8_t* ty, int R, const int32_t* frag_axis, const int64_t* move_off,
                           const int32_t* move_atoms,
                           const float* rot9, const float* tr3, int K, const float* cs, int S_w,
                           const uint8_t* kseq, double* step_scores, double* y_out,
@@ -376,7 +390,7 @@ double oracle_replay_pose(const int32_t* dims, const double* prm, const float* g
                 for (int k = 0; k < K; ++k) {
                     memcpy(yt, y_out, sizeof(double) * 3 * (size_t)A);
                     rotate_frag_csr(yt, frag_axis, move_off, move_atoms, r, (double)cs[2 * k], (double)cs[2 * k + 1]);
-                    step_scores[(sw * R + r) * K + k] = score(&pk, yt, A);
+                    step_scores[(sw * R + r) * K + k] = score(&pk, yt, A, ty);
                 }
             }
             int k = kseq[sw * R + r];
@@ -388,20 +402,21 @@ double oracle_replay_pose(const int32_t* dims, const double* prm, const float* g
             for (int m = 0; m < J; ++m) {
                 memcpy(yt, y_out, sizeof(double) * 3 * (size_t)A);
                 oracle_rigid_move(yt, A, qrot + 9 * m, dtr + 3 * m);
-                ref_scores[t * J + m] = score(&pk, yt, A);
+                ref_scores[t * J + m] = score(&pk, yt, A, ty);
             }
         oracle_rigid_move(y_out, A, qrot + 9 * mseq[t], dtr + 3 * mseq[t]);
     }
-    double s = score(&pk, y_out, A);
+    double s = score(&pk, y_out, A, ty);
     free(yt);
     return s;
 }
 
-/* Test hooks: g at arbitrary points, and a pose placement. */
-int oracle_grid_score_points(const int32_t* dims, const double* prm, const float* grid, int64_t n, const double* pts, double* out) {
+/* Test hooks: g at arbitrary points (channel types[i], NULL = 0), and a pose placement. */
+int oracle_grid_score_points(const int32_t* dims, const double* prm, const float* grid, int64_t n, const double* pts,
+                             const uint8_t* types, double* out) {
     opocket pk;
     make_pocket(&pk, dims, prm, grid);
-    for (int64_t i = 0; i < n; ++i) out[i] = oracle_grid_score(&pk, pts + 3 * i);
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_grid_score(&pk, types ? types[i] : 0, pts + 3 * i);
     return 0;
 }
 

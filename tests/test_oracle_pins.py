@@ -21,7 +21,7 @@ import vsgen
 
 def mkpocket(G, origin=(0.0, 0.0, 0.0), h=1.0, center=None, kappa=1.0):
     G = np.ascontiguousarray(G, np.float32)
-    nz, ny, nx = G.shape
+    nz, ny, nx = G.shape[-3:]
     if center is None:
         center = tuple(origin[a] + h * (n - 1) / 2 for a, n in enumerate((nx, ny, nz)))
     return vsgen.Pocket(G, tuple(origin), float(h), tuple(center), float(kappa))
@@ -479,3 +479,125 @@ def test_refinement_replay_scores_every_move_and_never_raises_the_score(c1):
             prev = rs[t].min()
         assert rs[-1].min() == s or abs(rs[-1].min() - s) < 1e-12 * max(1.0, abs(s))
         assert r.best_score[i] <= base.pose_score[i, p] + 1e-12 * max(1.0, abs(base.pose_score[i, p]))
+
+
+# ----------------------------------------------------------------------------- per-atom-type grid channels (Q24)
+
+def _lib_ref_score_typed(pk, pts, types):
+    """Independent typed g (Q24): scipy trilinear on channel types[i] + kappa*h*L1 excess."""
+    out = np.empty(len(pts))
+    for t in range(pk.n_channels):
+        sel = np.asarray(types) == t
+        if sel.any():
+            sub = vsgen.Pocket(pk.grid[t], pk.origin, pk.spacing, pk.center, pk.out_slope)
+            out[sel] = lib_ref_score(sub, np.asarray(pts)[sel])
+    return out
+
+
+def test_typed_channels_match_scipy_per_channel():
+    """Every point is interpolated on ITS channel: scipy per channel, inside and outside the box."""
+    rng = np.random.default_rng(21)
+    G = rng.normal(size=(3, 9, 10, 11)).astype(np.float32)
+    pk = mkpocket(G, origin=(-3.0, 2.0, 1.0), h=0.75, kappa=2.5)
+    lo = np.array(pk.origin) - 3.0
+    hi = np.array(pk.origin) + 0.75 * np.array([10, 9, 8]) + 3.0
+    p = rng.uniform(lo, hi, size=(4000, 3))
+    t = rng.integers(0, 3, size=4000).astype(np.uint8)
+    assert np.max(np.abs(oracle.grid_score(pk, p, t) - _lib_ref_score_typed(pk, p, t))) < 1e-12
+    with pytest.raises(ValueError):
+        oracle.grid_score(pk, p[:2], np.array([0, 3], np.uint8))     # type >= T
+
+
+def test_typed_linear_channels_closed_form():
+    """Channel t = w_t . u + b_t (closed form, exact for trilinear interpolation inside the box): a
+    wrong channel index, a transposed channel stride or a dropped type fails it."""
+    n = 12
+    W = np.array([[0.5, -1.0, 2.0], [-2.0, 0.25, 1.0], [1.5, 1.5, -0.5], [0.0, -3.0, 0.75]])
+    b = np.array([1.0, -4.0, 2.5, 0.0])
+    Z, Y, X = np.meshgrid(np.arange(n), np.arange(n + 1), np.arange(n + 2), indexing="ij")
+    G = np.stack([W[t, 0] * X + W[t, 1] * Y + W[t, 2] * Z + b[t] for t in range(4)]).astype(np.float32)
+    pk = mkpocket(G)
+    rng = np.random.default_rng(22)
+    u = rng.uniform([0, 0, 0], [n + 1, n, n - 1], size=(3000, 3))
+    t = rng.integers(0, 4, size=3000)
+    want = np.einsum("ij,ij->i", W[t], u) + b[t]
+    assert np.max(np.abs(oracle.grid_score(pk, u, t.astype(np.uint8)) - want)) < 1e-9
+
+
+def test_typed_copies_reduce_to_untyped(c1):
+    """T identical channels: any typing docks exactly like the untyped pocket (bitwise)."""
+    L, pk, (rot, tr), cs = c1
+    pk3 = vsgen.Pocket(np.stack([pk.grid] * 3), pk.origin, pk.spacing, pk.center, pk.out_slope)
+    ty = vsgen.atom_types(L, n_types=3)
+    a = oracle.dock_batch(L, pk, rot, tr, cs)
+    b = oracle.dock_batch(L, pk3, rot, tr, cs, atom_type=ty)
+    for f in ("best_score", "best_pose", "angles", "xyz", "pose_score"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+
+
+def test_typed_single_type_docks_on_that_channel(c1):
+    """Every atom of type t: the result is the untyped docking on G_t."""
+    L, _, (rot, tr), cs = c1
+    pk = vsgen.typed_pocket(101, n_types=3)
+    for t in range(3):
+        pt = vsgen.Pocket(pk.grid[t], pk.origin, pk.spacing, pk.center, pk.out_slope)
+        a = oracle.dock_batch(L, pt, rot, tr, cs)
+        b = oracle.dock_batch(L, pk, rot, tr, cs, atom_type=np.full(int(L.atom_off[-1]), t, np.uint8))
+        assert np.array_equal(a.best_score, b.best_score) and np.array_equal(a.angles, b.angles)
+
+
+def test_typed_channel_relabelling_invariance(c1):
+    """Permuting the channels and relabelling the types the same way changes nothing."""
+    L, _, (rot, tr), cs = c1
+    pk = vsgen.typed_pocket(102, n_types=4)
+    ty = vsgen.atom_types(L, n_types=4)
+    perm = np.array([2, 0, 3, 1])                       # new channel perm[t] holds old channel t
+    Gp = np.empty_like(pk.grid)
+    Gp[perm] = pk.grid
+    pkp = vsgen.Pocket(Gp, pk.origin, pk.spacing, pk.center, pk.out_slope)
+    a = oracle.dock_batch(L, pk, rot, tr, cs, atom_type=ty)
+    b = oracle.dock_batch(L, pkp, rot, tr, cs, atom_type=perm[ty].astype(np.uint8))
+    assert np.array_equal(a.best_score, b.best_score) and np.array_equal(a.xyz, b.xyz)
+    # and the types matter: the untyped docking on channel 0 differs
+    c = oracle.dock_batch(L, pk, rot, tr, cs, atom_type=np.zeros_like(ty))
+    assert not np.array_equal(a.best_score, c.best_score)
+
+
+def test_typed_brute_force_star_ligands_greedy_is_exact():
+    """Star ligands (separable score) with random atom types: the greedy sweep is the exhaustive
+    optimum under the typed score computed by scipy per channel."""
+    rng = np.random.default_rng(23)
+    pk = vsgen.typed_pocket(101, n_types=4)
+    rot, tr = vsgen.pose_table(3)
+    cs = vsgen.angle_table(8)
+    K = cs.shape[0]
+    thetas = [math.atan2(float(cs[k, 1]), float(cs[k, 0])) for k in range(K)]
+    for arms in (1, 2, 3):
+        x, fr = _star_ligand(rng, arms)
+        ty = rng.integers(0, 4, size=len(x)).astype(np.uint8)
+        lib = vsgen.Library.from_ligands([(x, fr)])
+        r = oracle.dock_batch(lib, pk, rot, tr, cs, atom_type=ty)
+        best = math.inf
+        xc = x.astype(np.float64) - x.astype(np.float64).mean(0)
+        for p in range(rot.shape[0]):
+            y0 = xc @ rot[p].astype(np.float64).T + np.array(pk.center)
+            for combo in itertools.product(range(K), repeat=len(fr)):
+                y = y0.copy()
+                for (a, bb, mv), k in zip(fr, combo):
+                    u = (y[bb] - y[a]) / np.linalg.norm(y[bb] - y[a])
+                    y[mv] = Rotation.from_rotvec(thetas[k] * u).apply(y[mv] - y[bb]) + y[bb]
+                best = min(best, float(_lib_ref_score_typed(pk, y, ty).sum()))
+        assert abs(r.best_score[0] - best) < 1e-9 * max(1.0, abs(best))
+
+
+def test_atom_types_are_a_function_of_ligand_id_and_atom_index():
+    """The type recipe: slices and renumbered copies keep every atom's type."""
+    L = vsgen.ligands(200, 4)
+    t = vsgen.atom_types(L)
+    sub = vsgen.ligands(50, 4, first=100)
+    assert np.array_equal(vsgen.atom_types(sub), t[int(L.atom_off[100]):int(L.atom_off[150])])
+    L.atom_type = t
+    lp, perm = L.permuted(3)
+    assert np.array_equal(lp.atom_type[perm], t)
+    freq = np.bincount(vsgen.atom_types(vsgen.ligands(3000, 5)), minlength=4) / 1.0
+    assert np.allclose(freq / freq.sum(), vsgen.TYPE_FREQ, atol=0.01)

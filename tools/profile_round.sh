@@ -15,7 +15,7 @@ python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_${TAG}_
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-unsorted --no-cpu-baseline > /dev/null 2>&1
 # full capture of one dock launch (class 96) of a 200k-ligand library, and of the ingest kernel
-ncu --set full --clock-control none --import-source on -k regex:dock_kernel.96 -s 1 -c 1 -o gpurun_out/dock96_$TAG \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:dock_kernel<.int.96," -s 1 -c 1 -o gpurun_out/dock96_$TAG \
     python tools/dock_time.py 200000 > gpurun_out/ncu_dock_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:ingest -s 1 -c 1 -o gpurun_out/ingest_$TAG \
     python tools/dock_time.py 200000 > gpurun_out/ncu_ingest_$TAG.log 2>&1

@@ -119,6 +119,7 @@ class Library:
     move_atoms: np.ndarray  # int32 [sum |M_r|]
     n_moving: np.ndarray = field(default=None)  # int32 [n]: sum_r |M_r| (generator metadata)
     frags: np.ndarray = field(default=None)     # int32 [sum R, 4] range form, or None
+    atom_type: np.ndarray = field(default=None) # uint8 [sum A]: grid channel per atom (Q24), or None
 
     @staticmethod
     def from_ranges(ligand_id, atom_off, xyz, frag_off, frags, n_moving=None) -> "Library":
@@ -189,6 +190,9 @@ class Library:
         idx = np.asarray(idx, dtype=np.int64)
         ligs = [self.ligand(int(i)) for i in idx]
         out = Library.from_ligands(ligs, self.ligand_id[idx].copy())
+        if self.atom_type is not None:
+            out.atom_type = (np.concatenate([self.atom_type[int(self.atom_off[i]):int(self.atom_off[i + 1])] for i in idx])
+                             if len(idx) else np.zeros(0, np.uint8)).astype(np.uint8)
         if self.frags is not None:
             out.frags = (np.concatenate([self.ligand_ranges(int(i))[1] for i in idx]) if len(idx)
                          else np.zeros((0, 4), np.int32)).astype(np.int32).reshape(-1, 4)
@@ -209,7 +213,11 @@ class Library:
             ligs.append((nx, Frags(p[f.axis] if len(f) else f.axis, [p[m] for m in f.moves])))
             perms.append(p.astype(np.int64) + int(self.atom_off[i]))
         out = Library.from_ligands(ligs, self.ligand_id.copy())
-        return out, (np.concatenate(perms) if perms else np.zeros(0, np.int64))
+        perm = np.concatenate(perms) if perms else np.zeros(0, np.int64)
+        if self.atom_type is not None:
+            out.atom_type = np.empty_like(self.atom_type)
+            out.atom_type[perm] = self.atom_type
+        return out, perm
 
 
 def ligands(n: int, seed: int, atoms=(20, 120), rot=(0, 20), first: int = 0, nthreads: int | None = None) -> Library:
@@ -262,8 +270,13 @@ class Pocket:
 
     @property
     def dims(self):
-        nz, ny, nx = self.grid.shape
+        nz, ny, nx = self.grid.shape[-3:]
         return nx, ny, nz
+
+    @property
+    def n_channels(self) -> int:
+        """Grid channels T: a 4-D grid [T, nz, ny, nx] is a typed pocket (Q24)."""
+        return 1 if self.grid.ndim == 3 else int(self.grid.shape[0])
 
 
 def pocket(seed: int, n=32, spacing: float = 1.0, n_receptor: int = 96,
@@ -294,6 +307,79 @@ def pocket(seed: int, n=32, spacing: float = 1.0, n_receptor: int = 96,
         G += 5.0 * np.exp(-d2 / 2.0) - np.exp(-d2 / 8.0)
     return Pocket(G.astype(np.float32), tuple(float(v) for v in origin), float(spacing),
                   tuple(float(v) for v in c), float(out_slope))
+
+
+# ----------------------------------------------------------------------------- atom types (Q24)
+
+# Type t of a heavy atom (Q24 and section 4): 0 = C, 1 = N, 2 = O, 3 = S
+# with drug-like frequencies; the pair table gives the attractive well depth of ligand type t
+# against receptor type s (polar pairs bind more strongly, carbon-polar less).
+TYPE_FREQ = (0.70, 0.13, 0.14, 0.03)
+_WELL = np.array([[1.0, 0.6, 0.6, 1.1],
+                  [0.6, 1.4, 1.8, 0.7],
+                  [0.6, 1.8, 1.2, 0.7],
+                  [1.1, 0.7, 0.7, 1.3]])
+
+
+def _splitmix64_np(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser of uint64 counters, vectorised (the same mix as _splitmix64)."""
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def atom_types(lib: Library, seed: int = 11, n_types: int = 4) -> np.ndarray:
+    """uint8 type of every atom of ``lib`` (input order): a counter-based draw (splitmix64 of
+    (seed, ligand id, atom index)) from TYPE_FREQ restricted to the first n_types types.  A
+    function of the ligand id and atom index only, so slices and permutations keep their types."""
+    if not 1 <= n_types <= len(TYPE_FREQ):
+        raise ValueError("n_types must be in [1, 4]")
+    A = lib.n_atoms.astype(np.int64)
+    lid = np.repeat(lib.ligand_id.astype(np.uint64), A)
+    j = (np.arange(int(lib.atom_off[-1]), dtype=np.int64) - np.repeat(lib.atom_off[:-1], A)).astype(np.uint64)
+    with np.errstate(over="ignore"):
+        key = (np.uint64(seed) * np.uint64(0xD1B54A32D192ED03)) ^ (lid * np.uint64(0x9E3779B97F4A7C15)) ^ (
+            j * np.uint64(0xBF58476D1CE4E5B9))
+    u = (_splitmix64_np(key) >> np.uint64(11)).astype(np.float64) / 9007199254740992.0
+    cdf = np.cumsum(np.array(TYPE_FREQ[:n_types]) / sum(TYPE_FREQ[:n_types]))
+    return np.minimum(np.searchsorted(cdf, u, side="right"), n_types - 1).astype(np.uint8)
+
+
+def typed_pocket(seed: int, n_types: int = 4, n=32, spacing: float = 1.0, n_receptor: int = 96,
+                 shell=(9.0, 13.0), mouth_deg: float = 50.0, out_slope: float = 1.0,
+                 center_offset=(0.0, 0.0, 0.0), origin=(0.0, 0.0, 0.0)) -> Pocket:
+    """A typed pocket (Q24): the receptor of :func:`pocket` (same seed, same atoms) with a receptor
+    type per atom (drawn from TYPE_FREQ); channel t holds, for a ligand atom of type t, the same
+    confinement term plus per receptor atom s a repulsive core and an attractive well of depth
+    _WELL[t, type(s)].  Grid [n_types, nz, ny, nx] float32."""
+    base = pocket(seed, n, spacing, n_receptor, shell, mouth_deg, out_slope, center_offset, origin)
+    nx, ny, nz = base.dims
+    rng = np.random.Generator(np.random.PCG64(seed))
+    cos_half = math.cos(math.radians(mouth_deg / 2.0))
+    c = np.array(base.center)
+    pts = []
+    while len(pts) < n_receptor:   # the same draws as pocket(): the same receptor atoms
+        v = rng.normal(size=3)
+        v /= np.linalg.norm(v)
+        if v[2] > cos_half:
+            continue
+        pts.append(c + rng.uniform(shell[0], shell[1]) * v)
+    rt = np.random.Generator(np.random.PCG64(seed + 7919)).choice(4, size=n_receptor, p=TYPE_FREQ)
+    o = np.asarray(origin, np.float64)
+    Z, Y, X = np.meshgrid(o[2] + spacing * np.arange(nz), o[1] + spacing * np.arange(ny),
+                          o[0] + spacing * np.arange(nx), indexing="ij")
+    node = np.stack([X, Y, Z], axis=-1)
+    conf = 0.01 * np.sum((node - c) ** 2, axis=-1)
+    G = np.empty((n_types, nz, ny, nx), np.float64)
+    for t in range(n_types):
+        g = conf.copy()
+        for p, s in zip(pts, rt):
+            d2 = np.sum((node - p) ** 2, axis=-1)
+            g += 5.0 * np.exp(-d2 / 2.0) - _WELL[t, s] * np.exp(-d2 / 8.0)
+        G[t] = g
+    return Pocket(G.astype(np.float32), base.origin, base.spacing, base.center, base.out_slope)
 
 
 # ----------------------------------------------------------------------------- tables
