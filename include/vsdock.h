@@ -110,6 +110,14 @@ typedef struct {
  * host copy that is uploaded into the workspace at submit. */
 vs_status vs_load_pocket(vs_ctx* ctx, const vs_pocket_desc* desc, const float* grid, int32_t on_device, int32_t* pocket_id);
 
+/* Method variant (reading Q24): a TYPED pocket of n_channels grids
+ * G_0 .. G_{T-1} of one geometry (desc), grids = [T][nz][ny][nx] fp32 (host, or device with
+ * on_device = 1), 1 <= T <= 8.  A typed submit (vs_submit_typed) scores atom i of type t_i on
+ * G_{t_i} (the out-of-box term is shared); a plain vs_submit docks on G_0.  Each channel is
+ * copied like vs_load_pocket's grid (T padded copies).  Errors: as vs_load_pocket. */
+vs_status vs_load_pocket_typed(vs_ctx* ctx, const vs_pocket_desc* desc, int32_t n_channels, const float* grids,
+                               int32_t on_device, int32_t* pocket_id);
+
 /* a6 initial poses (Q7): P rotations rot[P*9] (row-major R_p) and translations
  * trans[P*3] (tau_p), host memory, fp32.  1 <= P <= 1024. */
 vs_status vs_set_pose_table(vs_ctx* ctx, int32_t P, const float* rot, const float* trans);
@@ -177,6 +185,14 @@ typedef struct {
  * Errors: VS_E_PARSE (first invalid ligand), VS_E_OVERFLOW_*, VS_E_NOFIT,
  * VS_E_WORKSPACE, VS_E_STATE (tables/pockets/workspace missing), VS_E_CUDA. */
 vs_status vs_submit(vs_ctx* ctx, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets);
+/* Q24: vs_submit with per-atom types atom_type[atom_off[n] - atom_off[0]] (u8, the caller's atom
+ * order, the same memory kind as batch->on_device: host copied, device borrowed, or mapped pinned
+ * host read in place for the owned ligands only).  Every pocket docks in the TYPED layout (DESIGN.md
+ * 6: the channel windows of the QUAD layout in shared memory, the padded channels in global
+ * memory behind them).  A type >= the channels of any docked pocket is VS_E_PARSE naming the
+ * ligand (rank-local, like a1's per-atom checks). */
+vs_status vs_submit_typed(vs_ctx* ctx, const vs_ligand_batch* batch, const uint8_t* atom_type,
+                          const int32_t* pocket_ids, int32_t n_pockets);
 vs_status vs_wait(vs_ctx* ctx);
 
 /* a9 per-ligand results for pocket slot s (index into the submit's pocket_ids),
@@ -264,6 +280,10 @@ vs_status vs_query_classes(vs_ctx* ctx, int32_t max_classes, vs_class_info* out,
 /* Test hook: g(y) (a8) of pocket_id at n points xyz[3n] (Angstrom, host), into
  * g_out[n] (host), computed by the dock kernel's own device function. */
 vs_status vs_score_points(vs_ctx* ctx, int32_t pocket_id, int64_t n, const float* xyz, float* g_out);
+/* Test hook (Q24): g_{types[i]}(xyz[i]) of a typed pocket (types[n] host, each < its channels),
+ * by the TYPED layout's device function. */
+vs_status vs_score_points_typed(vs_ctx* ctx, int32_t pocket_id, int64_t n, const float* xyz, const uint8_t* types,
+                                float* g_out);
 
 typedef struct {
     int64_t n_ligands, n_owned;

@@ -11,7 +11,8 @@ Greedy trajectories fork after a near-tie, so angle indices are compared in two 
    oracle trajectory has no near-tie (all step margins and the best-pose margin above the
    band), the GPU's best pose and angle indices must be bit-identical.
 
-Bands and tolerances are arguments so tests state them explicitly.
+Bands and tolerances are arguments so tests state them explicitly.  A library carrying
+``atom_type`` is replayed on its typed pocket's channels (Q24).
 """
 from __future__ import annotations
 
@@ -68,6 +69,7 @@ def check(lib, idx, pocket, rot, trans, cs, gpu_score, gpu_pose, gpu_angles, gpu
         R = len(fr)
         f0 = int(lib.frag_off[i])
         a0 = int(lib.atom_off[i])
+        ty = None if getattr(lib, "atom_type", None) is None else lib.atom_type[a0:a0 + len(x)]   # Q24
         p = int(gpu_pose[i])
         if not (0 <= p < P):
             rep.failures.append((i, f"best pose {p} out of range"))
@@ -82,7 +84,7 @@ def check(lib, idx, pocket, rot, trans, cs, gpu_score, gpu_pose, gpu_angles, gpu
             if n_ref:
                 mseq = gpu_pose_refine[i, q] if gpu_pose_refine is not None else gpu_refine[i]
                 s, y, steps, rsc = oracle.replay_pose(pocket, x, fr, rot[q], trans[q], cs, kseq, S_w, refine=refine,
-                                                      mseq=mseq, want_refine=True)
+                                                      mseq=mseq, want_refine=True, types=ty)
                 for st, m in zip(rsc, mseq):
                     rep.n_steps += 1
                     mn = float(st.min())
@@ -93,7 +95,7 @@ def check(lib, idx, pocket, rot, trans, cs, gpu_score, gpu_pose, gpu_angles, gpu
                     elif int(m) != int(np.argmin(st)):
                         rep.near_ties += 1
             else:
-                s, y, steps = oracle.replay_pose(pocket, x, fr, rot[q], trans[q], cs, kseq, S_w)
+                s, y, steps = oracle.replay_pose(pocket, x, fr, rot[q], trans[q], cs, kseq, S_w, types=ty)
             rep_scores[q] = s
             for st, k in zip(steps, kseq):
                 rep.n_steps += 1

@@ -28,6 +28,7 @@ namespace {
 
 struct PocketHost {
     vs_pocket_desc d;
+    int nch = 1;               // grid channels (Q24): nch padded copies back to back
     std::vector<float> grid;
 };
 
@@ -138,6 +139,7 @@ struct vs_ctx {
     float* d_xyz = nullptr;
     int32_t *d_frag_axis = nullptr, *d_move_atoms = nullptr;
     const uint64_t* d_lid = nullptr;   // ligand ids of the batch (null: ids = indices)
+    const uint8_t* d_types = nullptr;  // atom types of a typed submit (Q24), input order; null: untyped
     uint8_t* d_order = nullptr;        // a1: internal atom -> input atom, CSR by atom_off
     int4* d_frint = nullptr;           // a1: fragments in internal numbering {a, b, lo, hi}
     uint8_t* d_fown = nullptr;         // a1: own-region length per fragment
@@ -224,7 +226,9 @@ vs_status ensure_pinned(vs_ctx* c, size_t bytes) {
     return VS_OK;
 }
 
-PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
+// typed = a typed submit (Q24): every pocket runs the TYPED layout with its nch channels (a pocket
+// of one channel included); an untyped submit docks on channel 0 with the usual layouts
+PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid, bool typed = false, int nch = 1) {
     PocketDev p;
     p.grid = dgrid;
     p.nx = d.nx;
@@ -232,8 +236,18 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.nz = d.nz;
     p.grs = d.nx + 1;
     p.gps = (d.nx + 1) * (d.ny + 1);
-    p.mode = grid_mode(d.nx, d.ny, d.nz, d.spacing);
-    grid_strides(p.mode, d.nx, d.ny, &p.rs, &p.ps);
+    p.gcs = p.gps * (d.nz + 1);
+    p.nch = typed ? nch : 1;
+    p.qcs = 0;
+    p.mode = typed ? kGridTyped : grid_mode(d.nx, d.ny, d.nz, d.spacing);
+    const int QW = typed ? typed_window(nch) : kQuadWC;   // QUAD / TYPED window edge (cells)
+    if (typed) {
+        p.rs = QW;
+        p.ps = typed_plane_stride(QW);
+        p.qcs = typed_chan_stride(QW);
+    } else {
+        grid_strides(p.mode, d.nx, d.ny, &p.rs, &p.ps);
+    }
     // WIN: the 32^3-node window around the docking centre (clamped into the grid); QUAD: the
     // window of kQuadWC cells [w0, w0 + kQuadWC) around it, clamped so that it covers as many of
     // the grid's cells 0 .. n-1 (the top face n-1 is a cell with weight-0 pad corners) as it can
@@ -241,9 +255,9 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     int w0[3] = {0, 0, 0};
     // (QUAD keeps its cells below the top face n-1, so the fast path's cells are interior)
     p.qwc = 0;
-    if (p.mode == kGridWin || p.mode == kGridQuad) {
-        const int W = p.mode == kGridWin ? kWin : kQuadWC;
-        p.qwc = kQuadWC;
+    if (p.mode == kGridWin || p.mode == kGridQuad || p.mode == kGridTyped) {
+        const int W = p.mode == kGridWin ? kWin : QW;
+        p.qwc = QW;
         for (int a = 0; a < 3; ++a) {
             const double uc = ((double)d.center[a] - d.origin[a]) / d.spacing;
             int v = (int)std::lround(uc) - W / 2;
@@ -261,7 +275,7 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     for (int a = 0; a < 3; ++a)
         Z[a] = p.mode == kGridFix    ? 16
                : p.mode == kGridRT   ? n3[a] / 2
-               : p.mode == kGridQuad ? w0[a] + kQuadWC / 2
+               : p.mode == kGridQuad || p.mode == kGridTyped ? w0[a] + QW / 2
                                      : w0[a] + kWin / 2;
     p.lo_x = (float)-Z[0];
     p.lo_y = (float)-Z[1];
@@ -272,7 +286,7 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
     p.mx = 8388608.f + (float)Z[0];
     p.my = 8388608.f + (float)Z[1];
     p.mz = 8388608.f + (float)Z[2];
-    if (p.mode == kGridQuad) {   // 1.5 * 2^23 + Z - w0: the floor's bits give the window-relative cell
+    if (p.mode == kGridQuad || p.mode == kGridTyped) {   // 1.5 * 2^23 + Z - w0: the floor's bits give the window-relative cell
         p.mx = 12582912.f + (float)(Z[0] - w0[0]);
         p.my = 12582912.f + (float)(Z[1] - w0[1]);
         p.mz = 12582912.f + (float)(Z[2] - w0[2]);
@@ -291,12 +305,12 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid) {
 
 // Shared memory of the score_points hook's grid region (floats).
 size_t score_grid_floats(const PocketDev& pk) {
-    return dock_grid_floats(pk.mode == kGridFix ? kGridRT : pk.mode, pk.nz, pk.rs, pk.ps);
+    return dock_grid_floats(pk.mode == kGridFix ? kGridRT : pk.mode, pk.nz, pk.rs, pk.ps, pk.nch);
 }
 
 // Stage-1 workspace (known from the batch sizes alone).
 struct Stage1 {
-    size_t atom_off, frag_off, xyz, lid, frag_axis, move_off, move_atoms, order, frint, fown, lflag, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
+    size_t atom_off, frag_off, xyz, types, lid, frag_axis, move_off, move_atoms, order, frint, fown, lflag, featA, featR, featM, cell, status, maxAR, hist, cell_count, perm, bstart,
         bsize, weights, own_start, own_prefix, own_ac, own_rec_off, pose, cs, reftab, grids, end;
     int n_blocks;
     int64_t max_buckets;
@@ -317,6 +331,7 @@ Stage1 plan1(int64_t n, int64_t nA, int64_t nR, int64_t nM, int P, int K, size_t
     s.atom_off = r.add((n + 1) * 8);
     s.frag_off = r.add((n + 1) * 8);
     s.xyz = r.add(nA * 12);
+    s.types = r.add(nA);   // atom types of a typed submit (Q24)
     s.lid = r.add(n * 8);
     s.frag_axis = r.add(nR * 8);
     s.move_off = r.add((nR + 1) * 8);
@@ -395,6 +410,7 @@ const char* vcode_msg(int code) {
         case 10: return "atom listed twice in one moving set";
         case 11: return "moving sets not laminar (two fragments' moving sets overlap without nesting)";
         case 12: return "coordinate magnitude above 1e6 A";
+        case 13: return "atom type >= the grid channels of a docked pocket";
         default: return "invalid record";
     }
 }
@@ -407,7 +423,7 @@ int pow2_ceil(int K) {
 
 // Per atom class: template capacity, warps, ligands per CTA, occupancy b, Eq. 1 -- for one
 // grid layout (mode, nz planes of ps floats, row stride rs).
-vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz, int rs, int ps, int RC,
+vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz, int rs, int ps, int nch, int RC,
                        std::vector<ClassInfo>& out) {
     out.clear();
     for (size_t i = 0; i < atom_b.size(); ++i) {
@@ -445,7 +461,7 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz
             else if (base == 1) lcs = {2, 1};
             for (int LC : lcs) {
                 const DockLayout L =
-                    dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, c->P, c->K, c->cfg.n_sweeps, LC, RC, c->n_ref);
+                    dock_layout(ci.AC, NW, PPW, gm, nz, rs, ps, nch, c->P, c->K, c->cfg.n_sweeps, LC, RC, c->n_ref);
                 int b = 0;
                 CK(dock_occupancy(ci.AC, NW, PPW, gm, c->K, L.total, &b));
                 if (b >= 1) {
@@ -611,8 +627,11 @@ vs_status vs_set_angle_table(vs_ctx* c, int32_t K, const float* cos_sin) {
     return VS_OK;
 }
 
-vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, int32_t on_device, int32_t* pocket_id) {
+namespace {
+vs_status load_pocket_impl(vs_ctx* c, const vs_pocket_desc* d, int nch, const float* grid, int32_t on_device,
+                           int32_t* pocket_id) {
     if (!c || !d || !grid) return VS_E_ARG;
+    if (nch < 1 || nch > kMaxChannels) return fail(c, VS_E_ARG, "n_channels must be in [1, %d]", kMaxChannels);
     if (c->pockets.size() >= 16) return fail(c, VS_E_ARG, "at most 16 pockets");
     if (d->nx < 2 || d->ny < 2 || d->nz < 2) return fail(c, VS_E_ARG, "pocket dims must be >= 2");
     if ((int64_t)d->nx * d->ny * d->nz > (1 << 22)) return fail(c, VS_E_ARG, "pocket grid too large");
@@ -624,26 +643,39 @@ vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, 
     if (!std::isfinite(d->out_slope) || d->out_slope < 0.f) return fail(c, VS_E_ARG, "out_slope must be finite and >= 0");
     PocketHost ph;
     ph.d = *d;
+    ph.nch = nch;
     const size_t cnt = (size_t)d->nx * d->ny * d->nz;
-    std::vector<float> raw(cnt);
+    std::vector<float> raw(cnt * nch);
     if (on_device) {
-        CK(cudaMemcpy(raw.data(), grid, cnt * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(raw.data(), grid, cnt * nch * 4, cudaMemcpyDeviceToHost));
     } else {
-        std::memcpy(raw.data(), grid, cnt * 4);
+        std::memcpy(raw.data(), grid, cnt * nch * 4);
     }
-    for (size_t i = 0; i < cnt; ++i)
+    for (size_t i = 0; i < cnt * nch; ++i)
         if (!std::isfinite(raw[i])) return fail(c, VS_E_ARG, "pocket grid value %zu is not finite", i);
     // the device copy is PADDED: [nz+1][ny+1][nx+1] with zero pads, so a weight-0 corner read at
-    // node n stays inside the array (PocketDev::grid)
-    const size_t gx = (size_t)d->nx + 1, gy = (size_t)d->ny + 1;
-    ph.grid.assign(gx * gy * ((size_t)d->nz + 1), 0.f);
-    for (int z = 0; z < d->nz; ++z)
-        for (int y = 0; y < d->ny; ++y)
-            std::memcpy(&ph.grid[((size_t)z * gy + y) * gx], &raw[((size_t)z * d->ny + y) * d->nx], (size_t)d->nx * 4);
+    // node n stays inside the array (PocketDev::grid); typed pockets: nch padded copies back to back
+    const size_t gx = (size_t)d->nx + 1, gy = (size_t)d->ny + 1, gc = gx * gy * ((size_t)d->nz + 1);
+    ph.grid.assign(gc * nch, 0.f);
+    for (int t = 0; t < nch; ++t)
+        for (int z = 0; z < d->nz; ++z)
+            for (int y = 0; y < d->ny; ++y)
+                std::memcpy(&ph.grid[t * gc + ((size_t)z * gy + y) * gx], &raw[t * cnt + ((size_t)z * d->ny + y) * d->nx],
+                            (size_t)d->nx * 4);
     c->pockets.push_back(std::move(ph));
     ++c->tables_version;
     if (pocket_id) *pocket_id = (int32_t)c->pockets.size() - 1;
     return VS_OK;
+}
+}  // namespace
+
+vs_status vs_load_pocket(vs_ctx* c, const vs_pocket_desc* d, const float* grid, int32_t on_device, int32_t* pocket_id) {
+    return load_pocket_impl(c, d, 1, grid, on_device, pocket_id);
+}
+
+vs_status vs_load_pocket_typed(vs_ctx* c, const vs_pocket_desc* d, int32_t n_channels, const float* grids,
+                               int32_t on_device, int32_t* pocket_id) {
+    return load_pocket_impl(c, d, n_channels, grids, on_device, pocket_id);
 }
 
 vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n_frags, int64_t n_moving,
@@ -659,7 +691,8 @@ vs_status vs_workspace_size(vs_ctx* c, int64_t n_lig, int64_t n_atoms, int64_t n
     // Q16 fallback boundary 32*n for the last class can exceed the observed maximum
     ac_max = std::min(kMaxAtoms, std::max(ac_max, std::min(kMaxAtoms, roundup32(max_atoms))));
     const Stage1 s1 = plan1(n_lig, n_atoms, n_frags, n_moving, c->P, c->K, max_grid_bytes(c), n_pockets);
-    const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * rec_floats_of(ac_max), c->P,
+    // records sized for a typed submit (the larger form, Q24)
+    const Stage2 s2 = plan2(s1.end, n_lig, n_atoms, n_frags, (int64_t)n_lig * rec_floats_typed(ac_max, true), c->P,
                             c->cfg.n_sweeps, n_pockets, c->cfg.debug_poses != 0, c->n_ref);
     *bytes = s2.end + 4096;
     return VS_OK;
@@ -677,8 +710,11 @@ vs_status vs_set_workspace(vs_ctx* c, void* ptr, size_t bytes) {
     return VS_OK;
 }
 
-vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets) {
+namespace {
+vs_status submit_impl(vs_ctx* c, const vs_ligand_batch* batch, const uint8_t* atom_type, const int32_t* pocket_ids,
+                      int32_t n_pockets) {
     if (!c || !batch) return VS_E_ARG;
+    const bool typed = atom_type != nullptr;
     c->submitted = false;
     c->stats = vs_stats{};   // every field of the last submit, written below
     if (c->P < 1 || c->K < 1) return fail(c, VS_E_STATE, "set the pose and angle tables first");
@@ -797,6 +833,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         c->d_move_off = rebase ? (int64_t*)(W + s1.move_off) : (int64_t*)batch->move_off;
         c->d_move_atoms = (int32_t*)batch->move_atoms;
         c->d_lid = batch->ligand_id;
+        c->d_types = atom_type;
     } else if (batch->on_device == 2) {
         // mapped pinned host memory: the offsets are copied (every rank plans the whole batch);
         // coordinates, axes, moving atoms and ids are read by the kernels over PCIe, only for
@@ -812,11 +849,13 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             *out = at.devicePointer;
             return VS_OK;
         };
-        const void *px = nullptr, *pa = nullptr, *pm = nullptr, *pl = nullptr;
+        const void *px = nullptr, *pa = nullptr, *pm = nullptr, *pl = nullptr, *pt = nullptr;
         vs_status mst;
         if ((mst = mapped(batch->xyz, &px)) || (mst = mapped(batch->frag_axis, &pa)) ||
-            (mst = mapped(batch->move_atoms, &pm)) || (mst = mapped(batch->ligand_id, &pl)))
+            (mst = mapped(batch->move_atoms, &pm)) || (mst = mapped(batch->ligand_id, &pl)) ||
+            (mst = mapped(atom_type, &pt)))
             return mst;
+        c->d_types = (const uint8_t*)pt;
         c->d_atom_off = (int64_t*)(W + s1.atom_off);
         c->d_frag_off = (int64_t*)(W + s1.frag_off);
         c->d_move_off = (int64_t*)(W + s1.move_off);
@@ -832,6 +871,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         c->d_move_off = (int64_t*)(W + s1.move_off);
         c->d_move_atoms = (int32_t*)(W + s1.move_atoms);
         c->d_lid = batch->ligand_id ? (const uint64_t*)(W + s1.lid) : nullptr;
+        c->d_types = typed ? (const uint8_t*)(W + s1.types) : nullptr;
     }
 
     CK(cudaEventRecord(c->ev_prep0, ms));
@@ -854,7 +894,12 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         }
     }
     c->pkdev.clear();
-    for (int i = 0; i < n_pockets; ++i) c->pkdev.push_back(make_pocket_dev(c->pockets[pocket_ids[i]].d, c->d_grid[i]));
+    int n_types = kMaxChannels;   // typed submit: the fewest channels among the docked pockets
+    for (int i = 0; i < n_pockets; ++i) {
+        const PocketHost& ph = c->pockets[pocket_ids[i]];
+        c->pkdev.push_back(make_pocket_dev(ph.d, c->d_grid[i], typed, ph.nch));
+        n_types = std::min(n_types, ph.nch);
+    }
     if (n == 0) {
         c->buckets.clear();
         c->owned.clear();
@@ -875,6 +920,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             CK(cudaMemcpyAsync(c->d_move_off, batch->move_off, (nR + 1) * 8, cudaMemcpyHostToDevice, ms));
         }
         if (nM) CK(cudaMemcpyAsync(c->d_move_atoms, batch->move_atoms, nM * 4, cudaMemcpyHostToDevice, ms));
+        if (typed && nA) CK(cudaMemcpyAsync((void*)c->d_types, atom_type, nA, cudaMemcpyHostToDevice, ms));
         if (batch->ligand_id)
             CK(cudaMemcpyAsync((void*)c->d_lid, batch->ligand_id, n * 8, cudaMemcpyHostToDevice, ms));
     }
@@ -934,15 +980,16 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         int big = 0;
         for (int q = 0; q < n_pockets; ++q) {
             const PocketDev& pk = c->pkdev[q];
-            const std::vector<int> key = {pk.mode, pk.nz, pk.rs, pk.ps};
+            const std::vector<int> key = {pk.mode, pk.nz, pk.rs, pk.ps, pk.nch};
             int li = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
             if (li == (int)keys.size()) {
                 keys.push_back(key);
                 c->layout_classes.emplace_back();
-                st = plan_classes(c, c->atom_b, pk.mode, pk.nz, pk.rs, pk.ps, c->frag_cap, c->layout_classes.back());
+                st = plan_classes(c, c->atom_b, pk.mode, pk.nz, pk.rs, pk.ps, pk.nch, c->frag_cap,
+                                  c->layout_classes.back());
                 if (st) return st;
-                if (dock_grid_floats(pk.mode, pk.nz, pk.rs, pk.ps) >
-                    dock_grid_floats(keys[big][0], keys[big][1], keys[big][2], keys[big][3]))
+                if (dock_grid_floats(pk.mode, pk.nz, pk.rs, pk.ps, pk.nch) >
+                    dock_grid_floats(keys[big][0], keys[big][1], keys[big][2], keys[big][3], keys[big][4]))
                     big = li;
             }
             c->pk_layout[q] = li;
@@ -1039,7 +1086,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         // what the kernels read in place for the owned ligands
         uint64_t oa = 0, of = 0, om = 0, on = 0;
         for (int b : mine) {
-            oa += bsum[4 * (size_t)b + 1];
+            oa += bsum[4 * (size_t)b + 1];   // owned atoms
             of += bsum[4 * (size_t)b + 2];
             om += bsum[4 * (size_t)b + 3];
             on += (uint64_t)c->buckets[b].size;
@@ -1047,8 +1094,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         const uint64_t offs = (uint64_t)(n + 1) * 16 + (uint64_t)(nR + 1) * 8;
         c->stats.h2d_bytes = batch->on_device == 1 ? 0
                              : batch->on_device == 2
-                                 ? offs + 12 * oa + 8 * of + 4 * om + (batch->ligand_id ? 8 * on : 0)
-                                 : offs + (uint64_t)nA * 12 + (uint64_t)nR * 8 + (uint64_t)nM * 4 +
+                                 ? offs + (typed ? 13 : 12) * oa + 8 * of + 4 * om + (batch->ligand_id ? 8 * on : 0)
+                                 : offs + (uint64_t)nA * (typed ? 13 : 12) + (uint64_t)nR * 8 + (uint64_t)nM * 4 +
                                        (batch->ligand_id ? (uint64_t)n * 8 : 0);
     }
     // fused mode: group the owned buckets by atom class (LPT order kept inside a class)
@@ -1067,7 +1114,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         const vs_bucket& b = c->buckets[c->owned[i]];
         c->owned_prefix[i + 1] = c->owned_prefix[i] + b.size;
         c->owned_rec_off[i] = rec_floats;
-        rec_floats += (int64_t)b.size * rec_floats_of(b.kernel_atoms);
+        rec_floats += (int64_t)b.size * rec_floats_typed(b.kernel_atoms, typed);
         evals += (double)b.weight;
     }
     c->total_slots = c->owned_prefix[no];
@@ -1122,7 +1169,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     }
     // ---- a1 ingest of this rank's ligands: per-atom validation, laminar check, canonical
     // renumbering (errors are rank-local: parallel.py carries them through the all-gather)
-    CK(launch_ingest(c->d_atom_off, c->d_xyz, c->d_frag_off, c->d_frag_axis, c->d_move_off, c->d_move_atoms, c->d_perm,
+    CK(launch_ingest(c->d_atom_off, c->d_xyz, c->d_types, n_types, c->d_frag_off, c->d_frag_axis, c->d_move_off, c->d_move_atoms, c->d_perm,
                      c->d_own_start, c->d_own_prefix, no, c->total_slots, c->d_order, c->d_frint, c->d_fown,
                      c->d_lflag, c->d_status + 2, ms));
     ++launches;
@@ -1137,7 +1184,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         }
     }
     CK(launch_pack(c->d_perm, c->d_own_start, c->d_own_prefix, c->d_own_ac, c->d_own_rec_off, no, c->total_slots,
-                   c->d_atom_off, c->d_xyz, c->d_order, c->d_frag_off, c->d_frint, c->d_fown, c->d_lflag, S_w,
+                   c->d_atom_off, c->d_xyz, c->d_types, c->d_order, c->d_frag_off, c->d_frint, c->d_fown, c->d_lflag, S_w,
                    c->d_rec, c->d_meta, ms));
     ++launches;
     for (int i = 0; i < n_pockets; ++i) {
@@ -1182,7 +1229,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         a.rec = c->d_rec + c->owned_rec_off[u.first];
         a.meta = c->d_meta + c->owned_prefix[u.first];
         a.n = u.slots;
-        a.rec_floats = rec_floats_of(b.kernel_atoms);
+        a.rec_floats = rec_floats_typed(b.kernel_atoms, typed);
         a.P = c->P;
         a.K = c->K;
         a.S_w = S_w;
@@ -1209,8 +1256,8 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
         if (fuse) {
             const ClassInfo& ci = c->layout_classes[c->pk_layout[0]][u.cls];
             const PocketDev& p0 = c->pkdev[0];
-            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, p0.mode, p0.nz, p0.rs, p0.ps, c->P, c->K, S_w,
-                                             ci.LC, c->frag_cap, c->n_ref);
+            const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, p0.mode, p0.nz, p0.rs, p0.ps, p0.nch, c->P,
+                                             c->K, S_w, ci.LC, c->frag_cap, c->n_ref);
             // cluster size g: the one that keeps the most SMs busy (clusters are placed whole
             // inside a GPC, so large clusters of 227 KB CTAs leave SMs idle); ties -> larger g
             int best_g = 1, best_sms = ci.b * c->sm_count, best_cl = 0;
@@ -1251,7 +1298,7 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
             site(a, 0, q);
             a.counter = d_counters + dock_launches;
             const DockLayout L = dock_layout(b.kernel_atoms, ci.NW, ci.PPW, a.pk[0].mode, a.pk[0].nz, a.pk[0].rs,
-                                             a.pk[0].ps, c->P, c->K, S_w, ci.LC, c->frag_cap, c->n_ref);
+                                             a.pk[0].ps, a.pk[0].nch, c->P, c->K, S_w, ci.LC, c->frag_cap, c->n_ref);
             const int rounds = (u.slots + ci.LC - 1) / ci.LC;
             const int grid = std::min(rounds, ci.b * c->sm_count);
             cudaStream_t s = c->workers[(dock_launches) % NS];
@@ -1275,6 +1322,18 @@ vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pock
     c->stats.evals_alg = evals * n_pockets;
     c->submitted = true;
     return VS_OK;
+}
+}  // namespace
+
+vs_status vs_submit(vs_ctx* c, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets) {
+    return submit_impl(c, batch, nullptr, pocket_ids, n_pockets);
+}
+
+vs_status vs_submit_typed(vs_ctx* c, const vs_ligand_batch* batch, const uint8_t* atom_type, const int32_t* pocket_ids,
+                          int32_t n_pockets) {
+    if (!atom_type && batch && batch->n > 0) return c ? fail(c, VS_E_ARG, "vs_submit_typed: null atom_type") : VS_E_ARG;
+    static const uint8_t none = 0;
+    return submit_impl(c, batch, atom_type ? atom_type : &none, pocket_ids, n_pockets);
 }
 
 vs_status vs_wait(vs_ctx* c) {
@@ -1483,33 +1542,53 @@ vs_status vs_query_classes(vs_ctx* c, int32_t max_classes, vs_class_info* out, i
     return VS_OK;
 }
 
-vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* xyz, float* g_out) {
+namespace {
+vs_status score_points_impl(vs_ctx* c, int32_t pocket_id, int64_t n, const float* xyz, const uint8_t* types,
+                            float* g_out) {
     if (!c || (n > 0 && (!xyz || !g_out))) return VS_E_ARG;
     if (pocket_id < 0 || pocket_id >= (int)c->pockets.size()) return fail(c, VS_E_ARG, "unknown pocket id");
     if (n == 0) return VS_OK;
+    if (types)
+        for (int64_t i = 0; i < n; ++i)
+            if (types[i] >= c->pockets[pocket_id].nch) return fail(c, VS_E_ARG, "point %lld: type >= channels", (long long)i);
     CK(cudaSetDevice(c->cfg.device));
     // test hook: temporary device buffers (not on the product path)
     const PocketHost& ph = c->pockets[pocket_id];
-    float *dg = nullptr, *dx = nullptr, *dout = nullptr;
+    float *dg = nullptr, *dx = nullptr, *dout = nullptr, *dt = nullptr;
     struct Free {   // released on every return path
-        float** p[3];
+        float** p[4];
         ~Free() {
             for (float** q : p)
                 if (*q) cudaFree(*q);
         }
-    } guard{{&dg, &dx, &dout}};
+    } guard{{&dg, &dx, &dout, &dt}};
     const size_t gb = ph.grid.size() * 4;
     CK(cudaMalloc(&dg, gb));
     CK(cudaMalloc(&dx, (size_t)n * 12));
     CK(cudaMalloc(&dout, (size_t)n * 4));
     CK(cudaMemcpy(dg, ph.grid.data(), gb, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dx, xyz, (size_t)n * 12, cudaMemcpyHostToDevice));
-    PocketDev pk = make_pocket_dev(ph.d, dg);
+    if (types) {
+        CK(cudaMalloc(&dt, (size_t)n));
+        CK(cudaMemcpy(dt, types, (size_t)n, cudaMemcpyHostToDevice));
+    }
+    PocketDev pk = make_pocket_dev(ph.d, dg, types != nullptr, ph.nch);
     const size_t smem = align16(score_grid_floats(pk) * 4);
-    CK(launch_score_points(pk, dx, n, dout, smem, c->main));
+    CK(launch_score_points(pk, dx, (const uint8_t*)dt, n, dout, smem, c->main));
     CK(cudaMemcpyAsync(g_out, dout, (size_t)n * 4, cudaMemcpyDeviceToHost, c->main));
     CK(cudaStreamSynchronize(c->main));
     return VS_OK;
+}
+}  // namespace
+
+vs_status vs_score_points(vs_ctx* c, int32_t pocket_id, int64_t n, const float* xyz, float* g_out) {
+    return score_points_impl(c, pocket_id, n, xyz, nullptr, g_out);
+}
+
+vs_status vs_score_points_typed(vs_ctx* c, int32_t pocket_id, int64_t n, const float* xyz, const uint8_t* types,
+                                float* g_out) {
+    if (n > 0 && !types) return c ? fail(c, VS_E_ARG, "vs_score_points_typed: null types") : VS_E_ARG;
+    return score_points_impl(c, pocket_id, n, xyz, types, g_out);
 }
 
 vs_status vs_plan_boundaries(int32_t n_atom_clusters, int32_t atom_ub, int32_t n_rot_clusters, int32_t rot_ub,

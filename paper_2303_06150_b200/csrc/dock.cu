@@ -51,6 +51,14 @@ int grid_mode(int nx, int ny, int nz, float spacing) {
     return rt <= (size_t)kWin * dk::kFixPS + 2048 ? kGridRT : kGridWin;
 }
 
+// TYPED (Q24): the largest window edge W <= kQuadWC whose nch channel windows fit the QUAD budget
+// (W = 20, 15, 13, 12, 11, 10, 10, 9 for 1..8 channels)
+int typed_window(int nch) {
+    int W = kQuadWC;
+    while (W > 2 && (size_t)nch * typed_chan_stride(W) > (size_t)kQuadPS * kQuadWC + 4) --W;
+    return W;
+}
+
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps) {
     if (mode == kGridQuad) {   // in quads (16 bytes)
         *rs = kQuadRS;
@@ -159,18 +167,20 @@ cudaError_t dock_cluster_occupancy(int AC, int NW, int PPW, int gmode, int K, si
     return cudaSuccess;
 }
 
-cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
-                                cudaStream_t st) {
-    const void* f = pk.mode == kGridFix    ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridFix>)
-                    : pk.mode == kGridRT   ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridRT>)
-                    : pk.mode == kGridQuad ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridQuad>)
-                                           : reinterpret_cast<const void*>(dk::score_points_kernel<kGridWin>);
+cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, const uint8_t* types, int64_t n, float* out,
+                                size_t smem, cudaStream_t st) {
+    const void* f = pk.mode == kGridFix     ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridFix>)
+                    : pk.mode == kGridRT    ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridRT>)
+                    : pk.mode == kGridQuad  ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridQuad>)
+                    : pk.mode == kGridTyped ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridTyped>)
+                                            : reinterpret_cast<const void*>(dk::score_points_kernel<kGridWin>);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (pk.mode == kGridFix) dk::score_points_kernel<kGridFix><<<148, 1024, smem, st>>>(pk, xyz, n, out);
-    else if (pk.mode == kGridRT) dk::score_points_kernel<kGridRT><<<148, 1024, smem, st>>>(pk, xyz, n, out);
-    else if (pk.mode == kGridQuad) dk::score_points_kernel<kGridQuad><<<148, 1024, smem, st>>>(pk, xyz, n, out);
-    else dk::score_points_kernel<kGridWin><<<148, 1024, smem, st>>>(pk, xyz, n, out);
+    if (pk.mode == kGridFix) dk::score_points_kernel<kGridFix><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
+    else if (pk.mode == kGridRT) dk::score_points_kernel<kGridRT><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
+    else if (pk.mode == kGridQuad) dk::score_points_kernel<kGridQuad><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
+    else if (pk.mode == kGridTyped) dk::score_points_kernel<kGridTyped><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
+    else dk::score_points_kernel<kGridWin><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
     return cudaGetLastError();
 }
 

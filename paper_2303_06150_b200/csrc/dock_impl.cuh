@@ -160,8 +160,8 @@ __device__ __forceinline__ GCell grid_cell(float ux, float uy, float uz, const P
         iz = pk.nz - 2;
         fz = 1.f;
     }
-    if (GM == kGridQuad) {
-        // QUAD: the floor constant is 1.5 * 2^23 + Z - w0 (PocketDev), so the bits give the
+    if (GM == kGridQuad || GM == kGridTyped) {
+        // QUAD / TYPED: the floor constant is 1.5 * 2^23 + Z - w0 (PocketDev), so the bits give the
         // WINDOW-relative cell directly (negative below the window)
         constexpr int d = kMagicBits - kQuadMagicBits;
         return GCell{ix + d, iy + d, iz + d, fxy, fz, e};
@@ -223,11 +223,42 @@ __device__ __forceinline__ float quad_fast_interior(const float* __restrict__ G,
     return lerp(l.x, l.y, c.fz);
 }
 
+// TYPED (Q24): the QUAD gathers on channel ch of the window (runtime strides rs = W, ps, qcs) or of
+// the padded global copy (channel stride gcs)
+__device__ __forceinline__ const float4* typed_quad(const float* __restrict__ G, const GCell& c, int ch,
+                                                    const PocketDev& pk) {
+    return reinterpret_cast<const float4*>(G) + c.ix + c.iy * pk.rs + c.iz * pk.ps + ch * pk.qcs;
+}
+__device__ __forceinline__ float typed_checked(const float* __restrict__ G, const GCell& c, int ch, const PocketDev& pk) {
+    if (__builtin_expect(__vimax3_u32((unsigned)c.ix, (unsigned)c.iy, (unsigned)c.iz) < (unsigned)pk.rs, 1)) {
+        const float4* q = typed_quad(G, c, ch, pk);
+        return quad_blend(q[0], q[pk.rs], c, pk.kh);
+    }
+    const int gr = pk.grs, gp = pk.gps;
+    const float* p = pk.grid + (size_t)ch * pk.gcs + (c.ix + pk.wx0) + (size_t)(c.iy + pk.wy0) * gr +
+                     (size_t)(c.iz + pk.wz0) * gp;
+    const float4 q0 = make_float4(__ldg(p), __ldg(p + gp), __ldg(p + 1), __ldg(p + gp + 1));
+    const float4 q1 = make_float4(__ldg(p + gr), __ldg(p + gp + gr), __ldg(p + gr + 1), __ldg(p + gp + gr + 1));
+    return quad_blend(q0, q1, c, pk.kh);
+}
+__device__ __forceinline__ float typed_fast_interior(const float* __restrict__ G, const GCell& c, int ch,
+                                                     const PocketDev& pk) {
+    const float4* q = typed_quad(G, c, ch, pk);
+    const float4 q0 = q[0], q1 = q[pk.rs];
+    const float2 l_0 = lerp2(make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), c.fxy.x);
+    const float2 l_1 = lerp2(make_float2(q1.x, q1.y), make_float2(q1.z, q1.w), c.fxy.x);
+    const float2 l = lerp2(l_0, l_1, c.fxy.y);
+    return lerp(l.x, l.y, c.fz);
+}
+
+// ch = the atom's grid channel (TYPED only; ignored by the other modes)
 template <int GM>
-__device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk) {
+__device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk,
+                                        int ch = 0) {
     const int RS = GM == kGridRT ? pk.rs : kFixRS, PS = GM == kGridRT ? pk.ps : kFixPS;
     const GCell cl = grid_cell<GM>(ux, uy, uz, pk);
     if (GM == kGridQuad) return quad_checked(G, cl, pk);
+    if (GM == kGridTyped) return typed_checked(G, cl, ch, pk);
     const int ix = cl.ix, iy = cl.iy, iz = cl.iz;
     const float2 fxy = cl.fxy;
     const float fz = cl.fz, e = cl.e;
@@ -298,16 +329,20 @@ __device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk, size_
     const int n4 = (int)(align16(zero_floats * 4) / 16);
     for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    if (pk.mode == kGridQuad) {
+    if (pk.mode == kGridQuad || pk.mode == kGridTyped) {
         // node (x, y, z) of the window <- (G[x,y,z], G[x,y,z+1], G[x+1,y,z], G[x+1,y,z+1]) from the
-        // padded global copy; nodes beyond the grid's pads stay zero (never read with weight > 0)
+        // padded global copy; nodes beyond the grid's pads stay zero (never read with weight > 0).
+        // TYPED: one window per channel, qcs quads apart
         float4* Q = reinterpret_cast<float4*>(sG);
-        const int NX = min(kQuadWC, pk.nx - pk.wx0), NY = min(kQuadWC + 1, pk.ny - pk.wy0),
-                  NZ = min(kQuadWC, pk.nz - pk.wz0);
-        for (int row = w; row < NY * NZ; row += nw) {
-            const int z = row / NY, y = row - z * NY;
-            const float* src = pk.grid + (size_t)(pk.wz0 + z) * pk.gps + (size_t)(pk.wy0 + y) * pk.grs + pk.wx0;
-            float4* dst = Q + z * kQuadPS + y * kQuadRS;
+        const bool typed = pk.mode == kGridTyped;
+        const int W = typed ? pk.rs : kQuadWC, RS = typed ? pk.rs : kQuadRS, PS = typed ? pk.ps : kQuadPS;
+        const int NX = min(W, pk.nx - pk.wx0), NY = min(W + 1, pk.ny - pk.wy0), NZ = min(W, pk.nz - pk.wz0);
+        for (int row = w; row < NY * NZ * pk.nch; row += nw) {
+            const int ch = row / (NY * NZ), zy = row - ch * (NY * NZ);
+            const int z = zy / NY, y = zy - z * NY;
+            const float* src = pk.grid + (size_t)ch * pk.gcs + (size_t)(pk.wz0 + z) * pk.gps +
+                               (size_t)(pk.wy0 + y) * pk.grs + pk.wx0;
+            float4* dst = Q + (size_t)ch * pk.qcs + z * PS + y * RS;
             for (int x = lane; x < NX; x += 32)
                 dst[x] = make_float4(src[x], src[x + pk.gps], src[x + 1], src[x + pk.gps + 1]);
         }
@@ -350,8 +385,23 @@ struct PoseBuf {
 // batch (one vote), so the common case is two LDS.128 per point with no per-point branch.
 template <int U, int GM>
 __device__ __forceinline__ void grid_batch(const float* __restrict__ G, const float4 (&v)[4], const PocketDev& pk,
-                                           float (&g)[U]) {
-    if (GM == kGridQuad) {
+                                           float (&g)[U], const int (&ch)[4]) {
+    if (GM == kGridTyped) {   // Q24: the QUAD vote on the channel windows
+        GCell cl[U];
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            cl[u] = quad_cell_fast(v[u].x, v[u].y, v[u].z, pk);
+            all = all && quad_in_fast(cl[u], pk.qwc);
+        }
+        if (__all_sync(FULL, all)) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = typed_fast_interior(G, cl[u], ch[u], pk);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, v[u].x, v[u].y, v[u].z, pk, ch[u]);
+        }
+    } else if (GM == kGridQuad) {
         GCell cl[U];
         bool all = true;
 #pragma unroll
@@ -375,20 +425,23 @@ __device__ __forceinline__ void grid_batch(const float* __restrict__ G, const fl
 // U independent sweep evaluations per lane: atoms j0, j0 + apw, ... (j < hi), rotated by M,
 // scored, summed into acc in ascending order; the atoms j < own_end (the step's finalised own
 // region) are also summed into own; the rotated atoms stay in kp[0..U).
+// ty = the record's atom types (TYPED, Q24; unused otherwise).
 template <int U, int GM, int AC>
 __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, const float* __restrict__ G,
-                                           const PocketDev& pk, int j0, int apw, int hi, int own_end, float& acc,
-                                           float& own, float4 (&kp)[4]) {
+                                           const PocketDev& pk, const uint8_t* __restrict__ ty, int j0, int apw,
+                                           int hi, int own_end, float& acc, float& own, float4 (&kp)[4]) {
     float4 v[U];
     float g[U];
+    int ch[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = j0 + u * apw;
         v[u] = B.get(j < hi ? j : j0);
+        if (GM == kGridTyped) ch[u] = ty[j < hi ? j : j0];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) kp[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
-    grid_batch<U, GM>(G, kp, pk, g);
+    grid_batch<U, GM>(G, kp, pk, g, ch);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = j0 + u * apw;
@@ -463,6 +516,7 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
     const uint32_t* rfr = reinterpret_cast<const uint32_t*>(rec + 3 * AC);
     const uint8_t* rown = reinterpret_cast<const uint8_t*>(rec + 3 * AC + 32);
     const uint32_t hdr = reinterpret_cast<const uint32_t*>(rec + 3 * AC + 40)[0];
+    const uint8_t* ty = reinterpret_cast<const uint8_t*>(rec + rec_floats_of(AC));   // TYPED records only (Q24)
     // finalised own regions: with ancestors swept before descendants, the atoms
     // whose innermost moving set is r (the first rown[r] atoms of r's range) never move after
     // step r of the last sweep, so the winner's partial sum over them is their final score;
@@ -501,11 +555,11 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 float4 kp[4];
                 int st = 0;
                 for (; st + 4 <= nst; st += 4)
-                    eval_batch<4, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp);
+                    eval_batch<4, GM>(B, M, G, pk, ty, lo + st * apw + jl, apw, hi, own_end, acc, own, kp);
                 switch (nst - st) {
-                    case 3: eval_batch<3, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
-                    case 2: eval_batch<2, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
-                    case 1: eval_batch<1, GM>(B, M, G, pk, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
+                    case 3: eval_batch<3, GM>(B, M, G, pk, ty, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
+                    case 2: eval_batch<2, GM>(B, M, G, pk, ty, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
+                    case 1: eval_batch<1, GM>(B, M, G, pk, ty, lo + st * apw + jl, apw, hi, own_end, acc, own, kp); break;
                     default: break;
                 }
                 // sum over the pass atoms (lanes of equal k: xor offsets K .. LPP/2, ascending)
@@ -577,11 +631,11 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
                 float acc = 0.f, own = 0.f;
                 float4 kp[4];
                 int st = 0;
-                for (; st + 4 <= nst; st += 4) eval_batch<4, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp);
+                for (; st + 4 <= nst; st += 4) eval_batch<4, GM>(B, M, G, pk, ty, st * apw + jl, apw, A, 0, acc, own, kp);
                 switch (nst - st) {
-                    case 3: eval_batch<3, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp); break;
-                    case 2: eval_batch<2, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp); break;
-                    case 1: eval_batch<1, GM>(B, M, G, pk, st * apw + jl, apw, A, 0, acc, own, kp); break;
+                    case 3: eval_batch<3, GM>(B, M, G, pk, ty, st * apw + jl, apw, A, 0, acc, own, kp); break;
+                    case 2: eval_batch<2, GM>(B, M, G, pk, ty, st * apw + jl, apw, A, 0, acc, own, kp); break;
+                    case 1: eval_batch<1, GM>(B, M, G, pk, ty, st * apw + jl, apw, A, 0, acc, own, kp); break;
                     default: break;
                 }
 #pragma unroll
@@ -620,14 +674,14 @@ __device__ __forceinline__ void dock_poses(const float* __restrict__ rec, int A,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {   // (lanes diverge on the last trip: no warp vote here)
             const float4 v = B.get(i + u * LPP);
-            g[u] = grid_g<GM>(G, v.x, v.y, v.z, pk);
+            g[u] = grid_g<GM>(G, v.x, v.y, v.z, pk, GM == kGridTyped ? ty[i + u * LPP] : 0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, g[u]);
     }
     for (; i < n_final; i += LPP) {
         const float4 v = B.get(i);
-        acc = __fadd_rn(acc, grid_g<GM>(G, v.x, v.y, v.z, pk));
+        acc = __fadd_rn(acc, grid_g<GM>(G, v.x, v.y, v.z, pk, GM == kGridTyped ? ty[i] : 0));
     }
 #pragma unroll
     for (int o = LPP / 2; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
@@ -950,7 +1004,8 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
     const PocketDev& pk = a.pk[site];
     const SiteOut& so = a.out[site];
     const int LC = a.ligs_per_cta;
-    const DockLayout L = dock_layout(AC, NW, PPW, GM, pk.nz, pk.rs, pk.ps, a.P, a.K, a.S_w, LC, a.frag_cap, a.n_ref);
+    const DockLayout L =
+        dock_layout(AC, NW, PPW, GM, pk.nz, pk.rs, pk.ps, pk.nch, a.P, a.K, a.S_w, LC, a.frag_cap, a.n_ref);
     float* sG = reinterpret_cast<float*>(smem + L.grid);
     float* sBuf = reinterpret_cast<float*>(smem + L.buf);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, h = lane / LPP;
@@ -1067,16 +1122,17 @@ __global__ void __launch_bounds__(NW * 32, 1) dock_kernel(const DockArgs a) {
 
 template <int GM>
 __global__ void __launch_bounds__(1024) score_points_kernel(const PocketDev pk, const float* __restrict__ xyz,
-                                                            int64_t n, float* __restrict__ out) {
+                                                            const uint8_t* __restrict__ types, int64_t n,
+                                                            float* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem[];
     float* sG = reinterpret_cast<float*>(smem);
-    stage_grid(sG, pk, dock_grid_floats(GM == kGridFix ? kGridRT : GM, pk.nz, pk.rs, pk.ps));
+    stage_grid(sG, pk, dock_grid_floats(GM == kGridFix ? kGridRT : GM, pk.nz, pk.rs, pk.ps, pk.nch));
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float ux = __fmul_rn(__fsub_rn(xyz[3 * i], pk.ox), pk.inv_h);
         const float uy = __fmul_rn(__fsub_rn(xyz[3 * i + 1], pk.oy), pk.inv_h);
         const float uz = __fmul_rn(__fsub_rn(xyz[3 * i + 2], pk.oz), pk.inv_h);
-        out[i] = grid_g<GM>(sG, ux, uy, uz, pk);
+        out[i] = grid_g<GM>(sG, ux, uy, uz, pk, types ? types[i] : 0);
     }
 }
 
@@ -1084,13 +1140,35 @@ using DockFn = void (*)(const DockArgs);
 
 template <int AC, int GM>
 DockFn pick_ac(int NW, int PPW, int K, bool ms) {
-    if (ms) {   // fused multi-site launches: the production lane map only (FIX grids, PPW 4, K 8)
-        if ((GM != kGridFix && GM != kGridQuad) || PPW != 4 || K != 8) return nullptr;
-        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, true>
-               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, true>
-               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, true>
-               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8, true>
-                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8, true> : nullptr);
+    if (ms) {   // fused multi-site launches: the production lane map only (FIX / QUAD grids, PPW 4, K 8)
+        if constexpr (GM == kGridFix || GM == kGridQuad) {
+            if (PPW != 4 || K != 8) return nullptr;
+            return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, true>
+                   : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, true>
+                   : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, true>
+                   : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8, true>
+                              : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8, true> : nullptr);
+        } else {
+            return nullptr;
+        }
+    }
+    if constexpr (GM == kGridTyped) {   // typed launches (Q24): the 4-poses-per-warp lane maps only
+        if (PPW != 4) return nullptr;
+        if (K == 8)
+            return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, false>
+                   : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, false>
+                   : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, false>
+                   : NW == 10 ? dock_kernel<AC, 10, 4, GM, 8, false>
+                              : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 8, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 8, false> : nullptr));
+        return NW == 16 ? dock_kernel<AC, 16, 4, GM, 0, false>
+               : NW == 13 ? dock_kernel<AC, 13, 4, GM, 0, false>
+               : NW == 12 ? dock_kernel<AC, 12, 4, GM, 0, false>
+               : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0, false>
+                          : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0, false> : nullptr));
+    }
+    if constexpr (GM == kGridQuad && AC <= 64) {   // more warps for the small classes (latency hiding)
+        if (PPW == 4 && K == 8 && (NW == 20 || NW == 24))
+            return NW == 20 ? dock_kernel<AC, 20, 4, GM, 8, false> : dock_kernel<AC, 24, 4, GM, 8, false>;
     }
     if (PPW == 4 && K == 8 && GM != kGridRT)   // production path: compile-time K = 8
         return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, false>

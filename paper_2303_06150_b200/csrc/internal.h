@@ -33,11 +33,21 @@ constexpr int kMaxSweeps = 4;
 //         wavefronts per evaluation.  Cells outside the window read the padded global copy
 //         (L1 / L2), as WIN does.  Chosen whenever the window covers +-9 A around the centre
 //         (h >= 0.9 A) or the whole grid (grid_mode, dock.cu).
-constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3;
+//  4 TYPED per-atom-type grid channels (Q24): the QUAD layout per
+//         channel, T windows of W^3 cells side by side (W the largest edge <= kQuadWC whose T windows
+//         fit the QUAD budget: W = 20, 15, 12, 9 for T = 1, 2, 4, 8), runtime strides, each atom
+//         gathering from its own channel; cells outside the window read the padded global copy of
+//         that channel.
+constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3, kGridTyped = 4;
+constexpr int kMaxChannels = 8;   // grid channels of a typed pocket (atom types 0..7)
 constexpr int kWin = 32;   // window edge (nodes)
 constexpr int kQuadWC = 20;                  // QUAD window edge (cells per axis)
 constexpr int kQuadRS = kQuadWC;             // quads per row (x), rows per plane: kQuadWC + 1 (y + 1)
 constexpr int kQuadPS = kQuadRS * (kQuadWC + 1) + 3;   // quads per plane (423 = 3 mod 8: bank model)
+// TYPED window of W cells: plane stride W (W + 1) + 3 quads (kQuadPS's padding), channel stride
+// W planes + 4 quads
+__host__ __device__ inline int typed_plane_stride(int W) { return W * (W + 1) + 3; }
+__host__ __device__ inline int typed_chan_stride(int W) { return typed_plane_stride(W) * W + 4; }
 
 // Pocket as the dock kernel sees it.  Coordinates are kept in CENTRED grid units
 // v = (y - o)/h - Z with an integer shift Z per axis (16 for FIX, floor(n/2) for RT, the
@@ -49,9 +59,12 @@ struct PocketDev {
     int nx, ny, nz;
     int rs, ps;            // shared-memory row stride and plane stride (floats)
     int grs, gps;          // global padded row / plane stride (floats)
-    int mode;              // kGridFix / kGridRT / kGridWin
-    int wx0, wy0, wz0;     // WIN / QUAD: window origin (grid nodes)
-    int qwc;               // QUAD: fast cells [0, qwc) of the window, all interior (<= n-2) on every axis
+    int mode;              // kGridFix / kGridRT / kGridWin / kGridQuad / kGridTyped
+    int wx0, wy0, wz0;     // WIN / QUAD / TYPED: window origin (grid nodes)
+    int qwc;               // QUAD / TYPED: fast cells [0, qwc) of the window, all interior (<= n-2) on every axis
+    int nch;               // grid channels staged (TYPED: T; else 1)
+    int qcs;               // TYPED: shared-memory channel stride (quads); rs = W, ps = typed_plane_stride(W)
+    int gcs;               // global channel stride of the padded copy (floats)
     float lo_x, lo_y, lo_z;       // -Z          (u = 0)
     float top_x, top_y, top_z;    // n - 1 - Z   (u = n - 1)
     float mx, my, mz;             // 2^23 + Z    (exact)
@@ -101,8 +114,10 @@ struct DockArgs {
 
 // Packed ligand record of atom class AC (floats): x | y | z (3 AC), fragment table u32[32],
 // own-region lengths u8[32] (8 words), header (n_root | ancestors-first << 16) + 3 pad words;
-// a multiple of 4 floats (16-byte TMA granularity).
+// a multiple of 4 floats (16-byte TMA granularity).  Typed launches (Q24) append the atom types
+// u8[AC] (AC / 4 words).
 __host__ __device__ constexpr int rec_floats_of(int AC) { return 3 * AC + 44; }
+__host__ __device__ constexpr int rec_floats_typed(int AC, bool typed) { return rec_floats_of(AC) + (typed ? AC / 4 : 0); }
 
 // Per-pose coordinate buffer stride (floats): 3 AC + 8, i.e. 8 banks apart, so the 4 pose
 // groups of a warp write 8-atom blocks of (x, y) pairs in 2 wavefronts and of z in 1 (the
@@ -133,22 +148,24 @@ constexpr int kMaxRefineRounds = 8;
 // planes is the y overflow of row ny in the last plane (<= 34 rs - ps = 25 floats).  RT keeps
 // a zero plane + row.  WIN: the 32 window planes; the shared-memory path never reads past
 // local node 31 on any axis.
-__host__ __device__ inline size_t dock_grid_floats(int mode, int nz, int rs, int ps) {
-    return mode == kGridFix   ? (size_t)nz * ps + 32
-           : mode == kGridWin ? (size_t)kWin * ps
-           : mode == kGridQuad ? (size_t)4 * kQuadPS * kQuadWC
-                              : (size_t)(nz + 1) * ps + rs + 2;
+// TYPED: nch channels of typed_chan_stride(rs) quads (rs = W).
+__host__ __device__ inline size_t dock_grid_floats(int mode, int nz, int rs, int ps, int nch = 1) {
+    return mode == kGridFix    ? (size_t)nz * ps + 32
+           : mode == kGridWin   ? (size_t)kWin * ps
+           : mode == kGridQuad  ? (size_t)4 * kQuadPS * kQuadWC
+           : mode == kGridTyped ? (size_t)4 * typed_chan_stride(rs) * nch
+                                : (size_t)(nz + 1) * ps + rs + 2;
 }
-__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int mode, int nz, int rs, int ps, int P,
-                                                  int K, int S_w, int LC, int RC, int n_ref) {
+__host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int mode, int nz, int rs, int ps, int nch,
+                                                  int P, int K, int S_w, int LC, int RC, int n_ref) {
     DockLayout L;
     size_t o = 0;
-    L.grid = o;  o += align16(dock_grid_floats(mode, nz, rs, ps) * 4);
+    L.grid = o;  o += align16(dock_grid_floats(mode, nz, rs, ps, nch) * 4);
     L.buf = o;   o += (size_t)NW * PPW * pose_stride_of(AC, NW, PPW) * 4;   // (x,y)|z per pose
     L.pose = o;   // pose table: read per warp item from global (L1-resident), no shared copy
     L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
     size_t q = 0;
-    L.rec_o = q;   q += align16((size_t)LC * rec_floats_of(AC) * 4);
+    L.rec_o = q;   q += align16((size_t)LC * rec_floats_typed(AC, mode == kGridTyped) * 4);
     L.meta_o = q;  q += (size_t)LC * 16;
     L.score_o = q; q += align16((size_t)LC * P * 4);
     L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC, n_ref));
@@ -167,6 +184,8 @@ __host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
 }
 // Grid mode and shared-memory strides (row rs, plane ps) of an nx x ny x nz grid.
 int grid_mode(int nx, int ny, int nz, float spacing);
+// TYPED window edge (cells) for nch channels
+int typed_window(int nch);
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).
@@ -174,7 +193,8 @@ cudaError_t launch_rebase(const int64_t* src, int64_t* dst, int64_t count, int64
 cudaError_t launch_features(const int64_t* atom_off, const int64_t* frag_off, const int64_t* move_off, int64_t n,
                             int* featA, int* featR, int* featM, unsigned long long* status, int* maxAR, cudaStream_t st);
 // a1 ingest of the owned (packed) slots: validation, laminar check, canonical renumbering.
-cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
+cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const uint8_t* atom_type, int n_types,
+                          const int64_t* frag_off, const int32_t* frag_axis,
                           const int64_t* move_off, const int32_t* move_atoms, const uint32_t* perm,
                           const int64_t* owned_start, const int* owned_prefix, int n_owned, int total_slots,
                           uint8_t* order, int4* frint, uint8_t* fown, int* lflag, unsigned long long* status,
@@ -193,16 +213,17 @@ cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const 
 // Pack owned buckets.  slot_bucket_prefix[b] = first packed slot of owned bucket b (nb+1 entries).
 cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
-                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint,
-                        const uint8_t* fown, const int* lflag, int S_w, float* rec, int4* meta, cudaStream_t st);
+                        const float* xyz, const uint8_t* atom_type, const uint8_t* order, const int64_t* frag_off,
+                        const int4* frint, const uint8_t* fown, const int* lflag, int S_w, float* rec, int4* meta,
+                        cudaStream_t st);
 cudaError_t launch_dock(int AC, int NW, int PPW, const DockArgs& a, int grid, size_t smem, cudaStream_t st);
 cudaError_t dock_kernel_attrs(int AC, int NW, int PPW, int gmode, int K, cudaFuncAttributes* attr);
 cudaError_t dock_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int* blocks_per_sm);
 cudaError_t dock_cluster_occupancy(int AC, int NW, int PPW, int gmode, int K, size_t smem, int sites, int* clusters);
 cudaError_t launch_fill_results(float* best_score, int* best_pose, int64_t n, uint8_t* angles, int64_t n_ang,
                                 cudaStream_t st);
-cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, int64_t n, float* out, size_t smem,
-                                cudaStream_t st);
+cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, const uint8_t* types, int64_t n, float* out,
+                                size_t smem, cudaStream_t st);
 // top-k
 cudaError_t launch_make_keys(const int4* meta, int n_slots, const float* best_score, unsigned long long* keys,
                              cudaStream_t st, uint32_t index_offset = 0);

@@ -54,6 +54,7 @@ __device__ __forceinline__ int warp_sum_int(int v) {
 //  10 atom listed twice in one moving set
 //  7 axis atom inside its own moving set
 //  11 moving sets not laminar (two sets overlap without one containing the other)
+//  13 atom type >= the grid channels of a docked pocket (typed submits, Q24)
 // a1 (all ligands): features from the CSR offsets alone -- A, R, sum |M_r| -- and the two
 // range checks every rank must agree on before the plan (codes 1, 2 below).  The per-atom
 // checks and the renumbering (ingest_kernel) run only on the ligands this rank docks.
@@ -157,7 +158,8 @@ __device__ __forceinline__ int first_code(int code) {   // lowest lane's non-zer
 }
 
 __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
-    const int64_t* __restrict__ atom_off, const float* __restrict__ xyz, const int64_t* __restrict__ frag_off,
+    const int64_t* __restrict__ atom_off, const float* __restrict__ xyz, const uint8_t* __restrict__ atom_type,
+    int n_types, const int64_t* __restrict__ frag_off,
     const int32_t* __restrict__ frag_axis, const int64_t* __restrict__ move_off, const int32_t* __restrict__ move_atoms,
     const uint32_t* __restrict__ perm, const int64_t* __restrict__ owned_start, const int* __restrict__ owned_prefix,
     int n_owned, int total_slots, uint8_t* __restrict__ order, int4* __restrict__ frint, uint8_t* __restrict__ fown,
@@ -185,6 +187,11 @@ __global__ void __launch_bounds__(kIngestWarps * 32) ingest_kernel(
             }
             if (__any_sync(FULL, nf)) code = 3;
             else if (__any_sync(FULL, big)) code = 12;
+        }
+        if (code == 0 && atom_type) {   // Q24: every atom type names a channel of every docked pocket
+            bool bad = false;
+            for (int t = lane; t < A; t += 32) bad |= atom_type[a0 + t] >= n_types;
+            if (__any_sync(FULL, bad)) code = 13;
         }
         int fa = 0, fb = 0;
         int64_t m0 = 0;
@@ -570,6 +577,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
                                                    const int64_t* __restrict__ owned_rec_off, int n_owned,
                                                    int total_slots, const int64_t* __restrict__ atom_off,
                                                    const float* __restrict__ xyz,
+                                                   const uint8_t* __restrict__ atom_type,
                                                    const uint8_t* __restrict__ order,
                                                    const int64_t* __restrict__ frag_off,
                                                    const int4* __restrict__ frint,
@@ -583,7 +591,7 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     const uint32_t li = slot_ligand(slot, perm, owned_start, owned_prefix, n_owned, &b);
     const int s = slot - owned_prefix[b];
     const int AC = owned_ac[b];
-    float* r = rec + owned_rec_off[b] + (int64_t)s * rec_floats_of(AC);
+    float* r = rec + owned_rec_off[b] + (int64_t)s * rec_floats_typed(AC, atom_type != nullptr);
     const int64_t a0 = atom_off[li];
     const int A = (int)(atom_off[li + 1] - a0);
     const int64_t f0 = frag_off[li];
@@ -633,6 +641,10 @@ __global__ void __launch_bounds__(256) pack_kernel(const uint32_t* __restrict__ 
     uint8_t* ob = reinterpret_cast<uint8_t*>(r + 3 * AC + 32);
     ob[lane] = own;
     if (lane < 4) reinterpret_cast<uint32_t*>(r + 3 * AC + 40)[lane] = lane == 0 ? (uint32_t)lflag[li] : 0u;
+    if (atom_type) {   // typed record (Q24): the types in the canonical (internal) atom order, pads 0
+        uint8_t* tb = reinterpret_cast<uint8_t*>(r + rec_floats_of(AC));
+        for (int i = lane; i < AC; i += 32) tb[i] = i < A ? atom_type[a0 + ord[i]] : (uint8_t)0;
+    }
     if (lane == 0) meta[slot] = make_int4((int)li, A, R, (int)(S_w * f0));
 }
 
@@ -682,7 +694,8 @@ cudaError_t launch_features(const int64_t* atom_off, const int64_t* frag_off, co
     return cudaGetLastError();
 }
 
-cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64_t* frag_off, const int32_t* frag_axis,
+cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const uint8_t* atom_type, int n_types,
+                          const int64_t* frag_off, const int32_t* frag_axis,
                           const int64_t* move_off, const int32_t* move_atoms, const uint32_t* perm,
                           const int64_t* owned_start, const int* owned_prefix, int n_owned, int total_slots,
                           uint8_t* order, int4* frint, uint8_t* fown, int* lflag, unsigned long long* status,
@@ -690,7 +703,7 @@ cudaError_t launch_ingest(const int64_t* atom_off, const float* xyz, const int64
     if (total_slots <= 0) return cudaSuccess;
     int blocks = (total_slots + kIngestWarps - 1) / kIngestWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    ingest_kernel<<<blocks, kIngestWarps * 32, 0, st>>>(atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, perm,
+    ingest_kernel<<<blocks, kIngestWarps * 32, 0, st>>>(atom_off, xyz, atom_type, n_types, frag_off, frag_axis, move_off, move_atoms, perm,
                                                         owned_start, owned_prefix, n_owned, total_slots, order, frint,
                                                         fown, lflag, status);
     return cudaGetLastError();
@@ -738,11 +751,13 @@ cudaError_t launch_bucket_weights(const uint32_t* perm, const int* featA, const 
 
 cudaError_t launch_pack(const uint32_t* perm, const int64_t* owned_start, const int* owned_prefix, const int* owned_ac,
                         const int64_t* owned_rec_off, int n_owned_buckets, int total_slots, const int64_t* atom_off,
-                        const float* xyz, const uint8_t* order, const int64_t* frag_off, const int4* frint,
-                        const uint8_t* fown, const int* lflag, int S_w, float* rec, int4* meta, cudaStream_t st) {
+                        const float* xyz, const uint8_t* atom_type, const uint8_t* order, const int64_t* frag_off,
+                        const int4* frint, const uint8_t* fown, const int* lflag, int S_w, float* rec, int4* meta,
+                        cudaStream_t st) {
     if (total_slots <= 0) return cudaSuccess;
     pack_kernel<<<(total_slots + 7) / 8, 256, 0, st>>>(perm, owned_start, owned_prefix, owned_ac, owned_rec_off,
-                                                       n_owned_buckets, total_slots, atom_off, xyz, order, frag_off,
+                                                       n_owned_buckets, total_slots, atom_off, xyz, atom_type, order,
+                                                       frag_off,
                                                        frint, fown, lflag, S_w, rec, meta);
     return cudaGetLastError();
 }

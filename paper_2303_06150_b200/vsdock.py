@@ -26,7 +26,7 @@ SYMBOLS = ["vs_create", "vs_destroy", "vs_last_error", "vs_workspace_size", "vs_
            "vs_set_pose_table", "vs_set_angle_table", "vs_submit", "vs_wait", "vs_get_results", "vs_get_coords",
            "vs_get_pose_debug", "vs_local_topk", "vs_keys", "vs_select_keys", "vs_merge_topk", "vs_get_manifest", "vs_query_classes",
            "vs_score_points", "vs_get_stats", "vs_plan_boundaries", "vs_plan_lpt", "vs_set_refine_table", "vs_get_refine",
-           "vs_get_pose_refine_debug"]
+           "vs_get_pose_refine_debug", "vs_load_pocket_typed", "vs_submit_typed", "vs_score_points_typed"]
 
 
 class VsError(RuntimeError):
@@ -121,6 +121,9 @@ def load_library():
         "vs_get_stats": [P, ctypes.POINTER(vs_stats)],
         "vs_plan_boundaries": [I32, I32, I32, I32, P, ctypes.POINTER(I32), P, ctypes.POINTER(I32)],
         "vs_plan_lpt": [P, I32, I32, P, P],
+        "vs_load_pocket_typed": [P, ctypes.POINTER(vs_pocket_desc), I32, P, I32, ctypes.POINTER(I32)],
+        "vs_submit_typed": [P, ctypes.POINTER(vs_ligand_batch), P, P, I32],
+        "vs_score_points_typed": [P, I32, I64, P, P, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -261,12 +264,16 @@ class Engine:
         return out[: self._n, :, : self.n_ref]
 
     def load_pocket(self, pocket) -> int:
+        """Load a pocket grid [nz, ny, nx], or a typed pocket [T, nz, ny, nx] (Q24: vs_load_pocket_typed)."""
         g = np.ascontiguousarray(pocket.grid, np.float32)
-        nz, ny, nx = g.shape
+        nz, ny, nx = g.shape[-3:]
         d = vs_pocket_desc(nx, ny, nz, (ctypes.c_float * 3)(*pocket.origin), pocket.spacing,
                            (ctypes.c_float * 3)(*pocket.center), pocket.out_slope)
         pid = ctypes.c_int32()
-        self._check(self.lib.vs_load_pocket(self.h, ctypes.byref(d), _ptr(g), 0, ctypes.byref(pid)))
+        if g.ndim == 4:
+            self._check(self.lib.vs_load_pocket_typed(self.h, ctypes.byref(d), g.shape[0], _ptr(g), 0, ctypes.byref(pid)))
+        else:
+            self._check(self.lib.vs_load_pocket(self.h, ctypes.byref(d), _ptr(g), 0, ctypes.byref(pid)))
         return pid.value
 
     # ---- workspace
@@ -286,10 +293,11 @@ class Engine:
 
     # ---- the hot path
     def submit(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, pockets, on_device=None,
-               max_atoms=None):
+               max_atoms=None, atom_type=None):
         """Submit a CSR ligand batch in the general form of include/vsdock.h (numpy host arrays,
         pinned torch CPU tensors, or CUDA tensors; ``ligand_id`` may be None).  on_device: 0 host
-        (copied), 1 device, 2 pinned host read in place by the kernels (owned ligands only)."""
+        (copied), 1 device, 2 pinned host read in place by the kernels (owned ligands only).
+        ``atom_type`` (uint8 per atom, same memory kind): a typed submit (vs_submit_typed, Q24)."""
         n = int(atom_off.shape[0]) - 1
         if on_device is None:
             on_device = hasattr(xyz, "is_cuda") and xyz.is_cuda
@@ -306,12 +314,23 @@ class Engine:
         self.reserve(n, nA, nR, nM, max(1, min(256, max_atoms)), len(pockets))
         b = vs_ligand_batch(n, _ptr(ligand_id), _ptr(atom_off), _ptr(xyz), _ptr(frag_off), _ptr(frag_axis),
                             _ptr(move_off), _ptr(move_atoms), on_device)
-        self._batch_keep = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
-        self._check(self.lib.vs_submit(self.h, ctypes.byref(b), _ptr(pockets), len(pockets)))
+        self._batch_keep = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, atom_type)
+        if atom_type is not None:
+            if hasattr(atom_type, "data_ptr"):
+                assert str(atom_type.dtype) == "torch.uint8", "atom_type must be uint8"
+            else:
+                atom_type = np.ascontiguousarray(atom_type, np.uint8)
+                self._batch_keep = self._batch_keep[:-1] + (atom_type,)
+            self._check(self.lib.vs_submit_typed(self.h, ctypes.byref(b), _ptr(atom_type), _ptr(pockets), len(pockets)))
+        else:
+            self._check(self.lib.vs_submit(self.h, ctypes.byref(b), _ptr(pockets), len(pockets)))
         self._n, self._nA, self._nR = n, nA, nR
         self._npk = len(pockets)
 
     def submit_library(self, lib, pockets, **kw):
+        """Submit a vsgen.Library-like batch; its ``atom_type`` (if any) makes the submit typed (Q24)."""
+        if kw.get("atom_type") is None and getattr(lib, "atom_type", None) is not None:
+            kw["atom_type"] = lib.atom_type
         return self.submit(*lib.arrays(), pockets, **kw)
 
     def wait(self):
@@ -414,8 +433,14 @@ class Engine:
         self._check(self.lib.vs_get_stats(self.h, ctypes.byref(s)))
         return {f[0]: getattr(s, f[0]) for f in vs_stats._fields_}
 
-    def score_points(self, pocket_id, pts):
+    def score_points(self, pocket_id, pts, types=None):
+        """g at points (Angstrom) by the dock kernel's device function; ``types`` (Q24): the channel
+        of every point of a typed pocket (the TYPED layout's path)."""
         pts = np.ascontiguousarray(pts, np.float32).reshape(-1, 3)
         out = np.empty(pts.shape[0], np.float32)
-        self._check(self.lib.vs_score_points(self.h, pocket_id, pts.shape[0], _ptr(pts), _ptr(out)))
+        if types is not None:
+            t = np.ascontiguousarray(types, np.uint8).reshape(-1)
+            self._check(self.lib.vs_score_points_typed(self.h, pocket_id, pts.shape[0], _ptr(pts), _ptr(t), _ptr(out)))
+        else:
+            self._check(self.lib.vs_score_points(self.h, pocket_id, pts.shape[0], _ptr(pts), _ptr(out)))
         return out

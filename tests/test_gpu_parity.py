@@ -878,3 +878,112 @@ def test_refine_table_validation():
     with pytest.raises(VsError, match="non-finite"):
         e.set_refine(1, q, bad)
     e.set_refine(0)
+
+
+# ----------------------------------------------------------------------------- per-atom-type grid channels
+# (Q24): TYPED layout -- one QUAD window per channel in shared memory,
+# the padded channels in global memory behind them
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8])
+def test_typed_score_hook_vs_oracle(T):
+    """g_{t}(y) on every channel: inside the channel windows, outside them (global path) and outside
+    the grid, against the fp64 oracle; node exactness per channel."""
+    pk = vsgen.typed_pocket(101, n_types=min(T, 4))
+    if T > 4:   # 8 channels: the 4 typed ones and 4 scaled copies
+        pk = vsgen.Pocket(np.concatenate([pk.grid, 0.5 * pk.grid]), pk.origin, pk.spacing, pk.center, pk.out_slope)
+    e = engine()
+    pid = e.load_pocket(pk)
+    rng = np.random.default_rng(T)
+    pts = np.concatenate([rng.uniform(-5, 36, size=(30000, 3)),
+                          np.array(pk.center) + rng.normal(0, 5.0, size=(30000, 3))]).astype(np.float32)
+    t = rng.integers(0, T, size=len(pts)).astype(np.uint8)
+    g = e.score_points(pid, pts, types=t)
+    ref = oracle.grid_score(pk, pts.astype(np.float64), t)
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < 2e-6
+    nodes = rng.integers(0, 32, size=(4000, 3)).astype(np.float32)
+    tn = rng.integers(0, T, size=4000).astype(np.uint8)
+    g = e.score_points(pid, nodes, types=tn)
+    G = pk.grid if pk.grid.ndim == 4 else pk.grid[None]
+    assert np.array_equal(g, G[tn, nodes[:, 2].astype(int), nodes[:, 1].astype(int), nodes[:, 0].astype(int)])
+
+
+def _typed_lib(lib, T, seed=11):
+    lib.atom_type = vsgen.atom_types(lib, seed, n_types=min(T, 4))
+    return lib
+
+
+def test_typed_c1_full_parity_every_pose():
+    c = vsgen.CONFIGS["C1"]
+    lib = _typed_lib(vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"]), 4)
+    pk = vsgen.typed_pocket(101, n_types=4)
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
+    rep, r = check(e, lib, range(lib.n), pk, rot, tr, cs)
+    assert rep.independent_checked >= lib.n // 2 and rep.independent_equal == rep.independent_checked
+
+
+def test_typed_c2_sample_parity_and_layout_invariance(c2):
+    """C2 with 4 atom types: 300 ligands replayed (every pose), the independent oracle run
+    bit-identical outside near-ties; the same bits from the unsorted grid, a per-bucket launch and
+    a 3-stream submit; atom-permuted copies dock bit-identically (types follow their atoms)."""
+    c, lib0, _ = c2
+    lib = _typed_lib(lib0.subset(np.arange(lib0.n)), 4)
+    pk = vsgen.typed_pocket(101, n_types=4)
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
+    idx = np.random.default_rng(5).choice(lib.n, 300, replace=False)
+    rep, r = check(e, lib, idx, pk, rot, tr, cs)
+    assert rep.independent_equal == rep.independent_checked > 100
+    for kw in (dict(atom_clusters=1, rot_clusters=1), dict(launch_per_bucket=True, bucket_multiple=1),
+               dict(n_streams=3)):
+        e2, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False, **kw)
+        r2 = e2.results(0)
+        assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.angles, r2.angles)
+    sub = lib.subset(np.arange(200))
+    lp, perm = sub.permuted(9)
+    e3, *_ = run(sub, [pk], P=c["P"], K=c["K"], debug=False)
+    e4, *_ = run(lp, [pk], P=c["P"], K=c["K"], debug=False)
+    assert np.array_equal(e3.results(0).best_score, e4.results(0).best_score)
+    assert np.array_equal(e4.coords(0)[perm], e3.coords(0))
+
+
+def test_typed_copies_bit_identical_to_untyped(c2):
+    """T identical channels and random types: the TYPED layout gives the untyped QUAD bits (the same
+    blend on the same values); a typed pocket submitted untyped docks on channel 0."""
+    c, lib0, pk = c2
+    lib = lib0.subset(np.arange(2000))
+    e, *_ = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    r = e.results(0)
+    pk3 = vsgen.Pocket(np.stack([pk.grid] * 3), pk.origin, pk.spacing, pk.center, pk.out_slope)
+    lt = _typed_lib(lib.subset(np.arange(lib.n)), 3)
+    e2, *_ = run(lt, [pk3], P=c["P"], K=c["K"], debug=False)
+    r2 = e2.results(0)
+    assert np.array_equal(r.best_score, r2.best_score) and np.array_equal(r.angles, r2.angles)
+    assert np.array_equal(e.coords(0), e2.coords(0))
+    e3, *_ = run(lib, [pk3], P=c["P"], K=c["K"], debug=False)          # untyped submit: channel 0
+    assert np.array_equal(r.best_score, e3.results(0).best_score)
+
+
+def test_typed_refinement_two_pockets_and_type_errors():
+    """Typed docking with rigid refinement (Q23) into two typed pockets of different channel counts
+    in one submit, full parity; a type >= a docked pocket's channels is VS_E_PARSE naming the ligand."""
+    from paper_2303_06150_b200 import VsError
+    lib = _typed_lib(vsgen.ligands(24, 31, (20, 90), (0, 8)), 2)
+    pk2 = vsgen.typed_pocket(103, n_types=2)
+    pk4 = vsgen.typed_pocket(104, n_types=4, center_offset=(1.5, -1.0, 0.5))
+    q, d = vsgen.refine_table()
+    e = engine(debug_poses=True)
+    rot, tr, cs, ids = setup(e, [pk2, pk4], 8, 8)
+    e.set_refine(2, q, d)
+    e.submit_library(lib, ids)
+    e.wait()
+    for slot, pk in enumerate([pk2, pk4]):
+        r = e.results(slot)
+        ps, pa = e.pose_debug(slot)
+        rep = parity.check(lib, range(lib.n), pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, e.coords(slot),
+                           ps, pa, band=BAND, tol_score=TOL_S, tol_xyz=TOL_X, refine=(2, q, d),
+                           gpu_refine=e.refine(slot), gpu_pose_refine=e.pose_refine_debug(slot))
+        assert rep.ok, rep.summary() + "\n" + "\n".join(map(str, rep.failures[:10]))
+    bad = lib.subset(np.arange(lib.n))
+    bad.atom_type = bad.atom_type.copy()
+    bad.atom_type[int(bad.atom_off[5]) + 3] = 2                      # pk2 has channels 0, 1 only
+    with pytest.raises(VsError, match="ligand 5"):
+        e.submit_library(bad, ids)
