@@ -1143,6 +1143,9 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
     if (ms) {   // fused multi-site launches: the production lane map only (FIX / QUAD grids, PPW 4, K 8)
         if constexpr (GM == kGridFix || GM == kGridQuad) {
             if (PPW != 4 || K != 8) return nullptr;
+            if constexpr (GM == kGridQuad && AC <= 96) {
+                if (NW == 20) return dock_kernel<AC, 20, 4, GM, 8, true>;
+            }
             return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, true>
                    : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, true>
                    : NW == 12 ? dock_kernel<AC, 12, 4, GM, 8, true>
@@ -1166,9 +1169,8 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
                : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0, false>
                           : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0, false> : nullptr));
     }
-    if constexpr (GM == kGridQuad && AC <= 64) {   // more warps for the small classes (latency hiding)
-        if (PPW == 4 && K == 8 && (NW == 20 || NW == 24))
-            return NW == 20 ? dock_kernel<AC, 20, 4, GM, 8, false> : dock_kernel<AC, 24, 4, GM, 8, false>;
+    if constexpr (GM == kGridQuad && AC <= 96) {   // 20 warps (96 registers) where shared memory allows
+        if (PPW == 4 && K == 8 && NW == 20) return dock_kernel<AC, 20, 4, GM, 8, false>;
     }
     if (PPW == 4 && K == 8 && GM != kGridRT)   // production path: compile-time K = 8
         return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, false>

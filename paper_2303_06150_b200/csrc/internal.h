@@ -41,7 +41,7 @@ constexpr int kMaxSweeps = 4;
 constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3, kGridTyped = 4;
 constexpr int kMaxChannels = 8;   // grid channels of a typed pocket (atom types 0..7)
 constexpr int kWin = 32;   // window edge (nodes)
-constexpr int kQuadWC = 20;                  // QUAD window edge (cells per axis)
+constexpr int kQuadWC = 19;                  // QUAD window edge (cells per axis)
 constexpr int kQuadRS = kQuadWC;             // quads per row (x), rows per plane: kQuadWC + 1 (y + 1)
 constexpr int kQuadPS = kQuadRS * (kQuadWC + 1) + 3;   // quads per plane (423 = 3 mod 8: bank model)
 // TYPED window of W cells: plane stride W (W + 1) + 3 quads (kQuadPS's padding), channel stride

@@ -9,12 +9,15 @@ na, nr = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (6, 23)
 ATOMS = tuple(int(x) for x in os.environ.get("ATOMS", "20,120").split(","))
 lib = vsgen.ligands(n, 4, ATOMS)
 e = Engine(atom_clusters=na, rot_clusters=nr, launch_per_bucket=bool(int(os.environ.get("LPB", "0"))), bucket_multiple=int(os.environ.get("BM", "16")), n_streams=int(os.environ.get("NS", "4")))
-e.set_poses(*vsgen.pose_table(64)); e.set_angles(vsgen.angle_table(8)); pid = e.load_pocket(vsgen.pocket(101))
+T = int(os.environ.get("TYPED", "0"))   # > 0: typed submit with T atom types (Q24)
+e.set_poses(*vsgen.pose_table(64)); e.set_angles(vsgen.angle_table(8))
+pid = e.load_pocket(vsgen.typed_pocket(101, n_types=T) if T else vsgen.pocket(101))
 import torch
 d = [torch.from_numpy(a).cuda() for a in lib.arrays()]
+ty = torch.from_numpy(vsgen.atom_types(lib, n_types=T)).cuda() if T else None
 ms = []
 for it in range(4):
-    e.submit(*d, [pid], on_device=True); e.wait()
+    e.submit(*d, [pid], on_device=True, atom_type=ty); e.wait()
     ms.append(e.stats()["dock_ms"])
 st = e.stats()
 print(f"{os.environ.get('TAG','')} n={n} grid={na}x{nr} dock_ms={np.median(ms[1:]):.2f} prep_ms={st['prep_ms']:.2f} "
