@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--cpu-sample-every", type=int, default=250)
     ap.add_argument("--streams", type=int, default=4)
     ap.add_argument("--bucket-multiple", type=int, default=16)
+    ap.add_argument("--typed", type=int, default=0,
+                    help="T > 0: the per-atom-type variant (SURVEY 8(f) 4(c), Q24): typed pockets of T channels, "
+                         "T atom types per ligand")
     return ap.parse_args()
 
 
@@ -123,7 +126,11 @@ def workload(args):
     if args.poses:
         c["P"] = args.poses
     lib = vsgen.ligands(c["n"], c["seed"], c["atoms"], c["rot"])
-    pockets = [vsgen.pocket(s) for s in c["pockets"]]
+    if args.typed:
+        lib.atom_type = vsgen.atom_types(lib, n_types=args.typed)
+        pockets = [vsgen.typed_pocket(s, n_types=args.typed) for s in c["pockets"]]
+    else:
+        pockets = [vsgen.pocket(s) for s in c["pockets"]]
     rot, tr = vsgen.pose_table(c["P"])
     cs = vsgen.angle_table(c["K"])
     return c, lib, pockets, rot, tr, cs
@@ -135,6 +142,8 @@ def describe(c, args, world):
                         f"P={c['P']} poses, K={c['K']} angle steps, S_w=1",
             "global_batch": c["n"], "n_pockets": len(c["pockets"]), "P": c["P"], "K": c["K"],
             "bucketing": "6 atom x 23 rotamer clusters (paper P:337; 4 x 21 populated)",
+            "atom_types": (f"{args.typed} per-atom-type grid channels (SURVEY 8(f) 4(c), DESIGN Q24)" if args.typed
+                           else "none (one grid channel)"),
             "bucket_multiple": args.bucket_multiple, "streams": args.streams,
             "parallelism": f"dp{world} (LPT bucket shards, NCCL all_gather top-k merge)" if world > 1 else "dp1",
             "l2": "inputs larger than L2 (library ~1 GB HBM-resident)"}
@@ -222,8 +231,9 @@ def main():
     n = lib.n
 
     # library HBM-resident for `value`; pinned host copies for `e2e`
-    d_lib = [torch.from_numpy(a).to(dev) for a in lib.arrays()]
-    h_lib = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
+    arrs = list(lib.arrays()) + ([lib.atom_type] if args.typed else [])   # (+ atom types, Q24)
+    d_lib = [torch.from_numpy(a).to(dev) for a in arrs]
+    h_lib = [torch.from_numpy(a).pin_memory() for a in arrs]
     h2d_bytes = sum(t.numel() * t.element_size() for t in h_lib)
     max_atoms = int(lib.n_atoms.max())
 
@@ -240,7 +250,8 @@ def main():
     def step(e, ids, batch, on_device, host_out=None):
         failed = None
         try:
-            e.submit(*batch, ids, on_device=on_device, max_atoms=max_atoms)
+            e.submit(*batch[:7], ids, on_device=on_device, max_atoms=max_atoms,
+                     atom_type=batch[7] if len(batch) > 7 else None)
             e.wait()
         except VsError as err:     # rank-local a1 error: every rank learns it from the gather
             failed = err
@@ -317,7 +328,8 @@ def main():
         from paper_2303_06150_b200.pipeline import chunk_bounds
         chunks = args.e2e_chunks if args.e2e_chunks > 0 else (0 if n >= 250000 else 1)
         n_chunks = len(chunk_bounds(n, chunks)) - 1
-        run_e2e = lambda: pdk.run(*h_lib, k=K_TOP, chunks=chunks, max_atoms=max_atoms)
+        run_e2e = lambda: pdk.run(*h_lib[:7], k=K_TOP, chunks=chunks, max_atoms=max_atoms,
+                                  atom_type=h_lib[7] if len(h_lib) > 7 else None)
         for _ in range(args.warmup):
             run_e2e()
         torch.cuda.synchronize()

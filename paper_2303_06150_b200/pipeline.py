@@ -91,12 +91,15 @@ class PipelinedDocker:
         """Chunk [lo, hi) as views of the caller's arrays: offsets keep their library values (the
         library rebases them on the device, vs_ligand_batch), data arrays start at the chunk's
         first element -- no host-side arithmetic on the critical path."""
-        ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays
+        ids, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms = arrays[:7]
         a0, a1 = int(atom_off[lo]), int(atom_off[hi])
         f0, f1 = int(frag_off[lo]), int(frag_off[hi])
         m0, m1 = int(move_off[f0]), int(move_off[f1])
-        return ([ids[lo:hi], atom_off[lo:hi + 1], xyz[a0:a1], frag_off[lo:hi + 1], frag_axis[f0:f1],
-                 move_off[f0:f1 + 1], move_atoms[m0:m1]], (a0, a1, f0, f1))
+        out = [ids[lo:hi], atom_off[lo:hi + 1], xyz[a0:a1], frag_off[lo:hi + 1], frag_axis[f0:f1],
+               move_off[f0:f1 + 1], move_atoms[m0:m1]]
+        if len(arrays) > 7:            # atom types of a typed run (Q24), sliced like xyz
+            out.append(arrays[7][a0:a1])
+        return out, (a0, a1, f0, f1)
 
     def _issue_copy(self, arrays, lo, hi):
         """Chunk [lo, hi) to the device on the copy stream (pinned sources: asynchronous)."""
@@ -121,7 +124,7 @@ class PipelinedDocker:
 
     def run(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, k: int = 1000,
             chunks: int = 0, max_atoms: int = 256, group=None, coords: bool = True, first: int = 32,
-            growth: int = 4, zero_copy=None):
+            growth: int = 4, zero_copy=None, atom_type=None):
         """Dock the library (the C-ABI's general-form CSR arrays; pinned torch CPU tensors for
         overlapped copies) into every pocket of ``setup``.  ``zero_copy`` (default: with more than
         one rank): the kernels read each rank's ligands straight from the pinned host arrays
@@ -131,7 +134,8 @@ class PipelinedDocker:
         ``ligand_id`` [n], ``best_score`` / ``best_pose`` [pockets, n], ``angles`` [pockets, S_w * sum R],
         ``xyz`` [pockets, sum A, 3] (best-pose coordinates, input atom order; with ``coords``), and
         ``topk`` = per pocket (library index [m], score [m], ligand id [m]), merged across ranks.
-        The per-ligand arrays are reused buffers: copy them to keep them past the next run."""
+        The per-ligand arrays are reused buffers: copy them to keep them past the next run.
+        ``atom_type`` (uint8 per atom, pinned like the rest): a typed run (vs_submit_typed, Q24)."""
         from . import parallel
         from .vsdock import VsError
         torch = self._torch
@@ -151,6 +155,8 @@ class PipelinedDocker:
         all_keys = [torch.empty(max(1, n), dtype=torch.int64, device=self.dev) for _ in range(npk)]
         nkeys = [0] * npk
         arrays = (ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms)
+        if atom_type is not None:
+            arrays = arrays + (atom_type,)
         self.trace = []
         ne = len(self.engines)
         inflight = {} if zero_copy else {c: self._issue_copy(arrays, bounds[c], bounds[c + 1])
@@ -185,7 +191,8 @@ class PipelinedDocker:
                 # returns once the dock launches are queued; the read-backs below queue behind
                 # them on the same stream and run on the D2H engine while the other engine docks
                 try:
-                    e.submit(*dev, self.pocket_ids, on_device=mode, max_atoms=max_atoms)
+                    e.submit(*dev[:7], self.pocket_ids, on_device=mode, max_atoms=max_atoms,
+                             atom_type=dev[7] if len(dev) > 7 else None)
                 except VsError as err:       # rank-local a1 error: still join the collective below
                     failed = err
                     if err.ligand is not None:

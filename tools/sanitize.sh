@@ -4,7 +4,7 @@
 out=${1:-gpurun_out}
 mkdir -p "$out"
 for tool in memcheck racecheck synccheck; do
-  for case in c1 edge ring win; do
+  for case in ${CASES:-c1 edge ring win typed fused}; do
     extra=""
     [ "$tool" = "memcheck" ] && extra="--leak-check full"
     [ "$tool" = "racecheck" ] && extra="--racecheck-report all"

@@ -4,7 +4,10 @@ detection row, VERDICT r1 "missing" 7.  Usage: python tools/sanitize_case.py <ca
   c1      C1 (16 ligands, 32^3 FIX grid, P = 8, K = 8): every prep / dock / finalize / top-k kernel
   edge    a 14^3 grid (atoms on and beyond the faces: the top-face corner handling) + K = 6
   ring    launch_per_bucket with bucket capacity 1 on 8 streams: many tiny launches of the round ring
-  win     a 48^3 grid at 0.5 A (WIN mode: window + global corners)
+  win     a 48^3 grid at 0.5 A (window + global corners)
+  typed   4 atom types into a typed pocket (TYPED layout, Q24) with rigid refinement (Q23)
+  fused   3 pockets docked by one fused multi-site cluster launch per class (f1: multicast TMA,
+          cluster mbarriers, DSMEM ring writes)
 Exits non-zero if the results are not finite (the sanitizer's own report is the evidence)."""
 import os
 import sys
@@ -16,19 +19,23 @@ import vsgen
 from paper_2303_06150_b200 import Engine
 
 
-def run(lib, pk, P=8, K=8, **kw):
+def run(lib, pk, P=8, K=8, refine=False, **kw):
     e = Engine(**kw)
     rot, tr = vsgen.pose_table(P, tau=1.0)
     e.set_poses(rot, tr)
     e.set_angles(vsgen.angle_table(K))
-    pid = e.load_pocket(pk)
-    e.submit_library(lib, [pid])
+    if refine:
+        e.set_refine(2, *vsgen.refine_table())
+    pks = pk if isinstance(pk, list) else [pk]
+    pids = [e.load_pocket(q) for q in pks]
+    e.submit_library(lib, pids)
     e.wait()
-    r = e.results(0)
-    xyz = e.coords(0)
-    keys, nv = e.local_topk(0, 8)
-    idx, sc = e.merge_topk(keys[:nv], 8)
-    assert np.isfinite(r.best_score).all() and np.isfinite(xyz).all() and len(idx) == min(8, lib.n)
+    for s in range(len(pids)):
+        r = e.results(s)
+        xyz = e.coords(s)
+        keys, nv = e.local_topk(s, 8)
+        idx, sc = e.merge_topk(keys[:nv], 8)
+        assert np.isfinite(r.best_score).all() and np.isfinite(xyz).all() and len(idx) == min(8, lib.n)
     e.close()
 
 
@@ -42,6 +49,12 @@ elif case == "ring":
         n_streams=8)
 elif case == "win":
     run(vsgen.ligands(12, 5, (20, 90), (0, 8)), vsgen.pocket(108, n=48, spacing=0.5))
+elif case == "typed":
+    lib = vsgen.ligands(16, 1, (20, 60), (0, 6))
+    lib.atom_type = vsgen.atom_types(lib, n_types=4)
+    run(lib, vsgen.typed_pocket(101, n_types=4), refine=True)
+elif case == "fused":
+    run(vsgen.ligands(40, 9, (20, 90), (0, 8)), [vsgen.pocket(s) for s in (101, 102, 103)], P=16, fused_sites=True)
 else:
     raise SystemExit(f"unknown case {case}")
 print("case", case, "ok")
