@@ -435,7 +435,7 @@ vs_status plan_classes(vs_ctx* c, const std::vector<int>& atom_b, int gm, int nz
         // (poses per warp, warps per CTA): the first candidate of the policy whose shared
         // memory fits one CTA per SM and whose pose group holds the K angle lanes
         // (PPW poses x 32/PPW lanes).  VSDOCK_POLICY="4:16,2:16,..." overrides.
-        std::vector<std::pair<int, int>> cand = {{4, 20}, {4, 16}, {4, 13}, {4, 12}, {4, 10}, {4, 8}, {2, 16}, {2, 8}, {4, 4}, {1, 32}, {1, 16}};
+        std::vector<std::pair<int, int>> cand = {{4, 20}, {4, 18}, {4, 16}, {4, 15}, {4, 13}, {4, 12}, {4, 10}, {4, 8}, {2, 16}, {2, 8}, {4, 4}, {1, 32}, {1, 16}};
         if (const char* e = getenv("VSDOCK_POLICY")) {
             cand.clear();
             int a = 0, b2 = 0, n = 0;

@@ -51,11 +51,16 @@ int grid_mode(int nx, int ny, int nz, float spacing) {
     return rt <= (size_t)kWin * dk::kFixPS + 2048 ? kGridRT : kGridWin;
 }
 
-// TYPED (Q24): the largest window edge W <= kQuadWC whose nch channel windows fit the QUAD budget
-// (W = 20, 15, 13, 12, 11, 10, 10, 9 for 1..8 channels)
+// TYPED (Q24): the largest window edge W <= kQuadWC whose nch channel windows fit kTypedBudget
+// (W = 18, 15, 13, 12, 11, 10, 10, 9 for 1..8 channels)
 int typed_window(int nch) {
     int W = kQuadWC;
-    while (W > 2 && (size_t)nch * typed_chan_stride(W) > (size_t)kQuadPS * kQuadWC + 4) --W;
+    // VSDOCK_TYPED_BUDGET (measurement override): the channel windows' budget in quads
+    static const long budget = [] {
+        const char* e = getenv("VSDOCK_TYPED_BUDGET");
+        return e ? atol(e) : (long)kTypedBudget;
+    }();
+    while (W > 2 && (long)nch * typed_chan_stride(W) > budget) --W;
     return W;
 }
 

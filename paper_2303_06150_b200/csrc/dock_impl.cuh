@@ -1143,8 +1143,10 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
     if (ms) {   // fused multi-site launches: the production lane map only (FIX / QUAD grids, PPW 4, K 8)
         if constexpr (GM == kGridFix || GM == kGridQuad) {
             if (PPW != 4 || K != 8) return nullptr;
-            if constexpr (GM == kGridQuad && AC <= 96) {
-                if (NW == 20) return dock_kernel<AC, 20, 4, GM, 8, true>;
+            if constexpr (GM == kGridQuad) {
+                if constexpr (AC <= 96) if (NW == 20) return dock_kernel<AC, 20, 4, GM, 8, true>;
+                if constexpr (AC == 128) if (NW == 18) return dock_kernel<AC, 18, 4, GM, 8, true>;
+                if constexpr (AC == 160) if (NW == 15) return dock_kernel<AC, 15, 4, GM, 8, true>;
             }
             return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, true>
                    : NW == 13 ? dock_kernel<AC, 13, 4, GM, 8, true>
@@ -1169,8 +1171,12 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
                : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0, false>
                           : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0, false> : nullptr));
     }
-    if constexpr (GM == kGridQuad && AC <= 96) {   // 20 warps (96 registers) where shared memory allows
-        if (PPW == 4 && K == 8 && NW == 20) return dock_kernel<AC, 20, 4, GM, 8, false>;
+    if constexpr (GM == kGridQuad) {   // more warps where shared memory allows (latency hiding)
+        if (PPW == 4 && K == 8) {
+            if constexpr (AC <= 96) if (NW == 20) return dock_kernel<AC, 20, 4, GM, 8, false>;
+            if constexpr (AC == 128) if (NW == 18) return dock_kernel<AC, 18, 4, GM, 8, false>;
+            if constexpr (AC == 160) if (NW == 15) return dock_kernel<AC, 15, 4, GM, 8, false>;
+        }
     }
     if (PPW == 4 && K == 8 && GM != kGridRT)   // production path: compile-time K = 8
         return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, false>

@@ -35,19 +35,20 @@ constexpr int kMaxSweeps = 4;
 //         (h >= 0.9 A) or the whole grid (grid_mode, dock.cu).
 //  4 TYPED per-atom-type grid channels (Q24): the QUAD layout per
 //         channel, T windows of W^3 cells side by side (W the largest edge <= kQuadWC whose T windows
-//         fit the QUAD budget: W = 20, 15, 12, 9 for T = 1, 2, 4, 8), runtime strides, each atom
+//         fit kTypedBudget: W = 18, 15, 12, 9 for T = 1, 2, 4, 8), runtime strides, each atom
 //         gathering from its own channel; cells outside the window read the padded global copy of
 //         that channel.
 constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3, kGridTyped = 4;
 constexpr int kMaxChannels = 8;   // grid channels of a typed pocket (atom types 0..7)
 constexpr int kWin = 32;   // window edge (nodes)
-constexpr int kQuadWC = 19;                  // QUAD window edge (cells per axis)
+constexpr int kQuadWC = 18;                  // QUAD window edge (cells per axis)
 constexpr int kQuadRS = kQuadWC;             // quads per row (x), rows per plane: kQuadWC + 1 (y + 1)
 constexpr int kQuadPS = kQuadRS * (kQuadWC + 1) + 3;   // quads per plane (423 = 3 mod 8: bank model)
 // TYPED window of W cells: plane stride W (W + 1) + 3 quads (kQuadPS's padding), channel stride
 // W planes + 4 quads
 __host__ __device__ inline int typed_plane_stride(int W) { return W * (W + 1) + 3; }
 __host__ __device__ inline int typed_chan_stride(int W) { return typed_plane_stride(W) * W + 4; }
+constexpr int kTypedBudget = 8464;   // quads (135 KB) for the channel windows of a TYPED pocket
 
 // Pocket as the dock kernel sees it.  Coordinates are kept in CENTRED grid units
 // v = (y - o)/h - Z with an integer shift Z per axis (16 for FIX, floor(n/2) for RT, the
