@@ -987,3 +987,25 @@ def test_typed_refinement_two_pockets_and_type_errors():
     bad.atom_type[int(bad.atom_off[5]) + 3] = 2                      # pk2 has channels 0, 1 only
     with pytest.raises(VsError, match="ligand 5"):
         e.submit_library(bad, ids)
+
+
+def test_typed_pipelined_docker_matches_single_submit(c2):
+    """The public host API with atom types (PipelinedDocker.run(atom_type=...), Q24): chunked,
+    double-buffered, bit-identical to one typed submit, outputs pass parity on a sample."""
+    import torch
+    from paper_2303_06150_b200.pipeline import PipelinedDocker
+    c, lib0, _ = c2
+    lib = _typed_lib(lib0.subset(np.arange(3000)), 4)
+    pk = vsgen.typed_pocket(102, n_types=4)
+    e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+    r = e.results(0)
+    pd = PipelinedDocker()
+    pd.setup(rot, tr, cs, [pk])
+    h = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
+    out = pd.run(*h, k=50, chunks=3, atom_type=torch.from_numpy(lib.atom_type).pin_memory())
+    assert np.array_equal(out["best_score"][0], r.best_score) and np.array_equal(out["angles"][0], r.angles)
+    assert np.array_equal(out["xyz"][0], e.coords(0))
+    rep = parity.check(lib, np.arange(0, lib.n, 100), pk, rot, tr, cs, out["best_score"][0], out["best_pose"][0],
+                       out["angles"][0], out["xyz"][0], band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + str(rep.failures[:5])
+    pd.close()
