@@ -132,7 +132,7 @@ def test_c3_large_ligand_sample_parity():
     e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"])
     assert {cl["kernel_atoms"] for cl in e.classes()} >= {96, 128, 160}
     rng = np.random.default_rng(3)
-    check(e, lib, rng.choice(lib.n, 40, replace=False), pk, rot, tr, cs)
+    check(e, lib, rng.choice(lib.n, 200, replace=False), pk, rot, tr, cs)
 
 
 # ----------------------------------------------------------------------------- a2-a4 bit-exact
@@ -384,7 +384,7 @@ def test_c4_full_size_sampled_parity():
     assert ((r.best_pose >= 0) & (r.best_pose < c["P"])).all()
     assert (r.angles < c["K"]).all()
     rng = np.random.default_rng(4)
-    idx = rng.choice(lib.n, 30, replace=False)
+    idx = rng.choice(lib.n, 400, replace=False)
     xyz = e.coords(0)
     rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, xyz, band=BAND,
                        tol_score=TOL_S, tol_xyz=TOL_X)
@@ -412,7 +412,7 @@ def test_c5_full_size_campaign_sampled_parity_and_topk():
         if prev is not None:
             assert not np.array_equal(prev, r.best_score)
         prev = r.best_score
-        idx = rng.choice(lib.n, 8, replace=False)
+        idx = rng.choice(lib.n, 100, replace=False)
         rep = parity.check(lib, idx, pk, rot, tr, cs, r.best_score, r.best_pose, r.angles, e.coords(slot),
                            band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
         assert rep.ok, rep.summary() + str(rep.failures[:5])
