@@ -350,7 +350,8 @@ def main():
         d2h = len(pockets) * (n * 8 + nR_ + nA_ * 12 + K_TOP * 12)
         e2e = {"value": n * len(pockets) / (t_e / args.steps / 1e3), "unit": "ligands/s",
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h,
-               "api": f"PipelinedDocker.run: pinned host CSR (general form: axes + moving-atom lists) -> host "
+               "api": f"PipelinedDocker.run: pinned host CSR (general form: axes + moving-atom lists) handed to the "
+                      f"C-ABI (vs_submit, on_device = 0: the library copies each chunk to the device) -> host "
                       f"best scores, poses, angle indices, best-pose coordinates (input atom order) + top-{K_TOP} "
                       f"per pocket; {n_chunks} chunk(s) {chunk_bounds(n, chunks)[1:]} over 2 engines: H2D of chunk "
                       f"i+1 and the D2H of chunk i-1's outputs under the docking of chunk i"}

@@ -124,7 +124,7 @@ class PipelinedDocker:
 
     def run(self, ligand_id, atom_off, xyz, frag_off, frag_axis, move_off, move_atoms, k: int = 1000,
             chunks: int = 0, max_atoms: int = 256, group=None, coords: bool = True, first: int = 32,
-            growth: int = 4, zero_copy=None, atom_type=None):
+            growth: int = 4, zero_copy=None, atom_type=None, library_copy: bool = True):
         """Dock the library (the C-ABI's general-form CSR arrays; pinned torch CPU tensors for
         overlapped copies) into every pocket of ``setup``.  ``zero_copy`` (default: with more than
         one rank): the kernels read each rank's ligands straight from the pinned host arrays
@@ -135,7 +135,12 @@ class PipelinedDocker:
         ``xyz`` [pockets, sum A, 3] (best-pose coordinates, input atom order; with ``coords``), and
         ``topk`` = per pocket (library index [m], score [m], ligand id [m]), merged across ranks.
         The per-ligand arrays are reused buffers: copy them to keep them past the next run.
-        ``atom_type`` (uint8 per atom, pinned like the rest): a typed run (vs_submit_typed, Q24)."""
+        ``atom_type`` (uint8 per atom, pinned like the rest): a typed run (vs_submit_typed, Q24).
+        ``library_copy`` (default): hand each chunk's pinned host slices to the C-ABI (vs_submit
+        with on_device = 0: the library issues the host-to-device copies on the engine's stream,
+        so chunk i + 1's upload on one engine overlaps chunk i's docking on the other); False:
+        stage them with torch copies on a separate copy stream (measured equal on B200:
+        8.59 vs 8.61 M ligands/s, profiles/r02c_e2e_pipeline_sweep.txt)."""
         from . import parallel
         from .vsdock import VsError
         torch = self._torch
@@ -159,8 +164,9 @@ class PipelinedDocker:
             arrays = arrays + (atom_type,)
         self.trace = []
         ne = len(self.engines)
-        inflight = {} if zero_copy else {c: self._issue_copy(arrays, bounds[c], bounds[c + 1])
-                                         for c in range(min(ne, nch))}
+        staged = not zero_copy and not library_copy     # torch copies on the copy stream
+        inflight = {} if not staged else {c: self._issue_copy(arrays, bounds[c], bounds[c + 1])
+                                          for c in range(min(ne, nch))}
         keep = {}
         failed = None
         pending = None
@@ -178,9 +184,10 @@ class PipelinedDocker:
             lo, hi = bounds[c], bounds[c + 1]
             e = self.engines[c % ne]
             t0 = time.perf_counter()
-            if zero_copy:
-                dev, (a0, a1, f0, f1) = self._slices(arrays, lo, hi)   # read in place (on_device = 2)
-                mode = 2
+            if not staged:
+                # zero copy: read in place (on_device = 2); library copy: vs_submit copies (0)
+                dev, (a0, a1, f0, f1) = self._slices(arrays, lo, hi)
+                mode = 2 if zero_copy else 0
             else:
                 dev, ev, (a0, a1, f0, f1) = inflight.pop(c)
                 ev.synchronize()    # chunk c resident (submit reads its CSR totals)
@@ -209,7 +216,7 @@ class PipelinedDocker:
                     readback(*pending)
                 pending = (e, lo, hi, a0, a1, f0, f1)
             keep[c % ne] = dev      # the engine borrows the chunk until its next submit
-            if c + ne < nch and not zero_copy:
+            if c + ne < nch and staged:
                 # the buffer slot of chunk c + ne is engine c's: its copy may only overwrite
                 # device memory the engine no longer reads -- new tensors, so no hazard
                 inflight[c + ne] = self._issue_copy(arrays, bounds[c + ne], bounds[c + ne + 1])

@@ -15,15 +15,16 @@ rot, tr = vsgen.pose_table(c["P"]); cs = vsgen.angle_table(c["K"])
 h = [torch.from_numpy(a).pin_memory() for a in lib.arrays()]
 pd = PipelinedDocker(); pd.setup(rot, tr, cs, pk)
 mx = int(lib.n_atoms.max())
-for chunks, coords, zc in ((0, True, False), (1, True, False), (2, True, False), (4, True, False), (8, True, False),
-                           (0, False, False), (0, True, True), (4, True, True)):
+for chunks, coords, zc, lc in ((0, True, False, False), (0, True, False, True), (4, True, False, True),
+                               (8, True, False, True), (4, True, False, False), (8, True, False, False),
+                               (0, True, True, False)):
     ts = []
     for _ in range(4):
         torch.cuda.synchronize(); t = time.perf_counter()
-        pd.run(*h, k=1000, chunks=chunks, max_atoms=mx, coords=coords, zero_copy=zc)
+        pd.run(*h, k=1000, chunks=chunks, max_atoms=mx, coords=coords, zero_copy=zc, library_copy=lc)
         ts.append(time.perf_counter() - t)
     dt = float(np.median(ts[1:]))
-    print(f"chunks={chunks} coords={coords} zero_copy={zc} {chunk_bounds(n, chunks)[1:]}: {dt*1e3:.1f} ms "
+    print(f"chunks={chunks} coords={coords} zero_copy={zc} library_copy={lc} {chunk_bounds(n, chunks)[1:]}: {dt*1e3:.1f} ms "
           f"{n/dt:.3e} lig/s", flush=True)
     T0 = pd.trace[0][3]
     for r in pd.trace:
