@@ -237,6 +237,8 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid, bool type
     p.grs = d.nx + 1;
     p.gps = (d.nx + 1) * (d.ny + 1);
     p.gcs = p.gps * (d.nz + 1);
+    p.gq = reinterpret_cast<const float4*>(dgrid + pocket_quad_offset(d.nx, d.ny, d.nz, nch));
+    p.gqcs = d.nx * (d.ny + 1) * d.nz;
     p.nch = typed ? nch : 1;
     p.qcs = 0;
     p.mode = typed ? kGridTyped : grid_mode(d.nx, d.ny, d.nz, d.spacing);
@@ -632,6 +634,7 @@ vs_status load_pocket_impl(vs_ctx* c, const vs_pocket_desc* d, int nch, const fl
                            int32_t* pocket_id) {
     if (!c || !d || !grid) return VS_E_ARG;
     if (nch < 1 || nch > kMaxChannels) return fail(c, VS_E_ARG, "n_channels must be in [1, %d]", kMaxChannels);
+    if ((int64_t)d->nx * d->ny * d->nz * nch > (1 << 22)) return fail(c, VS_E_ARG, "pocket grid too large (nodes x channels > 2^22)");
     if (c->pockets.size() >= 16) return fail(c, VS_E_ARG, "at most 16 pockets");
     if (d->nx < 2 || d->ny < 2 || d->nz < 2) return fail(c, VS_E_ARG, "pocket dims must be >= 2");
     if ((int64_t)d->nx * d->ny * d->nz > (1 << 22)) return fail(c, VS_E_ARG, "pocket grid too large");
@@ -656,12 +659,31 @@ vs_status load_pocket_impl(vs_ctx* c, const vs_pocket_desc* d, int nch, const fl
     // the device copy is PADDED: [nz+1][ny+1][nx+1] with zero pads, so a weight-0 corner read at
     // node n stays inside the array (PocketDev::grid); typed pockets: nch padded copies back to back
     const size_t gx = (size_t)d->nx + 1, gy = (size_t)d->ny + 1, gc = gx * gy * ((size_t)d->nz + 1);
-    ph.grid.assign(gc * nch, 0.f);
+    ph.grid.assign(pocket_floats(d->nx, d->ny, d->nz, nch), 0.f);
     for (int t = 0; t < nch; ++t)
         for (int z = 0; z < d->nz; ++z)
             for (int y = 0; y < d->ny; ++y)
                 std::memcpy(&ph.grid[t * gc + ((size_t)z * gy + y) * gx], &raw[t * cnt + ((size_t)z * d->ny + y) * d->nx],
                             (size_t)d->nx * 4);
+    // the global QUAD copy behind it (PocketDev::gq): node (x, y, z) = (G[x,y,z], G[x,y,z+1], G[x+1,y,z],
+    // G[x+1,y,z+1]) of the padded copy, x < nx, y <= ny, z < nz -- a window miss reads 2 x 16 B
+    {
+        const size_t X = (size_t)d->nx, Y = (size_t)d->ny + 1, Z = (size_t)d->nz;
+        float* Q = &ph.grid[pocket_quad_offset(d->nx, d->ny, d->nz, nch)];
+        for (int t = 0; t < nch; ++t) {
+            const float* P = &ph.grid[t * gc];
+            for (size_t z = 0; z < Z; ++z)
+                for (size_t y = 0; y < Y; ++y)
+                    for (size_t x = 0; x < X; ++x) {
+                        const size_t i = x + gx * (y + gy * z), gp = gx * gy;
+                        float* q = Q + 4 * (((size_t)t * Z + z) * Y * X + y * X + x);
+                        q[0] = P[i];
+                        q[1] = P[i + gp];
+                        q[2] = P[i + 1];
+                        q[3] = P[i + gp + 1];
+                    }
+        }
+    }
     c->pockets.push_back(std::move(ph));
     ++c->tables_version;
     if (pocket_id) *pocket_id = (int32_t)c->pockets.size() - 1;
@@ -1261,10 +1283,17 @@ vs_status submit_impl(vs_ctx* c, const vs_ligand_batch* batch, const uint8_t* at
             // cluster size g: the one that keeps the most SMs busy (clusters are placed whole
             // inside a GPC, so large clusters of 227 KB CTAs leave SMs idle); ties -> larger g
             int best_g = 1, best_sms = ci.b * c->sm_count, best_cl = 0;
+            static const int force_g = [] {   // VSDOCK_CLUSTER=g: measurement override of the cluster size
+                const char* e = getenv("VSDOCK_CLUSTER");
+                return e ? atoi(e) : 0;
+            }();
             for (int g = std::min(n_pockets, kMaxSites); g >= 2; --g) {
                 int cl = 0;
                 CK(dock_cluster_occupancy(b.kernel_atoms, ci.NW, ci.PPW, p0.mode, c->K, L.total, g, &cl));
-                if (cl > 0 && (cl * g > best_sms || (best_g == 1 && cl * g * 100 >= best_sms * 97))) {
+                if (getenv("VSDOCK_CLUSTER_LOG"))
+                    fprintf(stderr, "class %d: cluster size %d -> %d clusters (%d SMs)\n", b.kernel_atoms, g, cl, cl * g);
+                if (force_g > 0 && g != force_g) continue;
+                if (cl > 0 && (force_g > 0 || cl * g > best_sms || (best_g == 1 && cl * g * 100 >= best_sms * 97))) {
                     best_g = g;
                     best_sms = cl * g;
                     best_cl = cl;

@@ -66,6 +66,10 @@ struct PocketDev {
     int nch;               // grid channels staged (TYPED: T; else 1)
     int qcs;               // TYPED: shared-memory channel stride (quads); rs = W, ps = typed_plane_stride(W)
     int gcs;               // global channel stride of the padded copy (floats)
+    const float4* gq;      // global QUAD copy behind the padded channels: node (x, y, z) of channel t at
+                           // gq[t * gqcs + x + y * nx + z * nx * (ny + 1)], x < nx, y <= ny, z < nz, holding
+                           // (G[x,y,z], G[x,y,z+1], G[x+1,y,z], G[x+1,y,z+1]) of the padded copy
+    int gqcs;              // its channel stride (quads)
     float lo_x, lo_y, lo_z;       // -Z          (u = 0)
     float top_x, top_y, top_z;    // n - 1 - Z   (u = n - 1)
     float mx, my, mz;             // 2^23 + Z    (exact)
@@ -187,6 +191,15 @@ __host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
 int grid_mode(int nx, int ny, int nz, float spacing);
 // TYPED window edge (cells) for nch channels
 int typed_window(int nch);
+// Host layout of a pocket's device copy (floats): nch padded channels [nz+1][ny+1][nx+1], then
+// (16-byte aligned) the global QUAD copy of every channel, nx * (ny + 1) * nz float4 each.
+inline size_t pocket_quad_offset(int nx, int ny, int nz, int nch) {
+    const size_t gc = (size_t)(nx + 1) * (ny + 1) * (nz + 1);
+    return (gc * nch + 3) & ~(size_t)3;
+}
+inline size_t pocket_floats(int nx, int ny, int nz, int nch) {
+    return pocket_quad_offset(nx, ny, nz, nch) + (size_t)4 * nx * (ny + 1) * nz * nch;
+}
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps);
 
 // Launchers (return cudaGetLastError()).
