@@ -1009,3 +1009,29 @@ def test_typed_pipelined_docker_matches_single_submit(c2):
                        out["angles"][0], out["xyz"][0], band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
     assert rep.ok, rep.summary() + str(rep.failures[:5])
     pd.close()
+
+
+def test_typed_large_noncubic_grid_window_misses():
+    """TYPED on a 48 x 40 x 44 grid at 0.75 A with the docking centre off-centre: the channel windows
+    cover only part of the pocket, so many cells come from the global QUAD copy (and beyond the
+    grid, the clamp + excess); score hook on every channel against the oracle, then docking parity
+    with every pose replayed."""
+    base = vsgen.typed_pocket(105, n_types=3, n=(48, 40, 44), spacing=0.75, center_offset=(2.0, -1.5, 1.0))
+    e = engine(debug_poses=True)
+    pid = e.load_pocket(base)
+    rng = np.random.default_rng(11)
+    lo = np.array(base.origin) - 3.0
+    hi = np.array(base.origin) + 0.75 * np.array([47, 39, 43]) + 3.0
+    pts = np.concatenate([rng.uniform(lo, hi, size=(30000, 3)),
+                          np.array(base.center) + rng.normal(0, 7.0, size=(30000, 3))]).astype(np.float32)
+    t = rng.integers(0, 3, size=len(pts)).astype(np.uint8)
+    g = e.score_points(pid, pts, types=t)
+    ref = oracle.grid_score(base, pts.astype(np.float64), t)
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < 2e-5     # 1/h inexact for h != 1
+    lib = _typed_lib(vsgen.ligands(24, 41, (20, 110), (0, 10)), 3)
+    rot, tr, cs = vsgen.pose_table(8)[0], vsgen.pose_table(8)[1], vsgen.angle_table(8)
+    e.set_poses(rot, tr)
+    e.set_angles(cs)
+    e.submit_library(lib, [pid])
+    e.wait()
+    check(e, lib, range(lib.n), base, rot, tr, cs)
