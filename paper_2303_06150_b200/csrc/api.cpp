@@ -241,12 +241,16 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid, bool type
     p.gqcs = d.nx * (d.ny + 1) * d.nz;
     p.nch = typed ? nch : 1;
     p.qcs = 0;
-    p.mode = typed ? kGridTyped : grid_mode(d.nx, d.ny, d.nz, d.spacing);
-    const int QW = typed ? typed_window(nch) : kQuadWC;   // QUAD / TYPED window edge (cells)
-    if (typed) {
+    int QW = kQuadWC;   // QUAD / TYPED / TYPED_S window edge (cells)
+    p.mode = typed ? typed_layout(nch, &QW) : grid_mode(d.nx, d.ny, d.nz, d.spacing);
+    if (p.mode == kGridTyped) {
         p.rs = QW;
         p.ps = typed_plane_stride(QW);
         p.qcs = typed_chan_stride(QW);
+    } else if (p.mode == kGridTypedS) {   // floats
+        p.rs = typeds_row(QW);
+        p.ps = typeds_plane(QW);
+        p.qcs = typeds_chan(QW);
     } else {
         grid_strides(p.mode, d.nx, d.ny, &p.rs, &p.ps);
     }
@@ -257,7 +261,7 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid, bool type
     int w0[3] = {0, 0, 0};
     // (QUAD keeps its cells below the top face n-1, so the fast path's cells are interior)
     p.qwc = 0;
-    if (p.mode == kGridWin || p.mode == kGridQuad || p.mode == kGridTyped) {
+    if (p.mode == kGridWin || p.mode == kGridQuad || typed_mode(p.mode)) {
         const int W = p.mode == kGridWin ? kWin : QW;
         p.qwc = QW;
         for (int a = 0; a < 3; ++a) {
@@ -277,7 +281,7 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid, bool type
     for (int a = 0; a < 3; ++a)
         Z[a] = p.mode == kGridFix    ? 16
                : p.mode == kGridRT   ? n3[a] / 2
-               : p.mode == kGridQuad || p.mode == kGridTyped ? w0[a] + QW / 2
+               : p.mode == kGridQuad || typed_mode(p.mode) ? w0[a] + QW / 2
                                      : w0[a] + kWin / 2;
     p.lo_x = (float)-Z[0];
     p.lo_y = (float)-Z[1];
@@ -288,7 +292,7 @@ PocketDev make_pocket_dev(const vs_pocket_desc& d, const float* dgrid, bool type
     p.mx = 8388608.f + (float)Z[0];
     p.my = 8388608.f + (float)Z[1];
     p.mz = 8388608.f + (float)Z[2];
-    if (p.mode == kGridQuad || p.mode == kGridTyped) {   // 1.5 * 2^23 + Z - w0: the floor's bits give the window-relative cell
+    if (p.mode == kGridQuad || typed_mode(p.mode)) {   // 1.5 * 2^23 + Z - w0: the floor's bits give the window-relative cell
         p.mx = 12582912.f + (float)(Z[0] - w0[0]);
         p.my = 12582912.f + (float)(Z[1] - w0[1]);
         p.mz = 12582912.f + (float)(Z[2] - w0[2]);

@@ -64,6 +64,24 @@ int typed_window(int nch) {
     return W;
 }
 
+// TYPED_S: the largest W <= kTypedSMaxW whose nch scalar channel windows fit the same budget
+// (4 kTypedBudget floats): W = 30, 24, 21, 18, 17, 16, 15, 14 for 1..8 channels.
+// Layout choice (measured): VSDOCK_TYPED_LAYOUT=quad|scalar overrides.
+int typed_layout(int nch, int* W) {
+    // (read at every pocket set-up, so one process can compare the two layouts)
+    const char* e = getenv("VSDOCK_TYPED_LAYOUT");
+    const int forced = !e ? -1 : strcmp(e, "scalar") == 0 ? kGridTypedS : strcmp(e, "quad") == 0 ? kGridTyped : -1;
+    const int mode = forced >= 0 ? forced : (nch >= 2 ? kGridTypedS : kGridTyped);
+    if (mode == kGridTyped) {
+        *W = typed_window(nch);
+        return mode;
+    }
+    int w = kTypedSMaxW;
+    while (w > 2 && (long)nch * typeds_chan(w) > 4L * kTypedBudget) --w;
+    *W = w;
+    return mode;
+}
+
 void grid_strides(int mode, int nx, int ny, int* rs, int* ps) {
     if (mode == kGridQuad) {   // in quads (16 bytes)
         *rs = kQuadRS;
@@ -178,6 +196,7 @@ cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, const uin
                     : pk.mode == kGridRT    ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridRT>)
                     : pk.mode == kGridQuad  ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridQuad>)
                     : pk.mode == kGridTyped ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridTyped>)
+                    : pk.mode == kGridTypedS ? reinterpret_cast<const void*>(dk::score_points_kernel<kGridTypedS>)
                                             : reinterpret_cast<const void*>(dk::score_points_kernel<kGridWin>);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -185,6 +204,7 @@ cudaError_t launch_score_points(const PocketDev& pk, const float* xyz, const uin
     else if (pk.mode == kGridRT) dk::score_points_kernel<kGridRT><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
     else if (pk.mode == kGridQuad) dk::score_points_kernel<kGridQuad><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
     else if (pk.mode == kGridTyped) dk::score_points_kernel<kGridTyped><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
+    else if (pk.mode == kGridTypedS) dk::score_points_kernel<kGridTypedS><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
     else dk::score_points_kernel<kGridWin><<<148, 1024, smem, st>>>(pk, xyz, types, n, out);
     return cudaGetLastError();
 }

@@ -160,8 +160,8 @@ __device__ __forceinline__ GCell grid_cell(float ux, float uy, float uz, const P
         iz = pk.nz - 2;
         fz = 1.f;
     }
-    if (GM == kGridQuad || GM == kGridTyped) {
-        // QUAD / TYPED: the floor constant is 1.5 * 2^23 + Z - w0 (PocketDev), so the bits give the
+    if (GM == kGridQuad || GM == kGridTyped || GM == kGridTypedS) {
+        // QUAD / TYPED / TYPED_S: the floor constant is 1.5 * 2^23 + Z - w0 (PocketDev), so the bits give the
         // WINDOW-relative cell directly (negative below the window)
         constexpr int d = kMagicBits - kQuadMagicBits;
         return GCell{ix + d, iy + d, iz + d, fxy, fz, e};
@@ -264,7 +264,36 @@ __device__ __forceinline__ float typed_addr_interior(const float* __restrict__ G
     return lerp(l.x, l.y, c.fz);
 }
 
-// ch = the atom's grid channel (TYPED only; ignored by the other modes)
+// TYPED_S (Q24, scalar channel windows): the 8 corners of cell a (window float index, channel
+// included) as the (z0, z1) pairs of x and x + 1 in rows y and y + 1 -- the values of the two
+// TYPED quads, blended in the same order, so bit-identical to TYPED
+__device__ __forceinline__ float typeds_addr_interior(const float* __restrict__ G, const QCell& c, int rs, int ps) {
+    const float* p = G + c.a;
+    const float2 l_0 = lerp2(make_float2(p[0], p[ps]), make_float2(p[1], p[ps + 1]), c.fxy.x);
+    const float2 l_1 = lerp2(make_float2(p[rs], p[rs + ps]), make_float2(p[rs + 1], p[rs + ps + 1]), c.fxy.x);
+    const float2 l = lerp2(l_0, l_1, c.fxy.y);
+    return lerp(l.x, l.y, c.fz);
+}
+// any cell (clamped, window-relative): the channel window (cells [0, W), W = rs - 2) or the padded
+// global copy of channel ch (L1 / L2)
+__device__ __forceinline__ float typeds_checked(const float* __restrict__ G, const GCell& c, int ch, const PocketDev& pk) {
+    const float* p;
+    int rs, ps;
+    if (__builtin_expect(__vimax3_u32((unsigned)c.ix, (unsigned)c.iy, (unsigned)c.iz) < (unsigned)(pk.rs - 2), 1)) {
+        rs = pk.rs;
+        ps = pk.ps;
+        p = G + c.ix + c.iy * rs + c.iz * ps + ch * pk.qcs;
+        return blend(make_float2(p[0], p[ps]), make_float2(p[1], p[ps + 1]), make_float2(p[rs], p[rs + ps]),
+                     make_float2(p[rs + 1], p[rs + ps + 1]), c.fxy, c.fz, pk.kh, c.e);
+    }
+    const int gr = pk.grs, gp = pk.gps;
+    p = pk.grid + (size_t)ch * pk.gcs + (c.ix + pk.wx0) + (size_t)(c.iy + pk.wy0) * gr + (size_t)(c.iz + pk.wz0) * gp;
+    return blend(make_float2(__ldg(p), __ldg(p + gp)), make_float2(__ldg(p + 1), __ldg(p + gp + 1)),
+                 make_float2(__ldg(p + gr), __ldg(p + gp + gr)), make_float2(__ldg(p + gr + 1), __ldg(p + gp + gr + 1)),
+                 c.fxy, c.fz, pk.kh, c.e);
+}
+
+// ch = the atom's grid channel (TYPED / TYPED_S only; ignored by the other modes)
 template <int GM>
 __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, float uy, float uz, const PocketDev& pk,
                                         int ch = 0) {
@@ -272,6 +301,7 @@ __device__ __forceinline__ float grid_g(const float* __restrict__ G, float ux, f
     const GCell cl = grid_cell<GM>(ux, uy, uz, pk);
     if (GM == kGridQuad) return quad_checked(G, cl, pk);
     if (GM == kGridTyped) return typed_checked(G, cl, ch, pk);
+    if (GM == kGridTypedS) return typeds_checked(G, cl, ch, pk);
     const int ix = cl.ix, iy = cl.iy, iz = cl.iz;
     const float2 fxy = cl.fxy;
     const float fz = cl.fz, e = cl.e;
@@ -342,6 +372,21 @@ __device__ __forceinline__ void stage_grid(float* sG, const PocketDev& pk, size_
     const int n4 = (int)(align16(zero_floats * 4) / 16);
     for (int t = threadIdx.x; t < n4; t += blockDim.x) reinterpret_cast<float4*>(sG)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
+    if (pk.mode == kGridTypedS) {
+        // TYPED_S: nodes [w0, w0 + W] of every channel (rs - 1 = W + 1 per axis), channels qcs
+        // floats apart; nodes beyond the padded copy stay zero (never read with weight > 0)
+        const int N = pk.rs - 1;
+        const int NX = min(N, pk.nx + 1 - pk.wx0), NY = min(N, pk.ny + 1 - pk.wy0), NZ = min(N, pk.nz + 1 - pk.wz0);
+        for (int row = w; row < NY * NZ * pk.nch; row += nw) {
+            const int ch = row / (NY * NZ), zy = row - ch * (NY * NZ);
+            const int z = zy / NY, y = zy - z * NY;
+            const float* src = pk.grid + (size_t)ch * pk.gcs + (size_t)(pk.wz0 + z) * pk.gps +
+                               (size_t)(pk.wy0 + y) * pk.grs + pk.wx0;
+            float* dst = sG + (size_t)ch * pk.qcs + z * pk.ps + y * pk.rs;
+            for (int x = lane; x < NX; x += 32) dst[x] = src[x];
+        }
+        return;
+    }
     if (pk.mode == kGridQuad || pk.mode == kGridTyped) {
         // node (x, y, z) of the window <- (G[x,y,z], G[x,y,z+1], G[x+1,y,z], G[x+1,y,z+1]) from the
         // padded global copy; nodes beyond the grid's pads stay zero (never read with weight > 0).
@@ -399,7 +444,23 @@ struct PoseBuf {
 template <int U, int GM>
 __device__ __forceinline__ void grid_batch(const float* __restrict__ G, const float4 (&v)[4], const PocketDev& pk,
                                            float (&g)[U], const int (&ch)[4]) {
-    if (GM == kGridTyped) {   // Q24: the QUAD vote on the channel windows
+    if (GM == kGridTypedS) {   // Q24, scalar channel windows: the same vote, eight LDS.32 per point
+        QCell cl[U];
+        bool all = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const GCell c = quad_cell_fast(v[u].x, v[u].y, v[u].z, pk);
+            all = all && quad_in_fast(c, pk.qwc);
+            cl[u] = QCell{c.ix + c.iy * pk.rs + c.iz * pk.ps + ch[u] * pk.qcs, c.fxy, c.fz};
+        }
+        if (__all_sync(FULL, all)) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = typeds_addr_interior(G, cl[u], pk.rs, pk.ps);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) g[u] = grid_g<GM>(G, v[u].x, v[u].y, v[u].z, pk, ch[u]);
+        }
+    } else if (GM == kGridTyped) {   // Q24: the QUAD vote on the channel windows
         QCell cl[U];
         bool all = true;
 #pragma unroll
@@ -453,7 +514,7 @@ __device__ __forceinline__ void eval_batch(const PoseBuf<AC>& B, const RotT& M, 
     for (int u = 0; u < U; ++u) {
         const int j = j0 + u * apw;
         v[u] = B.get(j < hi ? j : j0);
-        if (GM == kGridTyped) ch[u] = ty[j < hi ? j : j0];
+        if (typed_mode(GM)) ch[u] = ty[j < hi ? j : j0];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) kp[u] = apply_rot(M, v[u].x, v[u].y, v[u].z);
@@ -479,7 +540,7 @@ __device__ __forceinline__ void score_batch(const PoseBuf<AC>& B, const float* _
         const int j = j0 + u * stride;
         const int jj = j < n ? j : 0;
         v[u] = B.get(jj);
-        if (GM == kGridTyped) ch[u] = ty[jj];
+        if (typed_mode(GM)) ch[u] = ty[jj];
     }
     grid_batch<U, GM>(G, v, pk, g, ch);
 #pragma unroll
@@ -1190,7 +1251,7 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
             return nullptr;
         }
     }
-    if constexpr (GM == kGridTyped) {   // typed launches (Q24): the 4-poses-per-warp lane maps only
+    if constexpr (typed_mode(GM)) {   // typed launches (Q24): the 4-poses-per-warp lane maps only
         if (PPW != 4) return nullptr;
         if (K == 8)
             return NW == 16 ? dock_kernel<AC, 16, 4, GM, 8, false>

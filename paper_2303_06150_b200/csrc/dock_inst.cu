@@ -14,6 +14,7 @@ namespace dk {
 DockFn VSD_CAT(dock_pick_, VSD_AC)(int gmode, int NW, int PPW, int K, bool ms) {
     return gmode == kGridQuad    ? pick_ac<VSD_AC, kGridQuad>(NW, PPW, K, ms)
            : gmode == kGridTyped ? pick_ac<VSD_AC, kGridTyped>(NW, PPW, K, ms)
+           : gmode == kGridTypedS ? pick_ac<VSD_AC, kGridTypedS>(NW, PPW, K, ms)
            : gmode == kGridFix ? pick_ac<VSD_AC, kGridFix>(NW, PPW, K, ms)
            : gmode == kGridRT  ? pick_ac<VSD_AC, kGridRT>(NW, PPW, K, ms)
                                : pick_ac<VSD_AC, kGridWin>(NW, PPW, K, ms);

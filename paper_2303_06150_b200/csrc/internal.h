@@ -38,7 +38,13 @@ constexpr int kMaxSweeps = 4;
 //         fit kTypedBudget: W = 18, 15, 12, 9 for T = 1, 2, 4, 8), runtime strides, each atom
 //         gathering from its own channel; cells outside the window read the padded global copy of
 //         that channel.
-constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3, kGridTyped = 4;
+//  5 TYPED_S per-atom-type channels in the SCALAR layout: T windows of W^3 cells ((W + 1)^3 nodes of
+//         4 bytes, a quarter of a QUAD node) side by side, eight LDS.32 per point; for the same
+//         shared memory the window edge is ~1.6x the QUAD one (W = 18 instead of 12 at T = 4), so far
+//         fewer points miss it.  Cells outside read the padded global copy of their channel.  The
+//         same corner values and blend as TYPED: bit-identical results.
+constexpr int kGridFix = 0, kGridRT = 1, kGridWin = 2, kGridQuad = 3, kGridTyped = 4, kGridTypedS = 5;
+__host__ __device__ constexpr bool typed_mode(int m) { return m == kGridTyped || m == kGridTypedS; }
 constexpr int kMaxChannels = 8;   // grid channels of a typed pocket (atom types 0..7)
 constexpr int kWin = 32;   // window edge (nodes)
 constexpr int kQuadWC = 18;                  // QUAD window edge (cells per axis)
@@ -49,6 +55,12 @@ constexpr int kQuadPS = kQuadRS * (kQuadWC + 1) + 3;   // quads per plane (423 =
 __host__ __device__ inline int typed_plane_stride(int W) { return W * (W + 1) + 3; }
 __host__ __device__ inline int typed_chan_stride(int W) { return typed_plane_stride(W) * W + 4; }
 constexpr int kTypedBudget = 8464;   // quads (135 KB) for the channel windows of a TYPED pocket
+// TYPED_S window of W cells = W + 1 nodes per axis: row stride W + 2 floats, plane stride
+// (W + 2)(W + 1) + 7, channel stride W + 1 planes + 8 (the RT layout's padding)
+__host__ __device__ inline int typeds_row(int W) { return W + 2; }
+__host__ __device__ inline int typeds_plane(int W) { return (W + 2) * (W + 1) + 7; }
+__host__ __device__ inline int typeds_chan(int W) { return typeds_plane(W) * (W + 1) + 8; }
+constexpr int kTypedSMaxW = 30;   // TYPED_S window edge cap (cells)
 
 // Pocket as the dock kernel sees it.  Coordinates are kept in CENTRED grid units
 // v = (y - o)/h - Z with an integer shift Z per axis (16 for FIX, floor(n/2) for RT, the
@@ -60,7 +72,7 @@ struct PocketDev {
     int nx, ny, nz;
     int rs, ps;            // shared-memory row stride and plane stride (floats)
     int grs, gps;          // global padded row / plane stride (floats)
-    int mode;              // kGridFix / kGridRT / kGridWin / kGridQuad / kGridTyped
+    int mode;              // kGridFix / kGridRT / kGridWin / kGridQuad / kGridTyped / kGridTypedS
     int wx0, wy0, wz0;     // WIN / QUAD / TYPED: window origin (grid nodes)
     int qwc;               // QUAD / TYPED: fast cells [0, qwc) of the window, all interior (<= n-2) on every axis
     int nch;               // grid channels staged (TYPED: T; else 1)
@@ -159,6 +171,7 @@ __host__ __device__ inline size_t dock_grid_floats(int mode, int nz, int rs, int
            : mode == kGridWin   ? (size_t)kWin * ps
            : mode == kGridQuad  ? (size_t)4 * kQuadPS * kQuadWC
            : mode == kGridTyped ? (size_t)4 * typed_chan_stride(rs) * nch
+           : mode == kGridTypedS ? (size_t)(ps * (rs - 1) + 8) * nch
                                 : (size_t)(nz + 1) * ps + rs + 2;
 }
 __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int mode, int nz, int rs, int ps, int nch,
@@ -170,7 +183,7 @@ __host__ __device__ inline DockLayout dock_layout(int AC, int NW, int PPW, int m
     L.pose = o;   // pose table: read per warp item from global (L1-resident), no shared copy
     L.cs = o;     // angle table: each lane keeps its (cos, sin) in registers, no shared copy
     size_t q = 0;
-    L.rec_o = q;   q += align16((size_t)LC * rec_floats_typed(AC, mode == kGridTyped) * 4);
+    L.rec_o = q;   q += align16((size_t)LC * rec_floats_typed(AC, typed_mode(mode)) * 4);
     L.meta_o = q;  q += (size_t)LC * 16;
     L.score_o = q; q += align16((size_t)LC * P * 4);
     L.ang_o = q;   q += align16((size_t)LC * P * dock_ang_stride(S_w, RC, n_ref));
@@ -191,6 +204,9 @@ __host__ __device__ inline int ligs_per_cta(int NW, int PPW, int P) {
 int grid_mode(int nx, int ny, int nz, float spacing);
 // TYPED window edge (cells) for nch channels
 int typed_window(int nch);
+// TYPED layout of an nch-channel pocket: kGridTyped (QUAD windows) or kGridTypedS (scalar windows),
+// and its window edge W (cells)
+int typed_layout(int nch, int* W);
 // Host layout of a pocket's device copy (floats): nch padded channels [nz+1][ny+1][nx+1], then
 // (16-byte aligned) the global QUAD copy of every channel, nx * (ny + 1) * nz float4 each.
 inline size_t pocket_quad_offset(int nx, int ny, int nz, int nch) {

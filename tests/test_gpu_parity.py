@@ -1011,11 +1011,14 @@ def test_typed_pipelined_docker_matches_single_submit(c2):
     pd.close()
 
 
-def test_typed_large_noncubic_grid_window_misses():
-    """TYPED on a 48 x 40 x 44 grid at 0.75 A with the docking centre off-centre: the channel windows
-    cover only part of the pocket, so many cells come from the global QUAD copy (and beyond the
-    grid, the clamp + excess); score hook on every channel against the oracle, then docking parity
-    with every pose replayed."""
+@pytest.mark.parametrize("layout", ["quad", "scalar"])
+def test_typed_large_noncubic_grid_window_misses(layout, monkeypatch):
+    """TYPED on a 48 x 40 x 44 grid at 0.75 A with the docking centre off-centre, in both channel
+    layouts (QUAD windows / scalar windows, VSDOCK_TYPED_LAYOUT): the channel windows cover only
+    part of the pocket, so many cells come from the global copy (and beyond the grid, the clamp +
+    excess); score hook on every channel against the oracle, then docking parity with every pose
+    replayed."""
+    monkeypatch.setenv("VSDOCK_TYPED_LAYOUT", layout)
     base = vsgen.typed_pocket(105, n_types=3, n=(48, 40, 44), spacing=0.75, center_offset=(2.0, -1.5, 1.0))
     e = engine(debug_poses=True)
     pid = e.load_pocket(base)
@@ -1035,3 +1038,25 @@ def test_typed_large_noncubic_grid_window_misses():
     e.submit_library(lib, [pid])
     e.wait()
     check(e, lib, range(lib.n), base, rot, tr, cs)
+
+
+@pytest.mark.parametrize("T", [2, 3, 4])
+def test_typed_layouts_quad_and_scalar_bit_identical(c2, T, monkeypatch):
+    """The two TYPED channel layouts (QUAD windows: two LDS.128 per point; scalar windows of ~1.6x
+    the edge: eight LDS.32) read the same corner values and blend them in the same order, so a
+    typed submit docks bit-identically in both; the scalar layout's result passes parity on a
+    sample."""
+    c, lib0, _ = c2
+    lib = _typed_lib(lib0.subset(np.arange(1500)), T)
+    pk = vsgen.typed_pocket(106, n_types=T)
+    out = {}
+    for layout in ("quad", "scalar"):
+        monkeypatch.setenv("VSDOCK_TYPED_LAYOUT", layout)
+        e, rot, tr, cs = run(lib, [pk], P=c["P"], K=c["K"], debug=False)
+        out[layout] = (e.results(0), e.coords(0))
+    (rq, xq), (rs, xs) = out["quad"], out["scalar"]
+    assert np.array_equal(rq.best_score, rs.best_score) and np.array_equal(rq.angles, rs.angles)
+    assert np.array_equal(rq.best_pose, rs.best_pose) and np.array_equal(xq, xs)
+    rep = parity.check(lib, np.arange(0, lib.n, 50), pk, rot, tr, cs, rs.best_score, rs.best_pose, rs.angles, xs,
+                       band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
+    assert rep.ok, rep.summary() + str(rep.failures[:5])
