@@ -53,13 +53,15 @@ int grid_mode(int nx, int ny, int nz, float spacing) {
 
 // TYPED (Q24): the largest window edge W <= kQuadWC whose nch channel windows fit kTypedBudget
 // (W = 18, 15, 13, 12, 11, 10, 10, 9 for 1..8 channels)
+// VSDOCK_TYPED_BUDGET (measurement override): the channel windows' budget in quads (16 bytes)
+static long typed_budget() {
+    const char* e = getenv("VSDOCK_TYPED_BUDGET");
+    return e ? atol(e) : (long)kTypedBudget;
+}
+
 int typed_window(int nch) {
     int W = kQuadWC;
-    // VSDOCK_TYPED_BUDGET (measurement override): the channel windows' budget in quads
-    static const long budget = [] {
-        const char* e = getenv("VSDOCK_TYPED_BUDGET");
-        return e ? atol(e) : (long)kTypedBudget;
-    }();
+    const long budget = typed_budget();
     while (W > 2 && (long)nch * typed_chan_stride(W) > budget) --W;
     return W;
 }
@@ -77,7 +79,7 @@ int typed_layout(int nch, int* W) {
         return mode;
     }
     int w = kTypedSMaxW;
-    while (w > 2 && (long)nch * typeds_chan(w) > 4L * kTypedBudget) --w;
+    while (w > 2 && (long)nch * typeds_chan(w) > 4L * typed_budget()) --w;
     *W = w;
     return mode;
 }

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU call of round evidence (TAG=r02c): bench lines (C4 default, C5 with the fused multi-site
+# One GPU call of round evidence (TAG=r02d): bench lines (C4 default, C5 with the fused multi-site
 # leg, C3, C2, the typed variant, the reference arm), the ncu launch list of one bench step
 # (per-kernel time + DRAM bytes), ncu --set full of the heaviest dock launch (class 96, 200k-ligand
 # C4-shaped library) and of the a1 ingest kernel, summarised on the box (the reports stay in /tmp).
@@ -25,3 +25,7 @@ ncu --set full --clock-control none --import-source on -k regex:ingest -s 1 -c 1
     python tools/dock_time.py 200000 > gpurun_out/ncu_ingest_$TAG.log 2>&1
 python tools/ncu_summary.py /tmp/ingest_$TAG.ncu-rep > gpurun_out/ingest_${TAG}_ncu_summary.txt 2>&1
 tail -3 gpurun_out/ncu_dock_$TAG.log
+# full capture of one TYPED_S dock launch (class 96, 4 atom types)
+TYPED=4 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:dock_kernel<.int.96," -s 1 -c 1 \
+    -o /tmp/dock96t4_$TAG python tools/dock_time.py 200000 > gpurun_out/ncu_dock_t4_$TAG.log 2>&1
+python tools/ncu_summary.py /tmp/dock96t4_$TAG.ncu-rep > gpurun_out/dock96_typed4_${TAG}_ncu_summary.txt 2>&1
