@@ -5,7 +5,10 @@ detection row, VERDICT r1 "missing" 7.  Usage: python tools/sanitize_case.py <ca
   edge    a 14^3 grid (atoms on and beyond the faces: the top-face corner handling) + K = 6
   ring    launch_per_bucket with bucket capacity 1 on 8 streams: many tiny launches of the round ring
   win     a 48^3 grid at 0.5 A (window + global corners)
-  typed   4 atom types into a typed pocket (TYPED layout, Q24) with rigid refinement (Q23)
+  typed   4 atom types into a typed pocket (TYPED_S layout, Q24) with rigid refinement (Q23)
+  typedq  the same in the QUAD channel layout (VSDOCK_TYPED_LAYOUT=quad)
+  typedbig 3 atom types into a 48 x 40 x 44 typed pocket at 0.75 A, off-centre (TYPED_S window
+          misses through the padded global copies, clamp + excess beyond the grid)
   fused   3 pockets docked by one fused multi-site cluster launch per class (f1: multicast TMA,
           cluster mbarriers, DSMEM ring writes)
 Exits non-zero if the results are not finite (the sanitizer's own report is the evidence)."""
@@ -53,6 +56,15 @@ elif case == "typed":
     lib = vsgen.ligands(16, 1, (20, 60), (0, 6))
     lib.atom_type = vsgen.atom_types(lib, n_types=4)
     run(lib, vsgen.typed_pocket(101, n_types=4), refine=True)
+elif case == "typedq":
+    os.environ["VSDOCK_TYPED_LAYOUT"] = "quad"
+    lib = vsgen.ligands(16, 1, (20, 60), (0, 6))
+    lib.atom_type = vsgen.atom_types(lib, n_types=4)
+    run(lib, vsgen.typed_pocket(101, n_types=4), refine=True)
+elif case == "typedbig":
+    lib = vsgen.ligands(16, 41, (20, 110), (0, 10))
+    lib.atom_type = vsgen.atom_types(lib, n_types=3)
+    run(lib, vsgen.typed_pocket(105, n_types=3, n=(48, 40, 44), spacing=0.75, center_offset=(2.0, -1.5, 1.0)))
 elif case == "fused":
     run(vsgen.ligands(40, 9, (20, 90), (0, 8)), [vsgen.pocket(s) for s in (101, 102, 103)], P=16, fused_sites=True)
 else:
