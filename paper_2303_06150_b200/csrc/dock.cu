@@ -67,7 +67,7 @@ int typed_window(int nch) {
 }
 
 // TYPED_S: the largest W <= kTypedSMaxW whose nch scalar channel windows fit the same budget
-// (4 kTypedBudget floats): W = 30, 24, 21, 18, 17, 16, 15, 14 for 1..8 channels.
+// (4 kTypedBudget floats): W = 30, 24, 20, 18, 17, 16, 15, 14 for 1..8 channels.
 // Layout choice (measured): VSDOCK_TYPED_LAYOUT=quad|scalar overrides.
 int typed_layout(int nch, int* W) {
     // (read at every pocket set-up, so one process can compare the two layouts)

@@ -1264,7 +1264,7 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
                : NW == 12 ? dock_kernel<AC, 12, 4, GM, 0, false>
                : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0, false>
                           : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0, false> : nullptr));
-    }
+    } else {   // (else: typed layouts instantiate none of the lane maps below)
     if constexpr (GM == kGridQuad) {   // more warps where shared memory allows (latency hiding)
         if (PPW == 4 && K == 8) {
             if constexpr (AC <= 96) if (NW == 20) return dock_kernel<AC, 20, 4, GM, 8, false>;
@@ -1288,6 +1288,7 @@ DockFn pick_ac(int NW, int PPW, int K, bool ms) {
                : NW == 12 ? dock_kernel<AC, 12, 4, GM, 0, false>
                : NW == 10 ? dock_kernel<AC, 10, 4, GM, 0, false>
                           : (NW == 8 ? dock_kernel<AC, 8, 4, GM, 0, false> : (NW == 4 ? dock_kernel<AC, 4, 4, GM, 0, false> : nullptr));
+    }
     return nullptr;
 }
 
