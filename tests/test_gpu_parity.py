@@ -1060,3 +1060,29 @@ def test_typed_layouts_quad_and_scalar_bit_identical(c2, T, monkeypatch):
     rep = parity.check(lib, np.arange(0, lib.n, 50), pk, rot, tr, cs, rs.best_score, rs.best_pose, rs.angles, xs,
                        band=BAND, tol_score=TOL_S, tol_xyz=TOL_X)
     assert rep.ok, rep.summary() + str(rep.failures[:5])
+
+
+@pytest.mark.parametrize("layout", ["quad", "scalar"])
+def test_typed_grid_smaller_than_the_window(layout, monkeypatch):
+    """A 14^3 typed pocket (3 channels) is smaller than either layout's channel window (13 / 20 cells):
+    the windows clamp to the grid, nodes past its pads stay zero, and atoms outside the box take the
+    clamp + excess; score hook on every channel against the oracle, then docking parity with every
+    pose replayed."""
+    monkeypatch.setenv("VSDOCK_TYPED_LAYOUT", layout)
+    pk = vsgen.typed_pocket(107, n_types=3, n=14, spacing=1.0, shell=(4.0, 6.0), n_receptor=40)
+    e = engine(debug_poses=True)
+    pid = e.load_pocket(pk)
+    rng = np.random.default_rng(5)
+    pts = (np.array(pk.center) + rng.normal(0, 6.0, size=(20000, 3))).astype(np.float32)
+    t = rng.integers(0, 3, size=len(pts)).astype(np.uint8)
+    g = e.score_points(pid, pts, types=t)
+    ref = oracle.grid_score(pk, pts.astype(np.float64), t)
+    assert np.max(np.abs(g - ref) / np.maximum(1, np.abs(ref))) < 2e-6
+    lib = _typed_lib(vsgen.ligands(20, 43, (20, 70), (0, 8)), 3)
+    rot, tr = vsgen.pose_table(8, tau=1.0)
+    cs = vsgen.angle_table(8)
+    e.set_poses(rot, tr)
+    e.set_angles(cs)
+    e.submit_library(lib, [pid])
+    e.wait()
+    check(e, lib, range(lib.n), pk, rot, tr, cs)
