@@ -187,9 +187,11 @@ typedef struct {
 vs_status vs_submit(vs_ctx* ctx, const vs_ligand_batch* batch, const int32_t* pocket_ids, int32_t n_pockets);
 /* Q24: vs_submit with per-atom types atom_type[atom_off[n] - atom_off[0]] (u8, the caller's atom
  * order, the same memory kind as batch->on_device: host copied, device borrowed, or mapped pinned
- * host read in place for the owned ligands only).  Every pocket docks in the TYPED layout (DESIGN.md
- * 6: the channel windows of the QUAD layout in shared memory, the padded channels in global
- * memory behind them).  A type >= the channels of any docked pocket is VS_E_PARSE naming the
+ * host read in place for the owned ligands only).  Every pocket docks in a typed layout (DESIGN.md
+ * 6): TYPED for one channel (a QUAD window in shared memory), TYPED_S for two or more (one scalar
+ * window per channel, ~1.6x the edge for the same shared memory), the padded channels in global
+ * memory behind the windows; both give bit-identical results (environment override for
+ * measurement: VSDOCK_TYPED_LAYOUT=quad|scalar).  A type >= the channels of any docked pocket is VS_E_PARSE naming the
  * ligand (rank-local, like a1's per-atom checks). */
 vs_status vs_submit_typed(vs_ctx* ctx, const vs_ligand_batch* batch, const uint8_t* atom_type,
                           const int32_t* pocket_ids, int32_t n_pockets);
